@@ -1,0 +1,52 @@
+"""splitmix64 right-hand side keyed by the 64-bit global Lambda index.
+
+G = (j_g * nz + k) * nx_glob + i_g            (0-based, eqn:MemoryMapSingleGPU P:243)
+x = seed * GOLDEN + G ; z = x + GOLDEN
+z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9
+z = (z ^ (z >> 27)) * 0x94D049BB133111EB
+z ^= z >> 31
+f = (z >> 11) * 2^-53 * 2 - 1                 in [-1, 1)
+
+Pure integer arithmetic (wrap-around uint64), hence decomposition-independent
+and identical on host and device.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+
+
+def _mix(g: np.ndarray, seed: int) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        x = np.uint64(seed) * GOLDEN + g
+        z = x + GOLDEN
+        z = (z ^ (z >> np.uint64(30))) * _M1
+        z = (z ^ (z >> np.uint64(27))) * _M2
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53) * 2.0 - 1.0
+
+
+def rhs_lambda(nx_glob: int, ny: int, nz: int, seed: int = 0, y0: int = 0) -> np.ndarray:
+    """Rows y0..y0+ny-1 of the global field, Lambda layout, shape (ny, nz, nx_glob)."""
+    j = np.arange(y0, y0 + ny, dtype=np.uint64)[:, None, None]
+    k = np.arange(nz, dtype=np.uint64)[None, :, None]
+    i = np.arange(nx_glob, dtype=np.uint64)[None, None, :]
+    g = (j * np.uint64(nz) + k) * np.uint64(nx_glob) + i
+    return _mix(g, seed)
+
+
+def rhs_zc(nx_glob: int, ny: int, nz: int, seed: int = 0, y0: int = 0) -> np.ndarray:
+    """The same values in the oracle's z-contiguous layout, shape (ny, nx, nz)."""
+    return np.ascontiguousarray(np.transpose(rhs_lambda(nx_glob, ny, nz, seed, y0), (0, 2, 1)))
+
+
+def mode_zc(nx: int, ny: int, nz: int, p: int, q: int, r: int) -> np.ndarray:
+    """Separable mode sin(p pi (i+1)/(nx+1)) sin(q pi (j+1)/(ny+1)) cos(r pi (k+1/2)/nz),
+    z-contiguous (ny, nx, nz); (i, j) 0-based so i+1 is the paper's 1-based index."""
+    si = np.sin(p * np.pi * np.arange(1, nx + 1) / (nx + 1))
+    sj = np.sin(q * np.pi * np.arange(1, ny + 1) / (ny + 1))
+    ck = np.cos(r * np.pi * (np.arange(nz) + 0.5) / nz)
+    return np.ascontiguousarray(sj[:, None, None] * si[None, :, None] * ck[None, None, :])
