@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark: MG V-cycle and PCG solves to 1e-5 on B200 (BASELINE.json metric).
+
+One "step" is one pass of the whole hot path over one right-hand side: a
+multigrid solve (V-cycles of the fused line smoother, residual->restriction,
+RestrictSmooth, prolongation) AND a line-preconditioned CG solve (the two fused
+CG kernels with their reductions), both from u = 0 to ||r||/||r_0|| < 1e-5, on
+the same device-resident f.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl tpmg|reference]
+
+N = 1: BASELINE configs[1] (1024 x 1024 x 128, fp64).  N > 1 (torchrun, one
+rank per GPU, NCCL): weak scaling with the same 1024 x 1024 x 128 per GPU,
+global 1024 x 1024N (y-strips); --per-gpu-nx 2048 gives configs[3].
+Vectors are 1 GiB per GPU, far larger than the 126 MB L2, so no flush is
+needed between steps.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MG V-cycle & PCG time-to-1e-5 and achieved HBM GB/s at 1/2/4/8 B200"
+UNIT = "unknowns/s (MG + PCG solves to 1e-5, summed)"
+
+# Algorithmic (compulsory) HBM bytes per processed cell of each kernel class
+# (DESIGN.md "Kernels and their rooflines"); cells are level cells, fine cells
+# for the transfer kernels.
+BYTES_PER_CELL = {
+    "apply": 16, "residual": 16, "precondition": 16, "smooth": 24, "cg_direction": 24,
+    "cg_precondition": 48, "residual_restrict": 18, "restrict": 10, "prolong_add": 18, "dot": 8,
+}
+PAPER_FLOPS = {"cg": 54.0, "mg": 149.4}  # tab:KernelTable totals per cell per iteration
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["tpmg", "reference"], default="tpmg")
+    ap.add_argument("--per-gpu-nx", type=int, default=1024)
+    ap.add_argument("--nz", type=int, default=128)
+    ap.add_argument("--nu", type=float, default=8.4)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--eps", type=float, default=1e-5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--solver", choices=["both", "mg", "cg"], default="both")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(args, world):
+    nx = args.per_gpu_nx
+    ny = nx * world
+    name = ("C2: MG + PCG on 1024x1024x128 fp64, 1 B200" if world == 1 and nx == 1024 else
+            f"weak scaling: {nx}x{nx}x{args.nz} per GPU, global {nx}x{ny}x{args.nz}, {world} B200 y-strips")
+    return nx, ny, name
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.out = b""
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in self.out.decode(errors="ignore").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = sorted(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[q] for r in rows for q in range(4) if r[5 + q].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------- oracle legs
+
+def oracle_sample(nx, nz, nu, rows, seed, threads=None):
+    """Time the CPU oracle (as it stands) on a y-strip of `rows` rows of the workload:
+    one MG V-cycle (solve_mg, max_iter=1: norm + V-cycle + residual) and one PCG
+    iteration (solve_cg, max_iter=1: setup preconditioner + one iteration)."""
+    from oracle import oracle as O
+    from inputs import rhs_zc
+    if threads:
+        O.set_threads(threads)
+    p = O.Params(nx=nx, ny=rows, nz=nz, nu_cfl=nu)
+    f = rhs_zc(nx, rows, nz, seed=seed)
+    t0 = time.perf_counter()
+    O.solve_mg(p, f, eps=1e-30, max_iter=1)
+    t1 = time.perf_counter()
+    O.solve_cg(p, f, eps=1e-30, max_iter=1)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, O.num_threads()
+
+
+def run_reference(args):
+    """--impl reference: the oracle, as it stands, on the host cores (rank 0 only)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    nx, ny, name = workload(args, world)
+    rows = 32
+    scale = ny / rows
+    it_mg, it_cg = 9, 51  # iteration counts of the oracle at 128^2 x 128 (tests/test_oracle_pins)
+    for _ in range(args.warmup):
+        oracle_sample(nx, args.nz, args.nu, rows, args.seed)
+    t = 0.0
+    tm = tc = 0.0
+    for _ in range(args.steps):
+        a, b, cores = oracle_sample(nx, args.nz, args.nu, rows, args.seed)
+        tm += a; tc += b
+        t += scale * (it_mg * a + it_cg * b)
+    N = nx * ny * args.nz
+    value = 2 * N * args.steps / t
+    sample = (f"per step: oracle MG solve with max_iter=1 (norm + 1 V-cycle + residual) and PCG solve "
+              f"with max_iter=1 (setup + 1 iteration) on a {nx}x{rows}x{args.nz} y-strip of the workload; "
+              f"scaled x{scale:g} in cells and x{it_mg}/x{it_cg} in iterations (oracle counts, size-independent P:421)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (splitmix64 RHS, seed %d)" % args.seed,
+        "config": {"workload": name, "nx": nx, "ny": ny, "nz": args.nz, "nu_cfl": args.nu, "eps": args.eps,
+                   "levels": 5},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_1402_3545_b200 import build as B
+    B.build()
+    from paper_1402_3545_b200 import tpmg as T
+    from inputs import gpu as G
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    nx, ny, name = workload(args, world)
+    nz = args.nz
+    id128 = None
+    if world > 1:
+        obj = [T.tpmg_nccl_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        id128 = obj[0]
+    stream = torch.cuda.Stream(device=local)
+    params = T.make_params(nx, ny, nz=nz, nu_cfl=args.nu)
+    ctx = T.Context(params, rank=rank, nranks=world, id128=id128, device=local, stream=stream)
+    shape = ctx.shape(5)
+    f = torch.empty(shape, dtype=torch.float64, device=f"cuda:{local}")
+    u = torch.empty_like(f)
+    y0 = ctx.local_box(5)[0]
+    with torch.cuda.stream(stream):
+        G.fill_rhs(f, nx, y0=y0, seed=args.seed, stream=stream)
+    stream.synchronize()
+    n_glob = nx * ny * nz
+    do_mg = args.solver in ("both", "mg")
+    do_cg = args.solver in ("both", "cg")
+
+    def step():
+        r_mg = ctx.solve_mg(f, u, eps=args.eps) if do_mg else None
+        r_cg = ctx.solve_cg(f, u, eps=args.eps) if do_cg else None
+        return r_mg, r_cg
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ctx.stats_reset()
+    ctx.profile(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_mg = t_cg = 0.0
+    its = None
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            r_mg, r_cg = step()
+            t_mg += r_mg.seconds if r_mg else 0.0
+            t_cg += r_cg.seconds if r_cg else 0.0
+            its = (r_mg, r_cg)
+        ev1.record(stream)
+        barrier()
+    ms_local = ev0.elapsed_time(ev1)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    stats = ctx.stats()
+    ms = torch.tensor([ms_local], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    solves = (1 if do_mg else 0) + (1 if do_cg else 0)
+    value = solves * n_glob * args.steps / (ms * 1e-3)
+
+    # roofline of the dominant kernel class (largest share of device time)
+    peak, peak_src = measured_peak()
+    dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
+    roof = None
+    kernels = {}
+    for kname, (n, kms, cells) in prof.items():
+        gbs = cells * BYTES_PER_CELL[kname] / (kms * 1e-3) / 1e9 if kms > 0 else None
+        kernels[kname] = {"launches": n, "ms_total": round(kms, 4), "gbs": gbs and round(gbs, 1),
+                          "share": round(kms / ms, 4)}
+    if dom:
+        kname, (n, kms, cells) = dom
+        ach = cells * BYTES_PER_CELL[kname] / (kms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": kname, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_src,
+                "bytes_per_cell": BYTES_PER_CELL[kname],
+                "cells_per_launch": cells / n, "avg_launch_ms": kms / n}
+
+    def solver_block(r, t_total, kind):
+        if r is None:
+            return None
+        t = t_total / args.steps
+        n_it = r.iterations
+        useful = None
+        return {"iterations": n_it, "converged": r.converged, "rel_residual": r.rel_residual,
+                "time_to_solution_ms": round(1e3 * t, 3),
+                "unknowns_per_s": n_glob / t,
+                "paper_gflops": PAPER_FLOPS[kind] * n_glob * n_it / t / 1e9,
+                "ms_per_iteration": round(1e3 * t / max(n_it, 1), 4), "useful_gbs": useful}
+
+    line_extra = {"mg": solver_block(its[0], t_mg, "mg"), "pcg": solver_block(its[1], t_cg, "cg")}
+    # algorithmic HBM GB/s over the whole step (sum over kernel classes / step time)
+    alg_bytes = sum(cells * BYTES_PER_CELL[k] for k, (n, kms, cells) in prof.items())
+    hbm_gbs_step = alg_bytes / (ms_local * 1e-3) / 1e9
+
+    # end-to-end through the C ABI with host buffers (H2D of f and D2H of u inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        fh = f.cpu().pin_memory()
+        uh = torch.empty_like(fh).pin_memory()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            if do_mg:
+                ctx.solve_host(T.TPMG_SOLVER_MG, fh, uh, eps=args.eps)
+            if do_cg:
+                ctx.solve_host(T.TPMG_SOLVER_CG, fh, uh, eps=args.eps)
+        barrier()
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te = float(te.item())
+        nbytes = fh.numel() * 8 * world
+        e2e = {"value": solves * n_glob * args.steps / te, "unit": UNIT,
+               "h2d_bytes_per_step": solves * nbytes, "d2h_bytes_per_step": solves * nbytes}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rows = 128
+        a, b, cores = oracle_sample(nx, nz, args.nu, rows, args.seed)
+        scale = ny / rows
+        it_mg = its[0].iterations if its[0] else 0
+        it_cg = its[1].iterations if its[1] else 0
+        t_est = scale * ((it_mg * a if do_mg else 0) + (it_cg * b if do_cg else 0))
+        cpu = {"value": solves * n_glob / t_est, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": (f"oracle MG solve max_iter=1 ({a:.2f} s) and PCG solve max_iter=1 ({b:.2f} s) on a "
+                          f"{nx}x{rows}x{nz} y-strip of the workload, scaled x{scale:g} in cells and by the "
+                          f"iteration counts of this run ({it_mg} V-cycles, {it_cg} CG iterations)")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (splitmix64 uniform[-1,1) RHS keyed by global index, seed %d)" % args.seed,
+            "config": {"workload": name, "nx": nx, "ny": ny, "nz": nz, "nu_cfl": args.nu, "eps": args.eps,
+                       "levels": 5, "parallelism": f"y-strips x{world}" if world > 1 else "single GPU",
+                       "l2": "vectors 1 GiB/GPU >> 126 MB L2 (no flush needed)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": stats["kernel_launches"],
+            "clocks": clk.summary(),
+            "hbm_gbs_step": round(hbm_gbs_step, 1),
+            "kernels": kernels,
+            **line_extra,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

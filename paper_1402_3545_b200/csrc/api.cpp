@@ -1,0 +1,971 @@
+// api.cpp -- the C ABI of libtpmg.so (include/tpmg.h): context, per-level
+// operator tables, multigrid hierarchy, PCG, halo exchange and reductions.
+//
+// Host orchestration only: every arithmetic step of the hot path runs in the
+// sm_100a kernels of kernels.cu.  Multi-GPU plumbing is NCCL over NVLink:
+// halo slabs with ncclSend/ncclRecv (y-strip decomposition) and
+// ncclAllReduce for the solver's global sums.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tpmg.h"
+#include "kernels.cuh"
+
+using namespace tpmg;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct LevelData {
+    LevelConst lc{};
+    double* d_tab = nullptr;
+    double* u[2] = {nullptr, nullptr};  // MG iterate ping-pong (fine level: u[0] = caller's u)
+    int cur = 0;
+    double* f = nullptr;                // MG right-hand side (coarse levels)
+    double* slab_lo = nullptr;          // halo rows j = -1 / j = ny for this level (nranks > 1)
+    double* slab_hi = nullptr;
+    size_t n() const { return (size_t)lc.nx * (size_t)lc.ny * (size_t)lc.nz; }
+    size_t plane() const { return (size_t)lc.nx * (size_t)lc.nz; }
+};
+
+}  // namespace
+
+struct tpmg_ctx {
+    tpmg_params p{};
+    int rank = 0, nranks = 1, device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    int L = 0;
+    int64_t ny_loc = 0, y0 = 0;
+    std::vector<LevelData> lv;  // index 1..L
+    // reductions
+    double* d_partials = nullptr;
+    unsigned* d_ticket = nullptr;
+    double* d_scal = nullptr;   // CG per-iteration scalars / norms
+    int scal_cap = 0;
+    double* h_pinned = nullptr; // pinned host scalars
+    // work vectors (lazily allocated)
+    bool mg_ready = false, cg_ready = false;
+    double* scratch = nullptr;   // fine-size scratch (single-op ping-pong)
+    double *cg_r = nullptr, *cg_z = nullptr, *cg_p[2] = {nullptr, nullptr};
+    double *cg_zlo = nullptr, *cg_zhi = nullptr, *cg_plo[2] = {nullptr, nullptr}, *cg_phi[2] = {nullptr, nullptr};
+    double *host_f = nullptr, *host_u = nullptr;  // device buffers for tpmg_solve_host
+    ncclComm_t comm = nullptr;
+    tpmg_stats stats{};
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // profiling (tpmg_profile)
+    bool prof_on = false;
+    struct ProfRec { int cls; double cells; cudaEvent_t a, b; };
+    std::vector<ProfRec> prof_pending;
+    std::vector<cudaEvent_t> prof_pool;
+    int64_t prof_launches[TPMG_K_COUNT] = {};
+    double prof_ms[TPMG_K_COUNT] = {}, prof_cells[TPMG_K_COUNT] = {};
+    std::string err;
+};
+
+namespace {
+
+tpmg_status fail(tpmg_ctx* ctx, tpmg_status st, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->err = buf; else g_create_error = buf;
+    return st;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                  \
+    do {                                                                                     \
+        cudaError_t e_ = (expr);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail((ctx), TPMG_E_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                 \
+    } while (0)
+
+#define NCCL_TRY(ctx, expr)                                                                  \
+    do {                                                                                     \
+        ncclResult_t e_ = (expr);                                                            \
+        if (e_ != ncclSuccess)                                                               \
+            return fail((ctx), TPMG_E_NCCL, "%s: %s (%s:%d)", #expr, ncclGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                 \
+    } while (0)
+
+#define TRY(expr)                            \
+    do {                                     \
+        tpmg_status s_ = (expr);             \
+        if (s_ != TPMG_OK) return s_;        \
+    } while (0)
+
+Launcher launcher(tpmg_ctx* ctx)
+{
+    Launcher ln;
+    ln.stream = ctx->stream;
+    ln.num_sms = ctx->num_sms;
+    ln.launch_counter = &ctx->stats.kernel_launches;
+    return ln;
+}
+
+ReduceSlot slot(tpmg_ctx* ctx, double* result)
+{
+    return ReduceSlot{ctx->d_partials, ctx->d_ticket, result};
+}
+
+tpmg_status dev_alloc(tpmg_ctx* ctx, double** p, size_t n)
+{
+    if (*p) return TPMG_OK;
+    cudaError_t e = cudaMalloc((void**)p, sizeof(double) * (n ? n : 1));
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return fail(ctx, TPMG_E_OOM, "cudaMalloc(%zu doubles): %s", n, cudaGetErrorString(e));
+    }
+    return TPMG_OK;
+}
+
+tpmg_status check_level(tpmg_ctx* ctx, int level)
+{
+    if (!ctx) return TPMG_E_PARAM;
+    if (level < 1 || level > ctx->L) return fail(ctx, TPMG_E_RANGE, "level %d not in [1, %d]", level, ctx->L);
+    return TPMG_OK;
+}
+
+// ------------------------------------------------------------------ halos and reductions
+
+// Fill the halo slabs of `level` from the neighbours' boundary rows of x (nranks > 1).
+tpmg_status exchange(tpmg_ctx* ctx, int level, const double* x, double* lo, double* hi)
+{
+    if (ctx->nranks == 1) return TPMG_OK;
+    LevelData& L = ctx->lv[level];
+    const size_t plane = L.plane();
+    const double* first = x;
+    const double* last = x + (size_t)(L.lc.ny - 1) * plane;
+    NCCL_TRY(ctx, ncclGroupStart());
+    if (ctx->rank > 0) {
+        NCCL_TRY(ctx, ncclSend(first, plane, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
+        NCCL_TRY(ctx, ncclRecv(lo, plane, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
+    }
+    if (ctx->rank < ctx->nranks - 1) {
+        NCCL_TRY(ctx, ncclSend(last, plane, ncclDouble, ctx->rank + 1, ctx->comm, ctx->stream));
+        NCCL_TRY(ctx, ncclRecv(hi, plane, ncclDouble, ctx->rank + 1, ctx->comm, ctx->stream));
+    }
+    NCCL_TRY(ctx, ncclGroupEnd());
+    ++ctx->stats.halo_exchanges;
+    return TPMG_OK;
+}
+
+HaloField halo_of(tpmg_ctx* ctx, int level, const double* x)
+{
+    LevelData& L = ctx->lv[level];
+    return HaloField{x, ctx->rank > 0 ? L.slab_lo : nullptr, ctx->rank < ctx->nranks - 1 ? L.slab_hi : nullptr};
+}
+
+// Exchange x's halo into the level slabs and return the halo'd view.
+tpmg_status halo(tpmg_ctx* ctx, int level, const double* x, HaloField* out)
+{
+    TRY(exchange(ctx, level, x, ctx->lv[level].slab_lo, ctx->lv[level].slab_hi));
+    *out = halo_of(ctx, level, x);
+    return TPMG_OK;
+}
+
+tpmg_status allreduce(tpmg_ctx* ctx, double* d, int n)
+{
+    if (ctx->nranks == 1) return TPMG_OK;
+    NCCL_TRY(ctx, ncclAllReduce(d, d, n, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    ++ctx->stats.allreduces;
+    return TPMG_OK;
+}
+
+// Copy n device doubles to the pinned host buffer and wait.
+tpmg_status fetch(tpmg_ctx* ctx, const double* d, int n)
+{
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_pinned, d, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return TPMG_OK;
+}
+
+// ------------------------------------------------------------------ kernels (thin wrappers)
+
+LineArgs line_args(tpmg_ctx* ctx, int level)
+{
+    LineArgs a{};
+    a.L = ctx->lv[level].lc;
+    a.rho = ctx->p.rho;
+    a.scale = 1.0;
+    a.ratio = DevRatio{nullptr, -1, -1};
+    a.red = ReduceSlot{ctx->d_partials, ctx->d_ticket, nullptr};
+    return a;
+}
+
+// ------------------------------------------------------------------ profiling
+
+cudaEvent_t prof_event(tpmg_ctx* ctx)
+{
+    if (!ctx->prof_pool.empty()) {
+        cudaEvent_t e = ctx->prof_pool.back();
+        ctx->prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Bracket one kernel launch (class cls, `cells` grid cells) with events when profiling.
+struct ProfScope {
+    tpmg_ctx* ctx;
+    int cls;
+    double cells;
+    cudaEvent_t a = nullptr;
+    ProfScope(tpmg_ctx* c, int k, double n) : ctx(c), cls(k), cells(n)
+    {
+        if (ctx->prof_on) {
+            a = prof_event(ctx);
+            cudaEventRecord(a, ctx->stream);
+        }
+    }
+    ~ProfScope()
+    {
+        if (a) {
+            cudaEvent_t b = prof_event(ctx);
+            cudaEventRecord(b, ctx->stream);
+            ctx->prof_pending.push_back({cls, cells, a, b});
+        }
+    }
+};
+
+tpmg_status prof_collect(tpmg_ctx* ctx)
+{
+    if (ctx->prof_pending.empty()) return TPMG_OK;
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    for (auto& r : ctx->prof_pending) {
+        float ms = 0;
+        CUDA_TRY(ctx, cudaEventElapsedTime(&ms, r.a, r.b));
+        ctx->prof_launches[r.cls] += 1;
+        ctx->prof_ms[r.cls] += ms;
+        ctx->prof_cells[r.cls] += r.cells;
+        ctx->prof_pool.push_back(r.a);
+        ctx->prof_pool.push_back(r.b);
+    }
+    ctx->prof_pending.clear();
+    return TPMG_OK;
+}
+
+double level_cells(const LevelConst& l) { return (double)l.nx * (double)l.ny * (double)l.nz; }
+
+tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a)
+{
+    ProfScope ps(ctx, mode, level_cells(a.L));   // line modes map 1:1 onto TPMG_K_0..5
+    CUDA_TRY(ctx, launch_line(launcher(ctx), mode, a));
+    return TPMG_OK;
+}
+
+// out = u + rho M^-1 (f - A u) (out-of-place), optional sum r^2 into result
+tpmg_status smooth_once(tpmg_ctx* ctx, int level, const double* u, const double* f, double* out,
+                        double* result)
+{
+    LineArgs a = line_args(ctx, level);
+    TRY(halo(ctx, level, u, &a.h0));
+    a.q0 = f;
+    a.out0 = out;
+    a.red.result = result;
+    return run_line(ctx, MODE_SMOOTH, a);
+}
+
+// ------------------------------------------------------------------ multigrid
+
+tpmg_status mg_alloc(tpmg_ctx* ctx)
+{
+    if (ctx->mg_ready) return TPMG_OK;
+    for (int l = 1; l <= ctx->L; ++l) {
+        LevelData& L = ctx->lv[l];
+        if (l < ctx->L) {
+            TRY(dev_alloc(ctx, &L.u[0], L.n()));
+            TRY(dev_alloc(ctx, &L.f, L.n()));
+        }
+        TRY(dev_alloc(ctx, &L.u[1], L.n()));
+    }
+    ctx->mg_ready = true;
+    return TPMG_OK;
+}
+
+// Kernel RestrictSmooth preceded by the fine residual:
+// f^(l) = R (f^(l+1) - A u^(l+1)), u^(l) = rho M^-1 f^(l)   (zero initial guess)
+tpmg_status mg_restrict_smooth(tpmg_ctx* ctx, int l)
+{
+    LevelData& F = ctx->lv[l + 1];
+    LevelData& Cc = ctx->lv[l];
+    HaloField uf;
+    TRY(halo(ctx, l + 1, F.u[F.cur], &uf));
+    {
+        ProfScope ps(ctx, TPMG_K_RESIDUAL_RESTRICT, level_cells(F.lc));
+        CUDA_TRY(ctx, launch_residual_restrict(launcher(ctx), F.lc, Cc.lc, uf, F.f, Cc.f));
+    }
+    LineArgs a = line_args(ctx, l);
+    a.q0 = Cc.f;
+    a.out0 = Cc.u[0];
+    a.scale = ctx->p.rho;
+    Cc.cur = 0;
+    return run_line(ctx, MODE_PREC, a);
+}
+
+tpmg_status mg_smooth(tpmg_ctx* ctx, int l, double* result = nullptr)
+{
+    LevelData& L = ctx->lv[l];
+    TRY(smooth_once(ctx, l, L.u[L.cur], L.f, L.u[1 - L.cur], result));
+    L.cur ^= 1;
+    return TPMG_OK;
+}
+
+// Subroutine VCycle (alg:VCycle) with the readings [R5] of DESIGN.md.
+tpmg_status vcycle_rec(tpmg_ctx* ctx, int l)
+{
+    const tpmg_params& p = ctx->p;
+    if (l == 1) {
+        int s0 = 0;
+        if (ctx->L > 1) {
+            TRY(mg_restrict_smooth(ctx, 1));
+            s0 = 1;
+        }
+        for (int s = s0; s < p.coarse_sweeps; ++s) TRY(mg_smooth(ctx, 1));
+        return TPMG_OK;
+    }
+    if (l == ctx->L) {
+        for (int s = 0; s < p.pre; ++s) TRY(mg_smooth(ctx, l));
+    } else {
+        TRY(mg_restrict_smooth(ctx, l));
+        for (int s = 1; s < p.pre; ++s) TRY(mg_smooth(ctx, l));
+    }
+    TRY(vcycle_rec(ctx, l - 1));
+    LevelData& Cc = ctx->lv[l - 1];
+    LevelData& F = ctx->lv[l];
+    HaloField uc;
+    TRY(halo(ctx, l - 1, Cc.u[Cc.cur], &uc));
+    {
+        ProfScope ps(ctx, TPMG_K_PROLONG_ADD, level_cells(F.lc));
+        CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc, F.u[F.cur]));
+    }
+    for (int s = 0; s < p.post; ++s) TRY(mg_smooth(ctx, l));
+    return TPMG_OK;
+}
+
+// One V-cycle with the caller's fine-level u, f.  Leaves the result in u.
+tpmg_status vcycle_fine(tpmg_ctx* ctx, double* u, const double* f)
+{
+    LevelData& F = ctx->lv[ctx->L];
+    F.u[0] = u;
+    F.f = const_cast<double*>(f);
+    F.cur = 0;
+    TRY(vcycle_rec(ctx, ctx->L));
+    if (F.cur != 0) CUDA_TRY(ctx, cudaMemcpyAsync(u, F.u[1], sizeof(double) * F.n(), cudaMemcpyDeviceToDevice, ctx->stream));
+    F.cur = 0;
+    return TPMG_OK;
+}
+
+// Global ||f - A u||^2 of the fine level (into d_scal[slot]).
+tpmg_status fine_residual_norm2(tpmg_ctx* ctx, const double* u, const double* f, double* d_out)
+{
+    const int l = ctx->L;
+    LineArgs a = line_args(ctx, l);
+    TRY(halo(ctx, l, u, &a.h0));
+    a.q0 = f;
+    a.out0 = nullptr;
+    a.red.result = d_out;
+    TRY(run_line(ctx, MODE_RESID, a));
+    return allreduce(ctx, d_out, 1);
+}
+
+tpmg_status ensure_scal(tpmg_ctx* ctx, int n)
+{
+    if (n <= ctx->scal_cap) return TPMG_OK;
+    if (ctx->d_scal) cudaFree(ctx->d_scal);
+    ctx->d_scal = nullptr;
+    TRY(dev_alloc(ctx, &ctx->d_scal, (size_t)n));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_scal, 0, sizeof(double) * n, ctx->stream));
+    ctx->scal_cap = n;
+    return TPMG_OK;
+}
+
+void result_init(tpmg_result* res)
+{
+    if (!res) return;
+    res->iterations = 0;
+    res->converged = 0;
+    res->r0_norm = 0;
+    res->rel_residual = 0;
+    res->seconds = 0;
+}
+
+void record_hist(tpmg_result* res, int it, double v)
+{
+    if (res && res->history && it < res->history_cap) res->history[it] = v;
+}
+
+tpmg_status solve_mg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps, int max_iter,
+                          tpmg_result* res)
+{
+    TRY(mg_alloc(ctx));
+    TRY(ensure_scal(ctx, 8));
+    const LevelData& F = ctx->lv[ctx->L];
+    result_init(res);
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    CUDA_TRY(ctx, cudaMemsetAsync(u, 0, sizeof(double) * F.n(), ctx->stream));   // u_0 = 0 [R9]
+    // ||r_0|| = ||f - A 0|| = ||f||
+    {
+        ProfScope ps(ctx, TPMG_K_DOT, (double)F.n());
+        CUDA_TRY(ctx, launch_dot(launcher(ctx), f, f, (int64_t)F.n(), slot(ctx, ctx->d_scal)));
+    }
+    TRY(allreduce(ctx, ctx->d_scal, 1));
+    TRY(fetch(ctx, ctx->d_scal, 1));
+    const double r0 = std::sqrt(ctx->h_pinned[0]);
+    record_hist(res, 0, r0);
+    int it = 0;
+    bool conv = (r0 == 0.0);
+    double rel = conv ? 0.0 : 1.0;
+    while (!conv && it < max_iter) {
+        TRY(vcycle_fine(ctx, u, f));
+        TRY(fine_residual_norm2(ctx, u, f, ctx->d_scal + 1));
+        TRY(fetch(ctx, ctx->d_scal + 1, 1));
+        const double rn = std::sqrt(ctx->h_pinned[0]);
+        ++it;
+        record_hist(res, it, rn);
+        rel = rn / r0;
+        if (!(rn == rn)) return fail(ctx, TPMG_E_BREAKDOWN, "NaN residual after V-cycle %d", it);
+        if (rel < eps) conv = true;
+    }
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
+    float ms = 0;
+    CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    if (res) {
+        res->iterations = it;
+        res->converged = conv ? 1 : 0;
+        res->r0_norm = r0;
+        res->rel_residual = rel;
+        res->seconds = ms * 1e-3;
+    }
+    return TPMG_OK;
+}
+
+// ------------------------------------------------------------------ CG
+
+tpmg_status cg_alloc(tpmg_ctx* ctx)
+{
+    if (ctx->cg_ready) return TPMG_OK;
+    const LevelData& F = ctx->lv[ctx->L];
+    TRY(dev_alloc(ctx, &ctx->cg_r, F.n()));
+    TRY(dev_alloc(ctx, &ctx->cg_z, F.n()));
+    TRY(dev_alloc(ctx, &ctx->cg_p[0], F.n()));
+    TRY(dev_alloc(ctx, &ctx->cg_p[1], F.n()));
+    if (ctx->nranks > 1) {
+        TRY(dev_alloc(ctx, &ctx->cg_zlo, F.plane()));
+        TRY(dev_alloc(ctx, &ctx->cg_zhi, F.plane()));
+        for (int q = 0; q < 2; ++q) {
+            TRY(dev_alloc(ctx, &ctx->cg_plo[q], F.plane()));
+            TRY(dev_alloc(ctx, &ctx->cg_phi[q], F.plane()));
+        }
+    }
+    ctx->cg_ready = true;
+    return TPMG_OK;
+}
+
+// scalar slots of iteration n: sigma = 3n, ||r||^2 = 3n+1, zeta = <r, M^-1 r> = 3n+2
+inline int S_SIGMA(int n) { return 3 * n; }
+inline int S_RR(int n) { return 3 * n + 1; }
+inline int S_ZETA(int n) { return 3 * n + 2; }
+
+tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps, int max_iter,
+                          tpmg_result* res)
+{
+    TRY(cg_alloc(ctx));
+    TRY(ensure_scal(ctx, 3 * (max_iter + 2)));
+    const int l = ctx->L;
+    const LevelData& F = ctx->lv[l];
+    const size_t n = F.n(), plane = F.plane();
+    result_init(res);
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    CUDA_TRY(ctx, cudaMemsetAsync(u, 0, sizeof(double) * n, ctx->stream));          // u_0 = 0 [R9]
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->cg_p[0], 0, sizeof(double) * n, ctx->stream));
+    if (ctx->nranks > 1) {
+        CUDA_TRY(ctx, cudaMemsetAsync(ctx->cg_plo[0], 0, sizeof(double) * plane, ctx->stream));
+        CUDA_TRY(ctx, cudaMemsetAsync(ctx->cg_phi[0], 0, sizeof(double) * plane, ctx->stream));
+    }
+    const bool has_lo = ctx->rank > 0, has_hi = ctx->rank < ctx->nranks - 1;
+    // setup: r = f, z = M^-1 r, rr_0 = <r,r>, zeta_0 = <r,z>  (CGPREC with alpha = 0, p = 0)
+    {
+        LineArgs a = line_args(ctx, l);
+        a.h0 = HaloField{ctx->cg_p[0], nullptr, nullptr};
+        a.q0 = f;
+        a.q1 = u;
+        a.out0 = ctx->cg_r;
+        a.out1 = u;
+        a.out2 = ctx->cg_z;
+        a.red.result = ctx->d_scal + S_RR(0);
+        TRY(run_line(ctx, MODE_CGPREC, a));
+        TRY(allreduce(ctx, ctx->d_scal + S_RR(0), 2));
+        TRY(fetch(ctx, ctx->d_scal + S_RR(0), 2));
+    }
+    const double r0 = std::sqrt(ctx->h_pinned[0]);
+    record_hist(res, 0, r0);
+    int it = 0, cur = 0;
+    bool conv = (r0 == 0.0);
+    double rel = conv ? 0.0 : 1.0;
+    if (!conv && !(ctx->h_pinned[1] > 0))
+        return fail(ctx, TPMG_E_BREAKDOWN, "CG setup: <r, M^-1 r> = %g", ctx->h_pinned[1]);
+    while (!conv && it < max_iter) {
+        const int m = it + 1;
+        // halo of z (and p_old) for the direction kernel
+        HaloField hz{ctx->cg_z, nullptr, nullptr}, hp{ctx->cg_p[cur], nullptr, nullptr};
+        if (ctx->nranks > 1) {
+            TRY(exchange(ctx, l, ctx->cg_z, ctx->cg_zlo, ctx->cg_zhi));
+            hz = HaloField{ctx->cg_z, has_lo ? ctx->cg_zlo : nullptr, has_hi ? ctx->cg_zhi : nullptr};
+            hp = HaloField{ctx->cg_p[cur], has_lo ? ctx->cg_plo[cur] : nullptr, has_hi ? ctx->cg_phi[cur] : nullptr};
+        }
+        // (Fused) direction kernel: p = z + beta p, sigma = <p, A p>
+        {
+            LineArgs a = line_args(ctx, l);
+            a.h0 = hz;
+            a.h1 = hp;
+            a.out0 = ctx->cg_p[1 - cur];
+            a.ratio = (m == 1) ? DevRatio{ctx->d_scal, -1, -1}
+                               : DevRatio{ctx->d_scal, S_ZETA(m - 1), S_ZETA(m - 2)};
+            a.red.result = ctx->d_scal + S_SIGMA(m);
+            TRY(run_line(ctx, MODE_CGDIR, a));
+            TRY(allreduce(ctx, ctx->d_scal + S_SIGMA(m), 1));
+        }
+        HaloField hpn{ctx->cg_p[1 - cur], nullptr, nullptr};
+        if (ctx->nranks > 1) {
+            // halo of the new direction: exchanged (the local update z_halo + beta p_halo is a
+            // round-2 optimisation)
+            TRY(exchange(ctx, l, ctx->cg_p[1 - cur], ctx->cg_plo[1 - cur], ctx->cg_phi[1 - cur]));
+            hpn = HaloField{ctx->cg_p[1 - cur], has_lo ? ctx->cg_plo[1 - cur] : nullptr,
+                            has_hi ? ctx->cg_phi[1 - cur] : nullptr};
+        }
+        // (Fused) preconditioner kernel: r -= alpha A p, u += alpha p, z = M^-1 r, ||r||^2, <r,z>
+        {
+            LineArgs a = line_args(ctx, l);
+            a.h0 = hpn;
+            a.q0 = ctx->cg_r;
+            a.q1 = u;
+            a.out0 = ctx->cg_r;
+            a.out1 = u;
+            a.out2 = ctx->cg_z;
+            a.ratio = DevRatio{ctx->d_scal, S_ZETA(m - 1), S_SIGMA(m)};
+            a.red.result = ctx->d_scal + S_RR(m);
+            TRY(run_line(ctx, MODE_CGPREC, a));
+            TRY(allreduce(ctx, ctx->d_scal + S_RR(m), 2));
+        }
+        TRY(fetch(ctx, ctx->d_scal + S_SIGMA(m), 3));
+        const double sigma = ctx->h_pinned[0], rr = ctx->h_pinned[1], zeta = ctx->h_pinned[2];
+        it = m;
+        cur ^= 1;
+        const double rn = std::sqrt(rr);
+        record_hist(res, it, rn);
+        rel = rn / r0;
+        if (!(sigma > 0)) return fail(ctx, TPMG_E_BREAKDOWN, "CG iteration %d: <p, A p> = %g", it, sigma);
+        if (!(rn == rn)) return fail(ctx, TPMG_E_BREAKDOWN, "CG iteration %d: NaN residual", it);
+        if (rel < eps) { conv = true; break; }
+        if (!(zeta > 0)) return fail(ctx, TPMG_E_BREAKDOWN, "CG iteration %d: <r, M^-1 r> = %g", it, zeta);
+    }
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
+    float ms = 0;
+    CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    if (res) {
+        res->iterations = it;
+        res->converged = conv ? 1 : 0;
+        res->r0_norm = r0;
+        res->rel_residual = rel;
+        res->seconds = ms * 1e-3;
+    }
+    return TPMG_OK;
+}
+
+void params_fill_defaults(tpmg_params* p)
+{
+    if (p->nz == 0) p->nz = 128;
+    if (p->nu_cfl == 0) p->nu_cfl = 8.4;
+    if (p->H == 0) p->H = 0.01;
+    if (p->lambda == 0) p->lambda = 1.0;
+    if (p->levels == 0) p->levels = 5;
+    if (p->pre == 0) p->pre = 1;
+    if (p->post == 0) p->post = 1;
+    if (p->coarse_sweeps == 0) p->coarse_sweeps = 2;
+    if (p->rho == 0) p->rho = 2.0 / 3.0;
+}
+
+void ctx_free(tpmg_ctx* ctx)
+{
+    for (size_t l = 1; l < ctx->lv.size(); ++l) {
+        LevelData& L = ctx->lv[l];
+        cudaFree(L.d_tab);
+        if ((int)l < ctx->L) { cudaFree(L.u[0]); cudaFree(L.f); }
+        cudaFree(L.u[1]);
+        cudaFree(L.slab_lo);
+        cudaFree(L.slab_hi);
+    }
+    cudaFree(ctx->d_partials);
+    cudaFree(ctx->d_ticket);
+    cudaFree(ctx->d_scal);
+    cudaFree(ctx->scratch);
+    cudaFree(ctx->cg_r); cudaFree(ctx->cg_z); cudaFree(ctx->cg_p[0]); cudaFree(ctx->cg_p[1]);
+    cudaFree(ctx->cg_zlo); cudaFree(ctx->cg_zhi);
+    for (int q = 0; q < 2; ++q) { cudaFree(ctx->cg_plo[q]); cudaFree(ctx->cg_phi[q]); }
+    cudaFree(ctx->host_f); cudaFree(ctx->host_u);
+    if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    for (auto& r : ctx->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : ctx->prof_pool) cudaEventDestroy(e);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+
+extern "C" {
+
+int32_t tpmg_version(void) { return TPMG_VERSION_MAJOR * 1000 + TPMG_VERSION_MINOR; }
+
+void tpmg_params_default(tpmg_params* p)
+{
+    if (!p) return;
+    std::memset(p, 0, sizeof *p);
+    params_fill_defaults(p);
+}
+
+tpmg_status tpmg_nccl_id(void* id128)
+{
+    if (!id128) return fail(nullptr, TPMG_E_PARAM, "tpmg_nccl_id: NULL id");
+    ncclUniqueId id;
+    ncclResult_t e = ncclGetUniqueId(&id);
+    if (e != ncclSuccess) return fail(nullptr, TPMG_E_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(e));
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+    std::memcpy(id128, &id, 128);
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks, const void* id128,
+                        int32_t device, void* cuda_stream, tpmg_ctx** out)
+{
+    if (!params || !out) return fail(nullptr, TPMG_E_PARAM, "tpmg_create: NULL argument");
+    *out = nullptr;
+    tpmg_params p = *params;
+    params_fill_defaults(&p);
+    if (p.nx <= 0 || p.ny <= 0 || p.nz <= 0) return fail(nullptr, TPMG_E_PARAM, "grid %lld x %lld x %d must be positive", (long long)p.nx, (long long)p.ny, p.nz);
+    if (!(p.nu_cfl > 0) || !(p.H > 0) || !(p.lambda > 0)) return fail(nullptr, TPMG_E_PARAM, "nu_cfl, H, lambda must be > 0");
+    if (!(p.rho > 0 && p.rho < 2)) return fail(nullptr, TPMG_E_PARAM, "rho = %g not in (0, 2)", p.rho);
+    if (p.levels < 1 || p.levels > 24) return fail(nullptr, TPMG_E_PARAM, "levels = %d not in [1, 24]", p.levels);
+    if (p.pre < 0 || p.post < 0 || p.coarse_sweeps < 1) return fail(nullptr, TPMG_E_PARAM, "pre/post >= 0, coarse_sweeps >= 1");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(nullptr, TPMG_E_TOPOLOGY, "rank %d of %d", rank, nranks);
+    if (nranks > 1 && !id128) return fail(nullptr, TPMG_E_PARAM, "nranks > 1 needs the NCCL id");
+    const int64_t f = (int64_t)1 << (p.levels - 1);
+    if (p.nx % f) return fail(nullptr, TPMG_E_SHAPE, "nx = %lld not divisible by 2^(L-1) = %lld", (long long)p.nx, (long long)f);
+    if (p.ny % (f * nranks)) return fail(nullptr, TPMG_E_SHAPE, "ny = %lld not divisible by nranks * 2^(L-1) = %lld", (long long)p.ny, (long long)(f * nranks));
+    if (p.nz > line_max_nz()) return fail(nullptr, TPMG_E_SHAPE, "nz = %d exceeds the on-chip Thomas buffer (max %d)", p.nz, line_max_nz());
+
+    tpmg_ctx* ctx = new tpmg_ctx();
+    ctx->p = p;
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+    ctx->device = device;
+    ctx->stream = (cudaStream_t)cuda_stream;
+    ctx->L = p.levels;
+    ctx->ny_loc = p.ny / nranks;
+    ctx->y0 = (int64_t)rank * ctx->ny_loc;
+    auto bail = [&](tpmg_status st) {
+        g_create_error = ctx->err;
+        ctx_free(ctx);
+        delete ctx;
+        return st;
+    };
+#define CREATE_TRY(expr)                              \
+    do {                                              \
+        tpmg_status s__ = (expr);                     \
+        if (s__ != TPMG_OK) return bail(s__);         \
+    } while (0)
+#define CREATE_CUDA(expr)                                                                       \
+    do {                                                                                        \
+        cudaError_t e__ = (expr);                                                               \
+        if (e__ != cudaSuccess)                                                                 \
+            return bail(fail(ctx, TPMG_E_CUDA, "%s: %s", #expr, cudaGetErrorString(e__)));      \
+    } while (0)
+
+    CREATE_CUDA(cudaSetDevice(device));
+    CREATE_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+    CREATE_CUDA(cudaEventCreate(&ctx->ev0));
+    CREATE_CUDA(cudaEventCreate(&ctx->ev1));
+    CREATE_CUDA(cudaMallocHost((void**)&ctx->h_pinned, 64 * sizeof(double)));
+    CREATE_TRY(dev_alloc(ctx, &ctx->d_partials, (size_t)ctx->num_sms * 64 * 2));
+    CREATE_CUDA(cudaMalloc((void**)&ctx->d_ticket, sizeof(unsigned)));
+    CREATE_CUDA(cudaMemset(ctx->d_ticket, 0, sizeof(unsigned)));
+
+    // Coefficients: h = 1/nx, h_z = H/nz, omega = nu h / 2,
+    // c_l = omega^2 / h_l^2 with h_l = 2^(L-l) h [R4], gamma = omega^2 lambda^2 / h_z^2.
+    const double h = 1.0 / (double)p.nx;
+    const double hz = p.H / (double)p.nz;
+    const double omega = 0.5 * p.nu_cfl * h;
+    const double gamma = omega * omega * p.lambda * p.lambda / (hz * hz);
+    ctx->lv.resize(ctx->L + 1);
+    for (int l = 1; l <= ctx->L; ++l) {
+        LevelData& L = ctx->lv[l];
+        const int64_t fl = (int64_t)1 << (ctx->L - l);
+        const double hl = h * (double)fl;
+        L.lc.nx = p.nx / fl;
+        L.lc.ny = ctx->ny_loc / fl;
+        L.lc.nz = p.nz;
+        L.lc.c = omega * omega / (hl * hl);
+        L.lc.gamma = gamma;
+        // Thomas factors of the column block M_T = A_T: diag_k, 1/m_k, gamma/m_k
+        std::vector<double> tab(3 * (size_t)p.nz);
+        double mprev = 0.0;
+        for (int k = 0; k < p.nz; ++k) {
+            const double diag = 1.0 + 4.0 * L.lc.c + gamma * ((k > 0 ? 1.0 : 0.0) + (k < p.nz - 1 ? 1.0 : 0.0));
+            const double m = (k == 0) ? diag : diag - gamma * (gamma / mprev);
+            if (m == 0.0 || !std::isfinite(m)) return bail(fail(ctx, TPMG_E_SINGULAR, "zero Thomas pivot at level %d, k = %d", l, k));
+            tab[k] = diag;
+            tab[p.nz + k] = 1.0 / m;
+            tab[2 * p.nz + k] = (k < p.nz - 1) ? gamma / m : 0.0;
+            mprev = m;
+        }
+        CREATE_TRY(dev_alloc(ctx, &L.d_tab, tab.size()));
+        CREATE_CUDA(cudaMemcpy(L.d_tab, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice));
+        L.lc.tab = L.d_tab;
+        if (nranks > 1) {
+            CREATE_TRY(dev_alloc(ctx, &L.slab_lo, L.plane()));
+            CREATE_TRY(dev_alloc(ctx, &L.slab_hi, L.plane()));
+            CREATE_CUDA(cudaMemset(L.slab_lo, 0, sizeof(double) * L.plane()));
+            CREATE_CUDA(cudaMemset(L.slab_hi, 0, sizeof(double) * L.plane()));
+        }
+    }
+    if (nranks > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof id);
+        ncclResult_t e = ncclCommInitRank(&ctx->comm, nranks, id, rank);
+        if (e != ncclSuccess) return bail(fail(ctx, TPMG_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(e)));
+    }
+#undef CREATE_TRY
+#undef CREATE_CUDA
+    *out = ctx;
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_destroy(tpmg_ctx* ctx)
+{
+    if (!ctx) return TPMG_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream); else cudaDeviceSynchronize();
+    ctx_free(ctx);
+    delete ctx;
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_set_stream(tpmg_ctx* ctx, void* s)
+{
+    if (!ctx) return TPMG_E_PARAM;
+    ctx->stream = (cudaStream_t)s;
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_local_box(const tpmg_ctx* cctx, int32_t level, int64_t* y0, int64_t* nx, int64_t* ny,
+                           int32_t* nz)
+{
+    tpmg_ctx* ctx = const_cast<tpmg_ctx*>(cctx);
+    TRY(check_level(ctx, level));
+    const LevelData& L = ctx->lv[level];
+    if (y0) *y0 = ctx->y0 >> (ctx->L - level);
+    if (nx) *nx = L.lc.nx;
+    if (ny) *ny = L.lc.ny;
+    if (nz) *nz = L.lc.nz;
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_apply(tpmg_ctx* ctx, int32_t level, const double* x, double* y)
+{
+    TRY(check_level(ctx, level));
+    if (!x || !y) return fail(ctx, TPMG_E_PARAM, "tpmg_apply: NULL vector");
+    if (x == y) return fail(ctx, TPMG_E_SHAPE, "tpmg_apply: x and y must differ");
+    LineArgs a = line_args(ctx, level);
+    TRY(halo(ctx, level, x, &a.h0));
+    a.out0 = y;
+    return run_line(ctx, MODE_APPLY, a);
+}
+
+tpmg_status tpmg_residual(tpmg_ctx* ctx, int32_t level, const double* u, const double* f, double* r,
+                          double* norm2)
+{
+    TRY(check_level(ctx, level));
+    if (!u || !f) return fail(ctx, TPMG_E_PARAM, "tpmg_residual: NULL vector");
+    if (r == u) return fail(ctx, TPMG_E_SHAPE, "tpmg_residual: r must not alias u");
+    if (!r && !norm2) return TPMG_OK;
+    TRY(ensure_scal(ctx, 8));
+    LineArgs a = line_args(ctx, level);
+    TRY(halo(ctx, level, u, &a.h0));
+    a.q0 = f;
+    a.out0 = r;
+    a.red.result = norm2 ? ctx->d_scal + 4 : nullptr;
+    TRY(run_line(ctx, MODE_RESID, a));
+    if (norm2) {
+        TRY(allreduce(ctx, ctx->d_scal + 4, 1));
+        TRY(fetch(ctx, ctx->d_scal + 4, 1));
+        *norm2 = ctx->h_pinned[0];
+    }
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_precondition(tpmg_ctx* ctx, int32_t level, const double* r, double* z)
+{
+    TRY(check_level(ctx, level));
+    if (!r || !z) return fail(ctx, TPMG_E_PARAM, "tpmg_precondition: NULL vector");
+    if (r == z) return fail(ctx, TPMG_E_SHAPE, "tpmg_precondition: r and z must differ");
+    LineArgs a = line_args(ctx, level);
+    a.q0 = r;
+    a.out0 = z;
+    return run_line(ctx, MODE_PREC, a);
+}
+
+tpmg_status tpmg_smooth(tpmg_ctx* ctx, int32_t level, double* u, const double* f, int32_t sweeps)
+{
+    TRY(check_level(ctx, level));
+    if (!u || !f) return fail(ctx, TPMG_E_PARAM, "tpmg_smooth: NULL vector");
+    if (sweeps < 0) return fail(ctx, TPMG_E_PARAM, "tpmg_smooth: sweeps < 0");
+    if (sweeps == 0) return TPMG_OK;
+    if (u == f) return fail(ctx, TPMG_E_SHAPE, "tpmg_smooth: u and f must differ");
+    const LevelData& L = ctx->lv[level];
+    TRY(dev_alloc(ctx, &ctx->scratch, ctx->lv[ctx->L].n()));
+    double* bufs[2] = {u, ctx->scratch};
+    int cur = 0;
+    for (int s = 0; s < sweeps; ++s) {
+        TRY(smooth_once(ctx, level, bufs[cur], f, bufs[1 - cur], nullptr));
+        cur ^= 1;
+    }
+    if (cur) CUDA_TRY(ctx, cudaMemcpyAsync(u, ctx->scratch, sizeof(double) * L.n(), cudaMemcpyDeviceToDevice, ctx->stream));
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_restrict(tpmg_ctx* ctx, int32_t fine_level, const double* r_fine, double* f_coarse)
+{
+    TRY(check_level(ctx, fine_level));
+    if (fine_level < 2) return fail(ctx, TPMG_E_RANGE, "tpmg_restrict: fine_level %d < 2", fine_level);
+    if (!r_fine || !f_coarse) return fail(ctx, TPMG_E_PARAM, "tpmg_restrict: NULL vector");
+    ProfScope ps(ctx, TPMG_K_RESTRICT, level_cells(ctx->lv[fine_level].lc));
+    CUDA_TRY(ctx, launch_restrict(launcher(ctx), ctx->lv[fine_level].lc, ctx->lv[fine_level - 1].lc, r_fine, f_coarse));
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_prolong_add(tpmg_ctx* ctx, int32_t coarse_level, const double* u_coarse, double* u_fine)
+{
+    TRY(check_level(ctx, coarse_level));
+    if (coarse_level >= ctx->L) return fail(ctx, TPMG_E_RANGE, "tpmg_prolong_add: coarse_level %d >= L", coarse_level);
+    if (!u_coarse || !u_fine) return fail(ctx, TPMG_E_PARAM, "tpmg_prolong_add: NULL vector");
+    HaloField uc;
+    TRY(halo(ctx, coarse_level, u_coarse, &uc));
+    ProfScope ps(ctx, TPMG_K_PROLONG_ADD, level_cells(ctx->lv[coarse_level + 1].lc));
+    CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), ctx->lv[coarse_level].lc, ctx->lv[coarse_level + 1].lc, uc, u_fine));
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_vcycle(tpmg_ctx* ctx, double* u, const double* f)
+{
+    if (!ctx) return TPMG_E_PARAM;
+    if (!u || !f) return fail(ctx, TPMG_E_PARAM, "tpmg_vcycle: NULL vector");
+    if (u == f) return fail(ctx, TPMG_E_SHAPE, "tpmg_vcycle: u and f must differ");
+    TRY(mg_alloc(ctx));
+    TRY(vcycle_fine(ctx, u, f));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_solve_mg(tpmg_ctx* ctx, const double* f, double* u, double eps, int32_t max_iter,
+                          tpmg_result* res)
+{
+    if (!ctx) return TPMG_E_PARAM;
+    if (!u || !f) return fail(ctx, TPMG_E_PARAM, "tpmg_solve_mg: NULL vector");
+    if (u == f) return fail(ctx, TPMG_E_SHAPE, "tpmg_solve_mg: u and f must differ");
+    if (!(eps > 0) || max_iter < 0) return fail(ctx, TPMG_E_PARAM, "tpmg_solve_mg: eps > 0, max_iter >= 0");
+    return solve_mg_impl(ctx, f, u, eps, max_iter, res);
+}
+
+tpmg_status tpmg_solve_cg(tpmg_ctx* ctx, const double* f, double* u, double eps, int32_t max_iter,
+                          tpmg_result* res)
+{
+    if (!ctx) return TPMG_E_PARAM;
+    if (!u || !f) return fail(ctx, TPMG_E_PARAM, "tpmg_solve_cg: NULL vector");
+    if (u == f) return fail(ctx, TPMG_E_SHAPE, "tpmg_solve_cg: u and f must differ");
+    if (!(eps > 0) || max_iter < 0) return fail(ctx, TPMG_E_PARAM, "tpmg_solve_cg: eps > 0, max_iter >= 0");
+    return solve_cg_impl(ctx, f, u, eps, max_iter, res);
+}
+
+tpmg_status tpmg_solve_host(tpmg_ctx* ctx, tpmg_solver solver, const double* f_host, double* u_host,
+                            double eps, int32_t max_iter, tpmg_result* res)
+{
+    if (!ctx) return TPMG_E_PARAM;
+    if (!f_host || !u_host) return fail(ctx, TPMG_E_PARAM, "tpmg_solve_host: NULL buffer");
+    const size_t n = ctx->lv[ctx->L].n();
+    TRY(dev_alloc(ctx, &ctx->host_f, n));
+    TRY(dev_alloc(ctx, &ctx->host_u, n));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_f, f_host, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    tpmg_status st = (solver == TPMG_SOLVER_MG) ? tpmg_solve_mg(ctx, ctx->host_f, ctx->host_u, eps, max_iter, res)
+                                                : tpmg_solve_cg(ctx, ctx->host_f, ctx->host_u, eps, max_iter, res);
+    if (st != TPMG_OK) return st;
+    CUDA_TRY(ctx, cudaMemcpyAsync(u_host, ctx->host_u, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_get_stats(const tpmg_ctx* ctx, tpmg_stats* out)
+{
+    if (!ctx || !out) return TPMG_E_PARAM;
+    *out = ctx->stats;
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_stats_reset(tpmg_ctx* ctx)
+{
+    if (!ctx) return TPMG_E_PARAM;
+    ctx->stats = tpmg_stats{};
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_profile(tpmg_ctx* ctx, int32_t enable)
+{
+    if (!ctx) return TPMG_E_PARAM;
+    if (enable) {
+        TRY(prof_collect(ctx));
+        for (int k = 0; k < TPMG_K_COUNT; ++k) {
+            ctx->prof_launches[k] = 0;
+            ctx->prof_ms[k] = 0;
+            ctx->prof_cells[k] = 0;
+        }
+    }
+    ctx->prof_on = enable != 0;
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_profile_read(tpmg_ctx* ctx, int32_t kernel, int64_t* launches, double* ms, double* cells)
+{
+    if (!ctx) return TPMG_E_PARAM;
+    if (kernel < 0 || kernel >= TPMG_K_COUNT) return fail(ctx, TPMG_E_RANGE, "kernel class %d", kernel);
+    TRY(prof_collect(ctx));
+    if (launches) *launches = ctx->prof_launches[kernel];
+    if (ms) *ms = ctx->prof_ms[kernel];
+    if (cells) *cells = ctx->prof_cells[kernel];
+    return TPMG_OK;
+}
+
+const char* tpmg_last_error(const tpmg_ctx* ctx)
+{
+    if (!ctx) return g_create_error.c_str();
+    return ctx->err.c_str();
+}
+
+}  // extern "C"

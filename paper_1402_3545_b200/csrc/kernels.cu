@@ -1,0 +1,489 @@
+// kernels.cu -- sm_100a kernels of libtpmg (fp64, memory-bound; no tensor cores:
+// nothing on this path is a dense contraction).
+//
+// The central kernel, k_line, is the paper's "one thread per vertical column,
+// loop over k" design rebuilt for B200:
+//   * a CTA owns a TX x TY tile of columns (TX = 32 = one warp along the
+//     x-contiguous rows of the Lambda layout) and streams the
+//     tile's k-planes, with a 1-cell horizontal halo, through an NS-stage
+//     cp.async ring in shared memory, KB levels per stage;
+//   * the 7-point stencil (eqn:LocalMatrixStencil) reads the neighbours from
+//     shared memory, the vertical neighbours from registers (k-lag by one);
+//   * the Thomas forward sweep keeps the modified right-hand
+//     side g'_k of every column on chip (shared memory, 8*nz bytes/column), the
+//     backward sweep writes the result once: each vector crosses HBM once;
+//   * the CTA is persistent over tiles, and the next tile's loads are issued
+//     before the current tile's backward sweep.
+// Modes fuse the paper's kernels: Smooth in ONE out-of-place pass,
+// the preconditioner, and the two CG kernels (re-fused, see
+// DESIGN.md).  The Thomas factors of the column block are per-level tables
+// (every column has the same A_T in the flat box), so there is no per-cell
+// division.
+#include "kernels.cuh"
+
+#include <algorithm>
+
+namespace tpmg {
+namespace {
+
+constexpr int TX = 32;  // columns per tile row (one warp, 256 B per row segment)
+constexpr int KB = 8;   // vertical levels per pipeline stage
+constexpr int NS = 3;   // pipeline stages
+
+template <int MODE>
+struct Traits;
+template <> struct Traits<MODE_APPLY>  { static constexpr int NH = 1, NP = 0, THOMAS = 0, NR = 0; };
+template <> struct Traits<MODE_RESID>  { static constexpr int NH = 1, NP = 1, THOMAS = 0, NR = 1; };
+template <> struct Traits<MODE_PREC>   { static constexpr int NH = 0, NP = 1, THOMAS = 1, NR = 0; };
+template <> struct Traits<MODE_SMOOTH> { static constexpr int NH = 1, NP = 1, THOMAS = 1, NR = 1; };
+template <> struct Traits<MODE_CGDIR>  { static constexpr int NH = 2, NP = 0, THOMAS = 0, NR = 1; };
+template <> struct Traits<MODE_CGPREC> { static constexpr int NH = 1, NP = 2, THOMAS = 1, NR = 2; };
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid)
+{
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src),
+                 "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic grid reduction of NR values (see ReduceSlot).
+template <int NR>
+__device__ void grid_reduce(const ReduceSlot& red, const double (&acc)[NR > 0 ? NR : 1], double* scratch)
+{
+    if constexpr (NR > 0) {
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+        __shared__ bool is_last;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            double v = warp_sum(acc[r]);
+            if (lane == 0) scratch[r * 32 + warp] = v;
+        }
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                double s = 0.0;
+                for (int w = 0; w < nw; ++w) s += scratch[r * 32 + w];
+                red.partials[(size_t)blockIdx.x * NR + r] = s;
+            }
+            __threadfence();
+            unsigned t = atomicAdd(red.ticket, 1u);
+            is_last = (t == gridDim.x - 1);
+        }
+        __syncthreads();
+        if (is_last && warp == 0) {
+            __threadfence();
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                double s = 0.0;
+                for (unsigned b = lane; b < gridDim.x; b += 32) s += __ldcg(red.partials + (size_t)b * NR + r);
+                s = warp_sum(s);
+                if (lane == 0) red.result[r] = s;
+            }
+            if (lane == 0) *red.ticket = 0u;
+        }
+    }
+}
+
+template <int NH, int NP, int TY>
+struct Geom {
+    static constexpr int HX = TX + 2, HY = TY + 2, NT = TX * TY;
+    static constexpr int HALO_ROW = KB * HX;          // one (row, all kk) block
+    static constexpr int PLAIN_BASE = NH * HY * KB * HX;
+    static constexpr int STAGE = PLAIN_BASE + NP * TY * KB * TX;  // doubles per stage
+};
+
+// Issue the cp.async copies of one stage (levels k0..k0+KB-1 of the tile).
+// One warp per (field, row, level) segment; out-of-domain cells are zero-filled.
+template <int NH, int NP, int TY>
+__device__ __forceinline__ void load_stage(double* st, const LineArgs& a, int64_t i0, int64_t j0, int k0)
+{
+    using G = Geom<NH, NP, TY>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = G::NT / 32;
+    constexpr int NSEG_H = NH * G::HY * KB;
+    constexpr int NSEG = NSEG_H + NP * TY * KB;
+    const int64_t nx = a.L.nx, ny = a.L.ny;
+    const int nz = a.L.nz;
+    const int64_t plane = nx * (int64_t)nz;
+    for (int seg = warp; seg < NSEG; seg += NW) {
+        if (seg < NSEG_H) {
+            const int f = seg / (G::HY * KB);
+            const int rem = seg - f * (G::HY * KB);
+            const int r = rem / KB, kk = rem - (rem / KB) * KB;
+            const HaloField& H = (f == 0) ? a.h0 : a.h1;
+            const int64_t j = j0 - 1 + r;
+            const int k = k0 + kk;
+            const double* row = (j < 0) ? H.lo : (j >= ny ? H.hi : H.base + j * plane);
+            const bool rowok = (row != nullptr) && (k < nz);
+            double* dst = st + ((f * G::HY + r) * KB + kk) * G::HX;
+#pragma unroll
+            for (int x = lane; x < G::HX; x += 32) {
+                const int64_t i = i0 - 1 + x;
+                const bool ok = rowok && i >= 0 && i < nx;
+                cp_async8(dst + x, ok ? row + (int64_t)k * nx + i : H.base, ok);
+            }
+        } else {
+            const int s2 = seg - NSEG_H;
+            const int f = s2 / (TY * KB);
+            const int rem = s2 - f * (TY * KB);
+            const int r = rem / KB, kk = rem - (rem / KB) * KB;
+            const double* Q = (f == 0) ? a.q0 : a.q1;
+            const int64_t j = j0 + r;
+            const int k = k0 + kk;
+            const bool rowok = (j < ny) && (k < nz);
+            double* dst = st + G::PLAIN_BASE + ((f * TY + r) * KB + kk) * TX;
+            const int64_t i = i0 + lane;
+            const bool ok = rowok && i < nx;
+            cp_async8(dst + lane, ok ? Q + j * plane + (int64_t)k * nx + i : Q, ok);
+        }
+    }
+}
+
+template <int MODE, int TY>
+__global__ void __launch_bounds__(TX* TY) k_line(const LineArgs a)
+{
+    using T = Traits<MODE>;
+    constexpr int NH = T::NH, NP = T::NP, NR = T::NR;
+    using G = Geom<NH, NP, TY>;
+    constexpr int NT = G::NT;
+
+    extern __shared__ __align__(16) double smem[];
+    const int nz = a.L.nz;
+    const int64_t nx = a.L.nx, ny = a.L.ny;
+    const int tabn = (3 * nz + 1) & ~1;
+    double* tab = smem;                      // diag[nz], invm[nz], gim[nz]
+    double* stage = smem + tabn;             // NS stages
+    double* gbuf = stage + NS * G::STAGE;    // g'[nz][NT] (Thomas modes)
+    double* scratch = gbuf + (T::THOMAS ? nz * NT : 0);  // reduction scratch (64 doubles)
+
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    for (int q = tid; q < 3 * nz; q += NT) tab[q] = a.L.tab[q];
+    const double* diag = tab;
+    const double* invm = tab + nz;
+    const double* gim = tab + 2 * nz;
+    const double c = a.L.c, gamma = a.L.gamma;
+
+    double ratio = 0.0;
+    if constexpr (MODE == MODE_CGDIR || MODE == MODE_CGPREC)
+        if (a.ratio.num >= 0) ratio = a.ratio.s[a.ratio.num] / a.ratio.s[a.ratio.den];
+
+    double acc[NR > 0 ? NR : 1];
+#pragma unroll
+    for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
+    const bool want_red = (NR > 0) && (a.red.result != nullptr);
+
+    const int64_t ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
+    const int64_t ntiles = ntx * nty;
+    const int nch = (nz + KB - 1) / KB;
+    __syncthreads();
+
+    auto prologue = [&](int64_t tile) {
+        const int64_t i0 = (tile % ntx) * TX, j0 = (tile / ntx) * TY;
+#pragma unroll
+        for (int s = 0; s < NS - 1; ++s) {
+            if (s < nch) load_stage<NH, NP, TY>(stage + s * G::STAGE, a, i0, j0, s * KB);
+            cp_async_commit();
+        }
+    };
+
+    int64_t tile = blockIdx.x;
+    if (tile < ntiles) prologue(tile);
+    for (; tile < ntiles; tile += gridDim.x) {
+        const int64_t i0 = (tile % ntx) * TX, j0 = (tile / ntx) * TY;
+        const int64_t i = i0 + tx, j = j0 + ty;
+        const bool valid = (i < nx) && (j < ny);
+        const int64_t colbase = j * nx * (int64_t)nz + i;  // + k*nx
+
+        // rolling state for the k-lag: values at level km = k-1 and km-1
+        double um1 = 0.0, u0 = 0.0, S0 = 0.0, qa = 0.0, qb = 0.0, gprev = 0.0;
+
+        auto finalize = [&](int km, double up1) {
+            const double Mu = diag[km] * u0 - gamma * (um1 + up1);
+            const int64_t idx = colbase + (int64_t)km * nx;
+            double g = 0.0;
+            if constexpr (MODE == MODE_APPLY) {
+                if (valid) a.out0[idx] = Mu - c * S0;
+            } else if constexpr (MODE == MODE_RESID) {
+                const double r = qa - (Mu - c * S0);
+                if (valid) {
+                    if (a.out0) a.out0[idx] = r;
+                    acc[0] += r * r;
+                }
+            } else if constexpr (MODE == MODE_PREC) {
+                g = a.scale * qa;
+            } else if constexpr (MODE == MODE_SMOOTH) {
+                const double r = qa - (Mu - c * S0);
+                g = Mu + a.rho * r;   // = rho f + (M - rho A) u   (one-pass smoother)
+                if (valid) acc[0] += r * r;
+            } else if constexpr (MODE == MODE_CGDIR) {
+                const double Ap = Mu - c * S0;
+                if (valid) {
+                    a.out0[idx] = u0;
+                    acc[0] += u0 * Ap;
+                }
+            } else if constexpr (MODE == MODE_CGPREC) {
+                const double Ap = Mu - c * S0;
+                const double rn = qa - ratio * Ap;
+                const double un = qb + ratio * u0;
+                if (valid) {
+                    a.out0[idx] = rn;
+                    a.out1[idx] = un;
+                    acc[0] += rn * rn;
+                }
+                g = rn;
+            }
+            if constexpr (T::THOMAS) {
+                const double y = g + gamma * gprev;      // y = L^-1 g   (M = L D L^T)
+                const double gp = y * invm[km];          // g'_k = (g_k - s_k g'_{k-1}) / m_k
+                gbuf[km * NT + tid] = gp;
+                if constexpr (MODE == MODE_CGPREC)
+                    if (valid) acc[1] += gp * y;         // <g, M^-1 g> = sum y_k^2 / m_k
+                gprev = gp;
+            }
+        };
+
+        for (int ch = 0; ch < nch; ++ch) {
+            const int cn = ch + NS - 1;
+            if (cn < nch) load_stage<NH, NP, TY>(stage + (cn % NS) * G::STAGE, a, i0, j0, cn * KB);
+            cp_async_commit();
+            cp_async_wait<NS - 1>();
+            __syncthreads();
+            const double* st = stage + (ch % NS) * G::STAGE;
+#pragma unroll
+            for (int kk = 0; kk < KB; ++kk) {
+                const int k = ch * KB + kk;
+                if (k >= nz) break;
+                double ec = 0.0, S = 0.0, pa = 0.0, pb = 0.0;
+                if constexpr (NH >= 1) {
+                    const double* h = st + kk * G::HX;   // field 0, row r at + r*HALO_ROW
+                    const double* hc = h + (ty + 1) * G::HALO_ROW;
+                    ec = hc[tx + 1];
+                    S = (hc[tx] + hc[tx + 2]) + (h[ty * G::HALO_ROW + tx + 1] + h[(ty + 2) * G::HALO_ROW + tx + 1]);
+                    if constexpr (MODE == MODE_CGDIR) {
+                        const double* p = h + G::HY * G::HALO_ROW;  // field 1 = p_old
+                        const double* pc = p + (ty + 1) * G::HALO_ROW;
+                        ec = ec + ratio * pc[tx + 1];
+                        S = S + ratio * ((pc[tx] + pc[tx + 2]) + (p[ty * G::HALO_ROW + tx + 1] + p[(ty + 2) * G::HALO_ROW + tx + 1]));
+                    }
+                }
+                if constexpr (NP >= 1) pa = st[G::PLAIN_BASE + (ty * KB + kk) * TX + tx];
+                if constexpr (NP >= 2) pb = st[G::PLAIN_BASE + ((TY + ty) * KB + kk) * TX + tx];
+                if (k > 0) finalize(k - 1, ec);
+                um1 = u0; u0 = ec; S0 = S; qa = pa; qb = pb;
+            }
+            __syncthreads();
+        }
+        finalize(nz - 1, 0.0);
+
+        // issue the next tile's first stages before the backward sweep
+        if (tile + gridDim.x < ntiles) prologue(tile + gridDim.x);
+
+        if constexpr (T::THOMAS) {
+            double* out = (MODE == MODE_CGPREC) ? a.out2 : a.out0;
+            double x = 0.0;
+            for (int k = nz - 1; k >= 0; --k) {
+                x = gbuf[k * NT + tid] + gim[k] * x;    // x_k = g'_k - t'_k x_{k+1}
+                if (valid) out[colbase + (int64_t)k * nx] = x;
+            }
+        }
+    }
+    if (want_red) grid_reduce<NR>(a.red, acc, scratch);
+}
+
+template <int MODE, int TY>
+size_t line_smem_bytes(int nz)
+{
+    using T = Traits<MODE>;
+    using G = Geom<T::NH, T::NP, TY>;
+    size_t d = ((3 * nz + 1) & ~1) + (size_t)NS * G::STAGE + (T::THOMAS ? (size_t)nz * G::NT : 0) + 64;
+    return d * sizeof(double);
+}
+
+constexpr size_t kMaxSmem = 227 * 1024;
+
+template <int MODE, int TY>
+cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
+{
+    const size_t smem = line_smem_bytes<MODE, TY>(a.L.nz);
+    if (smem > kMaxSmem) return cudaErrorInvalidConfiguration;
+    auto kern = k_line<MODE, TY>;
+    static bool attr_set = false;   // per instantiation
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TX * TY, smem);
+    if (e != cudaSuccess) return e;
+    per_sm = std::max(per_sm, 1);
+    const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * ((a.L.ny + TY - 1) / TY);
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)ln.num_sms * per_sm);
+    if (grid <= 0) return cudaSuccess;
+    kern<<<(unsigned)grid, TX * TY, smem, ln.stream>>>(a);
+    if (ln.launch_counter) ++*ln.launch_counter;
+    return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_line_ty(const Launcher& ln, const LineArgs& a)
+{
+    if (line_smem_bytes<MODE, 4>(a.L.nz) <= kMaxSmem) return launch_line_t<MODE, 4>(ln, a);
+    if (line_smem_bytes<MODE, 2>(a.L.nz) <= kMaxSmem) return launch_line_t<MODE, 2>(ln, a);
+    return launch_line_t<MODE, 1>(ln, a);
+}
+
+// ------------------------------------------------------------------ simple streaming kernels
+
+__device__ __forceinline__ double ld_halo(const HaloField& F, int64_t i, int64_t j, int k, int64_t nx,
+                                          int64_t ny, int nz)
+{
+    if (i < 0 || i >= nx) return 0.0;
+    const double* row = (j < 0) ? F.lo : (j >= ny ? F.hi : F.base + j * nx * (int64_t)nz);
+    if (!row) return 0.0;
+    return __ldg(row + (int64_t)k * nx + i);
+}
+
+// r = f - A u at one fine cell, direct loads (used by the fused residual-restriction)
+__device__ __forceinline__ double resid_cell(const LevelConst& F, const HaloField& u, const double* f,
+                                             int64_t i, int64_t j, int k)
+{
+    const int64_t nx = F.nx, ny = F.ny;
+    const int nz = F.nz;
+    const double uc = ld_halo(u, i, j, k, nx, ny, nz);
+    const double ud = (k > 0) ? ld_halo(u, i, j, k - 1, nx, ny, nz) : 0.0;
+    const double uu = (k < nz - 1) ? ld_halo(u, i, j, k + 1, nx, ny, nz) : 0.0;
+    const double S = (ld_halo(u, i - 1, j, k, nx, ny, nz) + ld_halo(u, i + 1, j, k, nx, ny, nz)) +
+                     (ld_halo(u, i, j - 1, k, nx, ny, nz) + ld_halo(u, i, j + 1, k, nx, ny, nz));
+    const double Mu = F.tab[k] * uc - F.gamma * (ud + uu);
+    return __ldg(f + (j * nz + k) * nx + i) - (Mu - F.c * S);
+}
+
+__global__ void k_residual_restrict(const LevelConst F, const LevelConst Cc, const HaloField u,
+                                    const double* __restrict__ f, double* __restrict__ fc)
+{
+    const int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    const int64_t J = blockIdx.z;
+    if (I >= Cc.nx) return;
+    const double s = (resid_cell(F, u, f, 2 * I, 2 * J, k) + resid_cell(F, u, f, 2 * I + 1, 2 * J, k)) +
+                     (resid_cell(F, u, f, 2 * I, 2 * J + 1, k) + resid_cell(F, u, f, 2 * I + 1, 2 * J + 1, k));
+    fc[(J * Cc.nz + k) * Cc.nx + I] = 0.25 * s;
+}
+
+__global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double* __restrict__ r,
+                           double* __restrict__ fc)
+{
+    const int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    const int64_t J = blockIdx.z;
+    if (I >= Cc.nx) return;
+    const int64_t nx = F.nx;
+    const double* r0 = r + ((2 * J) * F.nz + k) * nx;
+    const double* r1 = r + ((2 * J + 1) * F.nz + k) * nx;
+    const double s = (__ldg(r0 + 2 * I) + __ldg(r0 + 2 * I + 1)) + (__ldg(r1 + 2 * I) + __ldg(r1 + 2 * I + 1));
+    fc[(J * Cc.nz + k) * Cc.nx + I] = 0.25 * s;
+}
+
+__global__ void k_prolong_add(const LevelConst Cc, const LevelConst F, const HaloField uc,
+                              double* __restrict__ uf)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    const int64_t j = blockIdx.z;
+    if (i >= F.nx) return;
+    const int64_t I = i >> 1, J = j >> 1;
+    const int64_t sx = (i & 1) ? 1 : -1, sy = (j & 1) ? 1 : -1;
+    const int64_t nxc = Cc.nx, nyc = Cc.ny;
+    const int nz = Cc.nz;
+    const double v = 9.0 * ld_halo(uc, I, J, k, nxc, nyc, nz) + 3.0 * ld_halo(uc, I + sx, J, k, nxc, nyc, nz) +
+                     3.0 * ld_halo(uc, I, J + sy, k, nxc, nyc, nz) + 1.0 * ld_halo(uc, I + sx, J + sy, k, nxc, nyc, nz);
+    double* p = uf + (j * F.nz + k) * F.nx + i;
+    *p = *p + v / 16.0;
+}
+
+__global__ void __launch_bounds__(256) k_dot(const double* __restrict__ x, const double* __restrict__ y,
+                                             int64_t n, ReduceSlot red)
+{
+    __shared__ double scratch[64];
+    double acc[1] = {0.0};
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+        acc[0] += x[q] * y[q];
+    grid_reduce<1>(red, acc, scratch);
+}
+
+}  // namespace
+
+int line_max_nz()
+{
+    // Thomas modes at TY = 1 are the binding case
+    int nz = 8;
+    while (line_smem_bytes<MODE_CGPREC, 1>(nz + 8) <= kMaxSmem) nz += 8;
+    return nz;
+}
+
+cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a)
+{
+    switch (mode) {
+    case MODE_APPLY: return launch_line_t<MODE_APPLY, 4>(ln, a);
+    case MODE_RESID: return launch_line_t<MODE_RESID, 4>(ln, a);
+    case MODE_PREC: return launch_line_ty<MODE_PREC>(ln, a);
+    case MODE_SMOOTH: return launch_line_ty<MODE_SMOOTH>(ln, a);
+    case MODE_CGDIR: return launch_line_t<MODE_CGDIR, 4>(ln, a);
+    case MODE_CGPREC: return launch_line_ty<MODE_CGPREC>(ln, a);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_residual_restrict(const Launcher& ln, const LevelConst& fine, const LevelConst& coarse,
+                                     HaloField u, const double* f, double* fc)
+{
+    dim3 block(64), grid((unsigned)((coarse.nx + 63) / 64), (unsigned)coarse.nz, (unsigned)coarse.ny);
+    if (coarse.ny <= 0 || coarse.nx <= 0) return cudaSuccess;
+    k_residual_restrict<<<grid, block, 0, ln.stream>>>(fine, coarse, u, f, fc);
+    if (ln.launch_counter) ++*ln.launch_counter;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const LevelConst& coarse,
+                            const double* r, double* fc)
+{
+    dim3 block(64), grid((unsigned)((coarse.nx + 63) / 64), (unsigned)coarse.nz, (unsigned)coarse.ny);
+    if (coarse.ny <= 0 || coarse.nx <= 0) return cudaSuccess;
+    k_restrict<<<grid, block, 0, ln.stream>>>(fine, coarse, r, fc);
+    if (ln.launch_counter) ++*ln.launch_counter;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, const LevelConst& fine,
+                               HaloField uc, double* uf)
+{
+    dim3 block(128), grid((unsigned)((fine.nx + 127) / 128), (unsigned)fine.nz, (unsigned)fine.ny);
+    if (fine.ny <= 0 || fine.nx <= 0) return cudaSuccess;
+    k_prolong_add<<<grid, block, 0, ln.stream>>>(coarse, fine, uc, uf);
+    if (ln.launch_counter) ++*ln.launch_counter;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dot(const Launcher& ln, const double* x, const double* y, int64_t n, ReduceSlot red)
+{
+    int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)ln.num_sms * 4);
+    grid = std::max<int64_t>(grid, 1);
+    k_dot<<<(unsigned)grid, 256, 0, ln.stream>>>(x, y, n, red);
+    if (ln.launch_counter) ++*ln.launch_counter;
+    return cudaGetLastError();
+}
+
+}  // namespace tpmg

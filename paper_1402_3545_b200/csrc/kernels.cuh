@@ -1,0 +1,93 @@
+// kernels.cuh -- launch interface of the sm_100a kernels of libtpmg.
+//
+// Every vector is fp64 in the paper's Lambda layout:
+//   idx(i, j, k) = (j * nz + k) * nx + i   (0-based, local rows j).
+// A "halo'd" field is read at the 4 horizontal neighbours; rows j = -1 and
+// j = ny come from the slabs lo / hi (one nz x nx plane each) or are zero
+// when the slab pointer is null (physical boundary, zero ghosts [R1]).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tpmg {
+
+// A field read with its horizontal neighbours.
+struct HaloField {
+    const double* base;  // owned rows
+    const double* lo;    // row j = -1 (nullptr: zero)
+    const double* hi;    // row j = ny (nullptr: zero)
+};
+
+// Per-level operator constants.
+struct LevelConst {
+    int64_t nx, ny;     // local horizontal cells
+    int32_t nz;
+    double c;           // omega^2 / h_l^2        (minus alpha_{T,T'})
+    double gamma;       // omega^2 lambda^2 / h_z^2 (minus the vertical off-diagonal)
+    const double* tab;  // device: diag[nz], invm[nz], gim[nz] (Thomas factors of M_T)
+};
+
+// Deterministic reduction slot: per-block partials, a ticket counter and the
+// result (nvals doubles).  The last block to finish sums the partials in
+// block order, so the result is independent of scheduling.
+struct ReduceSlot {
+    double* partials;   // >= gridDim.x * nvals
+    unsigned* ticket;   // zero on entry, reset to zero by the last block
+    double* result;     // nvals doubles (device)
+};
+
+// Scalar ratio read on the device: value = num_idx < 0 ? 0 : s[num]/s[den].
+struct DevRatio {
+    const double* s;
+    int num, den;
+};
+
+enum LineMode : int {
+    MODE_APPLY = 0,   // out0 = A x                                   (halo: x)
+    MODE_RESID = 1,   // out0 = f - A u (optional), sum r^2           (halo: u; plain: f)
+    MODE_PREC = 2,    // out0 = scale * M^-1 r                        (plain: r)
+    MODE_SMOOTH = 3,  // out0 = u + rho M^-1 (f - A u), sum r^2       (halo: u; plain: f)
+    MODE_CGDIR = 4,   // p = z + beta p_old; out0 = p; sum <p, A p>   (halo: z, p_old)
+    MODE_CGPREC = 5,  // r -= alpha A p; u += alpha p; z = M^-1 r;
+                      // sums ||r||^2, <r, z>                         (halo: p; plain: r, u)
+};
+
+struct LineArgs {
+    LevelConst L;
+    double rho;        // smoother relaxation (MODE_SMOOTH)
+    double scale;      // MODE_PREC output scale (1 or rho for the zero-guess smooth)
+    HaloField h0, h1;  // halo'd inputs
+    const double* q0;  // plain inputs
+    const double* q1;
+    double* out0;
+    double* out1;
+    double* out2;
+    DevRatio ratio;    // beta (CGDIR) or alpha (CGPREC)
+    ReduceSlot red;    // result may be nullptr: no reduction
+};
+
+struct Launcher {
+    cudaStream_t stream;
+    int num_sms;
+    int64_t* launch_counter;
+};
+
+cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a);
+// Largest nz the on-chip Thomas buffer supports.
+int line_max_nz();
+
+// f_c = 1/4 sum of the 2x2 fine children of (f - A u)  (Residual + restriction, fused)
+cudaError_t launch_residual_restrict(const Launcher& ln, const LevelConst& fine,
+                                     const LevelConst& coarse, HaloField u, const double* f,
+                                     double* fc);
+// f_c = 1/4 sum of the 2x2 fine children of r (plain restriction)
+cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const LevelConst& coarse,
+                            const double* r, double* fc);
+// u_f += P u_c (bilinear, zero coarse ghosts)
+cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse,
+                               const LevelConst& fine, HaloField uc, double* uf);
+// result = sum x*y over n elements (deterministic)
+cudaError_t launch_dot(const Launcher& ln, const double* x, const double* y, int64_t n,
+                       ReduceSlot red);
+
+}  // namespace tpmg

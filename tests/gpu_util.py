@@ -1,0 +1,38 @@
+"""Helpers shared by the GPU parity tests (test infrastructure)."""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import oracle as O
+
+
+def lib():
+    from paper_1402_3545_b200 import build
+    build.build()
+    from paper_1402_3545_b200 import tpmg
+    return tpmg
+
+
+def ctx_for(p: O.Params, device: int = 0):
+    T = lib()
+    params = T.make_params(p.nx, p.ny, nz=p.nz, nu_cfl=p.nu_cfl, H=p.H, lam=p.lam, levels=p.L,
+                           pre=p.pre, post=p.post, coarse_sweeps=p.coarse_sweeps, rho=p.rho)
+    return T.Context(params, device=device)
+
+
+def to_dev(x_zc: np.ndarray):
+    """oracle layout (ny, nx, nz) -> CUDA tensor in Lambda layout (ny, nz, nx)."""
+    import torch
+    return torch.from_numpy(O.to_lambda(x_zc)).cuda()
+
+
+def to_host_zc(t) -> np.ndarray:
+    import torch
+    torch.cuda.synchronize()
+    return O.from_lambda(t.cpu().numpy())
+
+
+def rel_l2(a, b) -> float:
+    a = np.ravel(a); b = np.ravel(b)
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
