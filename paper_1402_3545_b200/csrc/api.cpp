@@ -5,14 +5,19 @@
 // sm_100a kernels of kernels.cu.  Multi-GPU plumbing is NCCL over NVLink:
 // halo slabs with ncclSend/ncclRecv (y-strip decomposition) and
 // ncclAllReduce for the solver's global sums.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/tpmg.h"
@@ -66,6 +71,9 @@ struct tpmg_ctx {
     struct ProfRec { int cls; double cells; cudaEvent_t a, b; };
     std::vector<ProfRec> prof_pending;
     std::vector<cudaEvent_t> prof_pool;
+    // TMA descriptors, cached by (address, nx, nz, ny, box x, box rows)
+    bool use_tma = true;
+    std::map<std::tuple<uintptr_t, int64_t, int, int64_t, int, int>, CUtensorMap> tmaps;
     int64_t prof_launches[TPMG_K_COUNT] = {};
     double prof_ms[TPMG_K_COUNT] = {}, prof_cells[TPMG_K_COUNT] = {};
     std::string err;
@@ -261,8 +269,93 @@ tpmg_status prof_collect(tpmg_ctx* ctx)
 
 double level_cells(const LevelConst& l) { return (double)l.nx * (double)l.ny * (double)l.nz; }
 
-tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a)
+// ------------------------------------------------------------------ TMA descriptors
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
 {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 3-D tiled map over an fp64 field [ny][nz][nx] (x fastest) with box (bx, KB, by).
+bool tensor_map(tpmg_ctx* ctx, const double* base, int64_t nx, int nz, int64_t ny, int bx, int by, CUtensorMap* out)
+{
+    auto key = std::make_tuple((uintptr_t)base, nx, nz, ny, bx, by);
+    auto it = ctx->tmaps.find(key);
+    if (it != ctx->tmaps.end()) {
+        *out = it->second;
+        return true;
+    }
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)nz, (cuuint64_t)ny};
+    cuuint64_t strides[2] = {(cuuint64_t)nx * 8, (cuuint64_t)nx * (cuuint64_t)nz * 8};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)kStageK, (cuuint32_t)by};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUtensorMap m;
+    CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    if (ctx->tmaps.size() > 4096) ctx->tmaps.clear();
+    ctx->tmaps.emplace(key, m);
+    *out = m;
+    return true;
+}
+
+void mode_fields(int mode, int* nh, int* np)
+{
+    static const int NH[6] = {1, 1, 0, 1, 2, 1}, NP[6] = {0, 1, 1, 1, 0, 2};
+    *nh = NH[mode];
+    *np = NP[mode];
+}
+
+// Fill a.tma for the TMA loader; falls back to cp.async when a field cannot be
+// described (odd nx: the row stride is not a multiple of 16 bytes; misaligned).
+void fill_tma(tpmg_ctx* ctx, int mode, LineArgs& a)
+{
+    a.use_tma = 0;
+    if (!ctx->use_tma) return;
+    const int64_t nx = a.L.nx, ny = a.L.ny;
+    const int nz = a.L.nz;
+    if (nx % 2) return;
+    const int TY = line_tile_rows(mode, nz);
+    int nh, np;
+    mode_fields(mode, &nh, &np);
+    const HaloField* H[2] = {&a.h0, &a.h1};
+    const double* Q[2] = {a.q0, a.q1};
+    auto aligned = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+    for (int f = 0; f < nh; ++f) {
+        TmaHalo& M = a.tma.h[f];
+        const HaloField& hf = *H[f];
+        if (!hf.base || !aligned(hf.base)) return;
+        if (!tensor_map(ctx, hf.base, nx, nz, ny, kTileX + 2, TY + 2, &M.main)) return;
+        if (!tensor_map(ctx, hf.base, nx, nz, ny, kTileX + 2, 1, &M.row)) return;
+        M.has_lo = hf.lo != nullptr;
+        M.has_hi = hf.hi != nullptr;
+        if (hf.lo && (!aligned(hf.lo) || !tensor_map(ctx, hf.lo, nx, nz, 1, kTileX + 2, 1, &M.lo))) return;
+        if (hf.hi && (!aligned(hf.hi) || !tensor_map(ctx, hf.hi, nx, nz, 1, kTileX + 2, 1, &M.hi))) return;
+    }
+    for (int f = 0; f < np; ++f) {
+        if (!Q[f] || !aligned(Q[f])) return;
+        if (!tensor_map(ctx, Q[f], nx, nz, ny, kTileX, TY, &a.tma.q[f])) return;
+    }
+    a.use_tma = 1;
+}
+
+tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
+{
+    LineArgs a = a0;
+    fill_tma(ctx, mode, a);
     ProfScope ps(ctx, mode, level_cells(a.L));   // line modes map 1:1 onto TPMG_K_0..5
     CUDA_TRY(ctx, launch_line(launcher(ctx), mode, a));
     return TPMG_OK;
@@ -680,6 +773,10 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
     ctx->device = device;
     ctx->stream = (cudaStream_t)cuda_stream;
     ctx->L = p.levels;
+    {
+        const char* ld = std::getenv("TPMG_LOADER");   // "cpasync" selects the cp.async loader
+        ctx->use_tma = !(ld && std::strcmp(ld, "cpasync") == 0);
+    }
     ctx->ny_loc = p.ny / nranks;
     ctx->y0 = (int64_t)rank * ctx->ny_loc;
     auto bail = [&](tpmg_status st) {

@@ -26,8 +26,8 @@
 namespace tpmg {
 namespace {
 
-constexpr int TX = 32;  // columns per tile row (one warp, 256 B per row segment)
-constexpr int KB = 8;   // vertical levels per pipeline stage
+constexpr int TX = kTileX;  // columns per tile row (one warp, 256 B per row segment)
+constexpr int KB = kStageK; // vertical levels per pipeline stage
 constexpr int NS = 3;   // pipeline stages
 
 template <int MODE>
@@ -151,18 +151,92 @@ __device__ __forceinline__ void load_stage(double* st, const LineArgs& a, int64_
     }
 }
 
-template <int MODE, int TY>
-__global__ void __launch_bounds__(TX* TY) k_line(const LineArgs a)
+// ------------------------------------------------------------------ TMA (bulk tensor copies)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Issue the TMA copies of one stage (thread 0 only).  Box layout in shared
+// memory is identical to load_stage's: halo field f, row r, level kk, x.
+template <int NH, int NP, int TY>
+__device__ __forceinline__ void tma_stage(double* st, const LineArgs& a, int64_t i0, int64_t j0, int k0,
+                                          uint64_t* bar)
+{
+    using G = Geom<NH, NP, TY>;
+    mbar_expect_tx(bar, (uint32_t)(G::STAGE * sizeof(double)));
+    const int64_t ny = a.L.ny;
+    const int x0 = (int)i0 - 1;
+#pragma unroll
+    for (int f = 0; f < NH; ++f) {
+        const TmaHalo& M = a.tma.h[f];
+        double* dst = st + f * G::HY * G::HALO_ROW;
+        const bool rows = (M.has_lo && j0 == 0) || (M.has_hi && j0 + TY >= ny);
+        if (!rows) {
+            tma_load_3d(dst, &M.main, x0, k0, (int)j0 - 1, bar);
+        } else {
+            for (int r = 0; r < G::HY; ++r) {
+                const int64_t j = j0 - 1 + r;
+                const CUtensorMap* m = &M.row;
+                int jj = (int)j;
+                if (j < 0 && M.has_lo) { m = &M.lo; jj = 0; }
+                else if (j == ny && M.has_hi) { m = &M.hi; jj = 0; }
+                tma_load_3d(dst + r * G::HALO_ROW, m, x0, k0, jj, bar);
+            }
+        }
+    }
+#pragma unroll
+    for (int f = 0; f < NP; ++f)
+        tma_load_3d(st + G::PLAIN_BASE + f * TY * KB * TX, &a.tma.q[f], (int)i0, k0, (int)j0, bar);
+}
+
+// The line kernel.  LOADER = 0: cp.async (all threads); 1: TMA (thread 0) with an
+// mbarrier per stage.  The CTA walks its tiles (tile = blockIdx.x + t*gridDim.x)
+// as one global sequence of KB-level chunks, so the loads of the next tile's
+// first chunks overlap the current tile's backward sweep.
+template <int MODE, int TY, int LOADER>
+__global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArgs a)
 {
     using T = Traits<MODE>;
     constexpr int NH = T::NH, NP = T::NP, NR = T::NR;
     using G = Geom<NH, NP, TY>;
     constexpr int NT = G::NT;
 
-    extern __shared__ __align__(16) double smem[];
+    extern __shared__ __align__(128) double smem[];
+    __shared__ __align__(8) uint64_t full_bar[NS];
     const int nz = a.L.nz;
     const int64_t nx = a.L.nx, ny = a.L.ny;
-    const int tabn = (3 * nz + 1) & ~1;
+    const int tabn = (3 * nz + 15) & ~15;    // keep the stages 128-byte aligned
     double* tab = smem;                      // diag[nz], invm[nz], gim[nz]
     double* stage = smem + tabn;             // NS stages
     double* gbuf = stage + NS * G::STAGE;    // g'[nz][NT] (Thomas modes)
@@ -174,6 +248,12 @@ __global__ void __launch_bounds__(TX* TY) k_line(const LineArgs a)
     const double* invm = tab + nz;
     const double* gim = tab + 2 * nz;
     const double c = a.L.c, gamma = a.L.gamma;
+    if constexpr (LOADER == 1) {
+        if (tid == 0) {
+            for (int s = 0; s < NS; ++s) mbar_init(&full_bar[s], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+    }
 
     double ratio = 0.0;
     if constexpr (MODE == MODE_CGDIR || MODE == MODE_CGPREC)
@@ -187,20 +267,43 @@ __global__ void __launch_bounds__(TX* TY) k_line(const LineArgs a)
     const int64_t ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
     const int64_t ntiles = ntx * nty;
     const int nch = (nz + KB - 1) / KB;
+    const int64_t my_tiles = (blockIdx.x < ntiles) ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const int64_t total = my_tiles * nch;
     __syncthreads();
 
-    auto prologue = [&](int64_t tile) {
-        const int64_t i0 = (tile % ntx) * TX, j0 = (tile / ntx) * TY;
-#pragma unroll
-        for (int s = 0; s < NS - 1; ++s) {
-            if (s < nch) load_stage<NH, NP, TY>(stage + s * G::STAGE, a, i0, j0, s * KB);
-            cp_async_commit();
+    // issue the loads of global chunk gi into slot gi % NS
+    auto issue = [&](int64_t gi) {
+        if (gi < total) {
+            const int64_t t = blockIdx.x + (gi / nch) * (int64_t)gridDim.x;
+            const int ch = (int)(gi % nch);
+            const int64_t i0 = (t % ntx) * TX, j0 = (t / ntx) * TY;
+            double* st = stage + (gi % NS) * G::STAGE;
+            if constexpr (LOADER == 0) {
+                load_stage<NH, NP, TY>(st, a, i0, j0, ch * KB);
+            } else {
+                if (tid == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    tma_stage<NH, NP, TY>(st, a, i0, j0, ch * KB, &full_bar[gi % NS]);
+                }
+            }
+        }
+        if constexpr (LOADER == 0) cp_async_commit();
+    };
+    auto wait = [&](int64_t gi) {
+        if constexpr (LOADER == 0) {
+            cp_async_wait<NS - 1>();
+            __syncthreads();
+        } else {
+            mbar_wait(&full_bar[gi % NS], (uint32_t)((gi / NS) & 1));
         }
     };
 
-    int64_t tile = blockIdx.x;
-    if (tile < ntiles) prologue(tile);
-    for (; tile < ntiles; tile += gridDim.x) {
+#pragma unroll
+    for (int s = 0; s < NS - 1; ++s) issue(s);
+
+    int64_t gi = 0;
+    for (int64_t tl = 0; tl < my_tiles; ++tl) {
+        const int64_t tile = blockIdx.x + tl * (int64_t)gridDim.x;
         const int64_t i0 = (tile % ntx) * TX, j0 = (tile / ntx) * TY;
         const int64_t i = i0 + tx, j = j0 + ty;
         const bool valid = (i < nx) && (j < ny);
@@ -254,13 +357,10 @@ __global__ void __launch_bounds__(TX* TY) k_line(const LineArgs a)
             }
         };
 
-        for (int ch = 0; ch < nch; ++ch) {
-            const int cn = ch + NS - 1;
-            if (cn < nch) load_stage<NH, NP, TY>(stage + (cn % NS) * G::STAGE, a, i0, j0, cn * KB);
-            cp_async_commit();
-            cp_async_wait<NS - 1>();
-            __syncthreads();
-            const double* st = stage + (ch % NS) * G::STAGE;
+        for (int ch = 0; ch < nch; ++ch, ++gi) {
+            issue(gi + NS - 1);
+            wait(gi);
+            const double* st = stage + (gi % NS) * G::STAGE;
 #pragma unroll
             for (int kk = 0; kk < KB; ++kk) {
                 const int k = ch * KB + kk;
@@ -283,12 +383,9 @@ __global__ void __launch_bounds__(TX* TY) k_line(const LineArgs a)
                 if (k > 0) finalize(k - 1, ec);
                 um1 = u0; u0 = ec; S0 = S; qa = pa; qb = pb;
             }
-            __syncthreads();
+            __syncthreads();   // slot gi % NS is free for chunk gi + NS
         }
         finalize(nz - 1, 0.0);
-
-        // issue the next tile's first stages before the backward sweep
-        if (tile + gridDim.x < ntiles) prologue(tile + gridDim.x);
 
         if constexpr (T::THOMAS) {
             double* out = (MODE == MODE_CGPREC) ? a.out2 : a.out0;
@@ -299,6 +396,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const LineArgs a)
             }
         }
     }
+    if constexpr (LOADER == 0) cp_async_wait<0>();
     if (want_red) grid_reduce<NR>(a.red, acc, scratch);
 }
 
@@ -307,24 +405,39 @@ size_t line_smem_bytes(int nz)
 {
     using T = Traits<MODE>;
     using G = Geom<T::NH, T::NP, TY>;
-    size_t d = ((3 * nz + 1) & ~1) + (size_t)NS * G::STAGE + (T::THOMAS ? (size_t)nz * G::NT : 0) + 64;
+    size_t d = ((3 * nz + 15) & ~15) + (size_t)NS * G::STAGE + (T::THOMAS ? (size_t)nz * G::NT : 0) + 64;
     return d * sizeof(double);
 }
 
-constexpr size_t kMaxSmem = 227 * 1024;
+constexpr size_t kMaxSmem = 227 * 1024 - 1024;  // leave room for static smem (barriers, flags)
 
-template <int MODE, int TY>
-cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
+// Dynamic shared memory available to a kernel: the opt-in maximum minus its static smem.
+template <typename K>
+size_t dyn_smem_limit(K kern)
+{
+    static int optin = 0;
+    if (!optin) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    }
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kern);
+    return (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
+}
+
+template <int MODE, int TY, int LOADER>
+cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
 {
     const size_t smem = line_smem_bytes<MODE, TY>(a.L.nz);
-    if (smem > kMaxSmem) return cudaErrorInvalidConfiguration;
-    auto kern = k_line<MODE, TY>;
-    static bool attr_set = false;   // per instantiation
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
+    auto kern = k_line<MODE, TY, LOADER>;
+    static size_t limit = 0;   // per instantiation
+    if (!limit) {
+        limit = dyn_smem_limit(kern);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
+    if (smem > limit) return cudaErrorInvalidConfiguration;
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TX * TY, smem);
     if (e != cudaSuccess) return e;
@@ -335,6 +448,12 @@ cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
     kern<<<(unsigned)grid, TX * TY, smem, ln.stream>>>(a);
     if (ln.launch_counter) ++*ln.launch_counter;
     return cudaGetLastError();
+}
+
+template <int MODE, int TY>
+cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
+{
+    return a.use_tma ? launch_line_l<MODE, TY, 1>(ln, a) : launch_line_l<MODE, TY, 0>(ln, a);
 }
 
 template <int MODE>
@@ -425,6 +544,16 @@ __global__ void __launch_bounds__(256) k_dot(const double* __restrict__ x, const
 }
 
 }  // namespace
+
+int line_tile_rows(int mode, int nz)
+{
+    switch (mode) {
+    case MODE_PREC: return line_smem_bytes<MODE_PREC, 4>(nz) <= kMaxSmem ? 4 : line_smem_bytes<MODE_PREC, 2>(nz) <= kMaxSmem ? 2 : 1;
+    case MODE_SMOOTH: return line_smem_bytes<MODE_SMOOTH, 4>(nz) <= kMaxSmem ? 4 : line_smem_bytes<MODE_SMOOTH, 2>(nz) <= kMaxSmem ? 2 : 1;
+    case MODE_CGPREC: return line_smem_bytes<MODE_CGPREC, 4>(nz) <= kMaxSmem ? 4 : line_smem_bytes<MODE_CGPREC, 2>(nz) <= kMaxSmem ? 2 : 1;
+    default: return 4;
+    }
+}
 
 int line_max_nz()
 {

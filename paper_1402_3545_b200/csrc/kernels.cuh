@@ -7,6 +7,7 @@
 // when the slab pointer is null (physical boundary, zero ghosts [R1]).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace tpmg {
@@ -52,6 +53,23 @@ enum LineMode : int {
                       // sums ||r||^2, <r, z>                         (halo: p; plain: r, u)
 };
 
+// TMA descriptors of one halo'd field: the whole (TY+2)-row box, a one-row box,
+// and the halo slabs (rows j = -1 / j = ny) when present.
+struct TmaHalo {
+    CUtensorMap main, row, lo, hi;
+    int has_lo, has_hi;
+};
+struct TmaMaps {
+    TmaHalo h[2];
+    CUtensorMap q[2];
+};
+
+// Tile geometry of the line kernels: TX = 32 columns along x per tile row,
+// TY rows per tile (4, or fewer when nz needs a larger Thomas buffer), KB
+// levels per pipeline stage.
+constexpr int kTileX = 32;
+constexpr int kStageK = 8;
+
 struct LineArgs {
     LevelConst L;
     double rho;        // smoother relaxation (MODE_SMOOTH)
@@ -64,6 +82,8 @@ struct LineArgs {
     double* out2;
     DevRatio ratio;    // beta (CGDIR) or alpha (CGPREC)
     ReduceSlot red;    // result may be nullptr: no reduction
+    int use_tma;       // 1: loads by TMA (tma must be filled), 0: cp.async
+    TmaMaps tma;
 };
 
 struct Launcher {
@@ -73,6 +93,8 @@ struct Launcher {
 };
 
 cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a);
+// Tile rows TY the launcher uses for `mode` at this nz (the TMA boxes depend on it).
+int line_tile_rows(int mode, int nz);
 // Largest nz the on-chip Thomas buffer supports.
 int line_max_nz();
 

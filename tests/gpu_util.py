@@ -13,8 +13,14 @@ def lib():
     return tpmg
 
 
-def ctx_for(p: O.Params, device: int = 0):
+def ctx_for(p: O.Params, device: int = 0, loader: str | None = None):
+    """loader: None (library default, TMA), "tma" or "cpasync" (TPMG_LOADER at creation)."""
+    import os
     T = lib()
+    if loader is not None:
+        os.environ["TPMG_LOADER"] = loader
+    else:
+        os.environ.pop("TPMG_LOADER", None)
     params = T.make_params(p.nx, p.ny, nz=p.nz, nu_cfl=p.nu_cfl, H=p.H, lam=p.lam, levels=p.L,
                            pre=p.pre, post=p.post, coarse_sweeps=p.coarse_sweeps, rho=p.rho)
     return T.Context(params, device=device)

@@ -36,9 +36,13 @@ def rand(shape, seed):
     return np.random.default_rng(seed).standard_normal(shape)
 
 
+LOADERS = ["tma", "cpasync"]
+
+
+@pytest.mark.parametrize("loader", LOADERS)
 @pytest.mark.parametrize("p", SHAPES, ids=IDS)
-def test_apply_residual_precondition_all_levels(p):
-    ctx = ctx_for(p)
+def test_apply_residual_precondition_all_levels(p, loader):
+    ctx = ctx_for(p, loader=loader)
     for level in range(1, p.L + 1):
         s = p.level_shape(level)
         x, f = rand(s, 1 + level), rand(s, 100 + level)
@@ -56,9 +60,10 @@ def test_apply_residual_precondition_all_levels(p):
         assert rel_l2(to_host_zc(z), O.precondition(p, f, level)) < TOL
 
 
+@pytest.mark.parametrize("loader", LOADERS)
 @pytest.mark.parametrize("p", SHAPES, ids=IDS)
-def test_smooth_all_levels(p):
-    ctx = ctx_for(p)
+def test_smooth_all_levels(p, loader):
+    ctx = ctx_for(p, loader=loader)
     for level in range(1, p.L + 1):
         s = p.level_shape(level)
         u, f = rand(s, 7 + level), rand(s, 70 + level)
@@ -82,9 +87,10 @@ def test_transfers_all_levels(p):
         assert rel_l2(to_host_zc(duf), O.prolong_add(p, uc, uf, fine - 1)) < TOL
 
 
+@pytest.mark.parametrize("loader", LOADERS)
 @pytest.mark.parametrize("p", SHAPES, ids=IDS)
-def test_vcycle(p):
-    ctx = ctx_for(p)
+def test_vcycle(p, loader):
+    ctx = ctx_for(p, loader=loader)
     s = p.level_shape(p.L)
     u, f = rand(s, 5), rand(s, 6)
     du = to_dev(u)
@@ -102,8 +108,9 @@ SOLVE_SHAPES = [
 
 @pytest.mark.parametrize("p", SOLVE_SHAPES, ids=[f"{p.nx}x{p.ny}x{p.nz}-nu{p.nu_cfl}" for p in SOLVE_SHAPES])
 @pytest.mark.parametrize("solver", ["mg", "cg"])
-def test_solve_parity(p, solver):
-    ctx = ctx_for(p)
+@pytest.mark.parametrize("loader", LOADERS)
+def test_solve_parity(p, solver, loader):
+    ctx = ctx_for(p, loader=loader)
     f = rhs_zc(p.nx, p.ny, p.nz, seed=0)
     u = ctx.empty(p.L)
     if solver == "mg":
