@@ -73,6 +73,7 @@ struct tpmg_ctx {
     std::vector<cudaEvent_t> prof_pool;
     // TMA descriptors, cached by (address, nx, nz, ny, box x, box rows)
     bool use_tma = true;
+    bool sync_debug = false;   // TPMG_SYNC_DEBUG=1: synchronise after every line kernel
     std::map<std::tuple<uintptr_t, int64_t, int, int64_t, int, int>, CUtensorMap> tmaps;
     int64_t prof_launches[TPMG_K_COUNT] = {};
     double prof_ms[TPMG_K_COUNT] = {}, prof_cells[TPMG_K_COUNT] = {};
@@ -358,6 +359,13 @@ tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
     fill_tma(ctx, mode, a);
     ProfScope ps(ctx, mode, level_cells(a.L));   // line modes map 1:1 onto TPMG_K_0..5
     CUDA_TRY(ctx, launch_line(launcher(ctx), mode, a));
+    if (ctx->sync_debug) {
+        cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess)
+            return fail(ctx, TPMG_E_CUDA, "line kernel mode %d (%s loader, nx=%lld ny=%lld nz=%d): %s", mode,
+                        a.use_tma ? "TMA" : "cp.async", (long long)a.L.nx, (long long)a.L.ny, a.L.nz,
+                        cudaGetErrorString(e));
+    }
     return TPMG_OK;
 }
 
@@ -776,6 +784,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
     {
         const char* ld = std::getenv("TPMG_LOADER");   // "cpasync" selects the cp.async loader
         ctx->use_tma = !(ld && std::strcmp(ld, "cpasync") == 0);
+        const char* sd = std::getenv("TPMG_SYNC_DEBUG");
+        ctx->sync_debug = sd && sd[0] == '1';
     }
     ctx->ny_loc = p.ny / nranks;
     ctx->y0 = (int64_t)rank * ctx->ny_loc;

@@ -232,8 +232,11 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     using G = Geom<NH, NP, TY>;
     constexpr int NT = G::NT;
 
-    extern __shared__ __align__(128) double smem[];
+    extern __shared__ __align__(128) double smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[NS];
+    // TMA destinations must be 128-byte aligned: align the dynamic window explicitly
+    double* smem = reinterpret_cast<double*>(
+        reinterpret_cast<char*>(smem_raw) + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
     const int nz = a.L.nz;
     const int64_t nx = a.L.nx, ny = a.L.ny;
     const int tabn = (3 * nz + 15) & ~15;    // keep the stages 128-byte aligned
@@ -405,7 +408,7 @@ size_t line_smem_bytes(int nz)
 {
     using T = Traits<MODE>;
     using G = Geom<T::NH, T::NP, TY>;
-    size_t d = ((3 * nz + 15) & ~15) + (size_t)NS * G::STAGE + (T::THOMAS ? (size_t)nz * G::NT : 0) + 64;
+    size_t d = ((3 * nz + 15) & ~15) + (size_t)NS * G::STAGE + (T::THOMAS ? (size_t)nz * G::NT : 0) + 64 + 16;
     return d * sizeof(double);
 }
 
