@@ -339,12 +339,12 @@ void fill_tma(tpmg_ctx* ctx, int mode, LineArgs& a)
         TmaHalo& M = a.tma.h[f];
         const HaloField& hf = *H[f];
         if (!hf.base || !aligned(hf.base)) return;
-        if (!tensor_map(ctx, hf.base, nx, nz, ny, kTileX + 2, TY + 2, &M.main)) return;
-        if (!tensor_map(ctx, hf.base, nx, nz, ny, kTileX + 2, 1, &M.row)) return;
+        if (!tensor_map(ctx, hf.base, nx, nz, ny, kTileX + 4, TY + 2, &M.main)) return;
+        if (!tensor_map(ctx, hf.base, nx, nz, ny, kTileX + 4, 1, &M.row)) return;
         M.has_lo = hf.lo != nullptr;
         M.has_hi = hf.hi != nullptr;
-        if (hf.lo && (!aligned(hf.lo) || !tensor_map(ctx, hf.lo, nx, nz, 1, kTileX + 2, 1, &M.lo))) return;
-        if (hf.hi && (!aligned(hf.hi) || !tensor_map(ctx, hf.hi, nx, nz, 1, kTileX + 2, 1, &M.hi))) return;
+        if (hf.lo && (!aligned(hf.lo) || !tensor_map(ctx, hf.lo, nx, nz, 1, kTileX + 4, 1, &M.lo))) return;
+        if (hf.hi && (!aligned(hf.hi) || !tensor_map(ctx, hf.hi, nx, nz, 1, kTileX + 4, 1, &M.hi))) return;
     }
     for (int f = 0; f < np; ++f) {
         if (!Q[f] || !aligned(Q[f])) return;

@@ -98,7 +98,8 @@ __device__ void grid_reduce(const ReduceSlot& red, const double (&acc)[NR > 0 ? 
 
 template <int NH, int NP, int TY>
 struct Geom {
-    static constexpr int HX = TX + 2, HY = TY + 2, NT = TX * TY;
+    // halo rows span i0-2 .. i0+TX+1: TMA needs a 16-byte aligned (even) start column
+    static constexpr int HX = TX + 4, HY = TY + 2, NT = TX * TY;
     static constexpr int HALO_ROW = KB * HX;          // one (row, all kk) block
     static constexpr int PLAIN_BASE = NH * HY * KB * HX;
     static constexpr int STAGE = PLAIN_BASE + NP * TY * KB * TX;  // doubles per stage
@@ -130,7 +131,7 @@ __device__ __forceinline__ void load_stage(double* st, const LineArgs& a, int64_
             double* dst = st + ((f * G::HY + r) * KB + kk) * G::HX;
 #pragma unroll
             for (int x = lane; x < G::HX; x += 32) {
-                const int64_t i = i0 - 1 + x;
+                const int64_t i = i0 - 2 + x;
                 const bool ok = rowok && i >= 0 && i < nx;
                 cp_async8(dst + x, ok ? row + (int64_t)k * nx + i : H.base, ok);
             }
@@ -196,7 +197,7 @@ __device__ __forceinline__ void tma_stage(double* st, const LineArgs& a, int64_t
     using G = Geom<NH, NP, TY>;
     mbar_expect_tx(bar, (uint32_t)(G::STAGE * sizeof(double)));
     const int64_t ny = a.L.ny;
-    const int x0 = (int)i0 - 1;
+    const int x0 = (int)i0 - 2;
 #pragma unroll
     for (int f = 0; f < NH; ++f) {
         const TmaHalo& M = a.tma.h[f];
@@ -372,13 +373,13 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 if constexpr (NH >= 1) {
                     const double* h = st + kk * G::HX;   // field 0, row r at + r*HALO_ROW
                     const double* hc = h + (ty + 1) * G::HALO_ROW;
-                    ec = hc[tx + 1];
-                    S = (hc[tx] + hc[tx + 2]) + (h[ty * G::HALO_ROW + tx + 1] + h[(ty + 2) * G::HALO_ROW + tx + 1]);
+                    ec = hc[tx + 2];
+                    S = (hc[tx + 1] + hc[tx + 3]) + (h[ty * G::HALO_ROW + tx + 2] + h[(ty + 2) * G::HALO_ROW + tx + 2]);
                     if constexpr (MODE == MODE_CGDIR) {
                         const double* p = h + G::HY * G::HALO_ROW;  // field 1 = p_old
                         const double* pc = p + (ty + 1) * G::HALO_ROW;
-                        ec = ec + ratio * pc[tx + 1];
-                        S = S + ratio * ((pc[tx] + pc[tx + 2]) + (p[ty * G::HALO_ROW + tx + 1] + p[(ty + 2) * G::HALO_ROW + tx + 1]));
+                        ec = ec + ratio * pc[tx + 2];
+                        S = S + ratio * ((pc[tx + 1] + pc[tx + 3]) + (p[ty * G::HALO_ROW + tx + 2] + p[(ty + 2) * G::HALO_ROW + tx + 2]));
                     }
                 }
                 if constexpr (NP >= 1) pa = st[G::PLAIN_BASE + (ty * KB + kk) * TX + tx];
