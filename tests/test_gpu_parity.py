@@ -19,6 +19,20 @@ from gpu_util import ctx_for, lib, rel_l2, to_dev, to_host_zc
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-11
+EPS = 2.220446049250313e-16
+
+
+def tol(p: O.Params, level=None) -> float:
+    """North-star bar 1e-11, or the forward-error bound of the column solve when the
+    column blocks are worse conditioned than any BASELINE configuration: rounding in
+    g = O((1 + 4c + 4 gamma) |u|) is amplified by ||M^-1|| = 1/(1 + 4c), i.e. by
+    kappa(M_T).  kappa(M_T) <= 2.5e3 for every BASELINE config (C1 is the worst), so
+    the bar there is exactly 1e-11; only the synthetic nz = 300 stress shape
+    (kappa(M_T) ~ 9e5) uses the bound.  See DESIGN.md "Tolerances"."""
+    level = p.L if level is None else level
+    c, g = p.c_h(level), p.gamma()
+    kappa_M = (1 + 4 * c + 4 * g) / (1 + 4 * c)
+    return max(TOL, 4 * EPS * kappa_M)
 
 SHAPES = [
     O.Params(nx=32, ny=32, nz=16),                      # C1 (BASELINE configs[0]), L = 5
@@ -49,15 +63,15 @@ def test_apply_residual_precondition_all_levels(p, loader):
         dx, df = to_dev(x), to_dev(f)
         y = ctx.empty(level)
         ctx.apply(level, dx, y)
-        assert rel_l2(to_host_zc(y), O.apply(p, x, level)) < TOL
+        assert rel_l2(to_host_zc(y), O.apply(p, x, level)) < tol(p, level)
         r = ctx.empty(level)
         n2 = ctx.residual(level, dx, df, r, want_norm2=True)
         want = O.residual(p, x, f, level)
-        assert rel_l2(to_host_zc(r), want) < TOL
+        assert rel_l2(to_host_zc(r), want) < tol(p, level)
         assert n2 == pytest.approx(float(np.sum(want * want)), rel=1e-12)
         z = ctx.empty(level)
         ctx.precondition(level, df, z)
-        assert rel_l2(to_host_zc(z), O.precondition(p, f, level)) < TOL
+        assert rel_l2(to_host_zc(z), O.precondition(p, f, level)) < tol(p, level)
 
 
 @pytest.mark.parametrize("loader", LOADERS)
@@ -70,7 +84,7 @@ def test_smooth_all_levels(p, loader):
         for sweeps in (1, 2):
             du = to_dev(u)
             ctx.smooth(level, du, to_dev(f), sweeps)
-            assert rel_l2(to_host_zc(du), O.smooth(p, u, f, level, sweeps)) < TOL
+            assert rel_l2(to_host_zc(du), O.smooth(p, u, f, level, sweeps)) < tol(p, level)
 
 
 @pytest.mark.parametrize("p", [q for q in SHAPES if q.L > 1], ids=[i for q, i in zip(SHAPES, IDS) if q.L > 1])
@@ -95,7 +109,7 @@ def test_vcycle(p, loader):
     u, f = rand(s, 5), rand(s, 6)
     du = to_dev(u)
     ctx.vcycle(du, to_dev(f))
-    assert rel_l2(to_host_zc(du), O.vcycle(p, u, f)) < TOL
+    assert rel_l2(to_host_zc(du), O.vcycle(p, u, f)) < tol(p)
 
 
 SOLVE_SHAPES = [
@@ -157,13 +171,16 @@ def test_solve_edge_cases():
 
 
 def test_single_level_hierarchy():
+    """L = 1: each 'V-cycle' is coarse_sweeps smoother steps; without coarse
+    grids it converges slowly, so compare a fixed number of cycles."""
     p = O.Params(nx=48, ny=32, nz=8, L=1, coarse_sweeps=3)
     ctx = ctx_for(p)
     f = rhs_zc(48, 32, 8, seed=2)
     u = ctx.empty(1)
-    res, ref = ctx.solve_mg(to_dev(f), u, max_iter=200), O.solve_mg(p, f, max_iter=200)
-    assert res.iterations == ref.iterations and res.converged
-    assert rel_l2(to_host_zc(u), ref.u) < 1e-9
+    res, ref = ctx.solve_mg(to_dev(f), u, max_iter=20), O.solve_mg(p, f, max_iter=20)
+    assert res.iterations == ref.iterations == 20 and not res.converged
+    assert np.allclose(res.history, ref.history, rtol=1e-10)
+    assert rel_l2(to_host_zc(u), ref.u) < 1e-10
 
 
 def test_solve_host_matches_device():
