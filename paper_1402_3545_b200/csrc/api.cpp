@@ -315,7 +315,7 @@ bool tensor_map(tpmg_ctx* ctx, const double* base, int64_t nx, int nz, int64_t n
 
 void mode_fields(int mode, int* nh, int* np)
 {
-    static const int NH[6] = {1, 1, 0, 1, 2, 1}, NP[6] = {0, 1, 1, 1, 0, 2};
+    static const int NH[7] = {1, 1, 0, 1, 2, 1, 1}, NP[7] = {0, 1, 1, 1, 0, 2, 1};
     *nh = NH[mode];
     *np = NP[mode];
 }
@@ -357,7 +357,7 @@ tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
 {
     LineArgs a = a0;
     fill_tma(ctx, mode, a);
-    ProfScope ps(ctx, mode, level_cells(a.L));   // line modes map 1:1 onto TPMG_K_0..5
+    ProfScope ps(ctx, mode == MODE_RESTRICT ? TPMG_K_RESIDUAL_RESTRICT : mode, level_cells(a.L));  // modes 0..5 = TPMG_K_0..5
     CUDA_TRY(ctx, launch_line(launcher(ctx), mode, a));
     if (ctx->sync_debug) {
         cudaError_t e = cudaStreamSynchronize(ctx->stream);
@@ -404,11 +404,12 @@ tpmg_status mg_restrict_smooth(tpmg_ctx* ctx, int l)
 {
     LevelData& F = ctx->lv[l + 1];
     LevelData& Cc = ctx->lv[l];
-    HaloField uf;
-    TRY(halo(ctx, l + 1, F.u[F.cur], &uf));
     {
-        ProfScope ps(ctx, TPMG_K_RESIDUAL_RESTRICT, level_cells(F.lc));
-        CUDA_TRY(ctx, launch_residual_restrict(launcher(ctx), F.lc, Cc.lc, uf, F.f, Cc.f));
+        LineArgs r = line_args(ctx, l + 1);
+        TRY(halo(ctx, l + 1, F.u[F.cur], &r.h0));
+        r.q0 = F.f;
+        r.out0 = Cc.f;
+        TRY(run_line(ctx, MODE_RESTRICT, r));
     }
     LineArgs a = line_args(ctx, l);
     a.q0 = Cc.f;
@@ -427,7 +428,9 @@ tpmg_status mg_smooth(tpmg_ctx* ctx, int l, double* result = nullptr)
 }
 
 // Subroutine VCycle (alg:VCycle) with the readings [R5] of DESIGN.md.
-tpmg_status vcycle_rec(tpmg_ctx* ctx, int l)
+// skip_pre: the first pre-smoothing step of level l has already been done (the MG
+// solve fuses it with the convergence test of the previous cycle).
+tpmg_status vcycle_rec(tpmg_ctx* ctx, int l, bool skip_pre = false)
 {
     const tpmg_params& p = ctx->p;
     if (l == 1) {
@@ -440,7 +443,7 @@ tpmg_status vcycle_rec(tpmg_ctx* ctx, int l)
         return TPMG_OK;
     }
     if (l == ctx->L) {
-        for (int s = 0; s < p.pre; ++s) TRY(mg_smooth(ctx, l));
+        for (int s = skip_pre ? 1 : 0; s < p.pre; ++s) TRY(mg_smooth(ctx, l));
     } else {
         TRY(mg_restrict_smooth(ctx, l));
         for (int s = 1; s < p.pre; ++s) TRY(mg_smooth(ctx, l));
@@ -458,17 +461,31 @@ tpmg_status vcycle_rec(tpmg_ctx* ctx, int l)
     return TPMG_OK;
 }
 
-// One V-cycle with the caller's fine-level u, f.  Leaves the result in u.
-tpmg_status vcycle_fine(tpmg_ctx* ctx, double* u, const double* f)
+// Bind the caller's fine-level u, f to the hierarchy.
+void bind_fine(tpmg_ctx* ctx, double* u, const double* f)
 {
     LevelData& F = ctx->lv[ctx->L];
     F.u[0] = u;
     F.f = const_cast<double*>(f);
     F.cur = 0;
-    TRY(vcycle_rec(ctx, ctx->L));
-    if (F.cur != 0) CUDA_TRY(ctx, cudaMemcpyAsync(u, F.u[1], sizeof(double) * F.n(), cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
+// Copy the fine iterate back into the caller's u if it ended in the work buffer.
+tpmg_status unbind_fine(tpmg_ctx* ctx)
+{
+    LevelData& F = ctx->lv[ctx->L];
+    if (F.cur != 0)
+        CUDA_TRY(ctx, cudaMemcpyAsync(F.u[0], F.u[1], sizeof(double) * F.n(), cudaMemcpyDeviceToDevice, ctx->stream));
     F.cur = 0;
     return TPMG_OK;
+}
+
+// One V-cycle with the caller's fine-level u, f.  Leaves the result in u.
+tpmg_status vcycle_fine(tpmg_ctx* ctx, double* u, const double* f)
+{
+    bind_fine(ctx, u, f);
+    TRY(vcycle_rec(ctx, ctx->L));
+    return unbind_fine(ctx);
 }
 
 // Global ||f - A u||^2 of the fine level (into d_scal[slot]).
@@ -531,16 +548,47 @@ tpmg_status solve_mg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
     int it = 0;
     bool conv = (r0 == 0.0);
     double rel = conv ? 0.0 : 1.0;
-    while (!conv && it < max_iter) {
-        TRY(vcycle_fine(ctx, u, f));
-        TRY(fine_residual_norm2(ctx, u, f, ctx->d_scal + 1));
-        TRY(fetch(ctx, ctx->d_scal + 1, 1));
-        const double rn = std::sqrt(ctx->h_pinned[0]);
-        ++it;
-        record_hist(res, it, rn);
-        rel = rn / r0;
-        if (!(rn == rn)) return fail(ctx, TPMG_E_BREAKDOWN, "NaN residual after V-cycle %d", it);
-        if (rel < eps) conv = true;
+    const bool fused_norm = ctx->L > 1 && ctx->p.pre >= 1;
+    if (!fused_norm) {
+        while (!conv && it < max_iter) {
+            TRY(vcycle_fine(ctx, u, f));
+            TRY(fine_residual_norm2(ctx, u, f, ctx->d_scal + 1));
+            TRY(fetch(ctx, ctx->d_scal + 1, 1));
+            const double rn = std::sqrt(ctx->h_pinned[0]);
+            ++it;
+            record_hist(res, it, rn);
+            rel = rn / r0;
+            if (!(rn == rn)) return fail(ctx, TPMG_E_BREAKDOWN, "NaN residual after V-cycle %d", it);
+            if (rel < eps) conv = true;
+        }
+    } else if (!conv && max_iter > 0) {
+        // The first fine pre-smooth of cycle it+1 also returns ||f - A u_it||^2 (its input's
+        // residual): the convergence test of cycle it costs no extra pass over u and f.  The
+        // pre-smooth writes the work buffer, so u_it is still in u when the test passes; the
+        // last (unused) pre-smooth is the price of the fusion.
+        LevelData& F = ctx->lv[ctx->L];
+        bind_fine(ctx, u, f);
+        TRY(vcycle_rec(ctx, ctx->L));     // cycle 1 (u_0 = 0)
+        TRY(unbind_fine(ctx));
+        it = 1;
+        while (true) {
+            bind_fine(ctx, u, f);
+            TRY(mg_smooth(ctx, ctx->L, ctx->d_scal + 1));
+            TRY(allreduce(ctx, ctx->d_scal + 1, 1));
+            TRY(fetch(ctx, ctx->d_scal + 1, 1));
+            const double rn = std::sqrt(ctx->h_pinned[0]);
+            record_hist(res, it, rn);
+            rel = rn / r0;
+            if (!(rn == rn)) return fail(ctx, TPMG_E_BREAKDOWN, "NaN residual after V-cycle %d", it);
+            if (rel < eps) conv = true;
+            if (conv || it >= max_iter) {
+                F.cur = 0;   // discard the speculative pre-smooth: u holds u_it
+                break;
+            }
+            TRY(vcycle_rec(ctx, ctx->L, /*skip_pre=*/true));
+            TRY(unbind_fine(ctx));
+            ++it;
+        }
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
     CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));

@@ -38,6 +38,7 @@ template <> struct Traits<MODE_PREC>   { static constexpr int NH = 0, NP = 1, TH
 template <> struct Traits<MODE_SMOOTH> { static constexpr int NH = 1, NP = 1, THOMAS = 1, NR = 1; };
 template <> struct Traits<MODE_CGDIR>  { static constexpr int NH = 2, NP = 0, THOMAS = 0, NR = 1; };
 template <> struct Traits<MODE_CGPREC> { static constexpr int NH = 1, NP = 2, THOMAS = 1, NR = 2; };
+template <> struct Traits<MODE_RESTRICT> { static constexpr int NH = 1, NP = 1, THOMAS = 0, NR = 0; };
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid)
 {
@@ -244,7 +245,10 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     double* tab = smem;                      // diag[nz], invm[nz], gim[nz]
     double* stage = smem + tabn;             // NS stages
     double* gbuf = stage + NS * G::STAGE;    // g'[nz][NT] (Thomas modes)
-    double* scratch = gbuf + (T::THOMAS ? nz * NT : 0);  // reduction scratch (64 doubles)
+    // MODE_RESTRICT: x-pair sums [2][TY][KB+1][TX/2] (a chunk completes up to KB+1 levels)
+    constexpr int RS = KB + 1;
+    double* rbuf = gbuf + (T::THOMAS ? nz * NT : 0);
+    double* scratch = rbuf + (MODE == MODE_RESTRICT ? 2 * TY * RS * (TX / 2) : 0);  // reduction scratch
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     for (int q = tid; q < 3 * nz; q += NT) tab[q] = a.L.tab[q];
@@ -315,6 +319,8 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 
         // rolling state for the k-lag: values at level km = k-1 and km-1
         double um1 = 0.0, u0 = 0.0, S0 = 0.0, qa = 0.0, qb = 0.0, gprev = 0.0;
+        double* rbuf_cur = rbuf;   // MODE_RESTRICT: buffer of the current chunk
+        int slot_base = 0;         // MODE_RESTRICT: level held in slot 0 of rbuf_cur
 
         auto finalize = [&](int km, double up1) {
             const double Mu = diag[km] * u0 - gamma * (um1 + up1);
@@ -340,6 +346,11 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                     a.out0[idx] = u0;
                     acc[0] += u0 * Ap;
                 }
+            } else if constexpr (MODE == MODE_RESTRICT) {
+                // r = f - A u, summed over the x-pair (2I, 2I+1) of fine columns
+                const double r = qa - (Mu - c * S0);
+                const double rs = r + __shfl_xor_sync(0xffffffffu, r, 1);
+                if ((tx & 1) == 0) rbuf_cur[(ty * RS + (km - slot_base)) * (TX / 2) + (tx >> 1)] = rs;
             } else if constexpr (MODE == MODE_CGPREC) {
                 const double Ap = Mu - c * S0;
                 const double rn = qa - ratio * Ap;
@@ -365,38 +376,89 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             issue(gi + NS - 1);
             wait(gi);
             const double* st = stage + (gi % NS) * G::STAGE;
+            // all shared-memory reads of the chunk first (independent of the Thomas
+            // recurrence), so one warp per SMSP still has KB levels of ILP
+            double ecv[KB], Sv[KB], pav[KB], pbv[KB];
 #pragma unroll
             for (int kk = 0; kk < KB; ++kk) {
-                const int k = ch * KB + kk;
-                if (k >= nz) break;
-                double ec = 0.0, S = 0.0, pa = 0.0, pb = 0.0;
+                ecv[kk] = 0.0; Sv[kk] = 0.0; pav[kk] = 0.0; pbv[kk] = 0.0;
                 if constexpr (NH >= 1) {
                     const double* h = st + kk * G::HX;   // field 0, row r at + r*HALO_ROW
                     const double* hc = h + (ty + 1) * G::HALO_ROW;
-                    ec = hc[tx + 2];
-                    S = (hc[tx + 1] + hc[tx + 3]) + (h[ty * G::HALO_ROW + tx + 2] + h[(ty + 2) * G::HALO_ROW + tx + 2]);
+                    ecv[kk] = hc[tx + 2];
+                    Sv[kk] = (hc[tx + 1] + hc[tx + 3]) + (h[ty * G::HALO_ROW + tx + 2] + h[(ty + 2) * G::HALO_ROW + tx + 2]);
                     if constexpr (MODE == MODE_CGDIR) {
                         const double* p = h + G::HY * G::HALO_ROW;  // field 1 = p_old
                         const double* pc = p + (ty + 1) * G::HALO_ROW;
-                        ec = ec + ratio * pc[tx + 2];
-                        S = S + ratio * ((pc[tx + 1] + pc[tx + 3]) + (p[ty * G::HALO_ROW + tx + 2] + p[(ty + 2) * G::HALO_ROW + tx + 2]));
+                        ecv[kk] = ecv[kk] + ratio * pc[tx + 2];
+                        Sv[kk] = Sv[kk] + ratio * ((pc[tx + 1] + pc[tx + 3]) + (p[ty * G::HALO_ROW + tx + 2] + p[(ty + 2) * G::HALO_ROW + tx + 2]));
                     }
                 }
-                if constexpr (NP >= 1) pa = st[G::PLAIN_BASE + (ty * KB + kk) * TX + tx];
-                if constexpr (NP >= 2) pb = st[G::PLAIN_BASE + ((TY + ty) * KB + kk) * TX + tx];
-                if (k > 0) finalize(k - 1, ec);
-                um1 = u0; u0 = ec; S0 = S; qa = pa; qb = pb;
+                if constexpr (NP >= 1) pav[kk] = st[G::PLAIN_BASE + (ty * KB + kk) * TX + tx];
+                if constexpr (NP >= 2) pbv[kk] = st[G::PLAIN_BASE + ((TY + ty) * KB + kk) * TX + tx];
             }
             __syncthreads();   // slot gi % NS is free for chunk gi + NS
+            if constexpr (MODE == MODE_RESTRICT) {
+                rbuf_cur = rbuf + (gi & 1) * (TY * RS * (TX / 2));
+                slot_base = ch * KB - 1;   // this chunk completes levels ch*KB-1 .. ch*KB+KB-2
+            }
+#pragma unroll
+            for (int kk = 0; kk < KB; ++kk) {
+                const int k = ch * KB + kk;
+                if (k < nz) {
+                    if (k > 0) finalize(k - 1, ecv[kk]);
+                    um1 = u0; u0 = ecv[kk]; S0 = Sv[kk]; qa = pav[kk]; qb = pbv[kk];
+                }
+            }
+            if (ch == nch - 1) finalize(nz - 1, 0.0);
+            if constexpr (MODE == MODE_RESTRICT) {
+                // f_c(I, J, k) = 1/4 (x-pair sum of row 2J + x-pair sum of row 2J+1)
+                __syncthreads();
+                const int lo = (ch == 0) ? 0 : ch * KB - 1;
+                const int hi = (ch == nch - 1) ? nz - 1 : ch * KB + KB - 2;
+                const int64_t nxc = nx >> 1, nyc = ny >> 1;
+                const int nlev = hi - lo + 1;
+                for (int it = tid; it < (TY / 2) * RS * (TX / 2); it += NT) {
+                    const int l = it % (TX / 2);
+                    const int sl = (it / (TX / 2)) % RS;
+                    const int jp = it / ((TX / 2) * RS);
+                    const int km = lo + sl;
+                    if (sl < nlev) {
+                        const int slot = km - slot_base;
+                        const int64_t I = (i0 >> 1) + l, J = (j0 >> 1) + jp;
+                        if (I < nxc && J < nyc)
+                            a.out0[(J * nz + km) * nxc + I] =
+                                0.25 * (rbuf_cur[((2 * jp) * RS + slot) * (TX / 2) + l] +
+                                        rbuf_cur[((2 * jp + 1) * RS + slot) * (TX / 2) + l]);
+                    }
+                }
+            }
         }
-        finalize(nz - 1, 0.0);
 
         if constexpr (T::THOMAS) {
-            double* out = (MODE == MODE_CGPREC) ? a.out2 : a.out0;
+            // backward substitution x_k = g'_k - t'_k x_{k+1}, KB levels per step with
+            // the shared-memory loads issued ahead of the dependent FMA chain
+            double* op = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase + (int64_t)(nz - 1) * nx;
             double x = 0.0;
-            for (int k = nz - 1; k >= 0; --k) {
-                x = gbuf[k * NT + tid] + gim[k] * x;    // x_k = g'_k - t'_k x_{k+1}
-                if (valid) out[colbase + (int64_t)k * nx] = x;
+            int k = nz - 1;
+            for (; k >= KB - 1; k -= KB) {
+                double gv[KB], gm[KB];
+#pragma unroll
+                for (int q = 0; q < KB; ++q) {
+                    gv[q] = gbuf[(k - q) * NT + tid];
+                    gm[q] = gim[k - q];
+                }
+#pragma unroll
+                for (int q = 0; q < KB; ++q) {
+                    x = gv[q] + gm[q] * x;
+                    if (valid) *op = x;
+                    op -= nx;
+                }
+            }
+            for (; k >= 0; --k) {
+                x = gbuf[k * NT + tid] + gim[k] * x;
+                if (valid) *op = x;
+                op -= nx;
             }
         }
     }
@@ -409,7 +471,8 @@ size_t line_smem_bytes(int nz)
 {
     using T = Traits<MODE>;
     using G = Geom<T::NH, T::NP, TY>;
-    size_t d = ((3 * nz + 15) & ~15) + (size_t)NS * G::STAGE + (T::THOMAS ? (size_t)nz * G::NT : 0) + 64 + 16;
+    size_t d = ((3 * nz + 15) & ~15) + (size_t)NS * G::STAGE + (T::THOMAS ? (size_t)nz * G::NT : 0) + 64 + 16 +
+               (MODE == MODE_RESTRICT ? 2 * TY * (KB + 1) * (TX / 2) : 0);
     return d * sizeof(double);
 }
 
@@ -520,21 +583,37 @@ __global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double
     fc[(J * Cc.nz + k) * Cc.nx + I] = 0.25 * s;
 }
 
-__global__ void k_prolong_add(const LevelConst Cc, const LevelConst F, const HaloField uc,
-                              double* __restrict__ uf)
+// u_f += P u_c: one thread per coarse cell (I, J, k) updates its 2 x 2 fine children
+// with 16-byte loads/stores; the 3 x 3 coarse neighbourhood comes through L1.
+__global__ void __launch_bounds__(256) k_prolong_add(const LevelConst Cc, const LevelConst F, const HaloField uc,
+                                                     double* __restrict__ uf)
 {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int k = blockIdx.y;
-    const int64_t j = blockIdx.z;
-    if (i >= F.nx) return;
-    const int64_t I = i >> 1, J = j >> 1;
-    const int64_t sx = (i & 1) ? 1 : -1, sy = (j & 1) ? 1 : -1;
     const int64_t nxc = Cc.nx, nyc = Cc.ny;
     const int nz = Cc.nz;
-    const double v = 9.0 * ld_halo(uc, I, J, k, nxc, nyc, nz) + 3.0 * ld_halo(uc, I + sx, J, k, nxc, nyc, nz) +
-                     3.0 * ld_halo(uc, I, J + sy, k, nxc, nyc, nz) + 1.0 * ld_halo(uc, I + sx, J + sy, k, nxc, nyc, nz);
-    double* p = uf + (j * F.nz + k) * F.nx + i;
-    *p = *p + v / 16.0;
+    const int64_t n = nxc * nyc * (int64_t)nz;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t I = q % nxc;
+        const int64_t Jk = q / nxc;
+        const int k = (int)(Jk % nz);
+        const int64_t J = Jk / nz;
+        double cc[3][3];
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+            for (int dx = -1; dx <= 1; ++dx) cc[dy + 1][dx + 1] = ld_halo(uc, I + dx, J + dy, k, nxc, nyc, nz);
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {          // fine row 2J + b: sy = -1 (b = 0), +1 (b = 1)
+            const int sy = b ? 2 : 0;
+            // fine columns 2I (sx = -1) and 2I+1 (sx = +1)
+            const double v0 = 9.0 * cc[1][1] + 3.0 * cc[1][0] + 3.0 * cc[sy][1] + 1.0 * cc[sy][0];
+            const double v1 = 9.0 * cc[1][1] + 3.0 * cc[1][2] + 3.0 * cc[sy][1] + 1.0 * cc[sy][2];
+            double2* p = reinterpret_cast<double2*>(uf + ((2 * J + b) * F.nz + k) * F.nx + 2 * I);
+            double2 w = *p;
+            w.x = w.x + v0 / 16.0;
+            w.y = w.y + v1 / 16.0;
+            *p = w;
+        }
+    }
 }
 
 __global__ void __launch_bounds__(256) k_dot(const double* __restrict__ x, const double* __restrict__ y,
@@ -576,6 +655,7 @@ cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a)
     case MODE_SMOOTH: return launch_line_ty<MODE_SMOOTH>(ln, a);
     case MODE_CGDIR: return launch_line_t<MODE_CGDIR, 4>(ln, a);
     case MODE_CGPREC: return launch_line_ty<MODE_CGPREC>(ln, a);
+    case MODE_RESTRICT: return launch_line_t<MODE_RESTRICT, 4>(ln, a);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -603,9 +683,10 @@ cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const Le
 cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, const LevelConst& fine,
                                HaloField uc, double* uf)
 {
-    dim3 block(128), grid((unsigned)((fine.nx + 127) / 128), (unsigned)fine.nz, (unsigned)fine.ny);
-    if (fine.ny <= 0 || fine.nx <= 0) return cudaSuccess;
-    k_prolong_add<<<grid, block, 0, ln.stream>>>(coarse, fine, uc, uf);
+    const int64_t n = coarse.nx * coarse.ny * (int64_t)coarse.nz;
+    if (n <= 0) return cudaSuccess;
+    const int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)ln.num_sms * 8);
+    k_prolong_add<<<(unsigned)grid, 256, 0, ln.stream>>>(coarse, fine, uc, uf);
     if (ln.launch_counter) ++*ln.launch_counter;
     return cudaGetLastError();
 }

@@ -51,6 +51,7 @@ enum LineMode : int {
     MODE_CGDIR = 4,   // p = z + beta p_old; out0 = p; sum <p, A p>   (halo: z, p_old)
     MODE_CGPREC = 5,  // r -= alpha A p; u += alpha p; z = M^-1 r;
                       // sums ||r||^2, <r, z>                         (halo: p; plain: r, u)
+    MODE_RESTRICT = 6,// out0 (coarse) = R (f - A u): fine residual restricted (halo: u; plain: f)
 };
 
 // TMA descriptors of one halo'd field: the whole (TY+2)-row box, a one-row box,
