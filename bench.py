@@ -298,6 +298,7 @@ def main():
     if not args.no_e2e:
         fh = f.cpu().pin_memory()
         uh = torch.empty_like(fh).pin_memory()
+        ctx.solve_host(T.TPMG_SOLVER_MG, fh, uh, eps=args.eps)   # untimed: allocates the staging buffers
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
