@@ -22,6 +22,7 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <type_traits>
 
 namespace tpmg {
 namespace {
@@ -272,47 +273,65 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
     const bool want_red = (NR > 0) && (a.red.result != nullptr);
 
-    const int64_t ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
-    const int64_t ntiles = ntx * nty;
+    // 32-bit bookkeeping (tiles < 2^31); the producer and consumer walk the same chunk
+    // sequence with incremental cursors (no per-chunk integer division).
+    const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + TY - 1) / TY);
+    const int ntiles = ntx * nty;
     const int nch = (nz + KB - 1) / KB;
-    const int64_t my_tiles = (blockIdx.x < ntiles) ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const int64_t total = my_tiles * nch;
+    const int my_tiles = ((int)blockIdx.x < ntiles) ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    const int total = my_tiles * nch;
     __syncthreads();
 
-    // issue the loads of global chunk gi into slot gi % NS
-    auto issue = [&](int64_t gi) {
-        if (gi < total) {
-            const int64_t t = blockIdx.x + (gi / nch) * (int64_t)gridDim.x;
-            const int ch = (int)(gi % nch);
-            const int64_t i0 = (t % ntx) * TX, j0 = (t / ntx) * TY;
-            double* st = stage + (gi % NS) * G::STAGE;
+    // producer cursor: next chunk to load
+    int p_count = 0, p_ch = 0, p_slot = 0, p_tile = blockIdx.x;
+    int p_i0 = (p_tile % ntx) * TX, p_j0 = (p_tile / ntx) * TY;
+    auto issue = [&]() {
+        if (p_count < total) {
+            double* st = stage + p_slot * G::STAGE;
             if constexpr (LOADER == 0) {
-                load_stage<NH, NP, TY>(st, a, i0, j0, ch * KB);
+                load_stage<NH, NP, TY>(st, a, p_i0, p_j0, p_ch * KB);
             } else {
                 if (tid == 0) {
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                    tma_stage<NH, NP, TY>(st, a, i0, j0, ch * KB, &full_bar[gi % NS]);
+                    tma_stage<NH, NP, TY>(st, a, p_i0, p_j0, p_ch * KB, &full_bar[p_slot]);
                 }
+            }
+            ++p_count;
+            if (++p_slot == NS) p_slot = 0;
+            if (++p_ch == nch) {
+                p_ch = 0;
+                p_tile += gridDim.x;
+                p_i0 = (p_tile % ntx) * TX;
+                p_j0 = (p_tile / ntx) * TY;
             }
         }
         if constexpr (LOADER == 0) cp_async_commit();
     };
-    auto wait = [&](int64_t gi) {
+    // consumer cursor
+    int c_slot = 0;
+    uint32_t c_phase = 0;
+    auto wait = [&]() {
         if constexpr (LOADER == 0) {
             cp_async_wait<NS - 1>();
             __syncthreads();
         } else {
-            mbar_wait(&full_bar[gi % NS], (uint32_t)((gi / NS) & 1));
+            mbar_wait(&full_bar[c_slot], c_phase);
+        }
+    };
+    auto advance = [&]() {
+        if (++c_slot == NS) {
+            c_slot = 0;
+            c_phase ^= 1u;
         }
     };
 
 #pragma unroll
-    for (int s = 0; s < NS - 1; ++s) issue(s);
+    for (int s = 0; s < NS - 1; ++s) issue();
 
-    int64_t gi = 0;
-    for (int64_t tl = 0; tl < my_tiles; ++tl) {
-        const int64_t tile = blockIdx.x + tl * (int64_t)gridDim.x;
-        const int64_t i0 = (tile % ntx) * TX, j0 = (tile / ntx) * TY;
+    int gi = 0;
+    for (int tl = 0; tl < my_tiles; ++tl) {
+        const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
+        const int64_t i0 = (int64_t)(tile % ntx) * TX, j0 = (int64_t)(tile / ntx) * TY;
         const int64_t i = i0 + tx, j = j0 + ty;
         const bool valid = (i < nx) && (j < ny);
         const int64_t colbase = j * nx * (int64_t)nz + i;  // + k*nx
@@ -320,100 +339,123 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
         // rolling state for the k-lag: values at level km = k-1 and km-1
         double um1 = 0.0, u0 = 0.0, S0 = 0.0, qa = 0.0, qb = 0.0, gprev = 0.0;
         double* rbuf_cur = rbuf;   // MODE_RESTRICT: buffer of the current chunk
-        int slot_base = 0;         // MODE_RESTRICT: level held in slot 0 of rbuf_cur
+        // forward-pass outputs of level km live at ofw0/ofw1 (advanced by nx per level)
+        double* ofw0 = (MODE == MODE_APPLY || MODE == MODE_RESID || MODE == MODE_CGDIR || MODE == MODE_CGPREC) && a.out0
+                           ? a.out0 + colbase : nullptr;
+        double* ofw1 = (MODE == MODE_CGPREC) ? a.out1 + colbase : nullptr;
 
-        auto finalize = [&](int km, double up1) {
-            const double Mu = diag[km] * u0 - gamma * (um1 + up1);
-            const int64_t idx = colbase + (int64_t)km * nx;
+        // Complete level km (its upper neighbour up1 has arrived): stencil, the mode's
+        // pointwise work and one Thomas forward-elimination step.
+        auto finalize = [&](double up1, double dgk, double imk, double* gslot, int rslot) {
+            const double vs = um1 + up1;
+            const double Mu = fma(-gamma, vs, dgk * u0);          // (M_T u)_k
             double g = 0.0;
             if constexpr (MODE == MODE_APPLY) {
-                if (valid) a.out0[idx] = Mu - c * S0;
+                if (valid) *ofw0 = fma(-c, S0, Mu);                 // (A u)_k = (M_T u)_k - c sum(nbrs)
             } else if constexpr (MODE == MODE_RESID) {
-                const double r = qa - (Mu - c * S0);
+                const double r = fma(c, S0, qa) - Mu;               // f - A u
                 if (valid) {
-                    if (a.out0) a.out0[idx] = r;
-                    acc[0] += r * r;
+                    if (ofw0) *ofw0 = r;
+                    acc[0] = fma(r, r, acc[0]);
                 }
             } else if constexpr (MODE == MODE_PREC) {
                 g = a.scale * qa;
             } else if constexpr (MODE == MODE_SMOOTH) {
-                const double r = qa - (Mu - c * S0);
-                g = Mu + a.rho * r;   // = rho f + (M - rho A) u   (one-pass smoother)
-                if (valid) acc[0] += r * r;
+                const double r = fma(c, S0, qa) - Mu;               // f - A u
+                g = fma(a.rho, r, Mu);   // = rho f + (M - rho A) u   (one-pass smoother)
+                if (valid) acc[0] = fma(r, r, acc[0]);
             } else if constexpr (MODE == MODE_CGDIR) {
-                const double Ap = Mu - c * S0;
+                const double Ap = fma(-c, S0, Mu);
                 if (valid) {
-                    a.out0[idx] = u0;
-                    acc[0] += u0 * Ap;
+                    *ofw0 = u0;
+                    acc[0] = fma(u0, Ap, acc[0]);
                 }
             } else if constexpr (MODE == MODE_RESTRICT) {
                 // r = f - A u, summed over the x-pair (2I, 2I+1) of fine columns
-                const double r = qa - (Mu - c * S0);
+                const double r = fma(c, S0, qa) - Mu;
                 const double rs = r + __shfl_xor_sync(0xffffffffu, r, 1);
-                if ((tx & 1) == 0) rbuf_cur[(ty * RS + (km - slot_base)) * (TX / 2) + (tx >> 1)] = rs;
+                if ((tx & 1) == 0) rbuf_cur[(ty * RS + rslot) * (TX / 2) + (tx >> 1)] = rs;
             } else if constexpr (MODE == MODE_CGPREC) {
-                const double Ap = Mu - c * S0;
-                const double rn = qa - ratio * Ap;
-                const double un = qb + ratio * u0;
+                const double Ap = fma(-c, S0, Mu);
+                const double rn = fma(-ratio, Ap, qa);
+                const double un = fma(ratio, u0, qb);
                 if (valid) {
-                    a.out0[idx] = rn;
-                    a.out1[idx] = un;
-                    acc[0] += rn * rn;
+                    *ofw0 = rn;
+                    *ofw1 = un;
+                    acc[0] = fma(rn, rn, acc[0]);
                 }
                 g = rn;
             }
+            if constexpr (MODE == MODE_APPLY || MODE == MODE_RESID || MODE == MODE_CGDIR || MODE == MODE_CGPREC) {
+                if (ofw0) ofw0 += nx;
+                if constexpr (MODE == MODE_CGPREC) ofw1 += nx;
+            }
             if constexpr (T::THOMAS) {
-                const double y = g + gamma * gprev;      // y = L^-1 g   (M = L D L^T)
-                const double gp = y * invm[km];          // g'_k = (g_k - s_k g'_{k-1}) / m_k
-                gbuf[km * NT + tid] = gp;
+                const double y = fma(gamma, gprev, g);   // y = L^-1 g   (M = L D L^T)
+                const double gp = y * imk;               // g'_k = (g_k - s_k g'_{k-1}) / m_k
+                *gslot = gp;
                 if constexpr (MODE == MODE_CGPREC)
-                    if (valid) acc[1] += gp * y;         // <g, M^-1 g> = sum y_k^2 / m_k
+                    if (valid) acc[1] = fma(gp, y, acc[1]);   // <g, M^-1 g> = sum y_k^2 / m_k
                 gprev = gp;
             }
         };
 
-        for (int ch = 0; ch < nch; ++ch, ++gi) {
-            issue(gi + NS - 1);
-            wait(gi);
-            const double* st = stage + (gi % NS) * G::STAGE;
-            // all shared-memory reads of the chunk first (independent of the Thomas
-            // recurrence), so one warp per SMSP still has KB levels of ILP
+        // One KB-level chunk.  FULL: an interior chunk (ch >= 1, k0 + KB <= nz) needs no
+        // bounds checks.  All offsets are compile-time constants from per-chunk bases.
+        auto do_chunk = [&](auto full_t, int ch, const double* st) {
+            constexpr bool FULL = decltype(full_t)::value;
+            const int k0 = ch * KB;
             double ecv[KB], Sv[KB], pav[KB], pbv[KB];
+            const double* hp = st + (ty + 1) * G::HALO_ROW + tx + 2;           // own column
+            const double* pp = st + G::PLAIN_BASE + ty * (KB * TX) + tx;       // plain field 0
 #pragma unroll
             for (int kk = 0; kk < KB; ++kk) {
                 ecv[kk] = 0.0; Sv[kk] = 0.0; pav[kk] = 0.0; pbv[kk] = 0.0;
                 if constexpr (NH >= 1) {
-                    const double* h = st + kk * G::HX;   // field 0, row r at + r*HALO_ROW
-                    const double* hc = h + (ty + 1) * G::HALO_ROW;
-                    ecv[kk] = hc[tx + 2];
-                    Sv[kk] = (hc[tx + 1] + hc[tx + 3]) + (h[ty * G::HALO_ROW + tx + 2] + h[(ty + 2) * G::HALO_ROW + tx + 2]);
+                    const double* h = hp + kk * G::HX;
+                    ecv[kk] = h[0];
+                    Sv[kk] = (h[-1] + h[1]) + (h[-G::HALO_ROW] + h[G::HALO_ROW]);
                     if constexpr (MODE == MODE_CGDIR) {
                         const double* p = h + G::HY * G::HALO_ROW;  // field 1 = p_old
-                        const double* pc = p + (ty + 1) * G::HALO_ROW;
-                        ecv[kk] = ecv[kk] + ratio * pc[tx + 2];
-                        Sv[kk] = Sv[kk] + ratio * ((pc[tx + 1] + pc[tx + 3]) + (p[ty * G::HALO_ROW + tx + 2] + p[(ty + 2) * G::HALO_ROW + tx + 2]));
+                        ecv[kk] = fma(ratio, p[0], ecv[kk]);
+                        Sv[kk] = fma(ratio, (p[-1] + p[1]) + (p[-G::HALO_ROW] + p[G::HALO_ROW]), Sv[kk]);
                     }
                 }
-                if constexpr (NP >= 1) pav[kk] = st[G::PLAIN_BASE + (ty * KB + kk) * TX + tx];
-                if constexpr (NP >= 2) pbv[kk] = st[G::PLAIN_BASE + ((TY + ty) * KB + kk) * TX + tx];
+                if constexpr (NP >= 1) pav[kk] = pp[kk * TX];
+                if constexpr (NP >= 2) pbv[kk] = pp[TY * KB * TX + kk * TX];
             }
             __syncthreads();   // slot gi % NS is free for chunk gi + NS
-            if constexpr (MODE == MODE_RESTRICT) {
-                rbuf_cur = rbuf + (gi & 1) * (TY * RS * (TX / 2));
-                slot_base = ch * KB - 1;   // this chunk completes levels ch*KB-1 .. ch*KB+KB-2
-            }
+            if constexpr (MODE == MODE_RESTRICT) rbuf_cur = rbuf + (gi & 1) * (TY * RS * (TX / 2));
+            const double* dg = diag + (k0 - 1);      // level km = k0 - 1 + kk
+            const double* im = invm + (k0 - 1);
+            double* gb = gbuf + (k0 - 1) * NT + tid;
 #pragma unroll
             for (int kk = 0; kk < KB; ++kk) {
-                const int k = ch * KB + kk;
-                if (k < nz) {
-                    if (k > 0) finalize(k - 1, ecv[kk]);
+                const int k = k0 + kk;
+                if (FULL || k < nz) {
+                    if (FULL || k > 0) finalize(ecv[kk], dg[kk], im[kk], gb + kk * NT, kk);
                     um1 = u0; u0 = ecv[kk]; S0 = Sv[kk]; qa = pav[kk]; qb = pbv[kk];
                 }
             }
-            if (ch == nch - 1) finalize(nz - 1, 0.0);
+        };
+
+        for (int ch = 0; ch < nch; ++ch, ++gi) {
+            issue();
+            wait();
+            const double* st = stage + c_slot * G::STAGE;
+            advance();
+            if (ch >= 1 && (ch + 1) * KB <= nz)
+                do_chunk(std::true_type{}, ch, st);
+            else
+                do_chunk(std::false_type{}, ch, st);
+            if (ch == nch - 1)
+                finalize(0.0, diag[nz - 1], invm[nz - 1], gbuf + (nz - 1) * NT + tid, nz - ch * KB);
             if constexpr (MODE == MODE_RESTRICT) {
-                // f_c(I, J, k) = 1/4 (x-pair sum of row 2J + x-pair sum of row 2J+1)
+                // f_c(I, J, k) = 1/4 (x-pair sum of row 2J + x-pair sum of row 2J+1);
+                // this chunk completed levels ch*KB-1 .. ch*KB+KB-2 (and nz-1 if last), slot
+                // s holding level ch*KB-1+s
                 __syncthreads();
+                const int slot_base = ch * KB - 1;
                 const int lo = (ch == 0) ? 0 : ch * KB - 1;
                 const int hi = (ch == nch - 1) ? nz - 1 : ch * KB + KB - 2;
                 const int64_t nxc = nx >> 1, nyc = ny >> 1;
@@ -442,21 +484,23 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             double x = 0.0;
             int k = nz - 1;
             for (; k >= KB - 1; k -= KB) {
+                const double* gq = gbuf + (k - (KB - 1)) * NT + tid;   // levels k-KB+1 .. k
+                const double* mq = gim + (k - (KB - 1));
                 double gv[KB], gm[KB];
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
-                    gv[q] = gbuf[(k - q) * NT + tid];
-                    gm[q] = gim[k - q];
+                    gv[q] = gq[(KB - 1 - q) * NT];
+                    gm[q] = mq[KB - 1 - q];
                 }
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
-                    x = gv[q] + gm[q] * x;
+                    x = fma(gm[q], x, gv[q]);
                     if (valid) *op = x;
                     op -= nx;
                 }
             }
             for (; k >= 0; --k) {
-                x = gbuf[k * NT + tid] + gim[k] * x;
+                x = fma(gim[k], x, gbuf[k * NT + tid]);
                 if (valid) *op = x;
                 op -= nx;
             }
