@@ -117,6 +117,16 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` at this workload from the committed ncu --set full
+    capture (profiles/ncu_traffic.json, written by scripts/ncu_summary.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh)[kernel]["bytes"]
+    except Exception:
+        return None
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -271,8 +281,11 @@ def main():
     if dom:
         kname, (n, kms, cells) = dom
         ach = cells * BYTES_PER_CELL[kname] / (kms * 1e-3) / 1e9
+        traffic = ncu_traffic(kname) if (world == 1 and args.per_gpu_nx == 1024 and nz == 128) else None
         roof = {"bound": "hbm", "kernel": kname, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_src,
+                "frac": round(ach / peak, 4), "traffic": traffic,
+                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram read+write per launch)" if traffic else None,
+                "algorithmic_bytes_per_launch": cells / n * BYTES_PER_CELL[kname], "peak_source": peak_src,
                 "bytes_per_cell": BYTES_PER_CELL[kname],
                 "cells_per_launch": cells / n, "avg_launch_ms": kms / n}
 
