@@ -130,6 +130,15 @@ void tpmg_params_default(tpmg_params *p);
  * bytes); the caller broadcasts it to every rank (e.g. torch.distributed). */
 tpmg_status tpmg_nccl_id(void *id128);
 
+/* Domain decomposition without a GPU (host-only, pure): validates params for
+ * nranks y-strips exactly as tpmg_create does (TPMG_E_PARAM / TPMG_E_SHAPE /
+ * TPMG_E_TOPOLOGY) and returns rank `rank`'s first global row y0 and row count
+ * ny on level `level` (1..L; TPMG_E_RANGE otherwise).  Strips are contiguous and
+ * equal: ny_l = ny / (nranks 2^(L-l)), y0 = rank ny_l (columns never
+ * split P:306). */
+tpmg_status tpmg_partition(const tpmg_params *params, int32_t rank, int32_t nranks, int32_t level,
+                           int64_t *y0, int64_t *ny);
+
 /* Create a context on CUDA device `device` for rank `rank` of `nranks`.
  * id128: the NCCL unique id (ignored when nranks == 1, may be NULL).
  * cuda_stream: a cudaStream_t on `device`, or NULL for the legacy default

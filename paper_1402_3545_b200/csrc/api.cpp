@@ -803,11 +803,11 @@ tpmg_status tpmg_nccl_id(void* id128)
     return TPMG_OK;
 }
 
-tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks, const void* id128,
-                        int32_t device, void* cuda_stream, tpmg_ctx** out)
+namespace {
+// Parameter / topology validation shared by tpmg_partition and tpmg_create.
+tpmg_status validate(const tpmg_params* params, int32_t rank, int32_t nranks, tpmg_params* out)
 {
-    if (!params || !out) return fail(nullptr, TPMG_E_PARAM, "tpmg_create: NULL argument");
-    *out = nullptr;
+    if (!params) return fail(nullptr, TPMG_E_PARAM, "NULL params");
     tpmg_params p = *params;
     params_fill_defaults(&p);
     if (p.nx <= 0 || p.ny <= 0 || p.nz <= 0) return fail(nullptr, TPMG_E_PARAM, "grid %lld x %lld x %d must be positive", (long long)p.nx, (long long)p.ny, p.nz);
@@ -816,11 +816,35 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
     if (p.levels < 1 || p.levels > 24) return fail(nullptr, TPMG_E_PARAM, "levels = %d not in [1, 24]", p.levels);
     if (p.pre < 0 || p.post < 0 || p.coarse_sweeps < 1) return fail(nullptr, TPMG_E_PARAM, "pre/post >= 0, coarse_sweeps >= 1");
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(nullptr, TPMG_E_TOPOLOGY, "rank %d of %d", rank, nranks);
-    if (nranks > 1 && !id128) return fail(nullptr, TPMG_E_PARAM, "nranks > 1 needs the NCCL id");
     const int64_t f = (int64_t)1 << (p.levels - 1);
     if (p.nx % f) return fail(nullptr, TPMG_E_SHAPE, "nx = %lld not divisible by 2^(L-1) = %lld", (long long)p.nx, (long long)f);
     if (p.ny % (f * nranks)) return fail(nullptr, TPMG_E_SHAPE, "ny = %lld not divisible by nranks * 2^(L-1) = %lld", (long long)p.ny, (long long)(f * nranks));
     if (p.nz > line_max_nz()) return fail(nullptr, TPMG_E_SHAPE, "nz = %d exceeds the on-chip Thomas buffer (max %d)", p.nz, line_max_nz());
+    if (out) *out = p;
+    return TPMG_OK;
+}
+}  // namespace
+
+tpmg_status tpmg_partition(const tpmg_params* params, int32_t rank, int32_t nranks, int32_t level, int64_t* y0,
+                           int64_t* ny)
+{
+    tpmg_params p;
+    TRY(validate(params, rank, nranks, &p));
+    if (level < 1 || level > p.levels) return fail(nullptr, TPMG_E_RANGE, "level %d not in [1, %d]", level, p.levels);
+    const int64_t rows = p.ny / nranks >> (p.levels - level);
+    if (y0) *y0 = (int64_t)rank * rows;
+    if (ny) *ny = rows;
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks, const void* id128,
+                        int32_t device, void* cuda_stream, tpmg_ctx** out)
+{
+    if (!params || !out) return fail(nullptr, TPMG_E_PARAM, "tpmg_create: NULL argument");
+    *out = nullptr;
+    tpmg_params p;
+    TRY(validate(params, rank, nranks, &p));
+    if (nranks > 1 && !id128) return fail(nullptr, TPMG_E_PARAM, "nranks > 1 needs the NCCL id");
 
     tpmg_ctx* ctx = new tpmg_ctx();
     ctx->p = p;

@@ -55,6 +55,7 @@ _SIGS = {
     "tpmg_version": ([], _i32),
     "tpmg_params_default": ([_P(tpmg_params)], None),
     "tpmg_nccl_id": ([_vp], C.c_int),
+    "tpmg_partition": ([_P(tpmg_params), _i32, _i32, _i32, _P(_i64), _P(_i64)], C.c_int),
     "tpmg_create": ([_P(tpmg_params), _i32, _i32, _vp, _i32, _vp, _P(_vp)], C.c_int),
     "tpmg_destroy": ([_vp], C.c_int),
     "tpmg_set_stream": ([_vp, _vp], C.c_int),
@@ -122,6 +123,13 @@ def tpmg_nccl_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(_lib.tpmg_nccl_id(buf))
     return buf.raw
+
+
+def tpmg_partition(params: tpmg_params, rank: int, nranks: int, level: int):
+    """(y0, ny) of rank's strip on `level` (host-only, no GPU)."""
+    y0, ny = _i64(), _i64()
+    _check(_lib.tpmg_partition(C.byref(params), rank, nranks, level, C.byref(y0), C.byref(ny)))
+    return y0.value, ny.value
 
 
 def tpmg_create(params: tpmg_params, rank: int = 0, nranks: int = 1, id128: bytes | None = None,
