@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -74,6 +75,7 @@ struct tpmg_ctx {
     // TMA descriptors, cached by (address, nx, nz, ny, box x, box rows)
     bool use_tma = true;
     bool sync_debug = false;   // TPMG_SYNC_DEBUG=1: synchronise after every line kernel
+    int ksplit_cfg = 0;        // k-split kernel config (TPMG_KSPLIT: "0" off, "1" = 2x8, "2" = 4x4); -1 = off
     std::map<std::tuple<uintptr_t, int64_t, int, int64_t, int, int>, CUtensorMap> tmaps;
     int64_t prof_launches[TPMG_K_COUNT] = {};
     double prof_ms[TPMG_K_COUNT] = {}, prof_cells[TPMG_K_COUNT] = {};
@@ -288,9 +290,10 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
 }
 
 // 3-D tiled map over an fp64 field [ny][nz][nx] (x fastest) with box (bx, KB, by).
-bool tensor_map(tpmg_ctx* ctx, const double* base, int64_t nx, int nz, int64_t ny, int bx, int by, CUtensorMap* out)
+bool tensor_map(tpmg_ctx* ctx, const double* base, int64_t nx, int nz, int64_t ny, int bx, int by, CUtensorMap* out,
+                int bz = kStageK)
 {
-    auto key = std::make_tuple((uintptr_t)base, nx, nz, ny, bx, by);
+    auto key = std::make_tuple((uintptr_t)base, nx, nz, ny, bx, by * 1000 + bz);
     auto it = ctx->tmaps.find(key);
     if (it != ctx->tmaps.end()) {
         *out = it->second;
@@ -300,7 +303,7 @@ bool tensor_map(tpmg_ctx* ctx, const double* base, int64_t nx, int nz, int64_t n
     if (!enc) return false;
     cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)nz, (cuuint64_t)ny};
     cuuint64_t strides[2] = {(cuuint64_t)nx * 8, (cuuint64_t)nx * (cuuint64_t)nz * 8};
-    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)kStageK, (cuuint32_t)by};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)bz, (cuuint32_t)by};
     cuuint32_t estr[3] = {1, 1, 1};
     CUtensorMap m;
     CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
@@ -353,9 +356,45 @@ void fill_tma(tpmg_ctx* ctx, int mode, LineArgs& a)
     a.use_tma = 1;
 }
 
+// TMA descriptors for the k-split kernel (boxes of ksplit_boxes()).
+bool fill_tma_ksplit(tpmg_ctx* ctx, int mode, LineArgs& a)
+{
+    const int64_t nx = a.L.nx, ny = a.L.ny;
+    const int nz = a.L.nz;
+    const KsplitBoxes b = ksplit_boxes(mode, ctx->ksplit_cfg);
+    auto aligned = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+    if (mode == MODE_SMOOTH) {
+        const HaloField& hf = a.h0;
+        TmaHalo& M = a.tma.h[0];
+        if (!hf.base || !aligned(hf.base)) return false;
+        if (!tensor_map(ctx, hf.base, nx, nz, ny, b.hx, b.ty + 2, &M.main, b.depth)) return false;
+        M.has_lo = hf.lo != nullptr;
+        M.has_hi = hf.hi != nullptr;
+        if (hf.lo && (!aligned(hf.lo) || !tensor_map(ctx, hf.lo, nx, nz, 1, b.hx, 1, &M.lo, b.depth))) return false;
+        if (hf.hi && (!aligned(hf.hi) || !tensor_map(ctx, hf.hi, nx, nz, 1, b.hx, 1, &M.hi, b.depth))) return false;
+    }
+    if (!a.q0 || !aligned(a.q0)) return false;
+    if (!tensor_map(ctx, a.q0, nx, nz, ny, kTileX, b.ty, &a.tma.q[0], b.kb)) return false;
+    a.use_tma = 1;
+    return true;
+}
+
 tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
 {
     LineArgs a = a0;
+    if (ctx->use_tma && ctx->ksplit_cfg >= 0 && ksplit_supported(mode, a.L.nz, (int)a.L.nx) &&
+        fill_tma_ksplit(ctx, mode, a)) {
+        ProfScope ps(ctx, mode, level_cells(a.L));
+        CUDA_TRY(ctx, launch_line_ksplit(launcher(ctx), mode, ctx->ksplit_cfg, a));
+        if (ctx->sync_debug) {
+            cudaError_t e = cudaStreamSynchronize(ctx->stream);
+            if (e != cudaSuccess)
+                return fail(ctx, TPMG_E_CUDA, "k-split kernel mode %d (nx=%lld ny=%lld nz=%d): %s", mode,
+                            (long long)a.L.nx, (long long)a.L.ny, a.L.nz, cudaGetErrorString(e));
+        }
+        return TPMG_OK;
+    }
+    a = a0;
     fill_tma(ctx, mode, a);
     ProfScope ps(ctx, mode == MODE_RESTRICT ? TPMG_K_RESIDUAL_RESTRICT : mode, level_cells(a.L));  // modes 0..5 = TPMG_K_0..5
     CUDA_TRY(ctx, launch_line(launcher(ctx), mode, a));
@@ -856,6 +895,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
     {
         const char* ld = std::getenv("TPMG_LOADER");   // "cpasync" selects the cp.async loader
         ctx->use_tma = !(ld && std::strcmp(ld, "cpasync") == 0);
+        const char* ks = std::getenv("TPMG_KSPLIT");
+        ctx->ksplit_cfg = (ks && ks[0] == '0') ? -1 : (ks && ks[0] == '2') ? 1 : 0;
         const char* sd = std::getenv("TPMG_SYNC_DEBUG");
         ctx->sync_debug = sd && sd[0] == '1';
     }
@@ -905,16 +946,35 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         L.lc.c = omega * omega / (hl * hl);
         L.lc.gamma = gamma;
         // Thomas factors of the column block M_T = A_T: diag_k, 1/m_k, gamma/m_k
-        std::vector<double> tab(3 * (size_t)p.nz);
+        // Thomas factors of the column block M_T = A_T, per level k:
+        //   diag_k, 1/m_k, b_k = gamma/m_k (backward), a_k = gamma/m_{k-1} (forward, L of M = L D L^T),
+        //   and the k-split propagators over segments of kSegK levels:
+        //   P_k = prod_{j = k_s..k} a_j,  Q_k = prod_{j = k..k_e} b_j.
+        const int nz = p.nz;
+        std::vector<double> tab(6 * (size_t)nz);
+        double* t_diag = tab.data();
+        double* t_invm = t_diag + nz;
+        double* t_gim = t_invm + nz;
+        double* t_afw = t_gim + nz;
+        double* t_P = t_afw + nz;
+        double* t_Q = t_P + nz;
         double mprev = 0.0;
-        for (int k = 0; k < p.nz; ++k) {
-            const double diag = 1.0 + 4.0 * L.lc.c + gamma * ((k > 0 ? 1.0 : 0.0) + (k < p.nz - 1 ? 1.0 : 0.0));
+        for (int k = 0; k < nz; ++k) {
+            const double diag = 1.0 + 4.0 * L.lc.c + gamma * ((k > 0 ? 1.0 : 0.0) + (k < nz - 1 ? 1.0 : 0.0));
             const double m = (k == 0) ? diag : diag - gamma * (gamma / mprev);
             if (m == 0.0 || !std::isfinite(m)) return bail(fail(ctx, TPMG_E_SINGULAR, "zero Thomas pivot at level %d, k = %d", l, k));
-            tab[k] = diag;
-            tab[p.nz + k] = 1.0 / m;
-            tab[2 * p.nz + k] = (k < p.nz - 1) ? gamma / m : 0.0;
+            t_diag[k] = diag;
+            t_invm[k] = 1.0 / m;
+            t_gim[k] = (k < nz - 1) ? gamma / m : 0.0;
+            t_afw[k] = (k > 0) ? gamma / mprev : 0.0;
             mprev = m;
+        }
+        for (int k0 = 0; k0 < nz; k0 += kSegK) {
+            const int k1 = std::min(nz, k0 + kSegK) - 1;
+            double pr = 1.0;
+            for (int k = k0; k <= k1; ++k) { pr *= t_afw[k]; t_P[k] = pr; }
+            pr = 1.0;
+            for (int k = k1; k >= k0; --k) { pr *= t_gim[k]; t_Q[k] = pr; }
         }
         CREATE_TRY(dev_alloc(ctx, &L.d_tab, tab.size()));
         CREATE_CUDA(cudaMemcpy(L.d_tab, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice));

@@ -70,6 +70,7 @@ struct TmaMaps {
 // levels per pipeline stage.
 constexpr int kTileX = 32;
 constexpr int kStageK = 8;
+constexpr int kSegK = 32;   // k-split kernel: levels per column segment
 
 struct LineArgs {
     LevelConst L;
@@ -98,6 +99,17 @@ cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a);
 int line_tile_rows(int mode, int nz);
 // Largest nz the on-chip Thomas buffer supports.
 int line_max_nz();
+
+// k-split line kernel (kernels_ksplit.cu) for MODE_SMOOTH / MODE_PREC.
+struct KsplitBoxes {
+    int ty;      // tile rows
+    int kb;      // levels per chunk (f box depth)
+    int hx;      // halo'd row width (u box x extent)
+    int depth;   // u box depth (kb + 2)
+};
+bool ksplit_supported(int mode, int nz, int nx);
+KsplitBoxes ksplit_boxes(int mode, int cfg);
+cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const LineArgs& a);
 
 // f_c = 1/4 sum of the 2x2 fine children of (f - A u)  (Residual + restriction, fused)
 cudaError_t launch_residual_restrict(const Launcher& ln, const LevelConst& fine,

@@ -1,0 +1,299 @@
+// kernels_ksplit.cu -- the k-split line kernel (smoother and preconditioner).
+//
+// The one-thread-per-column kernel (kernels.cu) keeps a column's Thomas
+// intermediates g'_k in shared memory (8*nz bytes per column), which at nz = 128
+// limits an SM to 128 columns = one warp per SMSP, and the k-recurrence then
+// runs latency-bound.  Here each column is split into NSEG segments of SL = 32
+// levels handled by NSEG threads (the paper's outlook, "assign several threads
+// to work on each vertical column ... substructuring"):
+//
+//  forward   y = L^-1 g  (M_T = L D L^T, y_k = g_k + a_k y_{k-1}, a_k = gamma/m_{k-1})
+//            each thread: local recurrence from 0, yhat (32 values, in REGISTERS);
+//            true y_k = yhat_k + P_k Y_s, P_k = prod_{j=k_s..k} a_j (level tables),
+//            Y_s = y_{k_s - 1} chained through the segments' last values;
+//  scale     g'_k = y_k / m_k;
+//  backward  x_k = g'_k + b_k x_{k+1} (b_k = gamma/m_k): local xhat from 0, then
+//            x_k = xhat_k + Q_k X_s, Q_k = prod_{j=k..k_e} b_j, X_s = x_{k_e + 1}
+//            chained through the segments' first values.
+//
+// This is exact algebra on the same recurrences (only the rounding order
+// differs), so the result matches the oracle's Thomas solve to rounding.  With no
+// g' buffer in shared memory the CTA holds 2*NSEG (or 4*NSEG) warps.
+//
+// Shared memory per stage and segment: the u box (TY+2 rows, KB+2 levels: the
+// vertical neighbours of the chunk's first and last level come with the box, so
+// chunks are independent), two halo-slab rows (multi-GPU strip boundaries), and
+// the f box (TY rows, KB levels), all loaded by TMA into 128-byte aligned slots.
+#include "kernels.cuh"
+#include "device_util.cuh"
+
+#include <algorithm>
+
+namespace tpmg {
+namespace {
+using namespace dev;
+
+constexpr int TX = kTileX;
+constexpr int SL = kSegK;      // levels per segment
+constexpr int HX = TX + 4;     // halo'd row width (even start column for TMA)
+constexpr int NS2 = 2;         // pipeline stages
+
+__host__ __device__ constexpr int r16(int n) { return (n + 15) & ~15; }
+
+template <int MODE, int TY, int KB>
+struct KGeom {
+    static constexpr bool HALO = (MODE == MODE_SMOOTH);
+    static constexpr int D = KB + 2;                            // u box depth (levels k0-1 .. k0+KB)
+    static constexpr int UBOX = HALO ? r16((TY + 2) * D * HX) : 0;
+    static constexpr int SROW = HALO ? r16(D * HX) : 0;         // one halo-slab row
+    static constexpr int FBOX = TY * KB * TX;
+    static constexpr int SEGST = UBOX + 2 * SROW + FBOX;        // doubles per segment per stage
+};
+
+// Issue the TMA copies of step (tile origin i0, j0; chunk cc of every segment).
+template <int MODE, int TY, int KB, int NSEG>
+__device__ __forceinline__ void tma_step(double* st, const LineArgs& a, int i0, int j0, int cc, uint64_t* bar)
+{
+    using G = KGeom<MODE, TY, KB>;
+    const int ny = (int)a.L.ny;
+    uint32_t bytes = NSEG * G::FBOX * 8;
+    bool lo = false, hi = false;
+    if constexpr (G::HALO) {
+        bytes += NSEG * (TY + 2) * G::D * HX * 8;
+        lo = a.tma.h[0].has_lo && j0 == 0;
+        hi = a.tma.h[0].has_hi && j0 + TY >= ny;
+        bytes += NSEG * ((lo ? 1 : 0) + (hi ? 1 : 0)) * G::D * HX * 8;
+    }
+    mbar_expect_tx(bar, bytes);
+#pragma unroll
+    for (int s = 0; s < NSEG; ++s) {
+        double* seg = st + s * G::SEGST;
+        const int k0 = s * SL + cc * KB;
+        if constexpr (G::HALO) {
+            tma_load_3d(seg, &a.tma.h[0].main, i0 - 2, k0 - 1, j0 - 1, bar);
+            if (lo) tma_load_3d(seg + G::UBOX, &a.tma.h[0].lo, i0 - 2, k0 - 1, 0, bar);
+            if (hi) tma_load_3d(seg + G::UBOX + G::SROW, &a.tma.h[0].hi, i0 - 2, k0 - 1, 0, bar);
+        }
+        tma_load_3d(seg + G::UBOX + 2 * G::SROW, &a.tma.q[0], i0, k0, j0, bar);
+    }
+}
+
+template <int MODE, int TY, int NSEG, int KB>
+__global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_constant__ LineArgs a)
+{
+    using G = KGeom<MODE, TY, KB>;
+    constexpr int NT = 32 * TY * NSEG;
+    constexpr int NCC = SL / KB;           // chunks per segment
+    constexpr int STG = NSEG * G::SEGST;
+    constexpr bool NORM = (MODE == MODE_SMOOTH);
+
+    extern __shared__ __align__(128) double smem_raw[];
+    __shared__ __align__(8) uint64_t full_bar[NS2];
+    double* smem = reinterpret_cast<double*>(reinterpret_cast<char*>(smem_raw) +
+                                             ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
+    const int nz = a.L.nz;
+    const int64_t nx = a.L.nx, ny = a.L.ny;
+    double* tab = smem;                                 // diag, invm, gim, afw, Pfw, Qbw (nz each)
+    double* stage = smem + r16(6 * nz);
+    double* bnd = stage + NS2 * STG;                    // [2][TY][NSEG][32]
+    double* scratch = bnd + 2 * TY * NSEG * 32;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int s = warp % NSEG, ty = warp / NSEG;
+    for (int q = tid; q < 6 * nz; q += NT) tab[q] = a.L.tab[q];
+    const double* diag = tab;
+    const double* invm = tab + nz;
+    const double* gim = tab + 2 * nz;
+    const double* afw = tab + 3 * nz;
+    const double* Pfw = tab + 4 * nz;
+    const double* Qbw = tab + 5 * nz;
+    const double c = a.L.c, gamma = a.L.gamma, rho = a.rho, scale = a.scale;
+    if (tid == 0) {
+        for (int q = 0; q < NS2; ++q) mbar_init(&full_bar[q], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    double acc[1] = {0.0};
+
+    const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + TY - 1) / TY);
+    const int ntiles = ntx * nty;
+    const int my_tiles = ((int)blockIdx.x < ntiles) ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    const int total = my_tiles * NCC;
+    __syncthreads();
+
+    // producer (thread 0) and consumer cursors over the CTA's (tile, chunk) steps
+    int p_count = 0, p_cc = 0, p_slot = 0, p_tile = blockIdx.x;
+    auto issue = [&]() {
+        if (tid == 0 && p_count < total) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            tma_step<MODE, TY, KB, NSEG>(stage + p_slot * STG, a, (p_tile % ntx) * TX, (p_tile / ntx) * TY, p_cc,
+                                         &full_bar[p_slot]);
+        }
+        ++p_count;
+        if (++p_slot == NS2) p_slot = 0;
+        if (++p_cc == NCC) {
+            p_cc = 0;
+            p_tile += gridDim.x;
+        }
+    };
+    int c_slot = 0;
+    uint32_t c_phase = 0;
+
+#pragma unroll
+    for (int q = 0; q < NS2 - 1; ++q) issue();
+
+    for (int tl = 0; tl < my_tiles; ++tl) {
+        const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
+        const int i0 = (tile % ntx) * TX, j0 = (tile / ntx) * TY;
+        const int64_t i = i0 + lane, j = j0 + ty;
+        const bool valid = (i < nx) && (j < ny);
+        // halo rows of this warp's row j: south j-1, north j+1 (slab rows at strip boundaries)
+        const bool s_slab = G::HALO && a.tma.h[0].has_lo && j0 == 0 && ty == 0;
+        const bool n_slab = G::HALO && a.tma.h[0].has_hi && (j0 + ty + 1 == ny);
+
+        double yv[SL];
+        double yprev = 0.0;
+#pragma unroll
+        for (int cc = 0; cc < NCC; ++cc) {
+            issue();
+            mbar_wait(&full_bar[c_slot], c_phase);
+            const double* seg = stage + c_slot * STG + s * G::SEGST;
+            if (++c_slot == NS2) { c_slot = 0; c_phase ^= 1u; }
+            const double* fb = seg + G::UBOX + 2 * G::SROW + ty * (KB * TX) + lane;
+            double gv[KB], rv[KB];
+            if constexpr (G::HALO) {
+                const double* rc = seg + (ty + 1) * (G::D * HX) + lane + 2;                   // own row
+                const double* rs = s_slab ? seg + G::UBOX + lane + 2 : rc - G::D * HX;        // south row
+                const double* rn = n_slab ? seg + G::UBOX + G::SROW + lane + 2 : rc + G::D * HX;  // north row
+                double ud = rc[0], uc = rc[HX];
+#pragma unroll
+                for (int kk = 0; kk < KB; ++kk) {
+                    const int d = kk + 1;                 // box level of k = k0 + kk
+                    const int k = s * SL + cc * KB + kk;
+                    const double uu = rc[(d + 1) * HX];
+                    const double S = (rc[d * HX - 1] + rc[d * HX + 1]) + (rs[d * HX] + rn[d * HX]);
+                    const double Mu = fma(-gamma, ud + uu, diag[k] * uc);       // (M_T u)_k
+                    const double r = fma(c, S, fb[kk * TX]) - Mu;               // f - A u
+                    gv[kk] = fma(rho, r, Mu);            // g = (M - rho A) u + rho f  (one-pass smoother)
+                    rv[kk] = r;
+                    ud = uc;
+                    uc = uu;
+                }
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < KB; ++kk) { gv[kk] = scale * fb[kk * TX]; rv[kk] = 0.0; }
+            }
+            // local forward recurrence yhat_k = g_k + a_k yhat_{k-1} (yhat = 0 before the segment)
+#pragma unroll
+            for (int kk = 0; kk < KB; ++kk) {
+                const int k = s * SL + cc * KB + kk;
+                yprev = (cc == 0 && kk == 0) ? gv[kk] : fma(afw[k], yprev, gv[kk]);
+                yv[cc * KB + kk] = yprev;
+                if constexpr (NORM) acc[0] = fma(rv[kk], rv[kk], acc[0]);
+            }
+            __syncthreads();   // every warp is done with this slot
+        }
+
+        // chain the segments: Y_s = y_{k_s - 1} (true), from the segments' last yhat
+        double* bF = bnd + (ty * NSEG) * 32 + lane;               // [ty][seg][lane]
+        double* bB = bnd + TY * NSEG * 32 + (ty * NSEG) * 32 + lane;
+        bF[s * 32] = yv[SL - 1];
+        __syncthreads();
+        double Y = 0.0;
+#pragma unroll
+        for (int q = 0; q < NSEG - 1; ++q)
+            if (q < s) Y = fma(Pfw[(q + 1) * SL - 1], Y, bF[q * 32]);
+        // g'_k = (yhat_k + P_k Y) / m_k, then the local backward recurrence
+        const int kb = s * SL;
+#pragma unroll
+        for (int q = 0; q < SL; ++q) yv[q] = fma(Pfw[kb + q], Y, yv[q]) * invm[kb + q];
+        double xh = 0.0;
+#pragma unroll
+        for (int q = SL - 1; q >= 0; --q) {
+            xh = fma(gim[kb + q], xh, yv[q]);
+            yv[q] = xh;
+        }
+        bB[s * 32] = yv[0];
+        __syncthreads();
+        double X = 0.0;                                           // x_{k_e + 1} (true)
+#pragma unroll
+        for (int q = NSEG - 1; q >= 1; --q)
+            if (q > s) X = fma(Qbw[q * SL], X, bB[q * 32]);
+        double* op = a.out0 + (j * nz + kb) * nx + i;
+#pragma unroll
+        for (int q = 0; q < SL; ++q) {
+            const double x = fma(Qbw[kb + q], X, yv[q]);
+            if (valid) *op = x;
+            op += nx;
+        }
+        // bnd is reused by the next tile only after its forward chunks (>= 1 __syncthreads)
+    }
+    if (NORM && a.red.result != nullptr) grid_reduce<1>(a.red, acc, scratch);
+}
+
+template <int MODE, int TY, int NSEG, int KB>
+size_t ksmem(int nz)
+{
+    using G = KGeom<MODE, TY, KB>;
+    return (size_t)(r16(6 * nz) + NS2 * NSEG * G::SEGST + 2 * TY * NSEG * 32 + 64 + 16) * sizeof(double);
+}
+
+template <int MODE, int TY, int NSEG, int KB>
+cudaError_t launch_k(const Launcher& ln, const LineArgs& a)
+{
+    auto kern = k_linek<MODE, TY, NSEG, KB>;
+    const size_t smem = ksmem<MODE, TY, NSEG, KB>(a.L.nz);
+    static size_t limit = 0;
+    if (!limit) {
+        limit = dyn_smem_limit(kern);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
+        if (e != cudaSuccess) return e;
+    }
+    if (smem > limit) return cudaErrorInvalidConfiguration;
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * TY * NSEG, smem);
+    if (e != cudaSuccess) return e;
+    per_sm = std::max(per_sm, 1);
+    const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * ((a.L.ny + TY - 1) / TY);
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)ln.num_sms * per_sm);
+    if (grid <= 0) return cudaSuccess;
+    kern<<<(unsigned)grid, 32 * TY * NSEG, smem, ln.stream>>>(a);
+    if (ln.launch_counter) ++*ln.launch_counter;
+    return cudaGetLastError();
+}
+
+template <int MODE, int TY, int KB>
+cudaError_t launch_k_nseg(const Launcher& ln, const LineArgs& a)
+{
+    switch (a.L.nz / SL) {
+    case 1: return launch_k<MODE, TY, 1, KB>(ln, a);
+    case 2: return launch_k<MODE, TY, 2, KB>(ln, a);
+    case 4: return launch_k<MODE, TY, 4, KB>(ln, a);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace
+
+bool ksplit_supported(int mode, int nz, int nx)
+{
+    return (mode == MODE_SMOOTH || mode == MODE_PREC) && nz % SL == 0 &&
+           (nz / SL == 1 || nz / SL == 2 || nz / SL == 4) && nx % 2 == 0;
+}
+
+KsplitBoxes ksplit_boxes(int mode, int cfg)
+{
+    const int TY = (cfg == 1) ? 4 : 2, KB = (cfg == 1) ? 4 : 8;
+    (void)mode;
+    return KsplitBoxes{TY, KB, HX, KB + 2};
+}
+
+cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const LineArgs& a)
+{
+    if (mode == MODE_SMOOTH)
+        return cfg == 1 ? launch_k_nseg<MODE_SMOOTH, 4, 4>(ln, a) : launch_k_nseg<MODE_SMOOTH, 2, 8>(ln, a);
+    if (mode == MODE_PREC)
+        return cfg == 1 ? launch_k_nseg<MODE_PREC, 4, 4>(ln, a) : launch_k_nseg<MODE_PREC, 2, 8>(ln, a);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace tpmg

@@ -50,7 +50,7 @@ def rand(shape, seed):
     return np.random.default_rng(seed).standard_normal(shape)
 
 
-LOADERS = ["tma", "cpasync"]
+LOADERS = ["tma", "cpasync", "tma-noks", "tma-ks2"]
 
 
 @pytest.mark.parametrize("loader", LOADERS)
