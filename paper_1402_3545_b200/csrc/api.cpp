@@ -36,6 +36,7 @@ struct LevelData {
     double* u[2] = {nullptr, nullptr};  // MG iterate ping-pong (fine level: u[0] = caller's u)
     int cur = 0;
     double* f = nullptr;                // MG right-hand side (coarse levels)
+    KTables ktab{};                     // k-split tables (kernel parameter space)
     double* slab_lo = nullptr;          // halo rows j = -1 / j = ny for this level (nranks > 1)
     double* slab_hi = nullptr;
     size_t n() const { return (size_t)lc.nx * (size_t)lc.ny * (size_t)lc.nz; }
@@ -356,6 +357,14 @@ void fill_tma(tpmg_ctx* ctx, int mode, LineArgs& a)
     a.use_tma = 1;
 }
 
+// The level whose constants a LineArgs carries (by its table pointer).
+int level_of(tpmg_ctx* ctx, const LevelConst& lc)
+{
+    for (int l = 1; l <= ctx->L; ++l)
+        if (ctx->lv[l].lc.tab == lc.tab) return l;
+    return ctx->L;
+}
+
 // TMA descriptors for the k-split kernel (boxes of ksplit_boxes()).
 bool fill_tma_ksplit(tpmg_ctx* ctx, int mode, LineArgs& a)
 {
@@ -385,7 +394,8 @@ tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
     if (ctx->use_tma && ctx->ksplit_cfg >= 0 && ksplit_supported(mode, a.L.nz, (int)a.L.nx) &&
         fill_tma_ksplit(ctx, mode, a)) {
         ProfScope ps(ctx, mode, level_cells(a.L));
-        CUDA_TRY(ctx, launch_line_ksplit(launcher(ctx), mode, ctx->ksplit_cfg, a));
+        const KTables& kt = ctx->lv[level_of(ctx, a.L)].ktab;
+        CUDA_TRY(ctx, launch_line_ksplit(launcher(ctx), mode, ctx->ksplit_cfg, a, kt));
         if (ctx->sync_debug) {
             cudaError_t e = cudaStreamSynchronize(ctx->stream);
             if (e != cudaSuccess)
@@ -896,7 +906,7 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         const char* ld = std::getenv("TPMG_LOADER");   // "cpasync" selects the cp.async loader
         ctx->use_tma = !(ld && std::strcmp(ld, "cpasync") == 0);
         const char* ks = std::getenv("TPMG_KSPLIT");
-        ctx->ksplit_cfg = (ks && ks[0] == '0') ? -1 : (ks && ks[0] == '2') ? 1 : 0;
+        ctx->ksplit_cfg = (ks && ks[0] == '0') ? -1 : (ks && ks[0] == '2') ? 1 : (ks && ks[0] == '3') ? 2 : 0;
         const char* sd = std::getenv("TPMG_SYNC_DEBUG");
         ctx->sync_debug = sd && sd[0] == '1';
     }
@@ -976,6 +986,9 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
             pr = 1.0;
             for (int k = k1; k >= k0; --k) { pr *= t_gim[k]; t_Q[k] = pr; }
         }
+        if (nz <= kKsplitMaxNZ)
+            for (int q = 0; q < 6; ++q)
+                for (int k = 0; k < nz; ++k) L.ktab.t[q][k] = tab[(size_t)q * nz + k];
         CREATE_TRY(dev_alloc(ctx, &L.d_tab, tab.size()));
         CREATE_CUDA(cudaMemcpy(L.d_tab, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice));
         L.lc.tab = L.d_tab;

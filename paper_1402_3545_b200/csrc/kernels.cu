@@ -521,31 +521,47 @@ __global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double
     fc[(J * Cc.nz + k) * Cc.nx + I] = 0.25 * s;
 }
 
-// u_f += P u_c: one thread per coarse cell (I, J, k) updates its 2 x 2 fine children
-// with 16-byte loads/stores; the 3 x 3 coarse neighbourhood comes through L1.
-__global__ void __launch_bounds__(256) k_prolong_add(const LevelConst Cc, const LevelConst F, const HaloField uc,
+// u_f += P u_c: a thread owns coarse column (I, J) of a 32 x 4 block and walks k,
+// updating the 2 x 2 fine children with 16-byte loads/stores.  The 3 x 3 coarse
+// neighbourhood is read through L1 (neighbouring threads share it); no integer
+// division in the loop.
+__global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const LevelConst F, const HaloField uc,
                                                      double* __restrict__ uf)
 {
     const int64_t nxc = Cc.nx, nyc = Cc.ny;
     const int nz = Cc.nz;
-    const int64_t n = nxc * nyc * (int64_t)nz;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t I = q % nxc;
-        const int64_t Jk = q / nxc;
-        const int k = (int)(Jk % nz);
-        const int64_t J = Jk / nz;
+    const int64_t I = blockIdx.x * 32 + threadIdx.x;
+    const int64_t J = blockIdx.y * 4 + threadIdx.y;
+    if (I >= nxc || J >= nyc) return;
+    // coarse rows J-1, J, J+1 (halo slabs / zero ghosts outside)
+    const int64_t cplane = nxc * nz;
+    const double* rows[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const int64_t JJ = J - 1 + d;
+        rows[d] = (JJ < 0) ? uc.lo : (JJ >= nyc ? uc.hi : uc.base + JJ * cplane);
+    }
+    const bool hasW = I > 0, hasE = I < nxc - 1;
+    const int64_t fplane = F.nx * (int64_t)F.nz;
+    double* f0 = uf + (2 * J) * fplane + 2 * I;     // fine row 2J, level 0
+    double* f1 = f0 + fplane;                        // fine row 2J+1
+#pragma unroll 4
+    for (int k = 0; k < nz; ++k) {
         double cc[3][3];
 #pragma unroll
-        for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-            for (int dx = -1; dx <= 1; ++dx) cc[dy + 1][dx + 1] = ld_halo(uc, I + dx, J + dy, k, nxc, nyc, nz);
+        for (int d = 0; d < 3; ++d) {
+            const double* r = rows[d] ? rows[d] + (int64_t)k * nxc + I : nullptr;
+            cc[d][1] = r ? __ldg(r) : 0.0;
+            cc[d][0] = (r && hasW) ? __ldg(r - 1) : 0.0;
+            cc[d][2] = (r && hasE) ? __ldg(r + 1) : 0.0;
+        }
 #pragma unroll
         for (int b = 0; b < 2; ++b) {          // fine row 2J + b: sy = -1 (b = 0), +1 (b = 1)
             const int sy = b ? 2 : 0;
             // fine columns 2I (sx = -1) and 2I+1 (sx = +1)
             const double v0 = 9.0 * cc[1][1] + 3.0 * cc[1][0] + 3.0 * cc[sy][1] + 1.0 * cc[sy][0];
             const double v1 = 9.0 * cc[1][1] + 3.0 * cc[1][2] + 3.0 * cc[sy][1] + 1.0 * cc[sy][2];
-            double2* p = reinterpret_cast<double2*>(uf + ((2 * J + b) * F.nz + k) * F.nx + 2 * I);
+            double2* p = reinterpret_cast<double2*>((b ? f1 : f0) + (int64_t)k * F.nx);
             double2 w = *p;
             w.x = w.x + v0 / 16.0;
             w.y = w.y + v1 / 16.0;
@@ -621,10 +637,9 @@ cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const Le
 cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, const LevelConst& fine,
                                HaloField uc, double* uf)
 {
-    const int64_t n = coarse.nx * coarse.ny * (int64_t)coarse.nz;
-    if (n <= 0) return cudaSuccess;
-    const int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)ln.num_sms * 8);
-    k_prolong_add<<<(unsigned)grid, 256, 0, ln.stream>>>(coarse, fine, uc, uf);
+    if (coarse.nx <= 0 || coarse.ny <= 0) return cudaSuccess;
+    dim3 grid((unsigned)((coarse.nx + 31) / 32), (unsigned)((coarse.ny + 3) / 4)), block(32, 4);
+    k_prolong_add<<<grid, block, 0, ln.stream>>>(coarse, fine, uc, uf);
     if (ln.launch_counter) ++*ln.launch_counter;
     return cudaGetLastError();
 }

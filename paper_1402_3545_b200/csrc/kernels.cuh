@@ -101,6 +101,12 @@ int line_tile_rows(int mode, int nz);
 int line_max_nz();
 
 // k-split line kernel (kernels_ksplit.cu) for MODE_SMOOTH / MODE_PREC.
+// Per-level tables passed in the kernel parameter space: diag, 1/m, b = gamma/m,
+// a = gamma/m_{k-1}, forward propagator P, backward propagator Q.
+constexpr int kKsplitMaxNZ = 128;
+struct KTables {
+    double t[6][kKsplitMaxNZ];
+};
 struct KsplitBoxes {
     int ty;      // tile rows
     int kb;      // levels per chunk (f box depth)
@@ -109,7 +115,7 @@ struct KsplitBoxes {
 };
 bool ksplit_supported(int mode, int nz, int nx);
 KsplitBoxes ksplit_boxes(int mode, int cfg);
-cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const LineArgs& a);
+cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const LineArgs& a, const KTables& T);
 
 // f_c = 1/4 sum of the 2x2 fine children of (f - A u)  (Residual + restriction, fused)
 cudaError_t launch_residual_restrict(const Launcher& ln, const LevelConst& fine,

@@ -36,7 +36,6 @@ using namespace dev;
 constexpr int TX = kTileX;
 constexpr int SL = kSegK;      // levels per segment
 constexpr int HX = TX + 4;     // halo'd row width (even start column for TMA)
-constexpr int NS2 = 2;         // pipeline stages
 
 __host__ __device__ constexpr int r16(int n) { return (n + 15) & ~15; }
 
@@ -78,8 +77,9 @@ __device__ __forceinline__ void tma_step(double* st, const LineArgs& a, int i0, 
     }
 }
 
-template <int MODE, int TY, int NSEG, int KB>
-__global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_constant__ LineArgs a)
+template <int MODE, int TY, int NSEG, int KB, int NS2>
+__global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_constant__ LineArgs a,
+                                                             const __grid_constant__ KTables T)
 {
     using G = KGeom<MODE, TY, KB>;
     constexpr int NT = 32 * TY * NSEG;
@@ -93,20 +93,19 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
                                              ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
     const int nz = a.L.nz;
     const int64_t nx = a.L.nx, ny = a.L.ny;
-    double* tab = smem;                                 // diag, invm, gim, afw, Pfw, Qbw (nz each)
-    double* stage = smem + r16(6 * nz);
+    double* stage = smem;
     double* bnd = stage + NS2 * STG;                    // [2][TY][NSEG][32]
     double* scratch = bnd + 2 * TY * NSEG * 32;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int s = warp % NSEG, ty = warp / NSEG;
-    for (int q = tid; q < 6 * nz; q += NT) tab[q] = a.L.tab[q];
-    const double* diag = tab;
-    const double* invm = tab + nz;
-    const double* gim = tab + 2 * nz;
-    const double* afw = tab + 3 * nz;
-    const double* Pfw = tab + 4 * nz;
-    const double* Qbw = tab + 5 * nz;
+    // per-level tables in the kernel's parameter space: warp-uniform constant-bank reads
+    const double* diag = T.t[0];
+    const double* invm = T.t[1];
+    const double* gim = T.t[2];
+    const double* afw = T.t[3];
+    const double* Pfw = T.t[4];
+    const double* Qbw = T.t[5];
     const double c = a.L.c, gamma = a.L.gamma, rho = a.rho, scale = a.scale;
     if (tid == 0) {
         for (int q = 0; q < NS2; ++q) mbar_init(&full_bar[q], 1);
@@ -230,18 +229,18 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     if (NORM && a.red.result != nullptr) grid_reduce<1>(a.red, acc, scratch);
 }
 
-template <int MODE, int TY, int NSEG, int KB>
-size_t ksmem(int nz)
+template <int MODE, int TY, int NSEG, int KB, int NS2>
+size_t ksmem()
 {
     using G = KGeom<MODE, TY, KB>;
-    return (size_t)(r16(6 * nz) + NS2 * NSEG * G::SEGST + 2 * TY * NSEG * 32 + 64 + 16) * sizeof(double);
+    return (size_t)(NS2 * NSEG * G::SEGST + 2 * TY * NSEG * 32 + 64 + 16) * sizeof(double);
 }
 
-template <int MODE, int TY, int NSEG, int KB>
-cudaError_t launch_k(const Launcher& ln, const LineArgs& a)
+template <int MODE, int TY, int NSEG, int KB, int NS2>
+cudaError_t launch_k(const Launcher& ln, const LineArgs& a, const KTables& T)
 {
-    auto kern = k_linek<MODE, TY, NSEG, KB>;
-    const size_t smem = ksmem<MODE, TY, NSEG, KB>(a.L.nz);
+    auto kern = k_linek<MODE, TY, NSEG, KB, NS2>;
+    const size_t smem = ksmem<MODE, TY, NSEG, KB, NS2>();
     static size_t limit = 0;
     if (!limit) {
         limit = dyn_smem_limit(kern);
@@ -256,43 +255,54 @@ cudaError_t launch_k(const Launcher& ln, const LineArgs& a)
     const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * ((a.L.ny + TY - 1) / TY);
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)ln.num_sms * per_sm);
     if (grid <= 0) return cudaSuccess;
-    kern<<<(unsigned)grid, 32 * TY * NSEG, smem, ln.stream>>>(a);
+    kern<<<(unsigned)grid, 32 * TY * NSEG, smem, ln.stream>>>(a, T);
     if (ln.launch_counter) ++*ln.launch_counter;
     return cudaGetLastError();
 }
 
-template <int MODE, int TY, int KB>
-cudaError_t launch_k_nseg(const Launcher& ln, const LineArgs& a)
+template <int MODE, int TY, int KB, int NS2>
+cudaError_t launch_k_nseg(const Launcher& ln, const LineArgs& a, const KTables& T)
 {
     switch (a.L.nz / SL) {
-    case 1: return launch_k<MODE, TY, 1, KB>(ln, a);
-    case 2: return launch_k<MODE, TY, 2, KB>(ln, a);
-    case 4: return launch_k<MODE, TY, 4, KB>(ln, a);
+    case 1: return launch_k<MODE, TY, 1, KB, NS2>(ln, a, T);
+    case 2: return launch_k<MODE, TY, 2, KB, NS2>(ln, a, T);
+    case 4: return launch_k<MODE, TY, 4, KB, NS2>(ln, a, T);
     default: return cudaErrorInvalidValue;
     }
 }
+
+// configurations: 0 = 2 rows x 8 levels, 2 stages; 1 = 4 rows x 4 levels, 3 stages;
+// 2 = 2 rows x 4 levels, 2 stages (two CTAs per SM)
+struct Cfg { int ty, kb; };
+constexpr Cfg kCfg[3] = {{2, 8}, {4, 4}, {2, 4}};
 
 }  // namespace
 
 bool ksplit_supported(int mode, int nz, int nx)
 {
-    return (mode == MODE_SMOOTH || mode == MODE_PREC) && nz % SL == 0 &&
+    return (mode == MODE_SMOOTH || mode == MODE_PREC) && nz % SL == 0 && nz <= kKsplitMaxNZ &&
            (nz / SL == 1 || nz / SL == 2 || nz / SL == 4) && nx % 2 == 0;
 }
 
 KsplitBoxes ksplit_boxes(int mode, int cfg)
 {
-    const int TY = (cfg == 1) ? 4 : 2, KB = (cfg == 1) ? 4 : 8;
     (void)mode;
-    return KsplitBoxes{TY, KB, HX, KB + 2};
+    const Cfg c = kCfg[cfg < 0 || cfg > 2 ? 0 : cfg];
+    return KsplitBoxes{c.ty, c.kb, HX, c.kb + 2};
 }
 
-cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const LineArgs& a)
+cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const LineArgs& a, const KTables& T)
 {
-    if (mode == MODE_SMOOTH)
-        return cfg == 1 ? launch_k_nseg<MODE_SMOOTH, 4, 4>(ln, a) : launch_k_nseg<MODE_SMOOTH, 2, 8>(ln, a);
-    if (mode == MODE_PREC)
-        return cfg == 1 ? launch_k_nseg<MODE_PREC, 4, 4>(ln, a) : launch_k_nseg<MODE_PREC, 2, 8>(ln, a);
+    if (mode == MODE_SMOOTH) {
+        if (cfg == 1) return launch_k_nseg<MODE_SMOOTH, 4, 4, 3>(ln, a, T);
+        if (cfg == 2) return launch_k_nseg<MODE_SMOOTH, 2, 4, 2>(ln, a, T);
+        return launch_k_nseg<MODE_SMOOTH, 2, 8, 2>(ln, a, T);
+    }
+    if (mode == MODE_PREC) {   // no u box: deeper pipelines are cheap
+        if (cfg == 1) return launch_k_nseg<MODE_PREC, 4, 4, 6>(ln, a, T);
+        if (cfg == 2) return launch_k_nseg<MODE_PREC, 2, 4, 6>(ln, a, T);
+        return launch_k_nseg<MODE_PREC, 2, 8, 4>(ln, a, T);
+    }
     return cudaErrorInvalidValue;
 }
 
