@@ -526,12 +526,13 @@ __global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double
 // neighbourhood is read through L1 (neighbouring threads share it); no integer
 // division in the loop.
 __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const LevelConst F, const HaloField uc,
-                                                     double* __restrict__ uf)
+                                                     double* __restrict__ uf, int lpt)
 {
     const int64_t nxc = Cc.nx, nyc = Cc.ny;
     const int nz = Cc.nz;
     const int64_t I = blockIdx.x * 32 + threadIdx.x;
     const int64_t J = blockIdx.y * 4 + threadIdx.y;
+    const int kbeg = blockIdx.z * lpt, kend = min(nz, kbeg + lpt);   // levels of this thread
     if (I >= nxc || J >= nyc) return;
     // coarse rows J-1, J, J+1 (halo slabs / zero ghosts outside)
     const int64_t cplane = nxc * nz;
@@ -546,7 +547,7 @@ __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const 
     double* f0 = uf + (2 * J) * fplane + 2 * I;     // fine row 2J, level 0
     double* f1 = f0 + fplane;                        // fine row 2J+1
 #pragma unroll 4
-    for (int k = 0; k < nz; ++k) {
+    for (int k = kbeg; k < kend; ++k) {
         double cc[3][3];
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
@@ -638,8 +639,14 @@ cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, con
                                HaloField uc, double* uf)
 {
     if (coarse.nx <= 0 || coarse.ny <= 0) return cudaSuccess;
-    dim3 grid((unsigned)((coarse.nx + 31) / 32), (unsigned)((coarse.ny + 3) / 4)), block(32, 4);
-    k_prolong_add<<<grid, block, 0, ln.stream>>>(coarse, fine, uc, uf);
+    // levels per thread: enough threads to fill the GPU on the coarse levels
+    const int64_t cols = coarse.nx * coarse.ny;
+    const int64_t want = (int64_t)ln.num_sms * 2048;
+    int lpt = coarse.nz;
+    while (lpt > 4 && cols * ((coarse.nz + lpt - 1) / lpt) < want) lpt = (lpt + 1) / 2;
+    dim3 grid((unsigned)((coarse.nx + 31) / 32), (unsigned)((coarse.ny + 3) / 4), (unsigned)((coarse.nz + lpt - 1) / lpt)),
+        block(32, 4);
+    k_prolong_add<<<grid, block, 0, ln.stream>>>(coarse, fine, uc, uf, lpt);
     if (ln.launch_counter) ++*ln.launch_counter;
     return cudaGetLastError();
 }

@@ -93,19 +93,21 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
                                              ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
     const int nz = a.L.nz;
     const int64_t nx = a.L.nx, ny = a.L.ny;
-    double* stage = smem;
+    double* tab = smem;                                 // diag, invm, gim, afw, Pfw, Qbw (nz each)
+    double* stage = smem + r16(6 * nz);
     double* bnd = stage + NS2 * STG;                    // [2][TY][NSEG][32]
     double* scratch = bnd + 2 * TY * NSEG * 32;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int s = warp % NSEG, ty = warp / NSEG;
-    // per-level tables in the kernel's parameter space: warp-uniform constant-bank reads
-    const double* diag = T.t[0];
-    const double* invm = T.t[1];
-    const double* gim = T.t[2];
-    const double* afw = T.t[3];
-    const double* Pfw = T.t[4];
-    const double* Qbw = T.t[5];
+    // per-level tables, staged in shared memory (warp-uniform broadcast reads)
+    for (int q = tid; q < 6 * nz; q += NT) tab[q] = T.t[q / nz][q % nz];
+    const double* diag = tab;
+    const double* invm = tab + nz;
+    const double* gim = tab + 2 * nz;
+    const double* afw = tab + 3 * nz;
+    const double* Pfw = tab + 4 * nz;
+    const double* Qbw = tab + 5 * nz;
     const double c = a.L.c, gamma = a.L.gamma, rho = a.rho, scale = a.scale;
     if (tid == 0) {
         for (int q = 0; q < NS2; ++q) mbar_init(&full_bar[q], 1);
@@ -230,17 +232,17 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
 }
 
 template <int MODE, int TY, int NSEG, int KB, int NS2>
-size_t ksmem()
+size_t ksmem(int nz)
 {
     using G = KGeom<MODE, TY, KB>;
-    return (size_t)(NS2 * NSEG * G::SEGST + 2 * TY * NSEG * 32 + 64 + 16) * sizeof(double);
+    return (size_t)(r16(6 * nz) + NS2 * NSEG * G::SEGST + 2 * TY * NSEG * 32 + 64 + 16) * sizeof(double);
 }
 
 template <int MODE, int TY, int NSEG, int KB, int NS2>
 cudaError_t launch_k(const Launcher& ln, const LineArgs& a, const KTables& T)
 {
     auto kern = k_linek<MODE, TY, NSEG, KB, NS2>;
-    const size_t smem = ksmem<MODE, TY, NSEG, KB, NS2>();
+    const size_t smem = ksmem<MODE, TY, NSEG, KB, NS2>(a.L.nz);
     static size_t limit = 0;
     if (!limit) {
         limit = dyn_smem_limit(kern);
