@@ -76,7 +76,8 @@ struct tpmg_ctx {
     // TMA descriptors, cached by (address, nx, nz, ny, box x, box rows)
     bool use_tma = true;
     bool sync_debug = false;   // TPMG_SYNC_DEBUG=1: synchronise after every line kernel
-    int ksplit_cfg = 0;        // k-split kernel config (TPMG_KSPLIT: "0" off, "1" = 2x8, "2" = 4x4); -1 = off
+    int ksplit_cfg = 1;        // k-split config (TPMG_KSPLIT: "0" off, "1" 2x8/2 stages, "2" 4x4/3 stages
+                               // (default), "3" 2x4/2 stages); -1 = off
     std::map<std::tuple<uintptr_t, int64_t, int, int64_t, int, int>, CUtensorMap> tmaps;
     int64_t prof_launches[TPMG_K_COUNT] = {};
     double prof_ms[TPMG_K_COUNT] = {}, prof_cells[TPMG_K_COUNT] = {};
@@ -906,7 +907,7 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         const char* ld = std::getenv("TPMG_LOADER");   // "cpasync" selects the cp.async loader
         ctx->use_tma = !(ld && std::strcmp(ld, "cpasync") == 0);
         const char* ks = std::getenv("TPMG_KSPLIT");
-        ctx->ksplit_cfg = (ks && ks[0] == '0') ? -1 : (ks && ks[0] == '2') ? 1 : (ks && ks[0] == '3') ? 2 : 0;
+        ctx->ksplit_cfg = !ks ? 1 : ks[0] == '0' ? -1 : ks[0] == '1' ? 0 : ks[0] == '3' ? 2 : 1;
         const char* sd = std::getenv("TPMG_SYNC_DEBUG");
         ctx->sync_debug = sd && sd[0] == '1';
     }

@@ -16,7 +16,7 @@ def lib():
 def ctx_for(p: O.Params, device: int = 0, loader: str | None = None):
     """loader: None (library defaults: TMA loads, k-split Thomas where supported),
     "tma" (same), "cpasync" (cp.async loads, one-thread-per-column kernel), "tma-noks"
-    (TMA, k-split off), "tma-ks2" (TMA, k-split 4x4 config).  Read at tpmg_create."""
+    (TMA, k-split off), "tma-ks2" (TMA, k-split 2x8 config).  Read at tpmg_create."""
     import os
     T = lib()
     for var in ("TPMG_LOADER", "TPMG_KSPLIT"):
@@ -26,7 +26,7 @@ def ctx_for(p: O.Params, device: int = 0, loader: str | None = None):
     elif loader == "tma-noks":
         os.environ["TPMG_KSPLIT"] = "0"
     elif loader == "tma-ks2":
-        os.environ["TPMG_KSPLIT"] = "2"
+        os.environ["TPMG_KSPLIT"] = "1"   # the non-default k-split config (2 x 8 levels)
     params = T.make_params(p.nx, p.ny, nz=p.nz, nu_cfl=p.nu_cfl, H=p.H, lam=p.lam, levels=p.L,
                            pre=p.pre, post=p.post, coarse_sweeps=p.coarse_sweeps, rho=p.rho)
     return T.Context(params, device=device)
