@@ -59,6 +59,12 @@ struct tpmg_ctx {
     double* d_scal = nullptr;   // CG per-iteration scalars / norms
     int scal_cap = 0;
     double* h_pinned = nullptr; // pinned host scalars
+    // solver run-ahead: device flags per iteration, their pinned host copies, events
+    int* d_flags = nullptr;
+    int* h_flags = nullptr;
+    int flags_cap = 0;
+    const int* skip = nullptr;  // predicate put into every launch while set
+    cudaEvent_t ev_it[8] = {};
     // work vectors (lazily allocated)
     bool mg_ready = false, cg_ready = false;
     double* scratch = nullptr;   // fine-size scratch (single-op ping-pong)
@@ -215,6 +221,7 @@ LineArgs line_args(tpmg_ctx* ctx, int level)
     a.scale = 1.0;
     a.ratio = DevRatio{nullptr, -1, -1};
     a.red = ReduceSlot{ctx->d_partials, ctx->d_ticket, nullptr};
+    a.skip = ctx->skip;
     return a;
 }
 
@@ -505,7 +512,7 @@ tpmg_status vcycle_rec(tpmg_ctx* ctx, int l, bool skip_pre = false)
     TRY(halo(ctx, l - 1, Cc.u[Cc.cur], &uc));
     {
         ProfScope ps(ctx, TPMG_K_PROLONG_ADD, level_cells(F.lc));
-        CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc, F.u[F.cur]));
+        CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc, F.u[F.cur], ctx->skip));
     }
     for (int s = 0; s < p.post; ++s) TRY(mg_smooth(ctx, l));
     return TPMG_OK;
@@ -524,8 +531,7 @@ void bind_fine(tpmg_ctx* ctx, double* u, const double* f)
 tpmg_status unbind_fine(tpmg_ctx* ctx)
 {
     LevelData& F = ctx->lv[ctx->L];
-    if (F.cur != 0)
-        CUDA_TRY(ctx, cudaMemcpyAsync(F.u[0], F.u[1], sizeof(double) * F.n(), cudaMemcpyDeviceToDevice, ctx->stream));
+    if (F.cur != 0) CUDA_TRY(ctx, launch_copy(launcher(ctx), F.u[0], F.u[1], (int64_t)F.n(), ctx->skip));
     F.cur = 0;
     return TPMG_OK;
 }
@@ -562,6 +568,44 @@ tpmg_status ensure_scal(tpmg_ctx* ctx, int n)
     return TPMG_OK;
 }
 
+tpmg_status ensure_flags(tpmg_ctx* ctx, int n)
+{
+    if (n > ctx->flags_cap) {
+        if (ctx->d_flags) cudaFree(ctx->d_flags);
+        if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+        ctx->d_flags = nullptr;
+        ctx->h_flags = nullptr;
+        CUDA_TRY(ctx, cudaMalloc((void**)&ctx->d_flags, sizeof(int) * n));
+        CUDA_TRY(ctx, cudaMallocHost((void**)&ctx->h_flags, sizeof(int) * n));
+        ctx->flags_cap = n;
+    }
+    for (auto& e : ctx->ev_it)
+        if (!e) CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_flags, 0, sizeof(int) * n, ctx->stream));
+    return TPMG_OK;
+}
+
+// Copy flag[m] to the host ring and record its event.
+tpmg_status post_flag(tpmg_ctx* ctx, int m)
+{
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags + m, ctx->d_flags + m, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_it[m & 7], ctx->stream));
+    return TPMG_OK;
+}
+
+tpmg_status wait_flag(tpmg_ctx* ctx, int m, int* code)
+{
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev_it[m & 7]));
+    *code = ctx->h_flags[m];
+    return TPMG_OK;
+}
+
+// Clears the run-ahead predicate on every exit path of a solve.
+struct SkipGuard {
+    tpmg_ctx* ctx;
+    ~SkipGuard() { ctx->skip = nullptr; }
+};
+
 void result_init(tpmg_result* res)
 {
     if (!res) return;
@@ -581,7 +625,7 @@ tpmg_status solve_mg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
                           tpmg_result* res)
 {
     TRY(mg_alloc(ctx));
-    TRY(ensure_scal(ctx, 8));
+    TRY(ensure_scal(ctx, 8 + max_iter + 2));
     const LevelData& F = ctx->lv[ctx->L];
     result_init(res);
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
@@ -612,33 +656,50 @@ tpmg_status solve_mg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
             if (rel < eps) conv = true;
         }
     } else if (!conv && max_iter > 0) {
-        // The first fine pre-smooth of cycle it+1 also returns ||f - A u_it||^2 (its input's
-        // residual): the convergence test of cycle it costs no extra pass over u and f.  The
-        // pre-smooth writes the work buffer, so u_it is still in u when the test passes; the
-        // last (unused) pre-smooth is the price of the fusion.
-        LevelData& F = ctx->lv[ctx->L];
+        // The first fine pre-smooth of cycle n+1 also returns ||f - A u_n||^2 (its input's
+        // residual): the convergence test of cycle n costs no extra pass over u and f.  The
+        // pre-smooth writes the work buffer, so u_n is still in u when the test passes.
+        // Run-ahead: the test is evaluated on the device (k_mg_check -> flags[n]); every
+        // later kernel is predicated on it, so the host enqueues the next cycle before it
+        // reads flags[n] and the GPU never waits for the host.
+        const int LAG = 1;
+        SkipGuard guard{ctx};
+        TRY(ensure_flags(ctx, max_iter + 2));
+        double* norms = ctx->d_scal + 8;          // norms[n] = ||f - A u_n||^2
         bind_fine(ctx, u, f);
-        TRY(vcycle_rec(ctx, ctx->L));     // cycle 1 (u_0 = 0)
+        ctx->skip = nullptr;
+        TRY(vcycle_rec(ctx, ctx->L));             // cycle 1 (u_0 = 0)
         TRY(unbind_fine(ctx));
-        it = 1;
-        while (true) {
+        int checked = 0, stop_at = -1, code = 0;
+        for (int n = 1; n <= max_iter && stop_at < 0; ++n) {
+            ctx->skip = ctx->d_flags + (n - 1);
             bind_fine(ctx, u, f);
-            TRY(mg_smooth(ctx, ctx->L, ctx->d_scal + 1));
-            TRY(allreduce(ctx, ctx->d_scal + 1, 1));
-            TRY(fetch(ctx, ctx->d_scal + 1, 1));
-            const double rn = std::sqrt(ctx->h_pinned[0]);
-            record_hist(res, it, rn);
-            rel = rn / r0;
-            if (!(rn == rn)) return fail(ctx, TPMG_E_BREAKDOWN, "NaN residual after V-cycle %d", it);
-            if (rel < eps) conv = true;
-            if (conv || it >= max_iter) {
-                F.cur = 0;   // discard the speculative pre-smooth: u holds u_it
-                break;
+            TRY(mg_smooth(ctx, ctx->L, norms + n));
+            TRY(allreduce(ctx, norms + n, 1));
+            CUDA_TRY(ctx, launch_mg_check(launcher(ctx), norms + n, ctx->d_scal, n, eps, max_iter, ctx->d_flags));
+            TRY(post_flag(ctx, n));
+            ctx->skip = ctx->d_flags + n;
+            if (n < max_iter) {                   // cycle n+1 (skipped on the device once flags[n] != 0)
+                TRY(vcycle_rec(ctx, ctx->L, /*skip_pre=*/true));
+                TRY(unbind_fine(ctx));
             }
-            TRY(vcycle_rec(ctx, ctx->L, /*skip_pre=*/true));
-            TRY(unbind_fine(ctx));
-            ++it;
+            ctx->lv[ctx->L].cur = 0;
+            while (checked < n - LAG + 1 && stop_at < 0) {
+                ++checked;
+                TRY(wait_flag(ctx, checked, &code));
+                if (code) stop_at = checked;
+            }
         }
+        ctx->skip = nullptr;
+        it = stop_at > 0 ? stop_at : max_iter;
+        // history: one read of the norms
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        std::vector<double> nh(it + 1);
+        CUDA_TRY(ctx, cudaMemcpy(nh.data(), norms, sizeof(double) * (it + 1), cudaMemcpyDeviceToHost));
+        for (int n = 1; n <= it; ++n) record_hist(res, n, std::sqrt(nh[n]));
+        rel = std::sqrt(nh[it]) / r0;
+        if (code == 3) return fail(ctx, TPMG_E_BREAKDOWN, "NaN residual after V-cycle %d", it);
+        conv = (code == 1);
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
     CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
@@ -719,14 +780,27 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
     double rel = conv ? 0.0 : 1.0;
     if (!conv && !(ctx->h_pinned[1] > 0))
         return fail(ctx, TPMG_E_BREAKDOWN, "CG setup: <r, M^-1 r> = %g", ctx->h_pinned[1]);
-    while (!conv && it < max_iter) {
-        const int m = it + 1;
-        // halo of z (and p_old) for the direction kernel
+    // Run-ahead: iteration m's convergence / breakdown test runs on the device
+    // (k_cg_check -> flags[m]); iteration m+1's kernels are predicated on flags[m], so the
+    // host enqueues LAG iterations ahead and the GPU never idles waiting for the host.
+    const int LAG = 2;
+    SkipGuard guard{ctx};
+    TRY(ensure_flags(ctx, max_iter + 2));
+    int checked = 0, stop_at = -1, code = 0, enq = 0;
+    for (int m = 1; !conv && m <= max_iter && stop_at < 0; ++m) {
+        ctx->skip = ctx->d_flags + (m - 1);
+        // halo of z; the halo of p_old is local: p_halo <- z_halo + beta p_halo (same fma
+        // as the neighbour's own rows), so only z crosses NVLink
         HaloField hz{ctx->cg_z, nullptr, nullptr}, hp{ctx->cg_p[cur], nullptr, nullptr};
+        const DevRatio beta = (m == 1) ? DevRatio{ctx->d_scal, -1, -1}
+                                       : DevRatio{ctx->d_scal, S_ZETA(m - 1), S_ZETA(m - 2)};
         if (ctx->nranks > 1) {
             TRY(exchange(ctx, l, ctx->cg_z, ctx->cg_zlo, ctx->cg_zhi));
             hz = HaloField{ctx->cg_z, has_lo ? ctx->cg_zlo : nullptr, has_hi ? ctx->cg_zhi : nullptr};
             hp = HaloField{ctx->cg_p[cur], has_lo ? ctx->cg_plo[cur] : nullptr, has_hi ? ctx->cg_phi[cur] : nullptr};
+            CUDA_TRY(ctx, launch_cg_halo(launcher(ctx), has_lo ? ctx->cg_plo[1 - cur] : nullptr, hz.lo, hp.lo,
+                                         has_hi ? ctx->cg_phi[1 - cur] : nullptr, hz.hi, hp.hi, (int64_t)plane, beta,
+                                         ctx->skip));
         }
         // (Fused) direction kernel: p = z + beta p, sigma = <p, A p>
         {
@@ -734,20 +808,15 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
             a.h0 = hz;
             a.h1 = hp;
             a.out0 = ctx->cg_p[1 - cur];
-            a.ratio = (m == 1) ? DevRatio{ctx->d_scal, -1, -1}
-                               : DevRatio{ctx->d_scal, S_ZETA(m - 1), S_ZETA(m - 2)};
+            a.ratio = beta;
             a.red.result = ctx->d_scal + S_SIGMA(m);
             TRY(run_line(ctx, MODE_CGDIR, a));
             TRY(allreduce(ctx, ctx->d_scal + S_SIGMA(m), 1));
         }
         HaloField hpn{ctx->cg_p[1 - cur], nullptr, nullptr};
-        if (ctx->nranks > 1) {
-            // halo of the new direction: exchanged (the local update z_halo + beta p_halo is a
-            // round-2 optimisation)
-            TRY(exchange(ctx, l, ctx->cg_p[1 - cur], ctx->cg_plo[1 - cur], ctx->cg_phi[1 - cur]));
+        if (ctx->nranks > 1)
             hpn = HaloField{ctx->cg_p[1 - cur], has_lo ? ctx->cg_plo[1 - cur] : nullptr,
                             has_hi ? ctx->cg_phi[1 - cur] : nullptr};
-        }
         // (Fused) preconditioner kernel: r -= alpha A p, u += alpha p, z = M^-1 r, ||r||^2, <r,z>
         {
             LineArgs a = line_args(ctx, l);
@@ -762,17 +831,36 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
             TRY(run_line(ctx, MODE_CGPREC, a));
             TRY(allreduce(ctx, ctx->d_scal + S_RR(m), 2));
         }
-        TRY(fetch(ctx, ctx->d_scal + S_SIGMA(m), 3));
-        const double sigma = ctx->h_pinned[0], rr = ctx->h_pinned[1], zeta = ctx->h_pinned[2];
-        it = m;
+        CUDA_TRY(ctx, launch_cg_check(launcher(ctx), ctx->d_scal, m, eps, ctx->d_flags));
+        TRY(post_flag(ctx, m));
+        enq = m;
         cur ^= 1;
-        const double rn = std::sqrt(rr);
-        record_hist(res, it, rn);
-        rel = rn / r0;
-        if (!(sigma > 0)) return fail(ctx, TPMG_E_BREAKDOWN, "CG iteration %d: <p, A p> = %g", it, sigma);
-        if (!(rn == rn)) return fail(ctx, TPMG_E_BREAKDOWN, "CG iteration %d: NaN residual", it);
-        if (rel < eps) { conv = true; break; }
-        if (!(zeta > 0)) return fail(ctx, TPMG_E_BREAKDOWN, "CG iteration %d: <r, M^-1 r> = %g", it, zeta);
+        while (checked < m - LAG && stop_at < 0) {
+            ++checked;
+            TRY(wait_flag(ctx, checked, &code));
+            if (code) stop_at = checked;
+        }
+    }
+    while (stop_at < 0 && checked < enq) {
+        ++checked;
+        TRY(wait_flag(ctx, checked, &code));
+        if (code) stop_at = checked;
+    }
+    ctx->skip = nullptr;
+    if (!conv) {
+        it = stop_at > 0 ? stop_at : max_iter;
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        std::vector<double> sc(3 * (it + 1));
+        CUDA_TRY(ctx, cudaMemcpy(sc.data(), ctx->d_scal, sizeof(double) * sc.size(), cudaMemcpyDeviceToHost));
+        for (int m = 1; m <= it; ++m) record_hist(res, m, std::sqrt(sc[S_RR(m)]));
+        rel = std::sqrt(sc[S_RR(it)]) / r0;
+        if (code == 2) {
+            const double sg = sc[S_SIGMA(it)];
+            return fail(ctx, TPMG_E_BREAKDOWN, "CG iteration %d: %s = %g", it,
+                        !(sg > 0) ? "<p, A p>" : "<r, M^-1 r>", !(sg > 0) ? sg : sc[S_ZETA(it)]);
+        }
+        if (code == 3) return fail(ctx, TPMG_E_BREAKDOWN, "CG iteration %d: NaN residual", it);
+        conv = (code == 1);
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
     CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
@@ -820,6 +908,10 @@ void ctx_free(tpmg_ctx* ctx)
     for (int q = 0; q < 2; ++q) { cudaFree(ctx->cg_plo[q]); cudaFree(ctx->cg_phi[q]); }
     cudaFree(ctx->host_f); cudaFree(ctx->host_u);
     if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+    cudaFree(ctx->d_flags);
+    if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+    for (auto e : ctx->ev_it)
+        if (e) cudaEventDestroy(e);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     for (auto& r : ctx->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }

@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     using G = Geom<NH, NP, TY>;
     constexpr int NT = G::NT;
 
+    if (a.skip && *a.skip) return;   // solver run-ahead: this iteration is not needed
     extern __shared__ __align__(128) double smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[NS];
     // TMA destinations must be 128-byte aligned: align the dynamic window explicitly
@@ -526,8 +527,9 @@ __global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double
 // neighbourhood is read through L1 (neighbouring threads share it); no integer
 // division in the loop.
 __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const LevelConst F, const HaloField uc,
-                                                     double* __restrict__ uf, int lpt)
+                                                     double* __restrict__ uf, int lpt, const int* skip)
 {
+    if (skip && *skip) return;
     const int64_t nxc = Cc.nx, nyc = Cc.ny;
     const int nz = Cc.nz;
     const int64_t I = blockIdx.x * 32 + threadIdx.x;
@@ -636,7 +638,7 @@ cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const Le
 }
 
 cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, const LevelConst& fine,
-                               HaloField uc, double* uf)
+                               HaloField uc, double* uf, const int* skip)
 {
     if (coarse.nx <= 0 || coarse.ny <= 0) return cudaSuccess;
     // levels per thread: enough threads to fill the GPU on the coarse levels
@@ -646,7 +648,7 @@ cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, con
     while (lpt > 4 && cols * ((coarse.nz + lpt - 1) / lpt) < want) lpt = (lpt + 1) / 2;
     dim3 grid((unsigned)((coarse.nx + 31) / 32), (unsigned)((coarse.ny + 3) / 4), (unsigned)((coarse.nz + lpt - 1) / lpt)),
         block(32, 4);
-    k_prolong_add<<<grid, block, 0, ln.stream>>>(coarse, fine, uc, uf, lpt);
+    k_prolong_add<<<grid, block, 0, ln.stream>>>(coarse, fine, uc, uf, lpt, skip);
     if (ln.launch_counter) ++*ln.launch_counter;
     return cudaGetLastError();
 }

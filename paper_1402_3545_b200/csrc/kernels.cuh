@@ -85,6 +85,7 @@ struct LineArgs {
     DevRatio ratio;    // beta (CGDIR) or alpha (CGPREC)
     ReduceSlot red;    // result may be nullptr: no reduction
     int use_tma;       // 1: loads by TMA (tma must be filled), 0: cp.async
+    const int* skip;   // device flag: the kernel returns at once when *skip != 0 (solver run-ahead)
     TmaMaps tma;
 };
 
@@ -126,7 +127,22 @@ cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const Le
                             const double* r, double* fc);
 // u_f += P u_c (bilinear, zero coarse ghosts)
 cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse,
-                               const LevelConst& fine, HaloField uc, double* uf);
+                               const LevelConst& fine, HaloField uc, double* uf, const int* skip = nullptr);
+// dst = src (n doubles) unless *skip
+cudaError_t launch_copy(const Launcher& ln, double* dst, const double* src, int64_t n, const int* skip);
+
+// CG multi-GPU: p halo slabs updated locally, out = fma(beta, p, z) on each non-null slab.
+cudaError_t launch_cg_halo(const Launcher& ln, double* out_lo, const double* z_lo, const double* p_lo, double* out_hi,
+                           const double* z_hi, const double* p_hi, int64_t n, DevRatio beta, const int* skip);
+
+// Solver run-ahead: convergence / breakdown flags computed on the device.
+// Flag codes: 0 continue, 1 converged, 2 breakdown, 3 NaN, 4 iteration limit.
+// CG iteration m (m >= 1): scal[3m] = sigma, scal[3m+1] = ||r||^2, scal[3m+2] = zeta; m = 0 is the
+// setup (scal[1] = ||r_0||^2, scal[2] = zeta_0).  flags[m] = flags[m-1] if set, else the test.
+cudaError_t launch_cg_check(const Launcher& ln, const double* scal, int m, double eps, int* flags);
+// MG cycle n: norm2 = ||f - A u_n||^2, r0_2 = ||r_0||^2.
+cudaError_t launch_mg_check(const Launcher& ln, const double* norm2, const double* r0_2, int n, double eps,
+                            int max_iter, int* flags);
 // result = sum x*y over n elements (deterministic)
 cudaError_t launch_dot(const Launcher& ln, const double* x, const double* y, int64_t n,
                        ReduceSlot red);

@@ -81,6 +81,7 @@ template <int MODE, int TY, int NSEG, int KB, int NS2>
 __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_constant__ LineArgs a,
                                                              const __grid_constant__ KTables T)
 {
+    if (a.skip && *a.skip) return;   // solver run-ahead: this iteration is not needed
     using G = KGeom<MODE, TY, KB>;
     constexpr int NT = 32 * TY * NSEG;
     constexpr int NCC = SL / KB;           // chunks per segment

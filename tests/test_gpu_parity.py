@@ -170,6 +170,22 @@ def test_solve_edge_cases():
         ctx.restrict(1, u, zero)
 
 
+@pytest.mark.parametrize("solver", ["mg", "cg"])
+def test_iteration_limit(solver):
+    """max_iter stops the run-ahead loop exactly: the GPU returns the iterate after
+    max_iter iterations (device-side flags predicate the speculative ones away)."""
+    p = O.Params(nx=64, ny=64, nz=32)
+    ctx = ctx_for(p)
+    f = rhs_zc(64, 64, 32, seed=4)
+    u = ctx.empty(p.L)
+    k = 3 if solver == "mg" else 7
+    res = (ctx.solve_mg if solver == "mg" else ctx.solve_cg)(to_dev(f), u, max_iter=k)
+    ref = (O.solve_mg if solver == "mg" else O.solve_cg)(p, f, max_iter=k)
+    assert res.iterations == ref.iterations == k and not res.converged and not ref.converged
+    assert np.allclose(res.history, ref.history, rtol=1e-9)
+    assert rel_l2(to_host_zc(u), ref.u) < 1e-10
+
+
 def test_single_level_hierarchy():
     """L = 1: each 'V-cycle' is coarse_sweeps smoother steps; without coarse
     grids it converges slowly, so compare a fixed number of cycles."""
