@@ -583,7 +583,91 @@ __global__ void __launch_bounds__(256) k_dot(const double* __restrict__ x, const
     grid_reduce<1>(red, acc, scratch);
 }
 
+__global__ void __launch_bounds__(256) k_copy(double* __restrict__ dst, const double* __restrict__ src, int64_t n,
+                                              const int* skip)
+{
+    if (skip && *skip) return;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+        dst[q] = src[q];
+}
+
+__global__ void __launch_bounds__(256) k_cg_halo(double* out_lo, const double* z_lo, const double* p_lo, double* out_hi,
+                                                 const double* z_hi, const double* p_hi, int64_t n, DevRatio r,
+                                                 const int* skip)
+{
+    if (skip && *skip) return;
+    const double beta = (r.num >= 0) ? r.s[r.num] / r.s[r.den] : 0.0;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        if (out_lo) out_lo[q] = fma(beta, p_lo[q], z_lo[q]);   // same arithmetic as k_line<CGDIR>
+        if (out_hi) out_hi[q] = fma(beta, p_hi[q], z_hi[q]);
+    }
+}
+
+// Convergence test of PCG iteration m on the device: ||r_m|| / ||r_0|| < eps
+// (eqn:epsilonTolerance), breakdown when <p, A p> <= 0 or <r, M^-1 r> <= 0.
+__global__ void k_cg_check(const double* scal, int m, double eps, int* flags)
+{
+    const int prev = (m >= 1) ? flags[m - 1] : 0;
+    int code = prev;
+    if (!prev) {
+        const double rr0 = scal[1], rr = scal[3 * m + 1], zeta = scal[3 * m + 2];
+        if (m >= 1 && !(scal[3 * m] > 0.0)) code = 2;
+        else if (rr != rr) code = 3;
+        else if (rr0 == 0.0 || sqrt(rr) / sqrt(rr0) < eps) code = 1;
+        else if (!(zeta > 0.0)) code = 2;
+    }
+    flags[m] = code;
+}
+
+// Convergence test of MG cycle n: ||f - A u_n|| / ||r_0|| < eps, or the cycle limit.
+__global__ void k_mg_check(const double* norm2, const double* r0_2, int n, double eps, int max_iter, int* flags)
+{
+    const int prev = (n >= 1) ? flags[n - 1] : 0;
+    int code = prev;
+    if (!prev) {
+        const double rn2 = *norm2;
+        if (rn2 != rn2) code = 3;
+        else if (sqrt(rn2) / sqrt(*r0_2) < eps) code = 1;
+        else if (n >= max_iter) code = 4;
+    }
+    flags[n] = code;
+}
+
 }  // namespace
+
+cudaError_t launch_copy(const Launcher& ln, double* dst, const double* src, int64_t n, const int* skip)
+{
+    if (n <= 0) return cudaSuccess;
+    const int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)ln.num_sms * 8);
+    k_copy<<<(unsigned)grid, 256, 0, ln.stream>>>(dst, src, n, skip);
+    if (ln.launch_counter) ++*ln.launch_counter;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_halo(const Launcher& ln, double* out_lo, const double* z_lo, const double* p_lo, double* out_hi,
+                           const double* z_hi, const double* p_hi, int64_t n, DevRatio beta, const int* skip)
+{
+    if (!out_lo && !out_hi) return cudaSuccess;
+    const int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)ln.num_sms * 4);
+    k_cg_halo<<<(unsigned)grid, 256, 0, ln.stream>>>(out_lo, z_lo, p_lo, out_hi, z_hi, p_hi, n, beta, skip);
+    if (ln.launch_counter) ++*ln.launch_counter;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_check(const Launcher& ln, const double* scal, int m, double eps, int* flags)
+{
+    k_cg_check<<<1, 1, 0, ln.stream>>>(scal, m, eps, flags);
+    if (ln.launch_counter) ++*ln.launch_counter;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mg_check(const Launcher& ln, const double* norm2, const double* r0_2, int n, double eps,
+                            int max_iter, int* flags)
+{
+    k_mg_check<<<1, 1, 0, ln.stream>>>(norm2, r0_2, n, eps, max_iter, flags);
+    if (ln.launch_counter) ++*ln.launch_counter;
+    return cudaGetLastError();
+}
 
 int line_tile_rows(int mode, int nz)
 {

@@ -17,7 +17,7 @@
 //            chained through the segments' first values.
 //
 // This is exact algebra on the same recurrences (only the rounding order
-// differs), so the result matches the oracle's Thomas solve to rounding.  With no
+// differs), so the result matches a sequential Thomas solve to rounding.  With no
 // g' buffer in shared memory the CTA holds 2*NSEG (or 4*NSEG) warps.
 //
 // Shared memory per stage and segment: the u box (TY+2 rows, KB+2 levels: the

@@ -37,6 +37,13 @@ def test_header_symbols_exported(T):
     assert sorted(T.EXPORTED) == names
 
 
+def test_no_unresolved_library_symbols(T):
+    """Every tpmg symbol the library references is defined in it (dlopen(RTLD_NOW) would fail)."""
+    out = subprocess.run(["nm", "-D", "--undefined-only", T.LIB_PATH], capture_output=True, text=True).stdout
+    assert "tpmg" not in out, out
+    C.CDLL(T.LIB_PATH, mode=os.RTLD_NOW)
+
+
 def test_library_is_sm100a(T):
     out = subprocess.run(["cuobjdump", "--list-elf", T.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
