@@ -380,7 +380,7 @@ bool fill_tma_ksplit(tpmg_ctx* ctx, int mode, LineArgs& a)
     const int nz = a.L.nz;
     const KsplitBoxes b = ksplit_boxes(mode, ctx->ksplit_cfg);
     auto aligned = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
-    if (mode == MODE_SMOOTH) {
+    if (mode == MODE_SMOOTH || mode == MODE_RESTRICT) {
         const HaloField& hf = a.h0;
         TmaHalo& M = a.tma.h[0];
         if (!hf.base || !aligned(hf.base)) return false;

@@ -41,12 +41,16 @@ __host__ __device__ constexpr int r16(int n) { return (n + 15) & ~15; }
 
 template <int MODE, int TY, int KB>
 struct KGeom {
-    static constexpr bool HALO = (MODE == MODE_SMOOTH);
+    static constexpr bool HALO = (MODE == MODE_SMOOTH || MODE == MODE_RESTRICT);
     static constexpr int D = KB + 2;                            // u box depth (levels k0-1 .. k0+KB)
     static constexpr int UBOX = HALO ? r16((TY + 2) * D * HX) : 0;
     static constexpr int SROW = HALO ? r16(D * HX) : 0;         // one halo-slab row
     static constexpr int FBOX = TY * KB * TX;
     static constexpr int SEGST = UBOX + 2 * SROW + FBOX;        // doubles per segment per stage
+    // exchange buffer: Thomas segment chaining [2][TY][NSEG][32], or (MODE_RESTRICT)
+    // x-pair residual sums [2 (chunk parity)][TY][NSEG][KB][16]
+    template <int NSEG>
+    static constexpr int bnd() { return MODE == MODE_RESTRICT ? 2 * TY * NSEG * KB * 16 : 2 * TY * NSEG * 32; }
 };
 
 // Issue the TMA copies of step (tile origin i0, j0; chunk cc of every segment).
@@ -97,7 +101,7 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     double* tab = smem;                                 // diag, invm, gim, afw, Pfw, Qbw (nz each)
     double* stage = smem + r16(6 * nz);
     double* bnd = stage + NS2 * STG;                    // [2][TY][NSEG][32]
-    double* scratch = bnd + 2 * TY * NSEG * 32;
+    double* scratch = bnd + G::template bnd<NSEG>();
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int s = warp % NSEG, ty = warp / NSEG;
@@ -142,6 +146,7 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
 
 #pragma unroll
     for (int q = 0; q < NS2 - 1; ++q) issue();
+    int rstep = 0;   // MODE_RESTRICT: chunk counter (exchange-buffer parity)
 
     for (int tl = 0; tl < my_tiles; ++tl) {
         const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
@@ -184,6 +189,31 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
 #pragma unroll
                 for (int kk = 0; kk < KB; ++kk) { gv[kk] = scale * fb[kk * TX]; rv[kk] = 0.0; }
             }
+            if constexpr (MODE == MODE_RESTRICT) {
+                // f_c(I, J, k) = 1/4 (sum over the 2 x 2 fine children of f - A u):
+                // x-pairs by shuffle, y-pairs (rows ty, ty+1 = two warps) through shared memory
+                double* rb = bnd + (rstep++ & 1) * (TY * NSEG * KB * 16);
+#pragma unroll
+                for (int kk = 0; kk < KB; ++kk) {
+                    const double rsum = rv[kk] + __shfl_xor_sync(0xffffffffu, rv[kk], 1);
+                    if ((lane & 1) == 0) rb[((ty * NSEG + s) * KB + kk) * 16 + (lane >> 1)] = rsum;
+                }
+                __syncthreads();   // every warp is done with this slot; the x-pair sums are visible
+                if ((ty & 1) == 0) {
+                    const int64_t nxc = nx >> 1, nyc = ny >> 1;
+                    const int64_t J = (j0 + ty) >> 1;
+                    const int l = lane & 15;
+                    const int64_t I = (i0 >> 1) + l;
+#pragma unroll
+                    for (int kk = lane >> 4; kk < KB; kk += 2) {
+                        const int k = s * SL + cc * KB + kk;
+                        const double v = 0.25 * (rb[((ty * NSEG + s) * KB + kk) * 16 + l] +
+                                                 rb[(((ty + 1) * NSEG + s) * KB + kk) * 16 + l]);
+                        if (I < nxc && J < nyc) a.out0[(J * nz + k) * nxc + I] = v;
+                    }
+                }
+                continue;
+            }
             // local forward recurrence yhat_k = g_k + a_k yhat_{k-1} (yhat = 0 before the segment)
 #pragma unroll
             for (int kk = 0; kk < KB; ++kk) {
@@ -195,6 +225,7 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
             __syncthreads();   // every warp is done with this slot
         }
 
+        if constexpr (MODE == MODE_RESTRICT) continue;
         // chain the segments: Y_s = y_{k_s - 1} (true), from the segments' last yhat
         double* bF = bnd + (ty * NSEG) * 32 + lane;               // [ty][seg][lane]
         double* bB = bnd + TY * NSEG * 32 + (ty * NSEG) * 32 + lane;
@@ -236,7 +267,7 @@ template <int MODE, int TY, int NSEG, int KB, int NS2>
 size_t ksmem(int nz)
 {
     using G = KGeom<MODE, TY, KB>;
-    return (size_t)(r16(6 * nz) + NS2 * NSEG * G::SEGST + 2 * TY * NSEG * 32 + 64 + 16) * sizeof(double);
+    return (size_t)(r16(6 * nz) + NS2 * NSEG * G::SEGST + G::template bnd<NSEG>() + 64 + 16) * sizeof(double);
 }
 
 template <int MODE, int TY, int NSEG, int KB, int NS2>
@@ -283,7 +314,7 @@ constexpr Cfg kCfg[3] = {{2, 8}, {4, 4}, {2, 4}};
 
 bool ksplit_supported(int mode, int nz, int nx)
 {
-    return (mode == MODE_SMOOTH || mode == MODE_PREC) && nz % SL == 0 && nz <= kKsplitMaxNZ &&
+    return (mode == MODE_SMOOTH || mode == MODE_PREC || mode == MODE_RESTRICT) && nz % SL == 0 && nz <= kKsplitMaxNZ &&
            (nz / SL == 1 || nz / SL == 2 || nz / SL == 4) && nx % 2 == 0;
 }
 
@@ -305,6 +336,11 @@ cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const Line
         if (cfg == 1) return launch_k_nseg<MODE_PREC, 4, 4, 6>(ln, a, T);
         if (cfg == 2) return launch_k_nseg<MODE_PREC, 2, 4, 6>(ln, a, T);
         return launch_k_nseg<MODE_PREC, 2, 8, 4>(ln, a, T);
+    }
+    if (mode == MODE_RESTRICT) {   // no Thomas: the exchange buffer replaces the chaining buffer
+        if (cfg == 1) return launch_k_nseg<MODE_RESTRICT, 4, 4, 2>(ln, a, T);
+        if (cfg == 2) return launch_k_nseg<MODE_RESTRICT, 2, 4, 2>(ln, a, T);
+        return launch_k_nseg<MODE_RESTRICT, 2, 8, 2>(ln, a, T);
     }
     return cudaErrorInvalidValue;
 }

@@ -26,8 +26,12 @@ def main(rep, traffic_json=None):
     traffic = {}
     for r in data:
         name = r[c["Kernel Name"]]
-        m = re.search(r"k_line<(\d+), (\d+), (\d+)>", name)
-        label = f"k_line<{m.group(1)},{m.group(2)},{m.group(3)}> ({MODES.get(int(m.group(1)), '?')})" if m else name.split("(")[0][-30:]
+        m = re.search(r"k_line(k?)<(\d+), ([\d, ]+)>", name)
+        if m:
+            mode = int(m.group(2))
+            label = f"k_line{m.group(1)}<{m.group(2)},{m.group(3).replace(' ', '')}> ({MODES.get(mode, '?')})"
+        else:
+            label = name.split("(")[0][-30:]
         t = float(r[c["gpu__time_duration.sum"]])  # ms
         rd, wr = float(r[c["dram__bytes_read.sum"]]), float(r[c["dram__bytes_write.sum"]])  # GB
         gbs = (rd + wr) / (t * 1e-3)
@@ -37,8 +41,8 @@ def main(rep, traffic_json=None):
         print(f"| {label} | {r[c['Grid Size']]} | {t * 1e3:.1f} | {rd:.3f} | {wr:.3f} | {gbs:.0f} | "
               f"{float(r[c['sm__warps_active.avg.pct_of_peak_sustained_active']]):.1f} | {r[c['launch__registers_per_thread']]} | "
               + ", ".join(f"{n} {v:.2f}" for v, n in st) + " |")
-        if m and r[c["Grid Size"]].startswith("(148") or (m and int(m.group(1)) in (4, 6)):
-            cls = MODES.get(int(m.group(1)))
+        if m and (r[c["Grid Size"]].startswith("(148") or mode in (4, 6)):
+            cls = MODES.get(mode)
             if cls and cls not in traffic:
                 traffic[cls] = {"bytes": (rd + wr) * 1e9, "time_ms": t, "grid": r[c["Grid Size"]]}
     if traffic_json:

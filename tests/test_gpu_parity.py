@@ -42,6 +42,7 @@ SHAPES = [
     O.Params(nx=64, ny=64, nz=200, L=2, nu_cfl=10.0),   # Thomas buffer: 2 tile rows per CTA
     O.Params(nx=32, ny=16, nz=300, L=1),                # Thomas buffer: 1 tile row per CTA
     O.Params(nx=256, ny=256, nz=128, L=5),              # many tiles, paper's nz
+    O.Params(nx=80, ny=48, nz=64, L=3),                 # k-split with 2 segments, ragged x tiles
 ]
 IDS = [f"{p.nx}x{p.ny}x{p.nz}-L{p.L}" for p in SHAPES]
 
