@@ -37,6 +37,7 @@ UNIT = "unknowns/s (MG + PCG solves to 1e-5, summed)"
 BYTES_PER_CELL = {
     "apply": 16, "residual": 16, "precondition": 16, "smooth": 24, "cg_direction": 24,
     "cg_precondition": 48, "residual_restrict": 18, "restrict": 10, "prolong_add": 18, "dot": 8,
+    "smooth_prolong": 26,
 }
 PAPER_FLOPS = {"cg": 54.0, "mg": 149.4}  # tab:KernelTable totals per cell per iteration
 

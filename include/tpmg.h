@@ -234,7 +234,8 @@ typedef enum {
     TPMG_K_RESTRICT = 7,          /* f_c = R r */
     TPMG_K_PROLONG_ADD = 8,       /* u_f += P u_c */
     TPMG_K_DOT = 9,               /* global inner product */
-    TPMG_K_COUNT = 10
+    TPMG_K_SMOOTH_PROLONG = 10,   /* post-smooth of u + P u_c, prolongation fused */
+    TPMG_K_COUNT = 11
 } tpmg_kernel;
 
 /* Per-kernel-class device timing with CUDA events on the context stream.

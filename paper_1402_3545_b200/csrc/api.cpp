@@ -82,6 +82,7 @@ struct tpmg_ctx {
     // TMA descriptors, cached by (address, nx, nz, ny, box x, box rows)
     bool use_tma = true;
     bool sync_debug = false;   // TPMG_SYNC_DEBUG=1: synchronise after every line kernel
+    bool fuse_prolong = true;  // TPMG_FUSE_PROLONG=0: separate prolongation kernel
     int ksplit_cfg = 1;        // k-split config (TPMG_KSPLIT: "0" off, "1" 2x8/2 stages, "2" 4x4/3 stages
                                // (default), "3" 2x4/2 stages); -1 = off
     std::map<std::tuple<uintptr_t, int64_t, int, int64_t, int, int>, CUtensorMap> tmaps;
@@ -327,7 +328,7 @@ bool tensor_map(tpmg_ctx* ctx, const double* base, int64_t nx, int nz, int64_t n
 
 void mode_fields(int mode, int* nh, int* np)
 {
-    static const int NH[7] = {1, 1, 0, 1, 2, 1, 1}, NP[7] = {0, 1, 1, 1, 0, 2, 1};
+    static const int NH[8] = {1, 1, 0, 1, 2, 1, 1, 2}, NP[8] = {0, 1, 1, 1, 0, 2, 1, 1};
     *nh = NH[mode];
     *np = NP[mode];
 }
@@ -373,35 +374,47 @@ int level_of(tpmg_ctx* ctx, const LevelConst& lc)
     return ctx->L;
 }
 
-// TMA descriptors for the k-split kernel (boxes of ksplit_boxes()).
+// TMA descriptors for the k-split kernel (boxes of ksplit_boxes()): a halo'd field
+// gets a (TY+2)-row box, a one-row box and one-row slab boxes (strip boundaries).
+bool ksplit_halo_maps(tpmg_ctx* ctx, const HaloField& hf, int64_t nx, int nz, int64_t ny, int bx, int rows, int depth,
+                      TmaHalo& M)
+{
+    auto aligned = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+    if (!hf.base || !aligned(hf.base)) return false;
+    if (!tensor_map(ctx, hf.base, nx, nz, ny, bx, rows, &M.main, depth)) return false;
+    if (!tensor_map(ctx, hf.base, nx, nz, ny, bx, 1, &M.row, depth)) return false;
+    M.has_lo = hf.lo != nullptr;
+    M.has_hi = hf.hi != nullptr;
+    if (hf.lo && (!aligned(hf.lo) || !tensor_map(ctx, hf.lo, nx, nz, 1, bx, 1, &M.lo, depth))) return false;
+    if (hf.hi && (!aligned(hf.hi) || !tensor_map(ctx, hf.hi, nx, nz, 1, bx, 1, &M.hi, depth))) return false;
+    return true;
+}
+
 bool fill_tma_ksplit(tpmg_ctx* ctx, int mode, LineArgs& a)
 {
     const int64_t nx = a.L.nx, ny = a.L.ny;
     const int nz = a.L.nz;
     const KsplitBoxes b = ksplit_boxes(mode, ctx->ksplit_cfg);
-    auto aligned = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
-    if (mode == MODE_SMOOTH || mode == MODE_RESTRICT) {
-        const HaloField& hf = a.h0;
-        TmaHalo& M = a.tma.h[0];
-        if (!hf.base || !aligned(hf.base)) return false;
-        if (!tensor_map(ctx, hf.base, nx, nz, ny, b.hx, b.ty + 2, &M.main, b.depth)) return false;
-        M.has_lo = hf.lo != nullptr;
-        M.has_hi = hf.hi != nullptr;
-        if (hf.lo && (!aligned(hf.lo) || !tensor_map(ctx, hf.lo, nx, nz, 1, b.hx, 1, &M.lo, b.depth))) return false;
-        if (hf.hi && (!aligned(hf.hi) || !tensor_map(ctx, hf.hi, nx, nz, 1, b.hx, 1, &M.hi, b.depth))) return false;
-    }
-    if (!a.q0 || !aligned(a.q0)) return false;
+    if (mode == MODE_SMOOTH || mode == MODE_RESTRICT || mode == MODE_SMOOTH_PROLONG)
+        if (!ksplit_halo_maps(ctx, a.h0, nx, nz, ny, b.hx, b.ty + 2, b.depth, a.tma.h[0])) return false;
+    if (mode == MODE_SMOOTH_PROLONG)
+        if (!ksplit_halo_maps(ctx, a.h1, nx / 2, nz, ny / 2, b.hxc, b.ty / 2 + 2, b.depth, a.tma.h[1])) return false;
+    if (!a.q0 || ((uintptr_t)a.q0 & 15)) return false;
     if (!tensor_map(ctx, a.q0, nx, nz, ny, kTileX, b.ty, &a.tma.q[0], b.kb)) return false;
     a.use_tma = 1;
     return true;
 }
 
+bool ksplit_usable(tpmg_ctx* ctx, int mode, const LevelConst& lc)
+{
+    return ctx->use_tma && ctx->ksplit_cfg >= 0 && ksplit_supported(mode, lc.nz, (int)lc.nx);
+}
+
 tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
 {
     LineArgs a = a0;
-    if (ctx->use_tma && ctx->ksplit_cfg >= 0 && ksplit_supported(mode, a.L.nz, (int)a.L.nx) &&
-        fill_tma_ksplit(ctx, mode, a)) {
-        ProfScope ps(ctx, mode, level_cells(a.L));
+    if (ksplit_usable(ctx, mode, a.L) && fill_tma_ksplit(ctx, mode, a)) {
+        ProfScope ps(ctx, mode == MODE_SMOOTH_PROLONG ? TPMG_K_SMOOTH_PROLONG : mode, level_cells(a.L));
         const KTables& kt = ctx->lv[level_of(ctx, a.L)].ktab;
         CUDA_TRY(ctx, launch_line_ksplit(launcher(ctx), mode, ctx->ksplit_cfg, a, kt));
         if (ctx->sync_debug) {
@@ -412,6 +425,7 @@ tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
         }
         return TPMG_OK;
     }
+    if (mode == MODE_SMOOTH_PROLONG) return fail(ctx, TPMG_E_PARAM, "fused prolongation-smooth needs the k-split kernel");
     a = a0;
     fill_tma(ctx, mode, a);
     ProfScope ps(ctx, mode == MODE_RESTRICT ? TPMG_K_RESIDUAL_RESTRICT : mode, level_cells(a.L));  // modes 0..5 = TPMG_K_0..5
@@ -510,11 +524,24 @@ tpmg_status vcycle_rec(tpmg_ctx* ctx, int l, bool skip_pre = false)
     LevelData& F = ctx->lv[l];
     HaloField uc;
     TRY(halo(ctx, l - 1, Cc.u[Cc.cur], &uc));
-    {
+    int s0 = 0;
+    if (p.post >= 1 && ctx->fuse_prolong && ksplit_usable(ctx, MODE_SMOOTH_PROLONG, F.lc)) {
+        // Prolongate fused with the first post-smooth: u' = S(u + P u_c) without storing
+        // u + P u_c.  The halo of u is the one exchanged for the restriction (u has not
+        // changed since), the coarse halo was just exchanged.
+        LineArgs a = line_args(ctx, l);
+        a.h0 = halo_of(ctx, l, F.u[F.cur]);
+        a.h1 = uc;
+        a.q0 = F.f;
+        a.out0 = F.u[1 - F.cur];
+        TRY(run_line(ctx, MODE_SMOOTH_PROLONG, a));
+        F.cur ^= 1;
+        s0 = 1;
+    } else {
         ProfScope ps(ctx, TPMG_K_PROLONG_ADD, level_cells(F.lc));
         CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc, F.u[F.cur], ctx->skip));
     }
-    for (int s = 0; s < p.post; ++s) TRY(mg_smooth(ctx, l));
+    for (int s = s0; s < p.post; ++s) TRY(mg_smooth(ctx, l));
     return TPMG_OK;
 }
 
@@ -1000,6 +1027,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->use_tma = !(ld && std::strcmp(ld, "cpasync") == 0);
         const char* ks = std::getenv("TPMG_KSPLIT");
         ctx->ksplit_cfg = !ks ? 1 : ks[0] == '0' ? -1 : ks[0] == '1' ? 0 : ks[0] == '3' ? 2 : 1;
+        const char* fp = std::getenv("TPMG_FUSE_PROLONG");
+        ctx->fuse_prolong = !(fp && fp[0] == '0');
         const char* sd = std::getenv("TPMG_SYNC_DEBUG");
         ctx->sync_debug = sd && sd[0] == '1';
     }

@@ -52,6 +52,8 @@ enum LineMode : int {
     MODE_CGPREC = 5,  // r -= alpha A p; u += alpha p; z = M^-1 r;
                       // sums ||r||^2, <r, z>                         (halo: p; plain: r, u)
     MODE_RESTRICT = 6,// out0 (coarse) = R (f - A u): fine residual restricted (halo: u; plain: f)
+    MODE_SMOOTH_PROLONG = 7, // out0 = smooth(u + P u_c), sum r^2  (halo: u, coarse u_c; plain: f;
+                             // k-split kernel only)
 };
 
 // TMA descriptors of one halo'd field: the whole (TY+2)-row box, a one-row box,
@@ -113,6 +115,9 @@ struct KsplitBoxes {
     int kb;      // levels per chunk (f box depth)
     int hx;      // halo'd row width (u box x extent)
     int depth;   // u box depth (kb + 2)
+    int xo;      // u box starts at column i0 - xo
+    int hxc;     // coarse box row width (SMOOTH_PROLONG)
+    int xoc;     // coarse box starts at column i0/2 - xoc
 };
 bool ksplit_supported(int mode, int nz, int nx);
 KsplitBoxes ksplit_boxes(int mode, int cfg);

@@ -1,4 +1,5 @@
-// kernels_ksplit.cu -- the k-split line kernel (smoother and preconditioner).
+// kernels_ksplit.cu -- the k-split line kernel (smoother, preconditioner,
+// residual->restriction, and prolongation fused with the post-smooth).
 //
 // The one-thread-per-column kernel (kernels.cu) keeps a column's Thomas
 // intermediates g'_k in shared memory (8*nz bytes per column), which at nz = 128
@@ -18,12 +19,18 @@
 //
 // This is exact algebra on the same recurrences (only the rounding order
 // differs), so the result matches a sequential Thomas solve to rounding.  With no
-// g' buffer in shared memory the CTA holds 2*NSEG (or 4*NSEG) warps.
+// g' buffer in shared memory a CTA holds TY * NSEG warps.
 //
-// Shared memory per stage and segment: the u box (TY+2 rows, KB+2 levels: the
-// vertical neighbours of the chunk's first and last level come with the box, so
-// chunks are independent), two halo-slab rows (multi-GPU strip boundaries), and
-// the f box (TY rows, KB levels), all loaded by TMA into 128-byte aligned slots.
+// Shared memory per stage and segment (TMA, 128-byte aligned blocks):
+//   u box   (TY+2 rows) x (KB+2 levels) x HX columns starting at column i0-4: the
+//           vertical neighbours of the chunk's first and last level come with the
+//           box, so chunks are independent; each row block is 128-byte aligned so a
+//           tile on a strip boundary loads its halo row from the neighbour's slab
+//           with one TMA per row;
+//   f box   TY rows x KB levels x 32 columns;
+//   c box   (SMOOTH_PROLONG) the coarse u_c rows j0/2-1 .. j0/2+TY/2, columns
+//           i0/2-8 .. i0/2+23, KB+2 levels: the post-smooth's input u + P u_c is
+//           formed in shared memory (bilinear (9,3,3,1)/16, zero coarse ghosts).
 #include "kernels.cuh"
 #include "device_util.cuh"
 
@@ -35,23 +42,49 @@ using namespace dev;
 
 constexpr int TX = kTileX;
 constexpr int SL = kSegK;      // levels per segment
-constexpr int HX = TX + 4;     // halo'd row width (even start column for TMA)
+constexpr int HX = TX + 8;     // u box row width: columns i0-4 .. i0+35
+constexpr int XO = 4;          // box column of i0
+constexpr int HXC = 32;        // coarse box row width: coarse columns i0/2-8 .. i0/2+23
+constexpr int XOC = 8;         // coarse box column of i0/2
 
 __host__ __device__ constexpr int r16(int n) { return (n + 15) & ~15; }
 
 template <int MODE, int TY, int KB>
 struct KGeom {
-    static constexpr bool HALO = (MODE == MODE_SMOOTH || MODE == MODE_RESTRICT);
-    static constexpr int D = KB + 2;                            // u box depth (levels k0-1 .. k0+KB)
-    static constexpr int UBOX = HALO ? r16((TY + 2) * D * HX) : 0;
-    static constexpr int SROW = HALO ? r16(D * HX) : 0;         // one halo-slab row
+    static constexpr bool HALO = (MODE == MODE_SMOOTH || MODE == MODE_RESTRICT || MODE == MODE_SMOOTH_PROLONG);
+    static constexpr bool PROL = (MODE == MODE_SMOOTH_PROLONG);
+    static constexpr int D = KB + 2;                            // box depth (levels k0-1 .. k0+KB)
+    static constexpr int UROW = D * HX;                         // one u row block (128-byte multiple)
+    static constexpr int UBOX = HALO ? (TY + 2) * UROW : 0;
     static constexpr int FBOX = TY * KB * TX;
-    static constexpr int SEGST = UBOX + 2 * SROW + FBOX;        // doubles per segment per stage
+    static constexpr int CROWS = TY / 2 + 2;
+    static constexpr int CROW = D * HXC;
+    static constexpr int CBOX = PROL ? CROWS * CROW : 0;
+    static constexpr int SEGST = UBOX + FBOX + CBOX;            // doubles per segment per stage
+    static_assert((UROW * 8) % 128 == 0 && (CROW * 8) % 128 == 0 && (FBOX * 8) % 128 == 0, "TMA alignment");
     // exchange buffer: Thomas segment chaining [2][TY][NSEG][32], or (MODE_RESTRICT)
     // x-pair residual sums [2 (chunk parity)][TY][NSEG][KB][16]
     template <int NSEG>
     static constexpr int bnd() { return MODE == MODE_RESTRICT ? 2 * TY * NSEG * KB * 16 : 2 * TY * NSEG * 32; }
 };
+
+// Rows r0 .. r0+nrows-1 (local row index of the box's first row = jb) of a halo'd
+// field into dst: one box TMA when no row comes from a slab, else one TMA per row.
+__device__ __forceinline__ void tma_rows(double* dst, const TmaHalo& M, int rows, int rowst, int x, int k, int jb,
+                                         int nyl, uint64_t* bar)
+{
+    const bool per_row = (M.has_lo && jb < 0) || (M.has_hi && jb + rows - 1 >= nyl);
+    if (!per_row) {
+        tma_load_3d(dst, &M.main, x, k, jb, bar);
+        return;
+    }
+    for (int r = 0; r < rows; ++r) {
+        const int j = jb + r;
+        if (j == -1 && M.has_lo) tma_load_3d(dst + r * rowst, &M.lo, x, k, 0, bar);
+        else if (j == nyl && M.has_hi) tma_load_3d(dst + r * rowst, &M.hi, x, k, 0, bar);
+        else tma_load_3d(dst + r * rowst, &M.row, x, k, j, bar);   // out of range: zero fill
+    }
+}
 
 // Issue the TMA copies of step (tile origin i0, j0; chunk cc of every segment).
 template <int MODE, int TY, int KB, int NSEG>
@@ -59,25 +92,17 @@ __device__ __forceinline__ void tma_step(double* st, const LineArgs& a, int i0, 
 {
     using G = KGeom<MODE, TY, KB>;
     const int ny = (int)a.L.ny;
-    uint32_t bytes = NSEG * G::FBOX * 8;
-    bool lo = false, hi = false;
-    if constexpr (G::HALO) {
-        bytes += NSEG * (TY + 2) * G::D * HX * 8;
-        lo = a.tma.h[0].has_lo && j0 == 0;
-        hi = a.tma.h[0].has_hi && j0 + TY >= ny;
-        bytes += NSEG * ((lo ? 1 : 0) + (hi ? 1 : 0)) * G::D * HX * 8;
-    }
+    constexpr uint32_t bytes = NSEG * (G::UBOX + G::FBOX + G::CBOX) * 8;
     mbar_expect_tx(bar, bytes);
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) {
         double* seg = st + s * G::SEGST;
         const int k0 = s * SL + cc * KB;
-        if constexpr (G::HALO) {
-            tma_load_3d(seg, &a.tma.h[0].main, i0 - 2, k0 - 1, j0 - 1, bar);
-            if (lo) tma_load_3d(seg + G::UBOX, &a.tma.h[0].lo, i0 - 2, k0 - 1, 0, bar);
-            if (hi) tma_load_3d(seg + G::UBOX + G::SROW, &a.tma.h[0].hi, i0 - 2, k0 - 1, 0, bar);
-        }
-        tma_load_3d(seg + G::UBOX + 2 * G::SROW, &a.tma.q[0], i0, k0, j0, bar);
+        if constexpr (G::HALO) tma_rows(seg, a.tma.h[0], TY + 2, G::UROW, i0 - XO, k0 - 1, j0 - 1, ny, bar);
+        tma_load_3d(seg + G::UBOX, &a.tma.q[0], i0, k0, j0, bar);
+        if constexpr (G::PROL)
+            tma_rows(seg + G::UBOX + G::FBOX, a.tma.h[1], G::CROWS, G::CROW, i0 / 2 - XOC, k0 - 1, j0 / 2 - 1, ny / 2,
+                     bar);
     }
 }
 
@@ -90,7 +115,8 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     constexpr int NT = 32 * TY * NSEG;
     constexpr int NCC = SL / KB;           // chunks per segment
     constexpr int STG = NSEG * G::SEGST;
-    constexpr bool NORM = (MODE == MODE_SMOOTH);
+    constexpr bool NORM = (MODE == MODE_SMOOTH || MODE == MODE_SMOOTH_PROLONG);
+    constexpr bool THOMAS = (MODE != MODE_RESTRICT);
 
     extern __shared__ __align__(128) double smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[NS2];
@@ -98,9 +124,9 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
                                              ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
     const int nz = a.L.nz;
     const int64_t nx = a.L.nx, ny = a.L.ny;
-    double* tab = smem;                                 // diag, invm, gim, afw, Pfw, Qbw (nz each)
-    double* stage = smem + r16(6 * nz);
-    double* bnd = stage + NS2 * STG;                    // [2][TY][NSEG][32]
+    double* stage = smem;                               // NS2 stages (128-byte aligned)
+    double* tab = stage + NS2 * STG;                    // diag, invm, gim, afw, Pfw, Qbw (nz each)
+    double* bnd = tab + r16(6 * nz);
     double* scratch = bnd + G::template bnd<NSEG>();
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -153,31 +179,51 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
         const int i0 = (tile % ntx) * TX, j0 = (tile / ntx) * TY;
         const int64_t i = i0 + lane, j = j0 + ty;
         const bool valid = (i < nx) && (j < ny);
-        // halo rows of this warp's row j: south j-1, north j+1 (slab rows at strip boundaries)
-        const bool s_slab = G::HALO && a.tma.h[0].has_lo && j0 == 0 && ty == 0;
-        const bool n_slab = G::HALO && a.tma.h[0].has_hi && (j0 + ty + 1 == ny);
 
-        double yv[SL];
+        double yv[THOMAS ? SL : 1];
         double yprev = 0.0;
 #pragma unroll
         for (int cc = 0; cc < NCC; ++cc) {
             issue();
             mbar_wait(&full_bar[c_slot], c_phase);
-            const double* seg = stage + c_slot * STG + s * G::SEGST;
+            double* seg = stage + c_slot * STG + s * G::SEGST;
             if (++c_slot == NS2) { c_slot = 0; c_phase ^= 1u; }
-            const double* fb = seg + G::UBOX + 2 * G::SROW + ty * (KB * TX) + lane;
+            if constexpr (G::PROL) {
+                // u <- u + P u_c on the u box of this segment (the TY warps of the segment
+                // share it; named barrier s+1).  Only in-domain fine cells change: the zero
+                // ghosts stay zero; halo rows from a neighbour's slab get the correction too.
+                const double* cb = seg + G::UBOX + G::FBOX;
+                const int tseg = ty * 32 + lane;   // thread index within the segment's warps
+                const bool slo = a.tma.h[0].has_lo, shi = a.tma.h[0].has_hi;
+                for (int e = tseg; e < (TY + 2) * G::D * (TX + 2); e += TY * 32) {
+                    const int x = XO - 1 + e % (TX + 2);          // box columns read by the stencil
+                    const int rd = e / (TX + 2);
+                    const int d = rd % G::D, r = rd / G::D;
+                    const int ig = i0 - XO + x, jg = j0 - 1 + r;
+                    const bool in = ig >= 0 && ig < nx &&
+                                    ((jg >= 0 && jg < ny) || (jg == -1 && slo) || (jg == ny && shi));
+                    if (in) {
+                        const int cx = (ig >> 1) - (i0 >> 1) + XOC, cy = (jg >> 1) - (j0 >> 1) + 1;
+                        const int sx = (ig & 1) ? 1 : -1, sy = (jg & 1) ? HXC * G::D : -HXC * G::D;
+                        const double* cp = cb + (cy * G::D + d) * HXC + cx;
+                        const double v = 9.0 * cp[0] + 3.0 * cp[sx] + 3.0 * cp[sy] + 1.0 * cp[sy + sx];
+                        double* up = seg + (r * G::D + d) * HX + x;
+                        *up = *up + v / 16.0;
+                    }
+                }
+                asm volatile("bar.sync %0, %1;\n" ::"r"(s + 1), "r"(TY * 32) : "memory");
+            }
+            const double* fb = seg + G::UBOX + ty * (KB * TX) + lane;
             double gv[KB], rv[KB];
             if constexpr (G::HALO) {
-                const double* rc = seg + (ty + 1) * (G::D * HX) + lane + 2;                   // own row
-                const double* rs = s_slab ? seg + G::UBOX + lane + 2 : rc - G::D * HX;        // south row
-                const double* rn = n_slab ? seg + G::UBOX + G::SROW + lane + 2 : rc + G::D * HX;  // north row
+                const double* rc = seg + (ty + 1) * G::UROW + lane + XO;     // own row
                 double ud = rc[0], uc = rc[HX];
 #pragma unroll
                 for (int kk = 0; kk < KB; ++kk) {
-                    const int d = kk + 1;                 // box level of k = k0 + kk
+                    const int dd = kk + 1;                 // box level of k = k0 + kk
                     const int k = s * SL + cc * KB + kk;
-                    const double uu = rc[(d + 1) * HX];
-                    const double S = (rc[d * HX - 1] + rc[d * HX + 1]) + (rs[d * HX] + rn[d * HX]);
+                    const double uu = rc[(dd + 1) * HX];
+                    const double S = (rc[dd * HX - 1] + rc[dd * HX + 1]) + (rc[dd * HX - G::UROW] + rc[dd * HX + G::UROW]);
                     const double Mu = fma(-gamma, ud + uu, diag[k] * uc);       // (M_T u)_k
                     const double r = fma(c, S, fb[kk * TX]) - Mu;               // f - A u
                     gv[kk] = fma(rho, r, Mu);            // g = (M - rho A) u + rho f  (one-pass smoother)
@@ -213,52 +259,53 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
                     }
                 }
                 continue;
+            } else {
+                // local forward recurrence yhat_k = g_k + a_k yhat_{k-1} (yhat = 0 before the segment)
+#pragma unroll
+                for (int kk = 0; kk < KB; ++kk) {
+                    const int k = s * SL + cc * KB + kk;
+                    yprev = (cc == 0 && kk == 0) ? gv[kk] : fma(afw[k], yprev, gv[kk]);
+                    yv[cc * KB + kk] = yprev;
+                    if constexpr (NORM) acc[0] = fma(rv[kk], rv[kk], acc[0]);
+                }
+                __syncthreads();   // every warp is done with this slot
             }
-            // local forward recurrence yhat_k = g_k + a_k yhat_{k-1} (yhat = 0 before the segment)
+        }
+        if constexpr (THOMAS) {
+            // chain the segments: Y_s = y_{k_s - 1} (true), from the segments' last yhat
+            double* bF = bnd + (ty * NSEG) * 32 + lane;               // [ty][seg][lane]
+            double* bB = bnd + TY * NSEG * 32 + (ty * NSEG) * 32 + lane;
+            bF[s * 32] = yv[SL - 1];
+            __syncthreads();
+            double Y = 0.0;
 #pragma unroll
-            for (int kk = 0; kk < KB; ++kk) {
-                const int k = s * SL + cc * KB + kk;
-                yprev = (cc == 0 && kk == 0) ? gv[kk] : fma(afw[k], yprev, gv[kk]);
-                yv[cc * KB + kk] = yprev;
-                if constexpr (NORM) acc[0] = fma(rv[kk], rv[kk], acc[0]);
+            for (int q = 0; q < NSEG - 1; ++q)
+                if (q < s) Y = fma(Pfw[(q + 1) * SL - 1], Y, bF[q * 32]);
+            // g'_k = (yhat_k + P_k Y) / m_k, then the local backward recurrence
+            const int kb = s * SL;
+#pragma unroll
+            for (int q = 0; q < SL; ++q) yv[q] = fma(Pfw[kb + q], Y, yv[q]) * invm[kb + q];
+            double xh = 0.0;
+#pragma unroll
+            for (int q = SL - 1; q >= 0; --q) {
+                xh = fma(gim[kb + q], xh, yv[q]);
+                yv[q] = xh;
             }
-            __syncthreads();   // every warp is done with this slot
+            bB[s * 32] = yv[0];
+            __syncthreads();
+            double X = 0.0;                                           // x_{k_e + 1} (true)
+#pragma unroll
+            for (int q = NSEG - 1; q >= 1; --q)
+                if (q > s) X = fma(Qbw[q * SL], X, bB[q * 32]);
+            double* op = a.out0 + (j * nz + kb) * nx + i;
+#pragma unroll
+            for (int q = 0; q < SL; ++q) {
+                const double x = fma(Qbw[kb + q], X, yv[q]);
+                if (valid) *op = x;
+                op += nx;
+            }
+            // bnd is reused by the next tile only after its forward chunks (>= 1 __syncthreads)
         }
-
-        if constexpr (MODE == MODE_RESTRICT) continue;
-        // chain the segments: Y_s = y_{k_s - 1} (true), from the segments' last yhat
-        double* bF = bnd + (ty * NSEG) * 32 + lane;               // [ty][seg][lane]
-        double* bB = bnd + TY * NSEG * 32 + (ty * NSEG) * 32 + lane;
-        bF[s * 32] = yv[SL - 1];
-        __syncthreads();
-        double Y = 0.0;
-#pragma unroll
-        for (int q = 0; q < NSEG - 1; ++q)
-            if (q < s) Y = fma(Pfw[(q + 1) * SL - 1], Y, bF[q * 32]);
-        // g'_k = (yhat_k + P_k Y) / m_k, then the local backward recurrence
-        const int kb = s * SL;
-#pragma unroll
-        for (int q = 0; q < SL; ++q) yv[q] = fma(Pfw[kb + q], Y, yv[q]) * invm[kb + q];
-        double xh = 0.0;
-#pragma unroll
-        for (int q = SL - 1; q >= 0; --q) {
-            xh = fma(gim[kb + q], xh, yv[q]);
-            yv[q] = xh;
-        }
-        bB[s * 32] = yv[0];
-        __syncthreads();
-        double X = 0.0;                                           // x_{k_e + 1} (true)
-#pragma unroll
-        for (int q = NSEG - 1; q >= 1; --q)
-            if (q > s) X = fma(Qbw[q * SL], X, bB[q * 32]);
-        double* op = a.out0 + (j * nz + kb) * nx + i;
-#pragma unroll
-        for (int q = 0; q < SL; ++q) {
-            const double x = fma(Qbw[kb + q], X, yv[q]);
-            if (valid) *op = x;
-            op += nx;
-        }
-        // bnd is reused by the next tile only after its forward chunks (>= 1 __syncthreads)
     }
     if (NORM && a.red.result != nullptr) grid_reduce<1>(a.red, acc, scratch);
 }
@@ -267,7 +314,7 @@ template <int MODE, int TY, int NSEG, int KB, int NS2>
 size_t ksmem(int nz)
 {
     using G = KGeom<MODE, TY, KB>;
-    return (size_t)(r16(6 * nz) + NS2 * NSEG * G::SEGST + G::template bnd<NSEG>() + 64 + 16) * sizeof(double);
+    return (size_t)(NS2 * NSEG * G::SEGST + r16(6 * nz) + G::template bnd<NSEG>() + 64 + 16) * sizeof(double);
 }
 
 template <int MODE, int TY, int NSEG, int KB, int NS2>
@@ -305,8 +352,7 @@ cudaError_t launch_k_nseg(const Launcher& ln, const LineArgs& a, const KTables& 
     }
 }
 
-// configurations: 0 = 2 rows x 8 levels, 2 stages; 1 = 4 rows x 4 levels, 3 stages;
-// 2 = 2 rows x 4 levels, 2 stages (two CTAs per SM)
+// configurations (rows TY, levels per chunk KB): 0 = 2 x 8; 1 = 4 x 4 (default); 2 = 2 x 4
 struct Cfg { int ty, kb; };
 constexpr Cfg kCfg[3] = {{2, 8}, {4, 4}, {2, 4}};
 
@@ -314,23 +360,31 @@ constexpr Cfg kCfg[3] = {{2, 8}, {4, 4}, {2, 4}};
 
 bool ksplit_supported(int mode, int nz, int nx)
 {
-    return (mode == MODE_SMOOTH || mode == MODE_PREC || mode == MODE_RESTRICT) && nz % SL == 0 && nz <= kKsplitMaxNZ &&
-           (nz / SL == 1 || nz / SL == 2 || nz / SL == 4) && nx % 2 == 0;
+    // TMA row strides must be multiples of 16 bytes: even nx (and even coarse nx for the
+    // fused prolongation)
+    return (mode == MODE_SMOOTH || mode == MODE_PREC || mode == MODE_RESTRICT || mode == MODE_SMOOTH_PROLONG) &&
+           nz % SL == 0 && nz <= kKsplitMaxNZ && (nz / SL == 1 || nz / SL == 2 || nz / SL == 4) && nx % 2 == 0 &&
+           (mode != MODE_SMOOTH_PROLONG || nx % 4 == 0);
 }
 
 KsplitBoxes ksplit_boxes(int mode, int cfg)
 {
     (void)mode;
     const Cfg c = kCfg[cfg < 0 || cfg > 2 ? 0 : cfg];
-    return KsplitBoxes{c.ty, c.kb, HX, c.kb + 2};
+    return KsplitBoxes{c.ty, c.kb, HX, c.kb + 2, XO, HXC, XOC};
 }
 
 cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const LineArgs& a, const KTables& T)
 {
     if (mode == MODE_SMOOTH) {
         if (cfg == 1) return launch_k_nseg<MODE_SMOOTH, 4, 4, 3>(ln, a, T);
-        if (cfg == 2) return launch_k_nseg<MODE_SMOOTH, 2, 4, 2>(ln, a, T);
+        if (cfg == 2) return launch_k_nseg<MODE_SMOOTH, 2, 4, 3>(ln, a, T);
         return launch_k_nseg<MODE_SMOOTH, 2, 8, 2>(ln, a, T);
+    }
+    if (mode == MODE_SMOOTH_PROLONG) {
+        if (cfg == 1) return launch_k_nseg<MODE_SMOOTH_PROLONG, 4, 4, 2>(ln, a, T);
+        if (cfg == 2) return launch_k_nseg<MODE_SMOOTH_PROLONG, 2, 4, 3>(ln, a, T);
+        return launch_k_nseg<MODE_SMOOTH_PROLONG, 2, 8, 2>(ln, a, T);
     }
     if (mode == MODE_PREC) {   // no u box: deeper pipelines are cheap
         if (cfg == 1) return launch_k_nseg<MODE_PREC, 4, 4, 6>(ln, a, T);
@@ -338,8 +392,8 @@ cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const Line
         return launch_k_nseg<MODE_PREC, 2, 8, 4>(ln, a, T);
     }
     if (mode == MODE_RESTRICT) {   // no Thomas: the exchange buffer replaces the chaining buffer
-        if (cfg == 1) return launch_k_nseg<MODE_RESTRICT, 4, 4, 2>(ln, a, T);
-        if (cfg == 2) return launch_k_nseg<MODE_RESTRICT, 2, 4, 2>(ln, a, T);
+        if (cfg == 1) return launch_k_nseg<MODE_RESTRICT, 4, 4, 3>(ln, a, T);
+        if (cfg == 2) return launch_k_nseg<MODE_RESTRICT, 2, 4, 3>(ln, a, T);
         return launch_k_nseg<MODE_RESTRICT, 2, 8, 2>(ln, a, T);
     }
     return cudaErrorInvalidValue;

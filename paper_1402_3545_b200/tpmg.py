@@ -246,7 +246,8 @@ def tpmg_stats_reset(ctx: int) -> None:
 
 
 KERNEL_CLASSES = ["apply", "residual", "precondition", "smooth", "cg_direction",
-                  "cg_precondition", "residual_restrict", "restrict", "prolong_add", "dot"]
+                  "cg_precondition", "residual_restrict", "restrict", "prolong_add", "dot",
+                  "smooth_prolong"]
 
 
 def tpmg_profile(ctx: int, enable: bool) -> None:

@@ -19,7 +19,7 @@ def ctx_for(p: O.Params, device: int = 0, loader: str | None = None):
     (TMA, k-split off), "tma-ks2" (TMA, k-split 2x8 config).  Read at tpmg_create."""
     import os
     T = lib()
-    for var in ("TPMG_LOADER", "TPMG_KSPLIT"):
+    for var in ("TPMG_LOADER", "TPMG_KSPLIT", "TPMG_FUSE_PROLONG"):
         os.environ.pop(var, None)
     if loader == "cpasync":
         os.environ["TPMG_LOADER"] = "cpasync"
@@ -27,6 +27,8 @@ def ctx_for(p: O.Params, device: int = 0, loader: str | None = None):
         os.environ["TPMG_KSPLIT"] = "0"
     elif loader == "tma-ks2":
         os.environ["TPMG_KSPLIT"] = "1"   # the non-default k-split config (2 x 8 levels)
+    elif loader == "tma-nofuse":
+        os.environ["TPMG_FUSE_PROLONG"] = "0"
     params = T.make_params(p.nx, p.ny, nz=p.nz, nu_cfl=p.nu_cfl, H=p.H, lam=p.lam, levels=p.L,
                            pre=p.pre, post=p.post, coarse_sweeps=p.coarse_sweeps, rho=p.rho)
     return T.Context(params, device=device)
