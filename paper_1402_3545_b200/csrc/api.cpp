@@ -82,7 +82,9 @@ struct tpmg_ctx {
     // TMA descriptors, cached by (address, nx, nz, ny, box x, box rows)
     bool use_tma = true;
     bool sync_debug = false;   // TPMG_SYNC_DEBUG=1: synchronise after every line kernel
-    bool fuse_prolong = true;  // TPMG_FUSE_PROLONG=0: separate prolongation kernel
+    bool fuse_prolong = false; // TPMG_FUSE_PROLONG=1: prolongation fused into the post-smooth (k-split);
+                               // off by default: measured slower (the in-smem u + P u_c pass
+                               // costs more issue slots than the 16 B/cell it saves)
     int ksplit_cfg = 1;        // k-split config (TPMG_KSPLIT: "0" off, "1" 2x8/2 stages, "2" 4x4/3 stages
                                // (default), "3" 2x4/2 stages); -1 = off
     std::map<std::tuple<uintptr_t, int64_t, int, int64_t, int, int>, CUtensorMap> tmaps;
@@ -1028,7 +1030,7 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         const char* ks = std::getenv("TPMG_KSPLIT");
         ctx->ksplit_cfg = !ks ? 1 : ks[0] == '0' ? -1 : ks[0] == '1' ? 0 : ks[0] == '3' ? 2 : 1;
         const char* fp = std::getenv("TPMG_FUSE_PROLONG");
-        ctx->fuse_prolong = !(fp && fp[0] == '0');
+        ctx->fuse_prolong = fp && fp[0] == '1';
         const char* sd = std::getenv("TPMG_SYNC_DEBUG");
         ctx->sync_debug = sd && sd[0] == '1';
     }

@@ -27,8 +27,8 @@ def ctx_for(p: O.Params, device: int = 0, loader: str | None = None):
         os.environ["TPMG_KSPLIT"] = "0"
     elif loader == "tma-ks2":
         os.environ["TPMG_KSPLIT"] = "1"   # the non-default k-split config (2 x 8 levels)
-    elif loader == "tma-nofuse":
-        os.environ["TPMG_FUSE_PROLONG"] = "0"
+    elif loader == "tma-fuse":
+        os.environ["TPMG_FUSE_PROLONG"] = "1"
     params = T.make_params(p.nx, p.ny, nz=p.nz, nu_cfl=p.nu_cfl, H=p.H, lam=p.lam, levels=p.L,
                            pre=p.pre, post=p.post, coarse_sweeps=p.coarse_sweeps, rho=p.rho)
     return T.Context(params, device=device)

@@ -51,7 +51,7 @@ def rand(shape, seed):
     return np.random.default_rng(seed).standard_normal(shape)
 
 
-LOADERS = ["tma", "cpasync", "tma-noks", "tma-ks2", "tma-nofuse"]
+LOADERS = ["tma", "cpasync", "tma-noks", "tma-ks2", "tma-fuse"]
 
 
 @pytest.mark.parametrize("loader", LOADERS)
