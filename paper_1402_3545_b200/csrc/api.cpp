@@ -72,6 +72,13 @@ struct tpmg_ctx {
     double *cg_zlo = nullptr, *cg_zhi = nullptr, *cg_plo[2] = {nullptr, nullptr}, *cg_phi[2] = {nullptr, nullptr};
     double *host_f = nullptr, *host_u = nullptr;  // device buffers for tpmg_solve_host
     ncclComm_t comm = nullptr;
+    // overlap of halo exchanges with interior work (nranks > 1)
+    ncclComm_t comm_halo = nullptr;     // halo traffic on its own communicator and stream
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+    bool overlap = true;                // TPMG_OVERLAP=0 disables
+    int reserve_sms = 4;                // SMs left to NCCL while the interior runs
+    int cur_reserve = 0;
     tpmg_stats stats{};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // profiling (tpmg_profile)
@@ -134,12 +141,13 @@ Launcher launcher(tpmg_ctx* ctx)
     ln.stream = ctx->stream;
     ln.num_sms = ctx->num_sms;
     ln.launch_counter = &ctx->stats.kernel_launches;
+    ln.reserve_sms = ctx->cur_reserve;
     return ln;
 }
 
 ReduceSlot slot(tpmg_ctx* ctx, double* result)
 {
-    return ReduceSlot{ctx->d_partials, ctx->d_ticket, result};
+    return ReduceSlot{ctx->d_partials, ctx->d_ticket, result, 0};
 }
 
 tpmg_status dev_alloc(tpmg_ctx* ctx, double** p, size_t n)
@@ -163,24 +171,49 @@ tpmg_status check_level(tpmg_ctx* ctx, int level)
 // ------------------------------------------------------------------ halos and reductions
 
 // Fill the halo slabs of `level` from the neighbours' boundary rows of x (nranks > 1).
+tpmg_status exchange_on(tpmg_ctx* ctx, cudaStream_t st, ncclComm_t comm, size_t plane, int64_t nyl, const double* x,
+                        double* lo, double* hi)
+{
+    const double* first = x;
+    const double* last = x + (size_t)(nyl - 1) * plane;
+    NCCL_TRY(ctx, ncclGroupStart());
+    if (ctx->rank > 0) {
+        NCCL_TRY(ctx, ncclSend(first, plane, ncclDouble, ctx->rank - 1, comm, st));
+        NCCL_TRY(ctx, ncclRecv(lo, plane, ncclDouble, ctx->rank - 1, comm, st));
+    }
+    if (ctx->rank < ctx->nranks - 1) {
+        NCCL_TRY(ctx, ncclSend(last, plane, ncclDouble, ctx->rank + 1, comm, st));
+        NCCL_TRY(ctx, ncclRecv(hi, plane, ncclDouble, ctx->rank + 1, comm, st));
+    }
+    NCCL_TRY(ctx, ncclGroupEnd());
+    ++ctx->stats.halo_exchanges;
+    return TPMG_OK;
+}
+
+// Fill the halo slabs of `level` from the neighbours' boundary rows of x (nranks > 1),
+// in stream order on the context stream.
 tpmg_status exchange(tpmg_ctx* ctx, int level, const double* x, double* lo, double* hi)
 {
     if (ctx->nranks == 1) return TPMG_OK;
     LevelData& L = ctx->lv[level];
-    const size_t plane = L.plane();
-    const double* first = x;
-    const double* last = x + (size_t)(L.lc.ny - 1) * plane;
-    NCCL_TRY(ctx, ncclGroupStart());
-    if (ctx->rank > 0) {
-        NCCL_TRY(ctx, ncclSend(first, plane, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
-        NCCL_TRY(ctx, ncclRecv(lo, plane, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
-    }
-    if (ctx->rank < ctx->nranks - 1) {
-        NCCL_TRY(ctx, ncclSend(last, plane, ncclDouble, ctx->rank + 1, ctx->comm, ctx->stream));
-        NCCL_TRY(ctx, ncclRecv(hi, plane, ncclDouble, ctx->rank + 1, ctx->comm, ctx->stream));
-    }
-    NCCL_TRY(ctx, ncclGroupEnd());
-    ++ctx->stats.halo_exchanges;
+    return exchange_on(ctx, ctx->stream, ctx->comm, L.plane(), L.lc.ny, x, lo, hi);
+}
+
+// Start the exchange on the halo stream once everything enqueued so far on the
+// context stream is done; finish_async_exchange() makes the context stream wait for it.
+tpmg_status start_async_exchange(tpmg_ctx* ctx, int level, const double* x, double* lo, double* hi)
+{
+    LevelData& L = ctx->lv[level];
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_ready, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_ready, 0));
+    TRY(exchange_on(ctx, ctx->comm_stream, ctx->comm_halo, L.plane(), L.lc.ny, x, lo, hi));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_halo, ctx->comm_stream));
+    return TPMG_OK;
+}
+
+tpmg_status finish_async_exchange(tpmg_ctx* ctx)
+{
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
     return TPMG_OK;
 }
 
@@ -223,7 +256,7 @@ LineArgs line_args(tpmg_ctx* ctx, int level)
     a.rho = ctx->p.rho;
     a.scale = 1.0;
     a.ratio = DevRatio{nullptr, -1, -1};
-    a.red = ReduceSlot{ctx->d_partials, ctx->d_ticket, nullptr};
+    a.red = ReduceSlot{ctx->d_partials, ctx->d_ticket, nullptr, 0};
     a.skip = ctx->skip;
     return a;
 }
@@ -412,11 +445,22 @@ bool ksplit_usable(tpmg_ctx* ctx, int mode, const LevelConst& lc)
     return ctx->use_tma && ctx->ksplit_cfg >= 0 && ksplit_supported(mode, lc.nz, (int)lc.nx);
 }
 
+// Fraction of the level's cells a launch covers (interior / boundary tile rows).
+double part_cells(tpmg_ctx* ctx, int mode, const LineArgs& a)
+{
+    const double all = level_cells(a.L);
+    if (a.part == PART_ALL || a.L.ny <= 0) return all;
+    const int TY = line_launch_rows(mode, a.L.nz, (int)a.L.nx, ctx->use_tma ? 1 : 0, ctx->ksplit_cfg);
+    const int nty = (int)((a.L.ny + TY - 1) / TY);
+    const double rows = (a.part == PART_INTERIOR) ? (double)(nty - 2) * TY : (double)a.L.ny - (double)(nty - 2) * TY;
+    return all * rows / (double)a.L.ny;
+}
+
 tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
 {
     LineArgs a = a0;
     if (ksplit_usable(ctx, mode, a.L) && fill_tma_ksplit(ctx, mode, a)) {
-        ProfScope ps(ctx, mode == MODE_SMOOTH_PROLONG ? TPMG_K_SMOOTH_PROLONG : mode, level_cells(a.L));
+        ProfScope ps(ctx, mode == MODE_SMOOTH_PROLONG ? TPMG_K_SMOOTH_PROLONG : mode, part_cells(ctx, mode, a));
         const KTables& kt = ctx->lv[level_of(ctx, a.L)].ktab;
         CUDA_TRY(ctx, launch_line_ksplit(launcher(ctx), mode, ctx->ksplit_cfg, a, kt));
         if (ctx->sync_debug) {
@@ -430,7 +474,7 @@ tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
     if (mode == MODE_SMOOTH_PROLONG) return fail(ctx, TPMG_E_PARAM, "fused prolongation-smooth needs the k-split kernel");
     a = a0;
     fill_tma(ctx, mode, a);
-    ProfScope ps(ctx, mode == MODE_RESTRICT ? TPMG_K_RESIDUAL_RESTRICT : mode, level_cells(a.L));  // modes 0..5 = TPMG_K_0..5
+    ProfScope ps(ctx, mode == MODE_RESTRICT ? TPMG_K_RESIDUAL_RESTRICT : mode, part_cells(ctx, mode, a));  // modes 0..5 = TPMG_K_0..5
     CUDA_TRY(ctx, launch_line(launcher(ctx), mode, a));
     if (ctx->sync_debug) {
         cudaError_t e = cudaStreamSynchronize(ctx->stream);
@@ -442,16 +486,56 @@ tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
     return TPMG_OK;
 }
 
+// A line kernel whose halo'd input x needs an exchange first.  With several ranks the
+// exchange runs on the halo stream while the interior tile rows (which read no halo
+// row) run, leaving reserve_sms SMs to NCCL; the boundary tile rows follow once the
+// halo has arrived.  pre_boundary (optional) runs between the exchange and the
+// boundary launch (e.g. the CG p-halo update).
+template <typename PreBoundary>
+tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, LineArgs a, const double* x, double* lo, double* hi,
+                          PreBoundary pre_boundary)
+{
+    if (ctx->nranks == 1) {
+        TRY(pre_boundary());
+        return run_line(ctx, mode, a);
+    }
+    const LevelConst& lc = ctx->lv[level].lc;
+    const int TY = line_launch_rows(mode, lc.nz, (int)lc.nx, ctx->use_tma ? 1 : 0, ctx->ksplit_cfg);
+    const int nty = (int)((lc.ny + TY - 1) / TY);
+    if (!ctx->overlap || nty < 3) {
+        TRY(exchange_on(ctx, ctx->stream, ctx->comm, ctx->lv[level].plane(), lc.ny, x, lo, hi));
+        TRY(pre_boundary());
+        return run_line(ctx, mode, a);
+    }
+    TRY(start_async_exchange(ctx, level, x, lo, hi));
+    a.part = PART_INTERIOR;
+    ctx->cur_reserve = ctx->reserve_sms;
+    tpmg_status st = run_line(ctx, mode, a);
+    ctx->cur_reserve = 0;
+    TRY(st);
+    TRY(finish_async_exchange(ctx));
+    TRY(pre_boundary());
+    a.part = PART_BOUNDARY;
+    a.red.accumulate = 1;
+    return run_line(ctx, mode, a);
+}
+
+tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, const LineArgs& a, const double* x)
+{
+    LevelData& L = ctx->lv[level];
+    return run_line_halo(ctx, level, mode, a, x, L.slab_lo, L.slab_hi, [] { return TPMG_OK; });
+}
+
 // out = u + rho M^-1 (f - A u) (out-of-place), optional sum r^2 into result
 tpmg_status smooth_once(tpmg_ctx* ctx, int level, const double* u, const double* f, double* out,
                         double* result)
 {
     LineArgs a = line_args(ctx, level);
-    TRY(halo(ctx, level, u, &a.h0));
+    a.h0 = halo_of(ctx, level, u);
     a.q0 = f;
     a.out0 = out;
     a.red.result = result;
-    return run_line(ctx, MODE_SMOOTH, a);
+    return run_line_halo(ctx, level, MODE_SMOOTH, a, u);
 }
 
 // ------------------------------------------------------------------ multigrid
@@ -479,10 +563,10 @@ tpmg_status mg_restrict_smooth(tpmg_ctx* ctx, int l)
     LevelData& Cc = ctx->lv[l];
     {
         LineArgs r = line_args(ctx, l + 1);
-        TRY(halo(ctx, l + 1, F.u[F.cur], &r.h0));
+        r.h0 = halo_of(ctx, l + 1, F.u[F.cur]);
         r.q0 = F.f;
         r.out0 = Cc.f;
-        TRY(run_line(ctx, MODE_RESTRICT, r));
+        TRY(run_line_halo(ctx, l + 1, MODE_RESTRICT, r, F.u[F.cur]));
     }
     LineArgs a = line_args(ctx, l);
     a.q0 = Cc.f;
@@ -497,6 +581,31 @@ tpmg_status mg_smooth(tpmg_ctx* ctx, int l, double* result = nullptr)
     LevelData& L = ctx->lv[l];
     TRY(smooth_once(ctx, l, L.u[L.cur], L.f, L.u[1 - L.cur], result));
     L.cur ^= 1;
+    return TPMG_OK;
+}
+
+// u^(l+1) += P u^(l) with the coarse halo exchange overlapped (interior coarse rows first).
+tpmg_status prolong_overlapped(tpmg_ctx* ctx, int lc_)
+{
+    LevelData& Cc = ctx->lv[lc_];
+    LevelData& F = ctx->lv[lc_ + 1];
+    const HaloField uc = halo_of(ctx, lc_, Cc.u[Cc.cur]);
+    const double cells = level_cells(F.lc);
+    if (ctx->nranks == 1 || !ctx->overlap || Cc.lc.ny < 3) {
+        TRY(exchange(ctx, lc_, Cc.u[Cc.cur], Cc.slab_lo, Cc.slab_hi));
+        ProfScope ps(ctx, TPMG_K_PROLONG_ADD, cells);
+        CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc, F.u[F.cur], ctx->skip));
+        return TPMG_OK;
+    }
+    TRY(start_async_exchange(ctx, lc_, Cc.u[Cc.cur], Cc.slab_lo, Cc.slab_hi));
+    const double fb = 2.0 / (double)Cc.lc.ny;
+    {
+        ProfScope ps(ctx, TPMG_K_PROLONG_ADD, cells * (1.0 - fb));
+        CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc, F.u[F.cur], ctx->skip, PART_INTERIOR));
+    }
+    TRY(finish_async_exchange(ctx));
+    ProfScope ps(ctx, TPMG_K_PROLONG_ADD, cells * fb);
+    CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc, F.u[F.cur], ctx->skip, PART_BOUNDARY));
     return TPMG_OK;
 }
 
@@ -524,10 +633,11 @@ tpmg_status vcycle_rec(tpmg_ctx* ctx, int l, bool skip_pre = false)
     TRY(vcycle_rec(ctx, l - 1));
     LevelData& Cc = ctx->lv[l - 1];
     LevelData& F = ctx->lv[l];
-    HaloField uc;
-    TRY(halo(ctx, l - 1, Cc.u[Cc.cur], &uc));
+    HaloField uc = halo_of(ctx, l - 1, Cc.u[Cc.cur]);
+    const bool fuse = p.post >= 1 && ctx->fuse_prolong && ksplit_usable(ctx, MODE_SMOOTH_PROLONG, F.lc);
+    if (fuse) TRY(exchange(ctx, l - 1, Cc.u[Cc.cur], Cc.slab_lo, Cc.slab_hi));
     int s0 = 0;
-    if (p.post >= 1 && ctx->fuse_prolong && ksplit_usable(ctx, MODE_SMOOTH_PROLONG, F.lc)) {
+    if (fuse) {
         // Prolongate fused with the first post-smooth: u' = S(u + P u_c) without storing
         // u + P u_c.  The halo of u is the one exchanged for the restriction (u has not
         // changed since), the coarse halo was just exchanged.
@@ -540,8 +650,7 @@ tpmg_status vcycle_rec(tpmg_ctx* ctx, int l, bool skip_pre = false)
         F.cur ^= 1;
         s0 = 1;
     } else {
-        ProfScope ps(ctx, TPMG_K_PROLONG_ADD, level_cells(F.lc));
-        CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc, F.u[F.cur], ctx->skip));
+        TRY(prolong_overlapped(ctx, l - 1));
     }
     for (int s = s0; s < p.post; ++s) TRY(mg_smooth(ctx, l));
     return TPMG_OK;
@@ -824,14 +933,12 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
         const DevRatio beta = (m == 1) ? DevRatio{ctx->d_scal, -1, -1}
                                        : DevRatio{ctx->d_scal, S_ZETA(m - 1), S_ZETA(m - 2)};
         if (ctx->nranks > 1) {
-            TRY(exchange(ctx, l, ctx->cg_z, ctx->cg_zlo, ctx->cg_zhi));
             hz = HaloField{ctx->cg_z, has_lo ? ctx->cg_zlo : nullptr, has_hi ? ctx->cg_zhi : nullptr};
             hp = HaloField{ctx->cg_p[cur], has_lo ? ctx->cg_plo[cur] : nullptr, has_hi ? ctx->cg_phi[cur] : nullptr};
-            CUDA_TRY(ctx, launch_cg_halo(launcher(ctx), has_lo ? ctx->cg_plo[1 - cur] : nullptr, hz.lo, hp.lo,
-                                         has_hi ? ctx->cg_phi[1 - cur] : nullptr, hz.hi, hp.hi, (int64_t)plane, beta,
-                                         ctx->skip));
         }
-        // (Fused) direction kernel: p = z + beta p, sigma = <p, A p>
+        // (Fused) direction kernel: p = z + beta p, sigma = <p, A p>.  The z halo is
+        // exchanged while the interior runs; the p halo is local:
+        // p_halo <- z_halo + beta p_halo (same fma as the neighbour's own rows).
         {
             LineArgs a = line_args(ctx, l);
             a.h0 = hz;
@@ -839,7 +946,14 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
             a.out0 = ctx->cg_p[1 - cur];
             a.ratio = beta;
             a.red.result = ctx->d_scal + S_SIGMA(m);
-            TRY(run_line(ctx, MODE_CGDIR, a));
+            const int c2 = cur;
+            TRY(run_line_halo(ctx, l, MODE_CGDIR, a, ctx->cg_z, ctx->cg_zlo, ctx->cg_zhi, [&]() -> tpmg_status {
+                if (ctx->nranks > 1)
+                    CUDA_TRY(ctx, launch_cg_halo(launcher(ctx), has_lo ? ctx->cg_plo[1 - c2] : nullptr, hz.lo, hp.lo,
+                                                 has_hi ? ctx->cg_phi[1 - c2] : nullptr, hz.hi, hp.hi,
+                                                 (int64_t)plane, beta, ctx->skip));
+                return TPMG_OK;
+            }));
             TRY(allreduce(ctx, ctx->d_scal + S_SIGMA(m), 1));
         }
         HaloField hpn{ctx->cg_p[1 - cur], nullptr, nullptr};
@@ -945,7 +1059,11 @@ void ctx_free(tpmg_ctx* ctx)
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     for (auto& r : ctx->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ctx->prof_pool) cudaEventDestroy(e);
+    if (ctx->comm_halo) ncclCommDestroy(ctx->comm_halo);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
+    if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+    if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
+    if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
 }
 
 }  // namespace
@@ -1029,6 +1147,10 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->use_tma = !(ld && std::strcmp(ld, "cpasync") == 0);
         const char* ks = std::getenv("TPMG_KSPLIT");
         ctx->ksplit_cfg = !ks ? 1 : ks[0] == '0' ? -1 : ks[0] == '1' ? 0 : ks[0] == '3' ? 2 : 1;
+        const char* ov = std::getenv("TPMG_OVERLAP");
+        ctx->overlap = !(ov && ov[0] == '0');
+        const char* rs = std::getenv("TPMG_RESERVE_SMS");
+        if (rs) ctx->reserve_sms = std::max(0, std::atoi(rs));
         const char* fp = std::getenv("TPMG_FUSE_PROLONG");
         ctx->fuse_prolong = fp && fp[0] == '1';
         const char* sd = std::getenv("TPMG_SYNC_DEBUG");
@@ -1128,6 +1250,17 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         std::memcpy(&id, id128, sizeof id);
         ncclResult_t e = ncclCommInitRank(&ctx->comm, nranks, id, rank);
         if (e != ncclSuccess) return bail(fail(ctx, TPMG_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(e)));
+        // halo traffic: own communicator (few CTAs) and a high-priority stream
+        ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+        cfg.minCTAs = 1;
+        cfg.maxCTAs = 2;
+        e = ncclCommSplit(ctx->comm, 0, rank, &ctx->comm_halo, &cfg);
+        if (e != ncclSuccess) return bail(fail(ctx, TPMG_E_NCCL, "ncclCommSplit: %s", ncclGetErrorString(e)));
+        int lo_prio = 0, hi_prio = 0;
+        CREATE_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+        CREATE_CUDA(cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, hi_prio));
+        CREATE_CUDA(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
+        CREATE_CUDA(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
     }
 #undef CREATE_TRY
 #undef CREATE_CUDA

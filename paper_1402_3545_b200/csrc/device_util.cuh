@@ -60,7 +60,7 @@ __device__ void grid_reduce(const ReduceSlot& red, const double (&acc)[NR > 0 ? 
                 double s = 0.0;
                 for (unsigned b = lane; b < gridDim.x; b += 32) s += __ldcg(red.partials + (size_t)b * NR + r);
                 s = warp_sum(s);
-                if (lane == 0) red.result[r] = s;
+                if (lane == 0) red.result[r] = red.accumulate ? s + red.result[r] : s;
             }
             if (lane == 0) *red.ticket = 0u;
         }

@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     // 32-bit bookkeeping (tiles < 2^31); the producer and consumer walk the same chunk
     // sequence with incremental cursors (no per-chunk integer division).
     const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + TY - 1) / TY);
-    const int ntiles = ntx * nty;
+    const int ntiles = ntx * part_rows(a.part, nty);
     const int nch = (nz + KB - 1) / KB;
     const int my_tiles = ((int)blockIdx.x < ntiles) ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
     const int total = my_tiles * nch;
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 
     // producer cursor: next chunk to load
     int p_count = 0, p_ch = 0, p_slot = 0, p_tile = blockIdx.x;
-    int p_i0 = (p_tile % ntx) * TX, p_j0 = (p_tile / ntx) * TY;
+    int p_i0 = (p_tile % ntx) * TX, p_j0 = part_row(a.part, nty, p_tile / ntx) * TY;
     auto issue = [&]() {
         if (p_count < total) {
             double* st = stage + p_slot * G::STAGE;
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 p_ch = 0;
                 p_tile += gridDim.x;
                 p_i0 = (p_tile % ntx) * TX;
-                p_j0 = (p_tile / ntx) * TY;
+                p_j0 = part_row(a.part, nty, p_tile / ntx) * TY;
             }
         }
         if constexpr (LOADER == 0) cp_async_commit();
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     int gi = 0;
     for (int tl = 0; tl < my_tiles; ++tl) {
         const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
-        const int64_t i0 = (int64_t)(tile % ntx) * TX, j0 = (int64_t)(tile / ntx) * TY;
+        const int64_t i0 = (int64_t)(tile % ntx) * TX, j0 = (int64_t)part_row(a.part, nty, tile / ntx) * TY;
         const int64_t i = i0 + tx, j = j0 + ty;
         const bool valid = (i < nx) && (j < ny);
         const int64_t colbase = j * nx * (int64_t)nz + i;  // + k*nx
@@ -448,8 +448,8 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TX * TY, smem);
     if (e != cudaSuccess) return e;
     per_sm = std::max(per_sm, 1);
-    const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * ((a.L.ny + TY - 1) / TY);
-    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)ln.num_sms * per_sm);
+    const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * part_rows(a.part, (int)((a.L.ny + TY - 1) / TY));
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, ln.num_sms - ln.reserve_sms) * per_sm);
     if (grid <= 0) return cudaSuccess;
     kern<<<(unsigned)grid, TX * TY, smem, ln.stream>>>(a);
     if (ln.launch_counter) ++*ln.launch_counter;
@@ -527,13 +527,17 @@ __global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double
 // neighbourhood is read through L1 (neighbouring threads share it); no integer
 // division in the loop.
 __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const LevelConst F, const HaloField uc,
-                                                     double* __restrict__ uf, int lpt, const int* skip)
+                                                     double* __restrict__ uf, int lpt, const int* skip, int part)
 {
     if (skip && *skip) return;
     const int64_t nxc = Cc.nx, nyc = Cc.ny;
     const int nz = Cc.nz;
     const int64_t I = blockIdx.x * 32 + threadIdx.x;
-    const int64_t J = blockIdx.y * 4 + threadIdx.y;
+    // PART_INTERIOR: coarse rows 1 .. nyc-2 (no halo row read); PART_BOUNDARY: rows 0, nyc-1
+    int64_t J = blockIdx.y * 4 + threadIdx.y;
+    if (part == PART_INTERIOR) J += 1;
+    else if (part == PART_BOUNDARY) J = (J == 0) ? 0 : ((J == 1 && nyc > 1) ? nyc - 1 : nyc);
+    if (part == PART_INTERIOR && J >= nyc - 1) return;
     const int kbeg = blockIdx.z * lpt, kend = min(nz, kbeg + lpt);   // levels of this thread
     if (I >= nxc || J >= nyc) return;
     // coarse rows J-1, J, J+1 (halo slabs / zero ghosts outside)
@@ -669,6 +673,12 @@ cudaError_t launch_mg_check(const Launcher& ln, const double* norm2, const doubl
     return cudaGetLastError();
 }
 
+int line_launch_rows(int mode, int nz, int nx, int use_tma, int ksplit_cfg)
+{
+    if (use_tma && ksplit_cfg >= 0 && ksplit_supported(mode, nz, nx)) return ksplit_boxes(mode, ksplit_cfg).ty;
+    return line_tile_rows(mode, nz);
+}
+
 int line_tile_rows(int mode, int nz)
 {
     switch (mode) {
@@ -722,7 +732,7 @@ cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const Le
 }
 
 cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, const LevelConst& fine,
-                               HaloField uc, double* uf, const int* skip)
+                               HaloField uc, double* uf, const int* skip, int part)
 {
     if (coarse.nx <= 0 || coarse.ny <= 0) return cudaSuccess;
     // levels per thread: enough threads to fill the GPU on the coarse levels
@@ -732,7 +742,10 @@ cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, con
     while (lpt > 4 && cols * ((coarse.nz + lpt - 1) / lpt) < want) lpt = (lpt + 1) / 2;
     dim3 grid((unsigned)((coarse.nx + 31) / 32), (unsigned)((coarse.ny + 3) / 4), (unsigned)((coarse.nz + lpt - 1) / lpt)),
         block(32, 4);
-    k_prolong_add<<<grid, block, 0, ln.stream>>>(coarse, fine, uc, uf, lpt, skip);
+    if (part == PART_INTERIOR) grid.y = (unsigned)((std::max<int64_t>(coarse.ny - 2, 0) + 3) / 4);
+    if (part == PART_BOUNDARY) grid.y = 1;
+    if (grid.y == 0) return cudaSuccess;
+    k_prolong_add<<<grid, block, 0, ln.stream>>>(coarse, fine, uc, uf, lpt, skip, part);
     if (ln.launch_counter) ++*ln.launch_counter;
     return cudaGetLastError();
 }

@@ -35,7 +35,21 @@ struct ReduceSlot {
     double* partials;   // >= gridDim.x * nvals
     unsigned* ticket;   // zero on entry, reset to zero by the last block
     double* result;     // nvals doubles (device)
+    int accumulate;     // 1: result += sum (second launch of an interior/boundary pair)
 };
+
+// Tile-row subsets for overlapping a halo exchange with interior work:
+// PART_ALL every tile row; PART_INTERIOR rows 1 .. nty-2 (they read no halo row);
+// PART_BOUNDARY rows 0 and nty-1.
+enum TilePart : int { PART_ALL = 0, PART_INTERIOR = 1, PART_BOUNDARY = 2 };
+__host__ __device__ inline int part_rows(int part, int nty)
+{
+    return part == PART_ALL ? nty : part == PART_INTERIOR ? (nty > 2 ? nty - 2 : 0) : (nty < 2 ? nty : 2);
+}
+__host__ __device__ inline int part_row(int part, int nty, int idx)
+{
+    return part == PART_ALL ? idx : part == PART_INTERIOR ? idx + 1 : (idx == 0 ? 0 : nty - 1);
+}
 
 // Scalar ratio read on the device: value = num_idx < 0 ? 0 : s[num]/s[den].
 struct DevRatio {
@@ -88,6 +102,7 @@ struct LineArgs {
     ReduceSlot red;    // result may be nullptr: no reduction
     int use_tma;       // 1: loads by TMA (tma must be filled), 0: cp.async
     const int* skip;   // device flag: the kernel returns at once when *skip != 0 (solver run-ahead)
+    int part;          // TilePart: which tile rows this launch covers
     TmaMaps tma;
 };
 
@@ -95,7 +110,11 @@ struct Launcher {
     cudaStream_t stream;
     int num_sms;
     int64_t* launch_counter;
+    int reserve_sms;   // SMs left free (for NCCL kernels running concurrently)
 };
+
+// Tile rows of the line kernel that will run for (mode, nz, nx) (TY of the chosen kernel).
+int line_launch_rows(int mode, int nz, int nx, int use_tma, int ksplit_cfg);
 
 cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a);
 // Tile rows TY the launcher uses for `mode` at this nz (the TMA boxes depend on it).
@@ -132,7 +151,8 @@ cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const Le
                             const double* r, double* fc);
 // u_f += P u_c (bilinear, zero coarse ghosts)
 cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse,
-                               const LevelConst& fine, HaloField uc, double* uf, const int* skip = nullptr);
+                               const LevelConst& fine, HaloField uc, double* uf, const int* skip = nullptr,
+                               int part = PART_ALL);
 // dst = src (n doubles) unless *skip
 cudaError_t launch_copy(const Launcher& ln, double* dst, const double* src, int64_t n, const int* skip);
 

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     double acc[1] = {0.0};
 
     const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + TY - 1) / TY);
-    const int ntiles = ntx * nty;
+    const int ntiles = ntx * part_rows(a.part, nty);
     const int my_tiles = ((int)blockIdx.x < ntiles) ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
     const int total = my_tiles * NCC;
     __syncthreads();
@@ -157,8 +157,8 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     auto issue = [&]() {
         if (tid == 0 && p_count < total) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            tma_step<MODE, TY, KB, NSEG>(stage + p_slot * STG, a, (p_tile % ntx) * TX, (p_tile / ntx) * TY, p_cc,
-                                         &full_bar[p_slot]);
+            tma_step<MODE, TY, KB, NSEG>(stage + p_slot * STG, a, (p_tile % ntx) * TX,
+                                         part_row(a.part, nty, p_tile / ntx) * TY, p_cc, &full_bar[p_slot]);
         }
         ++p_count;
         if (++p_slot == NS2) p_slot = 0;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
 
     for (int tl = 0; tl < my_tiles; ++tl) {
         const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
-        const int i0 = (tile % ntx) * TX, j0 = (tile / ntx) * TY;
+        const int i0 = (tile % ntx) * TX, j0 = part_row(a.part, nty, tile / ntx) * TY;
         const int64_t i = i0 + lane, j = j0 + ty;
         const bool valid = (i < nx) && (j < ny);
 
@@ -333,8 +333,8 @@ cudaError_t launch_k(const Launcher& ln, const LineArgs& a, const KTables& T)
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * TY * NSEG, smem);
     if (e != cudaSuccess) return e;
     per_sm = std::max(per_sm, 1);
-    const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * ((a.L.ny + TY - 1) / TY);
-    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)ln.num_sms * per_sm);
+    const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * part_rows(a.part, (int)((a.L.ny + TY - 1) / TY));
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, ln.num_sms - ln.reserve_sms) * per_sm);
     if (grid <= 0) return cudaSuccess;
     kern<<<(unsigned)grid, 32 * TY * NSEG, smem, ln.stream>>>(a, T);
     if (ln.launch_counter) ++*ln.launch_counter;
