@@ -22,7 +22,7 @@
 // g' buffer in shared memory a CTA holds TY * NSEG warps.
 //
 // Shared memory per stage and segment (TMA, 128-byte aligned blocks):
-//   u box   (TY+2 rows) x (KB+2 levels) x HX columns starting at column i0-4: the
+//   u box   (TY+2 rows) x (KB+2 levels) x HX columns (see KGeom): the
 //           vertical neighbours of the chunk's first and last level come with the
 //           box, so chunks are independent; each row block is 128-byte aligned so a
 //           tile on a strip boundary loads its halo row from the neighbour's slab
@@ -42,26 +42,33 @@ using namespace dev;
 
 constexpr int TX = kTileX;
 constexpr int SL = kSegK;      // levels per segment
-constexpr int HX = TX + 8;     // u box row width: columns i0-4 .. i0+35
-constexpr int XO = 4;          // box column of i0
 constexpr int HXC = 32;        // coarse box row width: coarse columns i0/2-8 .. i0/2+23
 constexpr int XOC = 8;         // coarse box column of i0/2
 
 __host__ __device__ constexpr int r16(int n) { return (n + 15) & ~15; }
 
+// Two u-box layouts.  Smoother / restriction: rows of HX = 36 columns (i0-2 ..
+// i0+33) loaded as one box; at a strip boundary the halo row comes from the
+// neighbour's slab into a separate 128-byte aligned slot (SROW) and the stencil
+// reads it through a row pointer.  Fused prolongation: rows of 40 columns (i0-4 ..
+// i0+35) so every row block is 128-byte aligned and a slab row is loaded in place
+// (one TMA per row), because u + P u_c is formed on the whole box, slab rows included.
 template <int MODE, int TY, int KB>
 struct KGeom {
     static constexpr bool HALO = (MODE == MODE_SMOOTH || MODE == MODE_RESTRICT || MODE == MODE_SMOOTH_PROLONG);
     static constexpr bool PROL = (MODE == MODE_SMOOTH_PROLONG);
+    static constexpr int HX = PROL ? TX + 8 : TX + 4;           // u box row width
+    static constexpr int XO = PROL ? 4 : 2;                     // box column of i0
     static constexpr int D = KB + 2;                            // box depth (levels k0-1 .. k0+KB)
-    static constexpr int UROW = D * HX;                         // one u row block (128-byte multiple)
-    static constexpr int UBOX = HALO ? (TY + 2) * UROW : 0;
+    static constexpr int UROW = D * HX;                         // one u row block
+    static constexpr int UBOX = HALO ? r16((TY + 2) * UROW) : 0;
+    static constexpr int SROW = (HALO && !PROL) ? r16(UROW) : 0;  // one slab row slot
     static constexpr int FBOX = TY * KB * TX;
     static constexpr int CROWS = TY / 2 + 2;
     static constexpr int CROW = D * HXC;
     static constexpr int CBOX = PROL ? CROWS * CROW : 0;
-    static constexpr int SEGST = UBOX + FBOX + CBOX;            // doubles per segment per stage
-    static_assert((UROW * 8) % 128 == 0 && (CROW * 8) % 128 == 0 && (FBOX * 8) % 128 == 0, "TMA alignment");
+    static constexpr int SEGST = UBOX + 2 * SROW + FBOX + CBOX;  // doubles per segment per stage
+    static_assert(!PROL || ((UROW * 8) % 128 == 0 && (CROW * 8) % 128 == 0), "TMA row alignment");
     // exchange buffer: Thomas segment chaining [2][TY][NSEG][32], or (MODE_RESTRICT)
     // x-pair residual sums [2 (chunk parity)][TY][NSEG][KB][16]
     template <int NSEG>
@@ -92,17 +99,28 @@ __device__ __forceinline__ void tma_step(double* st, const LineArgs& a, int i0, 
 {
     using G = KGeom<MODE, TY, KB>;
     const int ny = (int)a.L.ny;
-    constexpr uint32_t bytes = NSEG * (G::UBOX + G::FBOX + G::CBOX) * 8;
+    uint32_t bytes = NSEG * ((G::HALO ? (TY + 2) * G::UROW : 0) + G::FBOX + G::CBOX) * 8;
+    bool lo = false, hi = false;
+    if constexpr (G::HALO && !G::PROL) {
+        lo = a.tma.h[0].has_lo && j0 == 0;
+        hi = a.tma.h[0].has_hi && j0 + TY >= ny;
+        bytes += NSEG * ((lo ? 1 : 0) + (hi ? 1 : 0)) * G::UROW * 8;
+    }
     mbar_expect_tx(bar, bytes);
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) {
         double* seg = st + s * G::SEGST;
         const int k0 = s * SL + cc * KB;
-        if constexpr (G::HALO) tma_rows(seg, a.tma.h[0], TY + 2, G::UROW, i0 - XO, k0 - 1, j0 - 1, ny, bar);
-        tma_load_3d(seg + G::UBOX, &a.tma.q[0], i0, k0, j0, bar);
-        if constexpr (G::PROL)
+        if constexpr (G::PROL) {
+            tma_rows(seg, a.tma.h[0], TY + 2, G::UROW, i0 - G::XO, k0 - 1, j0 - 1, ny, bar);
             tma_rows(seg + G::UBOX + G::FBOX, a.tma.h[1], G::CROWS, G::CROW, i0 / 2 - XOC, k0 - 1, j0 / 2 - 1, ny / 2,
                      bar);
+        } else if constexpr (G::HALO) {
+            tma_load_3d(seg, &a.tma.h[0].main, i0 - G::XO, k0 - 1, j0 - 1, bar);
+            if (lo) tma_load_3d(seg + G::UBOX, &a.tma.h[0].lo, i0 - G::XO, k0 - 1, 0, bar);
+            if (hi) tma_load_3d(seg + G::UBOX + G::SROW, &a.tma.h[0].hi, i0 - G::XO, k0 - 1, 0, bar);
+        }
+        tma_load_3d(seg + G::UBOX + 2 * G::SROW, &a.tma.q[0], i0, k0, j0, bar);
     }
 }
 
@@ -179,6 +197,9 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
         const int i0 = (tile % ntx) * TX, j0 = part_row(a.part, nty, tile / ntx) * TY;
         const int64_t i = i0 + lane, j = j0 + ty;
         const bool valid = (i < nx) && (j < ny);
+        // halo rows of this warp's row j kept in the slab slots (layout without in-place rows)
+        const bool s_slab = G::SROW && a.tma.h[0].has_lo && j0 == 0 && ty == 0;
+        const bool n_slab = G::SROW && a.tma.h[0].has_hi && (j0 + ty + 1 == ny);
 
         double yv[THOMAS ? SL : 1];
         double yprev = 0.0;
@@ -192,14 +213,14 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
                 // u <- u + P u_c on the u box of this segment (the TY warps of the segment
                 // share it; named barrier s+1).  Only in-domain fine cells change: the zero
                 // ghosts stay zero; halo rows from a neighbour's slab get the correction too.
-                const double* cb = seg + G::UBOX + G::FBOX;
+                const double* cb = seg + G::UBOX + 2 * G::SROW + G::FBOX;
                 const int tseg = ty * 32 + lane;   // thread index within the segment's warps
                 const bool slo = a.tma.h[0].has_lo, shi = a.tma.h[0].has_hi;
                 for (int e = tseg; e < (TY + 2) * G::D * (TX + 2); e += TY * 32) {
-                    const int x = XO - 1 + e % (TX + 2);          // box columns read by the stencil
+                    const int x = G::XO - 1 + e % (TX + 2);       // box columns read by the stencil
                     const int rd = e / (TX + 2);
                     const int d = rd % G::D, r = rd / G::D;
-                    const int ig = i0 - XO + x, jg = j0 - 1 + r;
+                    const int ig = i0 - G::XO + x, jg = j0 - 1 + r;
                     const bool in = ig >= 0 && ig < nx &&
                                     ((jg >= 0 && jg < ny) || (jg == -1 && slo) || (jg == ny && shi));
                     if (in) {
@@ -207,23 +228,26 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
                         const int sx = (ig & 1) ? 1 : -1, sy = (jg & 1) ? HXC * G::D : -HXC * G::D;
                         const double* cp = cb + (cy * G::D + d) * HXC + cx;
                         const double v = 9.0 * cp[0] + 3.0 * cp[sx] + 3.0 * cp[sy] + 1.0 * cp[sy + sx];
-                        double* up = seg + (r * G::D + d) * HX + x;
+                        double* up = seg + (r * G::D + d) * G::HX + x;
                         *up = *up + v / 16.0;
                     }
                 }
                 asm volatile("bar.sync %0, %1;\n" ::"r"(s + 1), "r"(TY * 32) : "memory");
             }
-            const double* fb = seg + G::UBOX + ty * (KB * TX) + lane;
+            const double* fb = seg + G::UBOX + 2 * G::SROW + ty * (KB * TX) + lane;
             double gv[KB], rv[KB];
             if constexpr (G::HALO) {
-                const double* rc = seg + (ty + 1) * G::UROW + lane + XO;     // own row
+                constexpr int HX = G::HX;
+                const double* rc = seg + (ty + 1) * G::UROW + lane + G::XO;                    // own row
+                const double* rs = s_slab ? seg + G::UBOX + lane + G::XO : rc - G::UROW;         // south row
+                const double* rn = n_slab ? seg + G::UBOX + G::SROW + lane + G::XO : rc + G::UROW;  // north row
                 double ud = rc[0], uc = rc[HX];
 #pragma unroll
                 for (int kk = 0; kk < KB; ++kk) {
                     const int dd = kk + 1;                 // box level of k = k0 + kk
                     const int k = s * SL + cc * KB + kk;
                     const double uu = rc[(dd + 1) * HX];
-                    const double S = (rc[dd * HX - 1] + rc[dd * HX + 1]) + (rc[dd * HX - G::UROW] + rc[dd * HX + G::UROW]);
+                    const double S = (rc[dd * HX - 1] + rc[dd * HX + 1]) + (rs[dd * HX] + rn[dd * HX]);
                     const double Mu = fma(-gamma, ud + uu, diag[k] * uc);       // (M_T u)_k
                     const double r = fma(c, S, fb[kk * TX]) - Mu;               // f - A u
                     gv[kk] = fma(rho, r, Mu);            // g = (M - rho A) u + rho f  (one-pass smoother)
@@ -369,9 +393,9 @@ bool ksplit_supported(int mode, int nz, int nx)
 
 KsplitBoxes ksplit_boxes(int mode, int cfg)
 {
-    (void)mode;
     const Cfg c = kCfg[cfg < 0 || cfg > 2 ? 0 : cfg];
-    return KsplitBoxes{c.ty, c.kb, HX, c.kb + 2, XO, HXC, XOC};
+    const bool prol = (mode == MODE_SMOOTH_PROLONG);
+    return KsplitBoxes{c.ty, c.kb, prol ? TX + 8 : TX + 4, c.kb + 2, prol ? 4 : 2, HXC, XOC};
 }
 
 cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const LineArgs& a, const KTables& T)
