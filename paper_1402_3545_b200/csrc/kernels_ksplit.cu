@@ -416,7 +416,7 @@ cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const Line
         return launch_k_nseg<MODE_PREC, 2, 8, 4>(ln, a, T);
     }
     if (mode == MODE_RESTRICT) {   // no Thomas: the exchange buffer replaces the chaining buffer
-        if (cfg == 1) return launch_k_nseg<MODE_RESTRICT, 4, 4, 3>(ln, a, T);
+        if (cfg == 1) return launch_k_nseg<MODE_RESTRICT, 4, 4, 2>(ln, a, T);
         if (cfg == 2) return launch_k_nseg<MODE_RESTRICT, 2, 4, 3>(ln, a, T);
         return launch_k_nseg<MODE_RESTRICT, 2, 8, 2>(ln, a, T);
     }
