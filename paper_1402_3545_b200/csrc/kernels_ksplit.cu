@@ -47,28 +47,30 @@ constexpr int XOC = 8;         // coarse box column of i0/2
 
 __host__ __device__ constexpr int r16(int n) { return (n + 15) & ~15; }
 
-// Two u-box layouts.  Smoother / restriction: rows of HX = 36 columns (i0-2 ..
-// i0+33) loaded as one box; at a strip boundary the halo row comes from the
-// neighbour's slab into a separate 128-byte aligned slot (SROW) and the stencil
-// reads it through a row pointer.  Fused prolongation: rows of 40 columns (i0-4 ..
-// i0+35) so every row block is 128-byte aligned and a slab row is loaded in place
-// (one TMA per row), because u + P u_c is formed on the whole box, slab rows included.
+// Two u-box layouts.  Smoother: rows of HX = 36 columns (i0-2 .. i0+33) loaded as
+// one box; at a strip boundary the halo row comes from the neighbour's slab into a
+// separate 128-byte aligned slot (SROW) and the stencil reads it through a row
+// pointer.  Restriction and fused prolongation ("in place"): rows of 40 columns
+// (i0-4 .. i0+35) so every row block is 128-byte aligned and a slab row is loaded in
+// place (one TMA per row); this layout needs no slab slots (restriction: 3 stages fit)
+// and lets the fused prolongation form u + P u_c on the whole box, slab rows included.
 template <int MODE, int TY, int KB>
 struct KGeom {
     static constexpr bool HALO = (MODE == MODE_SMOOTH || MODE == MODE_RESTRICT || MODE == MODE_SMOOTH_PROLONG);
     static constexpr bool PROL = (MODE == MODE_SMOOTH_PROLONG);
-    static constexpr int HX = PROL ? TX + 8 : TX + 4;           // u box row width
-    static constexpr int XO = PROL ? 4 : 2;                     // box column of i0
+    static constexpr bool INPLACE = PROL || MODE == MODE_RESTRICT;  // aligned rows, slab rows in place
+    static constexpr int HX = INPLACE ? TX + 8 : TX + 4;        // u box row width
+    static constexpr int XO = INPLACE ? 4 : 2;                  // box column of i0
     static constexpr int D = KB + 2;                            // box depth (levels k0-1 .. k0+KB)
     static constexpr int UROW = D * HX;                         // one u row block
     static constexpr int UBOX = HALO ? r16((TY + 2) * UROW) : 0;
-    static constexpr int SROW = (HALO && !PROL) ? r16(UROW) : 0;  // one slab row slot
+    static constexpr int SROW = (HALO && !INPLACE) ? r16(UROW) : 0;  // one slab row slot
     static constexpr int FBOX = TY * KB * TX;
     static constexpr int CROWS = TY / 2 + 2;
     static constexpr int CROW = D * HXC;
     static constexpr int CBOX = PROL ? CROWS * CROW : 0;
     static constexpr int SEGST = UBOX + 2 * SROW + FBOX + CBOX;  // doubles per segment per stage
-    static_assert(!PROL || ((UROW * 8) % 128 == 0 && (CROW * 8) % 128 == 0), "TMA row alignment");
+    static_assert(!INPLACE || ((UROW * 8) % 128 == 0 && (CROW * 8) % 128 == 0), "TMA row alignment");
     // exchange buffer: Thomas segment chaining [2][TY][NSEG][32], or (MODE_RESTRICT)
     // x-pair residual sums [2 (chunk parity)][TY][NSEG][KB][16]
     template <int NSEG>
@@ -101,7 +103,7 @@ __device__ __forceinline__ void tma_step(double* st, const LineArgs& a, int i0, 
     const int ny = (int)a.L.ny;
     uint32_t bytes = NSEG * ((G::HALO ? (TY + 2) * G::UROW : 0) + G::FBOX + G::CBOX) * 8;
     bool lo = false, hi = false;
-    if constexpr (G::HALO && !G::PROL) {
+    if constexpr (G::HALO && !G::INPLACE) {
         lo = a.tma.h[0].has_lo && j0 == 0;
         hi = a.tma.h[0].has_hi && j0 + TY >= ny;
         bytes += NSEG * ((lo ? 1 : 0) + (hi ? 1 : 0)) * G::UROW * 8;
@@ -111,10 +113,11 @@ __device__ __forceinline__ void tma_step(double* st, const LineArgs& a, int i0, 
     for (int s = 0; s < NSEG; ++s) {
         double* seg = st + s * G::SEGST;
         const int k0 = s * SL + cc * KB;
-        if constexpr (G::PROL) {
+        if constexpr (G::INPLACE) {
             tma_rows(seg, a.tma.h[0], TY + 2, G::UROW, i0 - G::XO, k0 - 1, j0 - 1, ny, bar);
-            tma_rows(seg + G::UBOX + G::FBOX, a.tma.h[1], G::CROWS, G::CROW, i0 / 2 - XOC, k0 - 1, j0 / 2 - 1, ny / 2,
-                     bar);
+            if constexpr (G::PROL)
+                tma_rows(seg + G::UBOX + G::FBOX, a.tma.h[1], G::CROWS, G::CROW, i0 / 2 - XOC, k0 - 1, j0 / 2 - 1,
+                         ny / 2, bar);
         } else if constexpr (G::HALO) {
             tma_load_3d(seg, &a.tma.h[0].main, i0 - G::XO, k0 - 1, j0 - 1, bar);
             if (lo) tma_load_3d(seg + G::UBOX, &a.tma.h[0].lo, i0 - G::XO, k0 - 1, 0, bar);
@@ -394,8 +397,8 @@ bool ksplit_supported(int mode, int nz, int nx)
 KsplitBoxes ksplit_boxes(int mode, int cfg)
 {
     const Cfg c = kCfg[cfg < 0 || cfg > 2 ? 0 : cfg];
-    const bool prol = (mode == MODE_SMOOTH_PROLONG);
-    return KsplitBoxes{c.ty, c.kb, prol ? TX + 8 : TX + 4, c.kb + 2, prol ? 4 : 2, HXC, XOC};
+    const bool inplace = (mode == MODE_SMOOTH_PROLONG || mode == MODE_RESTRICT);
+    return KsplitBoxes{c.ty, c.kb, inplace ? TX + 8 : TX + 4, c.kb + 2, inplace ? 4 : 2, HXC, XOC};
 }
 
 cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const LineArgs& a, const KTables& T)
@@ -416,7 +419,7 @@ cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const Line
         return launch_k_nseg<MODE_PREC, 2, 8, 4>(ln, a, T);
     }
     if (mode == MODE_RESTRICT) {   // no Thomas: the exchange buffer replaces the chaining buffer
-        if (cfg == 1) return launch_k_nseg<MODE_RESTRICT, 4, 4, 2>(ln, a, T);
+        if (cfg == 1) return launch_k_nseg<MODE_RESTRICT, 4, 4, 3>(ln, a, T);
         if (cfg == 2) return launch_k_nseg<MODE_RESTRICT, 2, 4, 3>(ln, a, T);
         return launch_k_nseg<MODE_RESTRICT, 2, 8, 2>(ln, a, T);
     }
