@@ -76,7 +76,8 @@ struct tpmg_ctx {
     ncclComm_t comm_halo = nullptr;     // halo traffic on its own communicator and stream
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
-    bool overlap = true;                // TPMG_OVERLAP=0 disables
+    bool overlap = false;               // TPMG_OVERLAP=1 enables (measured slower at N=4: the split
+                                        // launches cost more than the NCCL latency they hide)
     int reserve_sms = 4;                // SMs left to NCCL while the interior runs
     int cur_reserve = 0;
     tpmg_stats stats{};
@@ -1148,7 +1149,7 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         const char* ks = std::getenv("TPMG_KSPLIT");
         ctx->ksplit_cfg = !ks ? 1 : ks[0] == '0' ? -1 : ks[0] == '1' ? 0 : ks[0] == '3' ? 2 : 1;
         const char* ov = std::getenv("TPMG_OVERLAP");
-        ctx->overlap = !(ov && ov[0] == '0');
+        ctx->overlap = ov && ov[0] == '1';
         const char* rs = std::getenv("TPMG_RESERVE_SMS");
         if (rs) ctx->reserve_sms = std::max(0, std::atoi(rs));
         const char* fp = std::getenv("TPMG_FUSE_PROLONG");
