@@ -72,6 +72,23 @@ struct tpmg_ctx {
     double *cg_zlo = nullptr, *cg_zhi = nullptr, *cg_plo[2] = {nullptr, nullptr}, *cg_phi[2] = {nullptr, nullptr};
     double *host_f = nullptr, *host_u = nullptr;  // device buffers for tpmg_solve_host
     ncclComm_t comm = nullptr;
+    // halo channels (nranks > 1): 1..L = levels, L+1 = CG z.  Each has double-buffered slabs
+    // in one pool allocation; in P2P mode the neighbours write into them over NVLink.
+    struct Chan {
+        size_t plane = 0;
+        int64_t nyl = 0;
+        double* lo[2] = {nullptr, nullptr};
+        double* hi[2] = {nullptr, nullptr};
+        double** cur_lo = nullptr;      // where consumers look for the current slabs
+        double** cur_hi = nullptr;
+        int epoch = 0;
+        size_t off_lo[2] = {0, 0}, off_hi[2] = {0, 0}, off_flags = 0;  // byte offsets in the pool
+    };
+    std::vector<Chan> chans;
+    void* halo_pool = nullptr;
+    size_t halo_pool_bytes = 0;
+    bool p2p = false;                   // TPMG_HALO=nccl selects NCCL send/recv
+    char* peer_pool[2] = {nullptr, nullptr};   // [0] lower neighbour's pool, [1] upper's (IPC-mapped)
     // overlap of halo exchanges with interior work (nranks > 1)
     ncclComm_t comm_halo = nullptr;     // halo traffic on its own communicator and stream
     cudaStream_t comm_stream = nullptr;
@@ -191,14 +208,94 @@ tpmg_status exchange_on(tpmg_ctx* ctx, cudaStream_t st, ncclComm_t comm, size_t 
     return TPMG_OK;
 }
 
-// Fill the halo slabs of `level` from the neighbours' boundary rows of x (nranks > 1),
-// in stream order on the context stream.
-tpmg_status exchange(tpmg_ctx* ctx, int level, const double* x, double* lo, double* hi)
+// ---- device-initiated halo exchange over NVLink (P2P mode)
+PFN_cuStreamWaitValue32_v11070 g_wait_value = nullptr;
+PFN_cuStreamWriteValue32_v11070 g_write_value = nullptr;
+
+bool stream_memops()
+{
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_wait_value = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
+        p = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_write_value = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p);
+    }
+    return g_wait_value && g_write_value;
+}
+
+tpmg_status wait_value(tpmg_ctx* ctx, const void* addr, uint32_t v)
+{
+    CUresult r = g_wait_value((CUstream)ctx->stream, (CUdeviceptr)addr, v, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return fail(ctx, TPMG_E_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+    return TPMG_OK;
+}
+
+tpmg_status write_value(tpmg_ctx* ctx, void* addr, uint32_t v)
+{
+    CUresult r = g_write_value((CUstream)ctx->stream, (CUdeviceptr)addr, v, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) return fail(ctx, TPMG_E_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+    return TPMG_OK;
+}
+
+// Channel c exchange, epoch E, buffer b = E & 1.  Flags (uint32) of channel c in every
+// rank's pool: [0] data from the lower neighbour, [1] data from the upper, [2] ack from
+// the lower, [3] ack from the upper.  Stream order on the context stream:
+//   ack:   tell each neighbour I am done reading my slabs of epochs <= E-1;
+//   wait:  each neighbour is done reading its buffer b of epoch E-2 (double buffering);
+//   push:  one kernel stores my row 0 into the lower neighbour's hi[b] slab and my row
+//          ny-1 into the upper neighbour's lo[b] slab (remote stores over NVLink);
+//   flag:  write E into each neighbour's data flag (the write is fenced after the push);
+//   wait:  the neighbours' data for epoch E has arrived in my lo[b] / hi[b].
+// No kernel spins: the waits are stream memory operations.
+tpmg_status exchange_p2p(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int c, const double* x)
+{
+    const int E = ++ch.epoch;
+    const int b = E & 1;
+    const bool has_lo = ctx->rank > 0, has_hi = ctx->rank < ctx->nranks - 1;
+    char* mine = static_cast<char*>(ctx->halo_pool) + ch.off_flags;
+    char* lo_nb = has_lo ? ctx->peer_pool[0] + ch.off_flags : nullptr;
+    char* hi_nb = has_hi ? ctx->peer_pool[1] + ch.off_flags : nullptr;
+    (void)c;
+    if (E >= 2) {
+        if (has_lo) TRY(write_value(ctx, lo_nb + 3 * 4, (uint32_t)(E - 1)));   // lower nbr's "ack from upper"
+        if (has_hi) TRY(write_value(ctx, hi_nb + 2 * 4, (uint32_t)(E - 1)));   // upper nbr's "ack from lower"
+    }
+    if (E >= 3) {
+        if (has_lo) TRY(wait_value(ctx, mine + 2 * 4, (uint32_t)(E - 2)));
+        if (has_hi) TRY(wait_value(ctx, mine + 3 * 4, (uint32_t)(E - 2)));
+    }
+    double* dst_lo = has_lo ? reinterpret_cast<double*>(ctx->peer_pool[0] + ch.off_hi[b]) : nullptr;
+    double* dst_hi = has_hi ? reinterpret_cast<double*>(ctx->peer_pool[1] + ch.off_lo[b]) : nullptr;
+    CUDA_TRY(ctx, launch_halo_push(launcher(ctx), x, dst_lo, x + (size_t)(ch.nyl - 1) * ch.plane, dst_hi,
+                                   (int64_t)ch.plane));
+    if (has_lo) TRY(write_value(ctx, lo_nb + 1 * 4, (uint32_t)E));   // lower nbr's "data from upper"
+    if (has_hi) TRY(write_value(ctx, hi_nb + 0 * 4, (uint32_t)E));   // upper nbr's "data from lower"
+    if (has_lo) TRY(wait_value(ctx, mine + 0 * 4, (uint32_t)E));
+    if (has_hi) TRY(wait_value(ctx, mine + 1 * 4, (uint32_t)E));
+    *ch.cur_lo = ch.lo[b];
+    *ch.cur_hi = ch.hi[b];
+    ++ctx->stats.halo_exchanges;
+    return TPMG_OK;
+}
+
+// Fill the current halo slabs of channel c (a level, or the CG z channel) from the
+// neighbours' boundary rows of x (nranks > 1), in stream order on the context stream.
+tpmg_status exchange_chan(tpmg_ctx* ctx, int c, const double* x)
 {
     if (ctx->nranks == 1) return TPMG_OK;
-    LevelData& L = ctx->lv[level];
-    return exchange_on(ctx, ctx->stream, ctx->comm, L.plane(), L.lc.ny, x, lo, hi);
+    tpmg_ctx::Chan& ch = ctx->chans[c];
+    if (ctx->p2p) return exchange_p2p(ctx, ch, c, x);
+    return exchange_on(ctx, ctx->stream, ctx->comm, ch.plane, ch.nyl, x, *ch.cur_lo, *ch.cur_hi);
 }
+
+tpmg_status exchange(tpmg_ctx* ctx, int level, const double* x) { return exchange_chan(ctx, level, x); }
 
 // Start the exchange on the halo stream once everything enqueued so far on the
 // context stream is done; finish_async_exchange() makes the context stream wait for it.
@@ -227,7 +324,7 @@ HaloField halo_of(tpmg_ctx* ctx, int level, const double* x)
 // Exchange x's halo into the level slabs and return the halo'd view.
 tpmg_status halo(tpmg_ctx* ctx, int level, const double* x, HaloField* out)
 {
-    TRY(exchange(ctx, level, x, ctx->lv[level].slab_lo, ctx->lv[level].slab_hi));
+    TRY(exchange(ctx, level, x));
     *out = halo_of(ctx, level, x);
     return TPMG_OK;
 }
@@ -503,8 +600,9 @@ tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, LineArgs a, const 
     const LevelConst& lc = ctx->lv[level].lc;
     const int TY = line_launch_rows(mode, lc.nz, (int)lc.nx, ctx->use_tma ? 1 : 0, ctx->ksplit_cfg);
     const int nty = (int)((lc.ny + TY - 1) / TY);
-    if (!ctx->overlap || nty < 3) {
-        TRY(exchange_on(ctx, ctx->stream, ctx->comm, ctx->lv[level].plane(), lc.ny, x, lo, hi));
+    if (!ctx->overlap || ctx->p2p || nty < 3) {
+        TRY(exchange(ctx, level, x));
+        if (a.h0.base == x) a.h0 = halo_of(ctx, level, x);   // P2P: the current slab buffer alternates
         TRY(pre_boundary());
         return run_line(ctx, mode, a);
     }
@@ -592,10 +690,11 @@ tpmg_status prolong_overlapped(tpmg_ctx* ctx, int lc_)
     LevelData& F = ctx->lv[lc_ + 1];
     const HaloField uc = halo_of(ctx, lc_, Cc.u[Cc.cur]);
     const double cells = level_cells(F.lc);
-    if (ctx->nranks == 1 || !ctx->overlap || Cc.lc.ny < 3) {
-        TRY(exchange(ctx, lc_, Cc.u[Cc.cur], Cc.slab_lo, Cc.slab_hi));
+    if (ctx->nranks == 1 || !ctx->overlap || ctx->p2p || Cc.lc.ny < 3) {
+        TRY(exchange(ctx, lc_, Cc.u[Cc.cur]));
+        const HaloField uc2 = halo_of(ctx, lc_, Cc.u[Cc.cur]);   // current slabs after the exchange
         ProfScope ps(ctx, TPMG_K_PROLONG_ADD, cells);
-        CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc, F.u[F.cur], ctx->skip));
+        CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc2, F.u[F.cur], ctx->skip));
         return TPMG_OK;
     }
     TRY(start_async_exchange(ctx, lc_, Cc.u[Cc.cur], Cc.slab_lo, Cc.slab_hi));
@@ -635,8 +734,12 @@ tpmg_status vcycle_rec(tpmg_ctx* ctx, int l, bool skip_pre = false)
     LevelData& Cc = ctx->lv[l - 1];
     LevelData& F = ctx->lv[l];
     HaloField uc = halo_of(ctx, l - 1, Cc.u[Cc.cur]);
+    (void)uc;
     const bool fuse = p.post >= 1 && ctx->fuse_prolong && ksplit_usable(ctx, MODE_SMOOTH_PROLONG, F.lc);
-    if (fuse) TRY(exchange(ctx, l - 1, Cc.u[Cc.cur], Cc.slab_lo, Cc.slab_hi));
+    if (fuse) {
+        TRY(exchange(ctx, l - 1, Cc.u[Cc.cur]));
+        uc = halo_of(ctx, l - 1, Cc.u[Cc.cur]);
+    }
     int s0 = 0;
     if (fuse) {
         // Prolongate fused with the first post-smooth: u' = S(u + P u_c) without storing
@@ -865,8 +968,6 @@ tpmg_status cg_alloc(tpmg_ctx* ctx)
     TRY(dev_alloc(ctx, &ctx->cg_p[0], F.n()));
     TRY(dev_alloc(ctx, &ctx->cg_p[1], F.n()));
     if (ctx->nranks > 1) {
-        TRY(dev_alloc(ctx, &ctx->cg_zlo, F.plane()));
-        TRY(dev_alloc(ctx, &ctx->cg_zhi, F.plane()));
         for (int q = 0; q < 2; ++q) {
             TRY(dev_alloc(ctx, &ctx->cg_plo[q], F.plane()));
             TRY(dev_alloc(ctx, &ctx->cg_phi[q], F.plane()));
@@ -937,9 +1038,16 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
             hz = HaloField{ctx->cg_z, has_lo ? ctx->cg_zlo : nullptr, has_hi ? ctx->cg_zhi : nullptr};
             hp = HaloField{ctx->cg_p[cur], has_lo ? ctx->cg_plo[cur] : nullptr, has_hi ? ctx->cg_phi[cur] : nullptr};
         }
-        // (Fused) direction kernel: p = z + beta p, sigma = <p, A p>.  The z halo is
-        // exchanged while the interior runs; the p halo is local:
-        // p_halo <- z_halo + beta p_halo (same fma as the neighbour's own rows).
+        // (Fused) direction kernel: p = z + beta p, sigma = <p, A p>.  Only z crosses NVLink;
+        // the p halo is local: p_halo <- z_halo + beta p_halo (same fma as the neighbour's
+        // own rows).
+        if (ctx->nranks > 1) {
+            TRY(exchange_chan(ctx, l + 1, ctx->cg_z));
+            hz = HaloField{ctx->cg_z, has_lo ? ctx->cg_zlo : nullptr, has_hi ? ctx->cg_zhi : nullptr};
+            CUDA_TRY(ctx, launch_cg_halo(launcher(ctx), has_lo ? ctx->cg_plo[1 - cur] : nullptr, hz.lo, hp.lo,
+                                         has_hi ? ctx->cg_phi[1 - cur] : nullptr, hz.hi, hp.hi, (int64_t)plane, beta,
+                                         ctx->skip));
+        }
         {
             LineArgs a = line_args(ctx, l);
             a.h0 = hz;
@@ -947,14 +1055,7 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
             a.out0 = ctx->cg_p[1 - cur];
             a.ratio = beta;
             a.red.result = ctx->d_scal + S_SIGMA(m);
-            const int c2 = cur;
-            TRY(run_line_halo(ctx, l, MODE_CGDIR, a, ctx->cg_z, ctx->cg_zlo, ctx->cg_zhi, [&]() -> tpmg_status {
-                if (ctx->nranks > 1)
-                    CUDA_TRY(ctx, launch_cg_halo(launcher(ctx), has_lo ? ctx->cg_plo[1 - c2] : nullptr, hz.lo, hp.lo,
-                                                 has_hi ? ctx->cg_phi[1 - c2] : nullptr, hz.hi, hp.hi,
-                                                 (int64_t)plane, beta, ctx->skip));
-                return TPMG_OK;
-            }));
+            TRY(run_line(ctx, MODE_CGDIR, a));
             TRY(allreduce(ctx, ctx->d_scal + S_SIGMA(m), 1));
         }
         HaloField hpn{ctx->cg_p[1 - cur], nullptr, nullptr};
@@ -1020,6 +1121,72 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
     return TPMG_OK;
 }
 
+// Halo channels and their pool (nranks > 1).  P2P mode (default): the pool is exported
+// with cudaIpcGetMemHandle, the handles are all-gathered over NCCL, and each rank maps its
+// two neighbours' pools; the exchanges then run as remote stores (exchange_p2p).
+tpmg_status halo_setup(tpmg_ctx* ctx)
+{
+    const int L = ctx->L;
+    ctx->chans.assign(L + 2, tpmg_ctx::Chan{});
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += (bytes + 255) & ~(size_t)255;
+        return o;
+    };
+    for (int c = 1; c <= L + 1; ++c) {
+        tpmg_ctx::Chan& ch = ctx->chans[c];
+        const LevelData& lv = ctx->lv[c <= L ? c : L];
+        ch.plane = lv.plane();
+        ch.nyl = lv.lc.ny;
+        for (int b = 0; b < 2; ++b) {
+            ch.off_lo[b] = take(sizeof(double) * ch.plane);
+            ch.off_hi[b] = take(sizeof(double) * ch.plane);
+        }
+        ch.off_flags = take(4 * sizeof(uint32_t));
+    }
+    ctx->halo_pool_bytes = off;
+    CUDA_TRY(ctx, cudaMalloc(&ctx->halo_pool, off));
+    CUDA_TRY(ctx, cudaMemset(ctx->halo_pool, 0, off));
+    char* base = static_cast<char*>(ctx->halo_pool);
+    for (int c = 1; c <= L + 1; ++c) {
+        tpmg_ctx::Chan& ch = ctx->chans[c];
+        for (int b = 0; b < 2; ++b) {
+            ch.lo[b] = reinterpret_cast<double*>(base + ch.off_lo[b]);
+            ch.hi[b] = reinterpret_cast<double*>(base + ch.off_hi[b]);
+        }
+        ch.cur_lo = (c <= L) ? &ctx->lv[c].slab_lo : &ctx->cg_zlo;
+        ch.cur_hi = (c <= L) ? &ctx->lv[c].slab_hi : &ctx->cg_zhi;
+        *ch.cur_lo = ch.lo[0];
+        *ch.cur_hi = ch.hi[0];
+    }
+    const char* hm = std::getenv("TPMG_HALO");
+    ctx->p2p = !(hm && std::strcmp(hm, "nccl") == 0) && stream_memops();
+    if (!ctx->p2p) return TPMG_OK;
+    // exchange the pool handles
+    cudaIpcMemHandle_t mine;
+    CUDA_TRY(ctx, cudaIpcGetMemHandle(&mine, ctx->halo_pool));
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    char* d_all = nullptr;
+    CUDA_TRY(ctx, cudaMalloc((void**)&d_all, hb * ctx->nranks));
+    CUDA_TRY(ctx, cudaMemcpy(d_all + hb * ctx->rank, &mine, hb, cudaMemcpyHostToDevice));
+    NCCL_TRY(ctx, ncclAllGather(d_all + hb * ctx->rank, d_all, hb, ncclChar, ctx->comm, ctx->stream));
+    std::vector<char> all(hb * ctx->nranks);
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpy(all.data(), d_all, all.size(), cudaMemcpyDeviceToHost));
+    cudaFree(d_all);
+    for (int side = 0; side < 2; ++side) {
+        const int nb = ctx->rank + (side == 0 ? -1 : 1);
+        if (nb < 0 || nb >= ctx->nranks) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, all.data() + hb * nb, hb);
+        void* p = nullptr;
+        CUDA_TRY(ctx, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        ctx->peer_pool[side] = static_cast<char*>(p);
+    }
+    return TPMG_OK;
+}
+
 void params_fill_defaults(tpmg_params* p)
 {
     if (p->nz == 0) p->nz = 128;
@@ -1040,15 +1207,13 @@ void ctx_free(tpmg_ctx* ctx)
         cudaFree(L.d_tab);
         if ((int)l < ctx->L) { cudaFree(L.u[0]); cudaFree(L.f); }
         cudaFree(L.u[1]);
-        cudaFree(L.slab_lo);
-        cudaFree(L.slab_hi);
     }
     cudaFree(ctx->d_partials);
     cudaFree(ctx->d_ticket);
     cudaFree(ctx->d_scal);
     cudaFree(ctx->scratch);
     cudaFree(ctx->cg_r); cudaFree(ctx->cg_z); cudaFree(ctx->cg_p[0]); cudaFree(ctx->cg_p[1]);
-    cudaFree(ctx->cg_zlo); cudaFree(ctx->cg_zhi);
+    // cg_zlo / cg_zhi and the level slabs live in the halo pool
     for (int q = 0; q < 2; ++q) { cudaFree(ctx->cg_plo[q]); cudaFree(ctx->cg_phi[q]); }
     cudaFree(ctx->host_f); cudaFree(ctx->host_u);
     if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
@@ -1060,6 +1225,9 @@ void ctx_free(tpmg_ctx* ctx)
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     for (auto& r : ctx->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ctx->prof_pool) cudaEventDestroy(e);
+    for (auto pp : ctx->peer_pool)
+        if (pp) cudaIpcCloseMemHandle(pp);
+    cudaFree(ctx->halo_pool);
     if (ctx->comm_halo) ncclCommDestroy(ctx->comm_halo);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
@@ -1239,12 +1407,6 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         CREATE_TRY(dev_alloc(ctx, &L.d_tab, tab.size()));
         CREATE_CUDA(cudaMemcpy(L.d_tab, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice));
         L.lc.tab = L.d_tab;
-        if (nranks > 1) {
-            CREATE_TRY(dev_alloc(ctx, &L.slab_lo, L.plane()));
-            CREATE_TRY(dev_alloc(ctx, &L.slab_hi, L.plane()));
-            CREATE_CUDA(cudaMemset(L.slab_lo, 0, sizeof(double) * L.plane()));
-            CREATE_CUDA(cudaMemset(L.slab_hi, 0, sizeof(double) * L.plane()));
-        }
     }
     if (nranks > 1) {
         ncclUniqueId id;
@@ -1262,6 +1424,7 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         CREATE_CUDA(cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, hi_prio));
         CREATE_CUDA(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
         CREATE_CUDA(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
+        CREATE_TRY(halo_setup(ctx));
     }
 #undef CREATE_TRY
 #undef CREATE_CUDA

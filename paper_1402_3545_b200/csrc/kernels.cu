@@ -607,6 +607,16 @@ __global__ void __launch_bounds__(256) k_cg_halo(double* out_lo, const double* z
     }
 }
 
+template <typename V>
+__global__ void __launch_bounds__(256) k_halo_push(const V* __restrict__ src_first, V* dst_lo,
+                                                   const V* __restrict__ src_last, V* dst_hi, int64_t n)
+{
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        if (dst_lo) dst_lo[q] = src_first[q];
+        if (dst_hi) dst_hi[q] = src_last[q];
+    }
+}
+
 // Convergence test of PCG iteration m on the device: ||r_m|| / ||r_0|| < eps
 // (eqn:epsilonTolerance), breakdown when <p, A p> <= 0 or <r, M^-1 r> <= 0.
 __global__ void k_cg_check(const double* scal, int m, double eps, int* flags)
@@ -654,6 +664,23 @@ cudaError_t launch_cg_halo(const Launcher& ln, double* out_lo, const double* z_l
     if (!out_lo && !out_hi) return cudaSuccess;
     const int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)ln.num_sms * 4);
     k_cg_halo<<<(unsigned)grid, 256, 0, ln.stream>>>(out_lo, z_lo, p_lo, out_hi, z_hi, p_hi, n, beta, skip);
+    if (ln.launch_counter) ++*ln.launch_counter;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo_push(const Launcher& ln, const double* src_first, double* dst_lo, const double* src_last,
+                             double* dst_hi, int64_t n)
+{
+    if (!dst_lo && !dst_hi) return cudaSuccess;
+    const bool vec = (n % 2 == 0) && ((uintptr_t)src_first % 16 == 0) && ((uintptr_t)src_last % 16 == 0);
+    const int64_t m = vec ? n / 2 : n;
+    const unsigned grid = (unsigned)std::max<int64_t>(std::min<int64_t>((m + 255) / 256, (int64_t)ln.num_sms), 1);
+    if (vec)
+        k_halo_push<double2><<<grid, 256, 0, ln.stream>>>(
+            reinterpret_cast<const double2*>(src_first), reinterpret_cast<double2*>(dst_lo),
+            reinterpret_cast<const double2*>(src_last), reinterpret_cast<double2*>(dst_hi), m);
+    else
+        k_halo_push<double><<<grid, 256, 0, ln.stream>>>(src_first, dst_lo, src_last, dst_hi, m);
     if (ln.launch_counter) ++*ln.launch_counter;
     return cudaGetLastError();
 }
