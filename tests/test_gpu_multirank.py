@@ -26,6 +26,6 @@ def test_multirank_parity(world, overlap, halo):
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + (10 if halo == "p2p" else 0) + (20 if overlap == "1" else 0)),
            os.path.join(ROOT, "tests", "mr_worker.py")]
     env = dict(os.environ, TPMG_OVERLAP=overlap, TPMG_HALO=halo)
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 0, (r.stdout[-4000:], r.stderr[-4000:])
     assert f"MULTIRANK OK world={world}" in r.stdout
