@@ -210,7 +210,6 @@ tpmg_status exchange_on(tpmg_ctx* ctx, cudaStream_t st, ncclComm_t comm, size_t 
 
 // ---- device-initiated halo exchange over NVLink (P2P mode)
 PFN_cuStreamWaitValue32_v11070 g_wait_value = nullptr;
-PFN_cuStreamWriteValue32_v11070 g_write_value = nullptr;
 
 bool stream_memops()
 {
@@ -222,12 +221,8 @@ bool stream_memops()
         if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
             g_wait_value = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
-        p = nullptr;
-        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            g_write_value = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p);
     }
-    return g_wait_value && g_write_value;
+    return g_wait_value != nullptr;
 }
 
 tpmg_status wait_value(tpmg_ctx* ctx, const void* addr, uint32_t v)
@@ -237,46 +232,33 @@ tpmg_status wait_value(tpmg_ctx* ctx, const void* addr, uint32_t v)
     return TPMG_OK;
 }
 
-tpmg_status write_value(tpmg_ctx* ctx, void* addr, uint32_t v)
-{
-    CUresult r = g_write_value((CUstream)ctx->stream, (CUdeviceptr)addr, v, CU_STREAM_WRITE_VALUE_DEFAULT);
-    if (r != CUDA_SUCCESS) return fail(ctx, TPMG_E_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
-    return TPMG_OK;
-}
-
 // Channel c exchange, epoch E, buffer b = E & 1.  Flags (uint32) of channel c in every
-// rank's pool: [0] data from the lower neighbour, [1] data from the upper, [2] ack from
-// the lower, [3] ack from the upper.  Stream order on the context stream:
-//   ack:   tell each neighbour I am done reading my slabs of epochs <= E-1;
-//   wait:  each neighbour is done reading its buffer b of epoch E-2 (double buffering);
+// rank's pool: [0] data from the lower neighbour, [1] data from the upper, [2] push ticket.
 //   push:  one kernel stores my row 0 into the lower neighbour's hi[b] slab and my row
-//          ny-1 into the upper neighbour's lo[b] slab (remote stores over NVLink);
-//   flag:  write E into each neighbour's data flag (the write is fenced after the push);
-//   wait:  the neighbours' data for epoch E has arrived in my lo[b] / hi[b].
-// No kernel spins: the waits are stream memory operations.
+//          ny-1 into the upper neighbour's lo[b] slab (remote stores over NVLink); its last
+//          block fences (system scope) and writes E into both neighbours' data flags;
+//   wait:  stream memory operations wait until both neighbours' epoch-E data has arrived.
+// No acknowledgements are needed: a neighbour's epoch E-1 push is stream-ordered after its
+// kernels that read epoch E-2 (the slot b that epoch E overwrites), and I push epoch E
+// only after my stream saw its epoch E-1 data.  No kernel spins.
 tpmg_status exchange_p2p(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int c, const double* x)
 {
     const int E = ++ch.epoch;
     const int b = E & 1;
     const bool has_lo = ctx->rank > 0, has_hi = ctx->rank < ctx->nranks - 1;
     char* mine = static_cast<char*>(ctx->halo_pool) + ch.off_flags;
-    char* lo_nb = has_lo ? ctx->peer_pool[0] + ch.off_flags : nullptr;
-    char* hi_nb = has_hi ? ctx->peer_pool[1] + ch.off_flags : nullptr;
     (void)c;
-    if (E >= 2) {
-        if (has_lo) TRY(write_value(ctx, lo_nb + 3 * 4, (uint32_t)(E - 1)));   // lower nbr's "ack from upper"
-        if (has_hi) TRY(write_value(ctx, hi_nb + 2 * 4, (uint32_t)(E - 1)));   // upper nbr's "ack from lower"
-    }
-    if (E >= 3) {
-        if (has_lo) TRY(wait_value(ctx, mine + 2 * 4, (uint32_t)(E - 2)));
-        if (has_hi) TRY(wait_value(ctx, mine + 3 * 4, (uint32_t)(E - 2)));
-    }
-    double* dst_lo = has_lo ? reinterpret_cast<double*>(ctx->peer_pool[0] + ch.off_hi[b]) : nullptr;
-    double* dst_hi = has_hi ? reinterpret_cast<double*>(ctx->peer_pool[1] + ch.off_lo[b]) : nullptr;
-    CUDA_TRY(ctx, launch_halo_push(launcher(ctx), x, dst_lo, x + (size_t)(ch.nyl - 1) * ch.plane, dst_hi,
-                                   (int64_t)ch.plane));
-    if (has_lo) TRY(write_value(ctx, lo_nb + 1 * 4, (uint32_t)E));   // lower nbr's "data from upper"
-    if (has_hi) TRY(write_value(ctx, hi_nb + 0 * 4, (uint32_t)E));   // upper nbr's "data from lower"
+    HaloPush hp{};
+    hp.src_first = x;
+    hp.src_last = x + (size_t)(ch.nyl - 1) * ch.plane;
+    hp.n = (int64_t)ch.plane;
+    hp.dst_lo = has_lo ? reinterpret_cast<double*>(ctx->peer_pool[0] + ch.off_hi[b]) : nullptr;
+    hp.dst_hi = has_hi ? reinterpret_cast<double*>(ctx->peer_pool[1] + ch.off_lo[b]) : nullptr;
+    hp.flag_lo = has_lo ? reinterpret_cast<unsigned*>(ctx->peer_pool[0] + ch.off_flags + 1 * 4) : nullptr;  // its "from upper"
+    hp.flag_hi = has_hi ? reinterpret_cast<unsigned*>(ctx->peer_pool[1] + ch.off_flags + 0 * 4) : nullptr;  // its "from lower"
+    hp.ticket = reinterpret_cast<unsigned*>(mine + 2 * 4);
+    hp.epoch = (unsigned)E;
+    CUDA_TRY(ctx, launch_halo_push(launcher(ctx), hp));
     if (has_lo) TRY(wait_value(ctx, mine + 0 * 4, (uint32_t)E));
     if (has_hi) TRY(wait_value(ctx, mine + 1 * 4, (uint32_t)E));
     *ch.cur_lo = ch.lo[b];

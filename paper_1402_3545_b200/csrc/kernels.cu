@@ -608,12 +608,31 @@ __global__ void __launch_bounds__(256) k_cg_halo(double* out_lo, const double* z
 }
 
 template <typename V>
-__global__ void __launch_bounds__(256) k_halo_push(const V* __restrict__ src_first, V* dst_lo,
-                                                   const V* __restrict__ src_last, V* dst_hi, int64_t n)
+__global__ void __launch_bounds__(256) k_halo_push(const HaloPush hp, int64_t n)
 {
+    const V* sf = reinterpret_cast<const V*>(hp.src_first);
+    const V* sl = reinterpret_cast<const V*>(hp.src_last);
+    V* dl = reinterpret_cast<V*>(hp.dst_lo);
+    V* dh = reinterpret_cast<V*>(hp.dst_hi);
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-        if (dst_lo) dst_lo[q] = src_first[q];
-        if (dst_hi) dst_hi[q] = src_last[q];
+        if (dl) dl[q] = sf[q];
+        if (dh) dh[q] = sl[q];
+    }
+    // publish: every block's remote stores are fenced before its ticket; the last block
+    // writes the epoch into the neighbours' flags
+    __shared__ bool last;
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned t = atomicAdd(hp.ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence_system();
+        if (hp.flag_lo) asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(hp.flag_lo), "r"(hp.epoch) : "memory");
+        if (hp.flag_hi) asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(hp.flag_hi), "r"(hp.epoch) : "memory");
+        *hp.ticket = 0u;
     }
 }
 
@@ -668,19 +687,14 @@ cudaError_t launch_cg_halo(const Launcher& ln, double* out_lo, const double* z_l
     return cudaGetLastError();
 }
 
-cudaError_t launch_halo_push(const Launcher& ln, const double* src_first, double* dst_lo, const double* src_last,
-                             double* dst_hi, int64_t n)
+cudaError_t launch_halo_push(const Launcher& ln, const HaloPush& hp)
 {
-    if (!dst_lo && !dst_hi) return cudaSuccess;
-    const bool vec = (n % 2 == 0) && ((uintptr_t)src_first % 16 == 0) && ((uintptr_t)src_last % 16 == 0);
-    const int64_t m = vec ? n / 2 : n;
-    const unsigned grid = (unsigned)std::max<int64_t>(std::min<int64_t>((m + 255) / 256, (int64_t)ln.num_sms), 1);
-    if (vec)
-        k_halo_push<double2><<<grid, 256, 0, ln.stream>>>(
-            reinterpret_cast<const double2*>(src_first), reinterpret_cast<double2*>(dst_lo),
-            reinterpret_cast<const double2*>(src_last), reinterpret_cast<double2*>(dst_hi), m);
-    else
-        k_halo_push<double><<<grid, 256, 0, ln.stream>>>(src_first, dst_lo, src_last, dst_hi, m);
+    if (!hp.dst_lo && !hp.dst_hi) return cudaSuccess;
+    const bool vec = (hp.n % 2 == 0) && ((uintptr_t)hp.src_first % 16 == 0) && ((uintptr_t)hp.src_last % 16 == 0);
+    const int64_t m = vec ? hp.n / 2 : hp.n;
+    const unsigned grid = (unsigned)std::max<int64_t>(std::min<int64_t>((m + 255) / 256, 64), 1);
+    if (vec) k_halo_push<double2><<<grid, 256, 0, ln.stream>>>(hp, m);
+    else k_halo_push<double><<<grid, 256, 0, ln.stream>>>(hp, m);
     if (ln.launch_counter) ++*ln.launch_counter;
     return cudaGetLastError();
 }

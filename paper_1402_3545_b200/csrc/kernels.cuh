@@ -157,9 +157,21 @@ cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse,
 cudaError_t launch_copy(const Launcher& ln, double* dst, const double* src, int64_t n, const int* skip);
 
 // P2P halo exchange: dst_lo <- src_first (my row 0 into the lower neighbour's slab),
-// dst_hi <- src_last (my row ny-1 into the upper neighbour's); n doubles each, remote stores.
-cudaError_t launch_halo_push(const Launcher& ln, const double* src_first, double* dst_lo, const double* src_last,
-                             double* dst_hi, int64_t n);
+// dst_hi <- src_last (my row ny-1 into the upper neighbour's); n doubles each, remote
+// stores.  The last block to finish (ticket) fences at system scope and stores `epoch`
+// into the neighbours' data flags.
+struct HaloPush {
+    const double* src_first;
+    const double* src_last;
+    double* dst_lo;
+    double* dst_hi;
+    int64_t n;
+    unsigned* flag_lo;   // lower neighbour's "data from upper" flag (nullptr: no neighbour)
+    unsigned* flag_hi;   // upper neighbour's "data from lower" flag
+    unsigned* ticket;    // local completion counter (zero between launches)
+    unsigned epoch;
+};
+cudaError_t launch_halo_push(const Launcher& ln, const HaloPush& hp);
 
 // CG multi-GPU: p halo slabs updated locally, out = fma(beta, p, z) on each non-null slab.
 cudaError_t launch_cg_halo(const Launcher& ln, double* out_lo, const double* z_lo, const double* p_lo, double* out_hi,
