@@ -12,6 +12,7 @@ the same device-resident f.
 N = 1: BASELINE configs[1] (1024 x 1024 x 128, fp64).  N > 1 (torchrun, one
 rank per GPU, NCCL): weak scaling with the same 1024 x 1024 x 128 per GPU,
 global 1024 x 1024N (y-strips); --per-gpu-nx 2048 gives configs[3].
+--global-nx G: strong scaling of a fixed G x G x 128 grid (4096 = configs[4]).
 Vectors are 1 GiB per GPU, far larger than the 126 MB L2, so no flush is
 needed between steps.  Prints ONE JSON line on rank 0.
 """
@@ -56,6 +57,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--solver", choices=["both", "mg", "cg"], default="both")
+    ap.add_argument("--levels", type=int, default=5, help="multigrid levels L (P:418; 7 and 10 in sec:Robustness)")
+    ap.add_argument("--coarse-sweeps", type=int, default=2, help="smoother sweeps on the coarsest level (P:456)")
+    ap.add_argument("--global-nx", type=int, default=0,
+                    help="strong scaling: a fixed global nx x nx x nz grid split into y-strips (4096 = configs[4])")
     return ap.parse_args()
 
 
@@ -67,6 +72,9 @@ def dist_env():
 
 
 def workload(args, world):
+    if args.global_nx:
+        g = args.global_nx
+        return g, g, f"C5 strong scaling: {g}x{g}x{args.nz} global, {world} B200 y-strips of {g}x{g // world}"
     nx = args.per_gpu_nx
     ny = nx * world
     name = ("C2: MG + PCG on 1024x1024x128 fp64, 1 B200" if world == 1 and nx == 1024 else
@@ -138,7 +146,7 @@ def measured_peak():
 
 # ---------------------------------------------------------------------------- oracle legs
 
-def oracle_sample(nx, nz, nu, rows, seed, threads=None):
+def oracle_sample(nx, nz, nu, rows, seed, threads=None, levels=5, coarse_sweeps=2):
     """Time the CPU oracle (as it stands) on a y-strip of `rows` rows of the workload:
     one MG V-cycle (solve_mg, max_iter=1: norm + V-cycle + residual) and one PCG
     iteration (solve_cg, max_iter=1: setup preconditioner + one iteration)."""
@@ -146,7 +154,7 @@ def oracle_sample(nx, nz, nu, rows, seed, threads=None):
     from inputs import rhs_zc
     if threads:
         O.set_threads(threads)
-    p = O.Params(nx=nx, ny=rows, nz=nz, nu_cfl=nu)
+    p = O.Params(nx=nx, ny=rows, nz=nz, nu_cfl=nu, L=levels, coarse_sweeps=coarse_sweeps)
     f = rhs_zc(nx, rows, nz, seed=seed)
     t0 = time.perf_counter()
     O.solve_mg(p, f, eps=1e-30, max_iter=1)
@@ -162,16 +170,18 @@ def run_reference(args):
     if rank != 0:
         return
     nx, ny, name = workload(args, world)
-    rows = 32
+    rows = max(32, 1 << (args.levels - 1))
     scale = ny / rows
     it_mg, it_cg = 9, 51  # iteration counts of the oracle at 128^2 x 128 (tests/test_oracle_pins)
     for _ in range(args.warmup):
-        oracle_sample(nx, args.nz, args.nu, rows, args.seed)
+        oracle_sample(nx, args.nz, args.nu, rows, args.seed, levels=args.levels,
+                     coarse_sweeps=args.coarse_sweeps)
     t = 0.0
     wall = 0.0
     for _ in range(args.steps):
         w0 = time.perf_counter()
-        a, b, cores = oracle_sample(nx, args.nz, args.nu, rows, args.seed)
+        a, b, cores = oracle_sample(nx, args.nz, args.nu, rows, args.seed, levels=args.levels,
+                     coarse_sweeps=args.coarse_sweeps)
         wall += time.perf_counter() - w0
         t += scale * (it_mg * a + it_cg * b)
     N = nx * ny * args.nz
@@ -183,10 +193,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
         "extrapolated_ms_per_step": 1e3 * t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.global_nx else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (splitmix64 RHS, seed %d)" % args.seed,
         "config": {"workload": name, "nx": nx, "ny": ny, "nz": args.nz, "nu_cfl": args.nu, "eps": args.eps,
-                   "levels": 5},
+                   "levels": args.levels, "coarse_sweeps": args.coarse_sweeps},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -219,12 +229,12 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         id128 = obj[0]
     stream = torch.cuda.Stream(device=local)
-    params = T.make_params(nx, ny, nz=nz, nu_cfl=args.nu)
+    params = T.make_params(nx, ny, nz=nz, nu_cfl=args.nu, levels=args.levels, coarse_sweeps=args.coarse_sweeps)
     ctx = T.Context(params, rank=rank, nranks=world, id128=id128, device=local, stream=stream)
-    shape = ctx.shape(5)
+    shape = ctx.shape(args.levels)
     f = torch.empty(shape, dtype=torch.float64, device=f"cuda:{local}")
     u = torch.empty_like(f)
-    y0 = ctx.local_box(5)[0]
+    y0 = ctx.local_box(args.levels)[0]
     with torch.cuda.stream(stream):
         G.fill_rhs(f, nx, y0=y0, seed=args.seed, stream=stream)
     stream.synchronize()
@@ -284,7 +294,7 @@ def main():
     if dom:
         kname, (n, kms, cells) = dom
         ach = cells * BYTES_PER_CELL[kname] / (kms * 1e-3) / 1e9
-        traffic = ncu_traffic(kname) if (world == 1 and args.per_gpu_nx == 1024 and nz == 128) else None
+        traffic = ncu_traffic(kname) if (world == 1 and not args.global_nx and args.per_gpu_nx == 1024 and nz == 128) else None
         roof = {"bound": "hbm", "kernel": kname, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic,
                 "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram read+write per launch)" if traffic else None,
@@ -333,8 +343,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rows = 128
-        a, b, cores = oracle_sample(nx, nz, args.nu, rows, args.seed)
+        rows = max(128, 1 << (args.levels - 1))
+        a, b, cores = oracle_sample(nx, nz, args.nu, rows, args.seed, levels=args.levels,
+                                       coarse_sweeps=args.coarse_sweeps)
         scale = ny / rows
         it_mg = its[0].iterations if its[0] else 0
         it_cg = its[1].iterations if its[1] else 0
@@ -348,10 +359,10 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if args.global_nx else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (splitmix64 uniform[-1,1) RHS keyed by global index, seed %d)" % args.seed,
             "config": {"workload": name, "nx": nx, "ny": ny, "nz": nz, "nu_cfl": args.nu, "eps": args.eps,
-                       "levels": 5, "parallelism": f"y-strips x{world}" if world > 1 else "single GPU",
+                       "levels": args.levels, "coarse_sweeps": args.coarse_sweeps, "parallelism": f"y-strips x{world}" if world > 1 else "single GPU",
                        "l2": "vectors 1 GiB/GPU >> 126 MB L2 (no flush needed)"},
             "roofline": roof,
             "cpu_baseline": cpu,

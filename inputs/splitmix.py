@@ -50,3 +50,13 @@ def mode_zc(nx: int, ny: int, nz: int, p: int, q: int, r: int) -> np.ndarray:
     sj = np.sin(q * np.pi * np.arange(1, ny + 1) / (ny + 1))
     ck = np.cos(r * np.pi * (np.arange(nz) + 0.5) / nz)
     return np.ascontiguousarray(sj[:, None, None] * si[None, :, None] * ck[None, None, :])
+
+
+def mode_face_zc(nx: int, ny: int, nz: int, p: int, q: int, r: int) -> np.ndarray:
+    """Separable mode sin(p pi (i+1/2)/nx) sin(q pi (j+1/2)/ny) cos(r pi (k+1/2)/nz),
+    z-contiguous (ny, nx, nz), (i, j) 0-based: the sine vanishes on the boundary faces
+    (the cell-centred modes of the face-Dirichlet reading [R25])."""
+    si = np.sin(p * np.pi * (np.arange(nx) + 0.5) / nx)
+    sj = np.sin(q * np.pi * (np.arange(ny) + 0.5) / ny)
+    ck = np.cos(r * np.pi * (np.arange(nz) + 0.5) / nz)
+    return np.ascontiguousarray(sj[:, None, None] * si[None, :, None] * ck[None, None, :])

@@ -39,7 +39,7 @@ class _Params(C.Structure):
     _fields_ = [("nx", C.c_long), ("ny", C.c_long), ("nz", C.c_int),
                 ("nu_cfl", C.c_double), ("H", C.c_double), ("lam", C.c_double),
                 ("L", C.c_int), ("pre", C.c_int), ("post", C.c_int),
-                ("coarse_sweeps", C.c_int), ("rho", C.c_double)]
+                ("coarse_sweeps", C.c_int), ("rho", C.c_double), ("boundary", C.c_int)]
 
 
 @dataclass
@@ -57,10 +57,11 @@ class Params:
     post: int = 1
     coarse_sweeps: int = 2
     rho: float = 2.0 / 3.0
+    boundary: int = 0   # horizontal Dirichlet reading: 0 ghost zero [R1], 1 face [R25]
 
     def c(self) -> _Params:
         return _Params(self.nx, self.ny, self.nz, self.nu_cfl, self.H, self.lam, self.L,
-                       self.pre, self.post, self.coarse_sweeps, self.rho)
+                       self.pre, self.post, self.coarse_sweeps, self.rho, self.boundary)
 
     def level_shape(self, level: int) -> tuple[int, int, int]:
         f = 1 << (self.L - level)

@@ -50,7 +50,10 @@
  *     |T| = 1,  a_k = d_k = 1,
  *     alpha_{T,T'} = -omega^2/h_l^2           ("A_{(i,j),(i',j')} = -omega^2/h^2 I")
  *     alpha_T      = sum over the 4 faces of alpha_{T,T'} = -4 omega^2/h_l^2
- *                    (including boundary faces: ghost value 0 Dirichlet [R1])
+ *                    (including boundary faces: ghost value 0 Dirichlet [R1]);
+ *                    with boundary = 1 (face Dirichlet [R25]) a boundary face counts
+ *                    twice (the face is h_l/2 from the cell centre), so a column with
+ *                    nb boundary faces has alpha_T = (4 + nb) alpha_{T,T'}
  *     b_k = -omega^2 lambda^2/h_z^2 for k > 0, b_0 = 0          (Neumann)
  *     c_k = -omega^2 lambda^2/h_z^2 for k < nz-1, c_{nz-1} = 0
  * so that the interior diagonal is 1 + 4 omega^2/h^2 + 2 omega^2 lambda^2/h_z^2
@@ -61,9 +64,21 @@ typedef struct {
     int nz;           /* vertical levels (never coarsened) */
     double area;      /* |T| */
     double alpha_TT;  /* alpha_{T,T'} */
-    double alpha_T;   /* alpha_T */
+    double alpha_T;   /* alpha_T of an interior column */
+    int boundary;     /* 0: ghost-zero Dirichlet [R1]; 1: face Dirichlet [R25] */
     double *a, *b, *c, *d; /* vertical profiles, length nz */
 } or_op;
+
+/* alpha_T of column (i,j) ("alpha_T ... different for each horizontal grid cell").
+ * [R1]: every column has 4 alpha_{T,T'}.  [R25] (face Dirichlet, the cell-centred
+ * finite-volume boundary of P:131 and P:139): the flux through a boundary face is
+ * omega^2 (0 - u_T)/(h/2), i.e. 2 alpha_{T,T'} per boundary face. */
+static inline double or_alpha_T(const or_op *op, long i, long j)
+{
+    if (!op->boundary) return op->alpha_T;
+    int nb = (i == 0) + (i == op->nx - 1) + (j == 0) + (j == op->ny - 1);
+    return op->alpha_T + (double)nb * op->alpha_TT;
+}
 
 static inline size_t ZC(const or_op *op, long i, long j, long k)
 {
@@ -81,6 +96,7 @@ typedef struct {
     int pre, post;    /* smoothing steps (1 and 1) */
     int coarse_sweeps;/* smoother iterations on the coarsest level (2) */
     double rho;       /* rho_relax = 2/3 */
+    int boundary;     /* horizontal Dirichlet reading: 0 = ghost zero [R1], 1 = face [R25] */
 } or_params;
 
 /* Build the operator of level l (1 <= l <= L) by rediscretisation [R4]:
@@ -91,6 +107,7 @@ int or_op_init(const or_params *p, int l, or_op *op)
     if (p->nx <= 0 || p->ny <= 0 || p->nz <= 0 || p->L <= 0 || l < 1 || l > p->L)
         return OR_E_PARAM;
     if (!(p->nu_cfl > 0) || !(p->H > 0) || !(p->lambda > 0)) return OR_E_PARAM;
+    if (p->boundary != 0 && p->boundary != 1) return OR_E_PARAM;
     long f = 1L << (p->L - l);
     if (p->nx % f || p->ny % f) return OR_E_SHAPE;
     double h = 1.0 / (double)p->nx;              /* unit square, equidistant */
@@ -105,6 +122,7 @@ int or_op_init(const or_params *p, int l, or_op *op)
     op->area = 1.0;
     op->alpha_TT = -omega2 / (hl * hl);
     op->alpha_T = 4.0 * op->alpha_TT;
+    op->boundary = p->boundary;
     op->a = (double *)malloc(sizeof(double) * p->nz);
     op->b = (double *)malloc(sizeof(double) * p->nz);
     op->c = (double *)malloc(sizeof(double) * p->nz);
@@ -136,7 +154,7 @@ void or_apply_col(const or_op *op, const double *x, long i, long j, double *ycol
     for (int k = 0; k < nz; ++k) {
         double xk = x[ZC(op, i, j, k)];
         /* A_T x^(T) */
-        double y = op->area * op->a[k] * xk - op->alpha_T * op->d[k] * xk
+        double y = op->area * op->a[k] * xk - or_alpha_T(op, i, j) * op->d[k] * xk
                  + op->area * (-(op->b[k] + op->c[k])) * xk;
         if (k > 0) y += op->area * op->b[k] * x[ZC(op, i, j, k - 1)];
         if (k < nz - 1) y += op->area * op->c[k] * x[ZC(op, i, j, k + 1)];
@@ -205,23 +223,24 @@ int or_thomas(int n, const double *s, const double *dg, const double *t, const d
 
 /* The three diagonals of the column block A_T = M_T (M keeps only the
  * first term of eqn:TridiagonalPDE). */
-static void or_block_diagonals(const or_op *op, double *s, double *dg, double *t)
+static void or_block_diagonals(const or_op *op, long i, long j, double *s, double *dg, double *t)
 {
+    const double alpha_T = or_alpha_T(op, i, j);
     for (int k = 0; k < op->nz; ++k) {
         s[k] = op->area * op->b[k];
         t[k] = op->area * op->c[k];
-        dg[k] = op->area * op->a[k] - op->alpha_T * op->d[k]
+        dg[k] = op->area * op->a[k] - alpha_T * op->d[k]
               + op->area * (-(op->b[k] + op->c[k]));
     }
 }
 
-/* z = M^{-1} r for one column (vertical line relaxation). */
-int or_precondition_col(const or_op *op, const double *rcol, double *zcol)
+/* z = M^{-1} r for column (i,j) (vertical line relaxation). */
+int or_precondition_col(const or_op *op, const double *rcol, long i, long j, double *zcol)
 {
     const int nz = op->nz;
     double buf[5 * nz]; /* column workspace (no global temporaries) */
     double *s = buf, *dg = buf + nz, *t = buf + 2 * nz, *work = buf + 3 * nz;
-    or_block_diagonals(op, s, dg, t);
+    or_block_diagonals(op, i, j, s, dg, t);
     return or_thomas(nz, s, dg, t, rcol, zcol, work);
 }
 
@@ -232,7 +251,7 @@ int or_precondition(const or_op *op, const double *r, double *z)
 #pragma omp parallel for schedule(static)
     for (long j = 0; j < op->ny; ++j)
         for (long i = 0; i < op->nx; ++i) {
-            int st = or_precondition_col(op, r + ZC(op, i, j, 0), z + ZC(op, i, j, 0));
+            int st = or_precondition_col(op, r + ZC(op, i, j, 0), i, j, z + ZC(op, i, j, 0));
             if (st != OR_OK) {
 #pragma omp critical
                 status = st;
@@ -249,7 +268,7 @@ int or_smooth_col(const or_op *op, const double *u, const double *f, double rho,
     const int nz = op->nz;
     double r[nz], z[nz];
     or_residual_col(op, u, f, i, j, r);
-    int st = or_precondition_col(op, r, z);
+    int st = or_precondition_col(op, r, i, j, z);
     for (int k = 0; k < nz; ++k) ucol_out[k] = u[ZC(op, i, j, k)] + rho * z[k];
     return st;
 }
@@ -287,11 +306,22 @@ void or_restrict(const or_op *fine, const or_op *coarse, const double *rf, doubl
             }
 }
 
-/* Coarse value with zero ghosts outside the domain [R7]. */
+/* Coarse value with the ghosts of the boundary reading: zero outside the domain
+ * [R7]; with face Dirichlet [R25] the ghost is the linear continuation through the
+ * boundary value 0 on the face, u_c(-1) = -u_c(0) (per direction, so a corner ghost
+ * is +u_c of the corner cell). */
 static inline double or_coarse_at(const or_op *c, const double *uc, long I, long J, int k)
 {
-    if (I < 0 || I >= c->nx || J < 0 || J >= c->ny) return 0.0;
-    return uc[ZC(c, I, J, k)];
+    if (!c->boundary) {
+        if (I < 0 || I >= c->nx || J < 0 || J >= c->ny) return 0.0;
+        return uc[ZC(c, I, J, k)];
+    }
+    double sign = 1.0;
+    if (I < 0) { I = 0; sign = -sign; }
+    if (I >= c->nx) { I = c->nx - 1; sign = -sign; }
+    if (J < 0) { J = 0; sign = -sign; }
+    if (J >= c->ny) { J = c->ny - 1; sign = -sign; }
+    return sign * uc[ZC(c, I, J, k)];
 }
 
 /* Prolongation P_{l,l-1} and add: u_f += P u_c (Kernel "Prolongate", P:201,
@@ -300,7 +330,7 @@ static inline double or_coarse_at(const or_op *c, const double *uc, long I, long
  * cell (i,j) (0-based) has parent (I,J) = (i/2, j/2); its nearer coarse
  * neighbour in x is I+sx with sx = -1 for even i, +1 for odd i (likewise sy);
  *   u_f(i,j,k) += (9 u_c(I,J) + 3 u_c(I+sx,J) + 3 u_c(I,J+sy) + u_c(I+sx,J+sy)) / 16
- * with u_c = 0 outside the domain. */
+ * with u_c outside the domain from or_coarse_at (zero [R7] or reflected [R25]). */
 void or_prolong_add(const or_op *coarse, const or_op *fine, const double *uc, double *uf)
 {
 #pragma omp parallel for schedule(static)
@@ -579,7 +609,7 @@ int or_api_residual_cols(const or_params *p, int l, const double *u, const doubl
 
 int or_api_precondition_cols(const or_params *p, int l, const double *r, int ncols,
                              const long *ii, const long *jj, double *out)
-{ OR_WITH_OP(p, l, for (int m = 0; m < ncols; ++m) { int s_ = or_precondition_col(&op_, r + ZC(&op_, ii[m], jj[m], 0), out + (size_t)m * op_.nz); if (s_) st_ = s_; }); }
+{ OR_WITH_OP(p, l, for (int m = 0; m < ncols; ++m) { int s_ = or_precondition_col(&op_, r + ZC(&op_, ii[m], jj[m], 0), ii[m], jj[m], out + (size_t)m * op_.nz); if (s_) st_ = s_; }); }
 
 int or_api_smooth_cols(const or_params *p, int l, const double *u, const double *f, int ncols,
                        const long *ii, const long *jj, double *out)
