@@ -70,7 +70,7 @@ extern "C" {
 
 typedef enum {
     TPMG_OK = 0,
-    TPMG_E_PARAM = 1,     /* non-positive nu, H, lambda; rho not in (0,2); bad counts; NULL pointer */
+    TPMG_E_PARAM = 1,     /* non-positive nu, H, lambda; rho not in (0,2); bad counts or boundary; NULL pointer */
     TPMG_E_SHAPE = 2,     /* nx or ny not divisible by 2^(L-1); ny not divisible by nranks*2^(L-1);
                              nz too large for the on-chip Thomas buffer; x == y where forbidden */
     TPMG_E_RANGE = 3,     /* level not in [1, L] */
@@ -85,6 +85,18 @@ typedef enum {
 
 typedef enum { TPMG_SOLVER_CG = 0, TPMG_SOLVER_MG = 1 } tpmg_solver;
 
+/* Reading of the horizontal homogeneous Dirichlet condition on the
+ * cell-centred grid:
+ *   TPMG_BC_GHOST_ZERO [R1] (default): the value 0 sits in the ghost cell, every
+ *       column has alpha_T = 4 alpha_{T,T'}; coarse ghosts of the prolongation are 0 [R7];
+ *   TPMG_BC_FACE [R25]: the value 0 sits on the boundary face (half a cell away), a
+ *       column with nb boundary faces has alpha_T = (4 + nb) alpha_{T,T'}, its line
+ *       block M_T changes accordingly, and the prolongation's coarse ghost is the
+ *       linear continuation through 0 (-u_c across an edge, +u_c across a corner).
+ *       The boundary is then at the same place on every level, which keeps MG
+ *       robust for large nu_CFL (sec:Robustness). */
+typedef enum { TPMG_BC_GHOST_ZERO = 0, TPMG_BC_FACE = 1 } tpmg_boundary;
+
 /* Problem and solver parameters.  A zero field selects its default. */
 typedef struct {
     int64_t nx, ny;        /* GLOBAL horizontal cells of the finest level (required, > 0) */
@@ -96,6 +108,7 @@ typedef struct {
     int32_t pre, post;     /* smoothing steps per level; default 1, 1 */
     int32_t coarse_sweeps; /* smoother iterations on the coarsest level; default 2 */
     double rho;            /* block-Jacobi relaxation rho_relax; default 2/3 */
+    int32_t boundary;      /* tpmg_boundary; default TPMG_BC_GHOST_ZERO [R1] */
 } tpmg_params;
 
 /* Solve report.  history (optional, caller-owned HOST array of history_cap

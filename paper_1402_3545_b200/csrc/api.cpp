@@ -717,7 +717,8 @@ tpmg_status vcycle_rec(tpmg_ctx* ctx, int l, bool skip_pre = false)
     LevelData& F = ctx->lv[l];
     HaloField uc = halo_of(ctx, l - 1, Cc.u[Cc.cur]);
     (void)uc;
-    const bool fuse = p.post >= 1 && ctx->fuse_prolong && ksplit_usable(ctx, MODE_SMOOTH_PROLONG, F.lc);
+    const bool fuse = p.post >= 1 && ctx->fuse_prolong && p.boundary == TPMG_BC_GHOST_ZERO &&
+                      ksplit_usable(ctx, MODE_SMOOTH_PROLONG, F.lc);   // fused form: zero coarse ghosts only
     if (fuse) {
         TRY(exchange(ctx, l - 1, Cc.u[Cc.cur]));
         uc = halo_of(ctx, l - 1, Cc.u[Cc.cur]);
@@ -1255,6 +1256,8 @@ tpmg_status validate(const tpmg_params* params, int32_t rank, int32_t nranks, tp
     if (!(p.rho > 0 && p.rho < 2)) return fail(nullptr, TPMG_E_PARAM, "rho = %g not in (0, 2)", p.rho);
     if (p.levels < 1 || p.levels > 24) return fail(nullptr, TPMG_E_PARAM, "levels = %d not in [1, 24]", p.levels);
     if (p.pre < 0 || p.post < 0 || p.coarse_sweeps < 1) return fail(nullptr, TPMG_E_PARAM, "pre/post >= 0, coarse_sweeps >= 1");
+    if (p.boundary != TPMG_BC_GHOST_ZERO && p.boundary != TPMG_BC_FACE)
+        return fail(nullptr, TPMG_E_PARAM, "boundary = %d is not a tpmg_boundary", p.boundary);
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(nullptr, TPMG_E_TOPOLOGY, "rank %d of %d", rank, nranks);
     const int64_t f = (int64_t)1 << (p.levels - 1);
     if (p.nx % f) return fail(nullptr, TPMG_E_SHAPE, "nx = %lld not divisible by 2^(L-1) = %lld", (long long)p.nx, (long long)f);
@@ -1352,36 +1355,43 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         L.lc.nz = p.nz;
         L.lc.c = omega * omega / (hl * hl);
         L.lc.gamma = gamma;
-        // Thomas factors of the column block M_T = A_T: diag_k, 1/m_k, gamma/m_k
+        L.lc.bc = p.boundary;
+        L.lc.bnd_lo = (rank == 0) ? 1 : 0;               // local row 0 / ny-1 on the physical boundary
+        L.lc.bnd_hi = (rank == nranks - 1) ? 1 : 0;
         // Thomas factors of the column block M_T = A_T, per level k:
         //   diag_k, 1/m_k, b_k = gamma/m_k (backward), a_k = gamma/m_{k-1} (forward, L of M = L D L^T),
         //   and the k-split propagators over segments of kSegK levels:
         //   P_k = prod_{j = k_s..k} a_j,  Q_k = prod_{j = k..k_e} b_j.
+        // One table per column class: class nb = number of boundary faces of the column
+        // (face Dirichlet [R25]: alpha_T = -(4 + nb) c); ghost-zero Dirichlet has class 0 only.
         const int nz = p.nz;
-        std::vector<double> tab(6 * (size_t)nz);
-        double* t_diag = tab.data();
-        double* t_invm = t_diag + nz;
-        double* t_gim = t_invm + nz;
-        double* t_afw = t_gim + nz;
-        double* t_P = t_afw + nz;
-        double* t_Q = t_P + nz;
-        double mprev = 0.0;
-        for (int k = 0; k < nz; ++k) {
-            const double diag = 1.0 + 4.0 * L.lc.c + gamma * ((k > 0 ? 1.0 : 0.0) + (k < nz - 1 ? 1.0 : 0.0));
-            const double m = (k == 0) ? diag : diag - gamma * (gamma / mprev);
-            if (m == 0.0 || !std::isfinite(m)) return bail(fail(ctx, TPMG_E_SINGULAR, "zero Thomas pivot at level %d, k = %d", l, k));
-            t_diag[k] = diag;
-            t_invm[k] = 1.0 / m;
-            t_gim[k] = (k < nz - 1) ? gamma / m : 0.0;
-            t_afw[k] = (k > 0) ? gamma / mprev : 0.0;
-            mprev = m;
-        }
-        for (int k0 = 0; k0 < nz; k0 += kSegK) {
-            const int k1 = std::min(nz, k0 + kSegK) - 1;
-            double pr = 1.0;
-            for (int k = k0; k <= k1; ++k) { pr *= t_afw[k]; t_P[k] = pr; }
-            pr = 1.0;
-            for (int k = k1; k >= k0; --k) { pr *= t_gim[k]; t_Q[k] = pr; }
+        const int ncls = (p.boundary == TPMG_BC_FACE) ? kBoundaryClasses : 1;
+        std::vector<double> tab(6 * (size_t)nz * ncls);
+        for (int cls = 0; cls < ncls; ++cls) {
+            double* t_diag = tab.data() + (size_t)cls * 6 * nz;
+            double* t_invm = t_diag + nz;
+            double* t_gim = t_invm + nz;
+            double* t_afw = t_gim + nz;
+            double* t_P = t_afw + nz;
+            double* t_Q = t_P + nz;
+            double mprev = 0.0;
+            for (int k = 0; k < nz; ++k) {
+                const double diag = 1.0 + (4.0 + cls) * L.lc.c + gamma * ((k > 0 ? 1.0 : 0.0) + (k < nz - 1 ? 1.0 : 0.0));
+                const double m = (k == 0) ? diag : diag - gamma * (gamma / mprev);
+                if (m == 0.0 || !std::isfinite(m)) return bail(fail(ctx, TPMG_E_SINGULAR, "zero Thomas pivot at level %d, k = %d", l, k));
+                t_diag[k] = diag;
+                t_invm[k] = 1.0 / m;
+                t_gim[k] = (k < nz - 1) ? gamma / m : 0.0;
+                t_afw[k] = (k > 0) ? gamma / mprev : 0.0;
+                mprev = m;
+            }
+            for (int k0 = 0; k0 < nz; k0 += kSegK) {
+                const int k1 = std::min(nz, k0 + kSegK) - 1;
+                double pr = 1.0;
+                for (int k = k0; k <= k1; ++k) { pr *= t_afw[k]; t_P[k] = pr; }
+                pr = 1.0;
+                for (int k = k1; k >= k0; --k) { pr *= t_gim[k]; t_Q[k] = pr; }
+            }
         }
         if (nz <= kKsplitMaxNZ)
             for (int q = 0; q < 6; ++q)

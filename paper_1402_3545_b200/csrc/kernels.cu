@@ -162,10 +162,10 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     double* scratch = rbuf + (MODE == MODE_RESTRICT ? 2 * TY * RS * (TX / 2) : 0);  // reduction scratch
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-    for (int q = tid; q < 3 * nz; q += NT) tab[q] = a.L.tab[q];
-    const double* diag = tab;
-    const double* invm = tab + nz;
-    const double* gim = tab + 2 * nz;
+    for (int q = tid; q < 3 * nz; q += NT) tab[q] = a.L.tab[q];   // interior class (0)
+    const double* diag_s = tab;
+    const double* invm_s = tab + nz;
+    const double* gim_s = tab + 2 * nz;
     const double c = a.L.c, gamma = a.L.gamma;
     if constexpr (LOADER == 1) {
         if (tid == 0) {
@@ -239,12 +239,19 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     for (int s = 0; s < NS - 1; ++s) issue();
 
     int gi = 0;
-    for (int tl = 0; tl < my_tiles; ++tl) {
+    // One tile.  BND: the tile holds columns of other classes (face Dirichlet [R25]); each
+    // thread then reads its column's Thomas factors from the global class tables.
+    auto tile_body = [&](auto bnd_t, int tl) {
+        constexpr bool BND = decltype(bnd_t)::value;
         const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
         const int64_t i0 = (int64_t)(tile % ntx) * TX, j0 = (int64_t)part_row(a.part, nty, tile / ntx) * TY;
         const int64_t i = i0 + tx, j = j0 + ty;
         const bool valid = (i < nx) && (j < ny);
         const int64_t colbase = j * nx * (int64_t)nz + i;  // + k*nx
+        const double* ctab = BND ? a.L.tab + (size_t)column_class(a.L, i, j) * kTabArrays * nz : nullptr;
+        const double* diag = BND ? ctab : diag_s;
+        const double* invm = BND ? ctab + nz : invm_s;
+        const double* gim = BND ? ctab + 2 * nz : gim_s;
 
         // rolling state for the k-lag: values at level km = k-1 and km-1
         double um1 = 0.0, u0 = 0.0, S0 = 0.0, qa = 0.0, qb = 0.0, gprev = 0.0;
@@ -415,6 +422,13 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 op -= nx;
             }
         }
+    };
+    for (int tl = 0; tl < my_tiles; ++tl) {
+        const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
+        if (tile_on_boundary(a.L, (int64_t)(tile % ntx) * TX, (int64_t)part_row(a.part, nty, tile / ntx) * TY, TX, TY))
+            tile_body(std::true_type{}, tl);
+        else
+            tile_body(std::false_type{}, tl);
     }
     if constexpr (LOADER == 0) cp_async_wait<0>();
     if (want_red) grid_reduce<NR>(a.red, acc, scratch);
@@ -472,42 +486,6 @@ cudaError_t launch_line_ty(const Launcher& ln, const LineArgs& a)
 
 // ------------------------------------------------------------------ simple streaming kernels
 
-__device__ __forceinline__ double ld_halo(const HaloField& F, int64_t i, int64_t j, int k, int64_t nx,
-                                          int64_t ny, int nz)
-{
-    if (i < 0 || i >= nx) return 0.0;
-    const double* row = (j < 0) ? F.lo : (j >= ny ? F.hi : F.base + j * nx * (int64_t)nz);
-    if (!row) return 0.0;
-    return __ldg(row + (int64_t)k * nx + i);
-}
-
-// r = f - A u at one fine cell, direct loads (used by the fused residual-restriction)
-__device__ __forceinline__ double resid_cell(const LevelConst& F, const HaloField& u, const double* f,
-                                             int64_t i, int64_t j, int k)
-{
-    const int64_t nx = F.nx, ny = F.ny;
-    const int nz = F.nz;
-    const double uc = ld_halo(u, i, j, k, nx, ny, nz);
-    const double ud = (k > 0) ? ld_halo(u, i, j, k - 1, nx, ny, nz) : 0.0;
-    const double uu = (k < nz - 1) ? ld_halo(u, i, j, k + 1, nx, ny, nz) : 0.0;
-    const double S = (ld_halo(u, i - 1, j, k, nx, ny, nz) + ld_halo(u, i + 1, j, k, nx, ny, nz)) +
-                     (ld_halo(u, i, j - 1, k, nx, ny, nz) + ld_halo(u, i, j + 1, k, nx, ny, nz));
-    const double Mu = F.tab[k] * uc - F.gamma * (ud + uu);
-    return __ldg(f + (j * nz + k) * nx + i) - (Mu - F.c * S);
-}
-
-__global__ void k_residual_restrict(const LevelConst F, const LevelConst Cc, const HaloField u,
-                                    const double* __restrict__ f, double* __restrict__ fc)
-{
-    const int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int k = blockIdx.y;
-    const int64_t J = blockIdx.z;
-    if (I >= Cc.nx) return;
-    const double s = (resid_cell(F, u, f, 2 * I, 2 * J, k) + resid_cell(F, u, f, 2 * I + 1, 2 * J, k)) +
-                     (resid_cell(F, u, f, 2 * I, 2 * J + 1, k) + resid_cell(F, u, f, 2 * I + 1, 2 * J + 1, k));
-    fc[(J * Cc.nz + k) * Cc.nx + I] = 0.25 * s;
-}
-
 __global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double* __restrict__ r,
                            double* __restrict__ fc)
 {
@@ -549,6 +527,7 @@ __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const 
         rows[d] = (JJ < 0) ? uc.lo : (JJ >= nyc ? uc.hi : uc.base + JJ * cplane);
     }
     const bool hasW = I > 0, hasE = I < nxc - 1;
+    const bool face = Cc.bc != 0;   // else zero coarse ghosts [R7]
     const int64_t fplane = F.nx * (int64_t)F.nz;
     double* f0 = uf + (2 * J) * fplane + 2 * I;     // fine row 2J, level 0
     double* f1 = f0 + fplane;                        // fine row 2J+1
@@ -559,8 +538,17 @@ __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const 
         for (int d = 0; d < 3; ++d) {
             const double* r = rows[d] ? rows[d] + (int64_t)k * nxc + I : nullptr;
             cc[d][1] = r ? __ldg(r) : 0.0;
-            cc[d][0] = (r && hasW) ? __ldg(r - 1) : 0.0;
-            cc[d][2] = (r && hasE) ? __ldg(r + 1) : 0.0;
+            cc[d][0] = (r && hasW) ? __ldg(r - 1) : (face ? -cc[d][1] : 0.0);
+            cc[d][2] = (r && hasE) ? __ldg(r + 1) : (face ? -cc[d][1] : 0.0);
+        }
+        if (face) {
+            // face Dirichlet [R25]: a ghost row beyond the physical boundary is the reflected
+            // row with the opposite sign (so a corner ghost is +u_c of the corner cell)
+#pragma unroll
+            for (int d = 0; d < 3; d += 2)
+                if (!rows[d])
+#pragma unroll
+                    for (int x = 0; x < 3; ++x) cc[d][x] = -cc[1][x];
         }
 #pragma unroll
         for (int b = 0; b < 2; ++b) {          // fine row 2J + b: sy = -1 (b = 0), +1 (b = 1)
@@ -750,16 +738,6 @@ cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a)
     case MODE_RESTRICT: return launch_line_t<MODE_RESTRICT, 4>(ln, a);
     default: return cudaErrorInvalidValue;
     }
-}
-
-cudaError_t launch_residual_restrict(const Launcher& ln, const LevelConst& fine, const LevelConst& coarse,
-                                     HaloField u, const double* f, double* fc)
-{
-    dim3 block(64), grid((unsigned)((coarse.nx + 63) / 64), (unsigned)coarse.nz, (unsigned)coarse.ny);
-    if (coarse.ny <= 0 || coarse.nx <= 0) return cudaSuccess;
-    k_residual_restrict<<<grid, block, 0, ln.stream>>>(fine, coarse, u, f, fc);
-    if (ln.launch_counter) ++*ln.launch_counter;
-    return cudaGetLastError();
 }
 
 cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const LevelConst& coarse,

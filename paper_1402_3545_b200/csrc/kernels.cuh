@@ -25,8 +25,28 @@ struct LevelConst {
     int32_t nz;
     double c;           // omega^2 / h_l^2        (minus alpha_{T,T'})
     double gamma;       // omega^2 lambda^2 / h_z^2 (minus the vertical off-diagonal)
-    const double* tab;  // device: diag[nz], invm[nz], gim[nz] (Thomas factors of M_T)
+    const double* tab;  // device: per column class [diag, invm, gim, afw, P, Q][nz] (Thomas factors of M_T)
+    int32_t bc;         // tpmg_boundary: 0 ghost-zero [R1] (class 0 only), 1 face Dirichlet [R25]
+    int32_t bnd_lo, bnd_hi;   // local row 0 / ny-1 lies on the physical boundary
 };
+
+// Column classes of the face-Dirichlet reading: nb = number of boundary faces (0..4).
+constexpr int kBoundaryClasses = 5;
+constexpr int kTabArrays = 6;   // doubles per class: kTabArrays * nz
+
+// Does the tile of columns [i0, i0+tx) x [j0, j0+ty) contain a column whose line
+// block differs from the interior one (face Dirichlet only)?
+__host__ __device__ inline bool tile_on_boundary(const LevelConst& L, int64_t i0, int64_t j0, int tx, int ty)
+{
+    return L.bc && (i0 == 0 || i0 + tx >= L.nx || (L.bnd_lo && j0 == 0) || (L.bnd_hi && j0 + ty >= L.ny));
+}
+
+// Class (boundary-face count) of column (i, j); 0 for out-of-range columns.
+__host__ __device__ inline int column_class(const LevelConst& L, int64_t i, int64_t j)
+{
+    if (i < 0 || i >= L.nx || j < 0 || j >= L.ny) return 0;
+    return (i == 0) + (i == L.nx - 1) + (L.bnd_lo && j == 0) + (L.bnd_hi && j == L.ny - 1);
+}
 
 // Deterministic reduction slot: per-block partials, a ticket counter and the
 // result (nvals doubles).  The last block to finish sums the partials in
@@ -142,10 +162,6 @@ bool ksplit_supported(int mode, int nz, int nx);
 KsplitBoxes ksplit_boxes(int mode, int cfg);
 cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const LineArgs& a, const KTables& T);
 
-// f_c = 1/4 sum of the 2x2 fine children of (f - A u)  (Residual + restriction, fused)
-cudaError_t launch_residual_restrict(const Launcher& ln, const LevelConst& fine,
-                                     const LevelConst& coarse, HaloField u, const double* f,
-                                     double* fc);
 // f_c = 1/4 sum of the 2x2 fine children of r (plain restriction)
 cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const LevelConst& coarse,
                             const double* r, double* fc);

@@ -35,6 +35,7 @@
 #include "device_util.cuh"
 
 #include <algorithm>
+#include <type_traits>
 
 namespace tpmg {
 namespace {
@@ -153,13 +154,7 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int s = warp % NSEG, ty = warp / NSEG;
     // per-level tables, staged in shared memory (warp-uniform broadcast reads)
-    for (int q = tid; q < 6 * nz; q += NT) tab[q] = T.t[q / nz][q % nz];
-    const double* diag = tab;
-    const double* invm = tab + nz;
-    const double* gim = tab + 2 * nz;
-    const double* afw = tab + 3 * nz;
-    const double* Pfw = tab + 4 * nz;
-    const double* Qbw = tab + 5 * nz;
+    for (int q = tid; q < 6 * nz; q += NT) tab[q] = T.t[q / nz][q % nz];   // interior class (0)
     const double c = a.L.c, gamma = a.L.gamma, rho = a.rho, scale = a.scale;
     if (tid == 0) {
         for (int q = 0; q < NS2; ++q) mbar_init(&full_bar[q], 1);
@@ -195,11 +190,21 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     for (int q = 0; q < NS2 - 1; ++q) issue();
     int rstep = 0;   // MODE_RESTRICT: chunk counter (exchange-buffer parity)
 
-    for (int tl = 0; tl < my_tiles; ++tl) {
+    // One tile.  BND: the tile holds columns of other classes (face Dirichlet [R25]); each
+    // thread then reads its column's tables from the global class tables.
+    auto tile_body = [&](auto bnd_t, int tl) {
+        constexpr bool BND = decltype(bnd_t)::value;
         const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
         const int i0 = (tile % ntx) * TX, j0 = part_row(a.part, nty, tile / ntx) * TY;
         const int64_t i = i0 + lane, j = j0 + ty;
         const bool valid = (i < nx) && (j < ny);
+        const double* ct = BND ? a.L.tab + (size_t)column_class(a.L, i, j) * kTabArrays * nz : tab;
+        const double* diag = ct;
+        const double* invm = ct + nz;
+        const double* gim = ct + 2 * nz;
+        const double* afw = ct + 3 * nz;
+        const double* Pfw = ct + 4 * nz;
+        const double* Qbw = ct + 5 * nz;
         // halo rows of this warp's row j kept in the slab slots (layout without in-place rows)
         const bool s_slab = G::SROW && a.tma.h[0].has_lo && j0 == 0 && ty == 0;
         const bool n_slab = G::SROW && a.tma.h[0].has_hi && (j0 + ty + 1 == ny);
@@ -333,6 +338,13 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
             }
             // bnd is reused by the next tile only after its forward chunks (>= 1 __syncthreads)
         }
+    };
+    for (int tl = 0; tl < my_tiles; ++tl) {
+        const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
+        if (tile_on_boundary(a.L, (int64_t)(tile % ntx) * TX, (int64_t)part_row(a.part, nty, tile / ntx) * TY, TX, TY))
+            tile_body(std::true_type{}, tl);
+        else
+            tile_body(std::false_type{}, tl);
     }
     if (NORM && a.red.result != nullptr) grid_reduce<1>(a.red, acc, scratch);
 }

@@ -35,7 +35,7 @@ class tpmg_params(C.Structure):
     _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int32),
                 ("nu_cfl", C.c_double), ("H", C.c_double), ("lambda_", C.c_double),
                 ("levels", C.c_int32), ("pre", C.c_int32), ("post", C.c_int32),
-                ("coarse_sweeps", C.c_int32), ("rho", C.c_double)]
+                ("coarse_sweeps", C.c_int32), ("rho", C.c_double), ("boundary", C.c_int32)]
 
 
 class tpmg_result(C.Structure):
@@ -268,9 +268,10 @@ def tpmg_last_error(ctx: int | None) -> str:
 
 def make_params(nx: int, ny: int, nz: int = 0, nu_cfl: float = 0.0, H: float = 0.0,
                 lam: float = 0.0, levels: int = 0, pre: int = 0, post: int = 0,
-                coarse_sweeps: int = 0, rho: float = 0.0) -> tpmg_params:
-    """Zero fields select the library defaults (include/tpmg.h)."""
-    return tpmg_params(nx, ny, nz, nu_cfl, H, lam, levels, pre, post, coarse_sweeps, rho)
+                coarse_sweeps: int = 0, rho: float = 0.0, boundary: int = 0) -> tpmg_params:
+    """Zero fields select the library defaults (include/tpmg.h); boundary: 0 ghost-zero
+    Dirichlet [R1], 1 face Dirichlet [R25]."""
+    return tpmg_params(nx, ny, nz, nu_cfl, H, lam, levels, pre, post, coarse_sweeps, rho, boundary)
 
 
 class Context:

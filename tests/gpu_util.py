@@ -30,7 +30,8 @@ def ctx_for(p: O.Params, device: int = 0, loader: str | None = None):
     elif loader == "tma-fuse":
         os.environ["TPMG_FUSE_PROLONG"] = "1"
     params = T.make_params(p.nx, p.ny, nz=p.nz, nu_cfl=p.nu_cfl, H=p.H, lam=p.lam, levels=p.L,
-                           pre=p.pre, post=p.post, coarse_sweeps=p.coarse_sweeps, rho=p.rho)
+                           pre=p.pre, post=p.post, coarse_sweeps=p.coarse_sweeps, rho=p.rho,
+                           boundary=p.boundary)
     return T.Context(params, device=device)
 
 

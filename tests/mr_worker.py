@@ -31,8 +31,10 @@ def check(name, got, want, tol):
 obj = [T.tpmg_nccl_id() if rank == 0 else None]
 dist.broadcast_object_list(obj, src=0)
 nx, ny, nz, L = 64, 64 * world, 16, 5
-P = O.Params(nx=nx, ny=ny, nz=nz, L=L)
-ctx = T.Context(T.make_params(nx, ny, nz=nz, levels=L), rank=rank, nranks=world, id128=obj[0], device=local)
+BC = int(os.environ.get("TPMG_TEST_BOUNDARY", "0"))   # 1: face Dirichlet [R25]
+P = O.Params(nx=nx, ny=ny, nz=nz, L=L, boundary=BC)
+ctx = T.Context(T.make_params(nx, ny, nz=nz, levels=L, boundary=BC), rank=rank, nranks=world, id128=obj[0],
+                device=local)
 
 
 def strip(x_zc, level):

@@ -14,18 +14,18 @@ def ngpus():
     return torch.cuda.device_count()
 
 
-@pytest.mark.parametrize("world,overlap,halo", [(2, "0", "p2p"), (2, "0", "nccl"), (2, "1", "nccl"),
-                                               (4, "0", "p2p")])
-def test_multirank_parity(world, overlap, halo):
+@pytest.mark.parametrize("world,overlap,halo,bc", [(2, "0", "p2p", "0"), (2, "0", "nccl", "0"), (2, "1", "nccl", "0"),
+                                                  (4, "0", "p2p", "0"), (2, "0", "p2p", "1"), (4, "0", "nccl", "1")])
+def test_multirank_parity(world, overlap, halo, bc):
     """halo=p2p: device-initiated pushes into the neighbours' IPC-mapped slabs with
     stream-memory-op flags; halo=nccl: ncclSend/Recv.  overlap=1 (NCCL only): exchanges on
     their own stream/communicator, concurrent with the interior tile rows."""
     if ngpus() < world:
         pytest.skip(f"needs {world} GPUs, box has {ngpus()}")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + (10 if halo == "p2p" else 0) + (20 if overlap == "1" else 0)),
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + (10 if halo == "p2p" else 0) + (20 if overlap == "1" else 0) + (40 if bc == "1" else 0)),
            os.path.join(ROOT, "tests", "mr_worker.py")]
-    env = dict(os.environ, TPMG_OVERLAP=overlap, TPMG_HALO=halo)
+    env = dict(os.environ, TPMG_OVERLAP=overlap, TPMG_HALO=halo, TPMG_TEST_BOUNDARY=bc)
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 0, (r.stdout[-4000:], r.stderr[-4000:])
     assert f"MULTIRANK OK world={world}" in r.stdout

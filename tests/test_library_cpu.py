@@ -64,6 +64,7 @@ def test_version_and_defaults(T):
     (dict(nx=32, ny=32, rho=2.5), "TPMG_E_PARAM"),
     (dict(nx=40, ny=32), "TPMG_E_SHAPE"),         # 40 not divisible by 2^(5-1)
     (dict(nx=32, ny=24), "TPMG_E_SHAPE"),
+    (dict(nx=32, ny=32, boundary=2), "TPMG_E_PARAM"),
     (dict(nx=32, ny=32, nz=100000), "TPMG_E_SHAPE"),
 ])
 def test_create_rejects_bad_parameters(T, kw, status):
