@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--solver", choices=["both", "mg", "cg"], default="both")
     ap.add_argument("--levels", type=int, default=5, help="multigrid levels L (P:418; 7 and 10 in sec:Robustness)")
     ap.add_argument("--coarse-sweeps", type=int, default=2, help="smoother sweeps on the coarsest level (P:456)")
+    ap.add_argument("--boundary", type=int, default=0, choices=[0, 1],
+                    help="horizontal Dirichlet reading: 0 ghost zero [R1], 1 face [R25] (sec:Robustness runs)")
     ap.add_argument("--global-nx", type=int, default=0,
                     help="strong scaling: a fixed global nx x nx x nz grid split into y-strips (4096 = configs[4])")
     return ap.parse_args()
@@ -146,7 +148,7 @@ def measured_peak():
 
 # ---------------------------------------------------------------------------- oracle legs
 
-def oracle_sample(nx, nz, nu, rows, seed, threads=None, levels=5, coarse_sweeps=2):
+def oracle_sample(nx, nz, nu, rows, seed, threads=None, levels=5, coarse_sweeps=2, boundary=0):
     """Time the CPU oracle (as it stands) on a y-strip of `rows` rows of the workload:
     one MG V-cycle (solve_mg, max_iter=1: norm + V-cycle + residual) and one PCG
     iteration (solve_cg, max_iter=1: setup preconditioner + one iteration)."""
@@ -154,7 +156,7 @@ def oracle_sample(nx, nz, nu, rows, seed, threads=None, levels=5, coarse_sweeps=
     from inputs import rhs_zc
     if threads:
         O.set_threads(threads)
-    p = O.Params(nx=nx, ny=rows, nz=nz, nu_cfl=nu, L=levels, coarse_sweeps=coarse_sweeps)
+    p = O.Params(nx=nx, ny=rows, nz=nz, nu_cfl=nu, L=levels, coarse_sweeps=coarse_sweeps, boundary=boundary)
     f = rhs_zc(nx, rows, nz, seed=seed)
     t0 = time.perf_counter()
     O.solve_mg(p, f, eps=1e-30, max_iter=1)
@@ -175,13 +177,13 @@ def run_reference(args):
     it_mg, it_cg = 9, 51  # iteration counts of the oracle at 128^2 x 128 (tests/test_oracle_pins)
     for _ in range(args.warmup):
         oracle_sample(nx, args.nz, args.nu, rows, args.seed, levels=args.levels,
-                     coarse_sweeps=args.coarse_sweeps)
+                     coarse_sweeps=args.coarse_sweeps, boundary=args.boundary)
     t = 0.0
     wall = 0.0
     for _ in range(args.steps):
         w0 = time.perf_counter()
         a, b, cores = oracle_sample(nx, args.nz, args.nu, rows, args.seed, levels=args.levels,
-                     coarse_sweeps=args.coarse_sweeps)
+                     coarse_sweeps=args.coarse_sweeps, boundary=args.boundary)
         wall += time.perf_counter() - w0
         t += scale * (it_mg * a + it_cg * b)
     N = nx * ny * args.nz
@@ -196,7 +198,7 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "strong" if args.global_nx else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (splitmix64 RHS, seed %d)" % args.seed,
         "config": {"workload": name, "nx": nx, "ny": ny, "nz": args.nz, "nu_cfl": args.nu, "eps": args.eps,
-                   "levels": args.levels, "coarse_sweeps": args.coarse_sweeps},
+                   "levels": args.levels, "coarse_sweeps": args.coarse_sweeps, "boundary": args.boundary},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -229,7 +231,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         id128 = obj[0]
     stream = torch.cuda.Stream(device=local)
-    params = T.make_params(nx, ny, nz=nz, nu_cfl=args.nu, levels=args.levels, coarse_sweeps=args.coarse_sweeps)
+    params = T.make_params(nx, ny, nz=nz, nu_cfl=args.nu, levels=args.levels, coarse_sweeps=args.coarse_sweeps,
+                           boundary=args.boundary)
     ctx = T.Context(params, rank=rank, nranks=world, id128=id128, device=local, stream=stream)
     shape = ctx.shape(args.levels)
     f = torch.empty(shape, dtype=torch.float64, device=f"cuda:{local}")
@@ -345,7 +348,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rows = max(128, 1 << (args.levels - 1))
         a, b, cores = oracle_sample(nx, nz, args.nu, rows, args.seed, levels=args.levels,
-                                       coarse_sweeps=args.coarse_sweeps)
+                                       coarse_sweeps=args.coarse_sweeps, boundary=args.boundary)
         scale = ny / rows
         it_mg = its[0].iterations if its[0] else 0
         it_cg = its[1].iterations if its[1] else 0
@@ -362,7 +365,7 @@ def main():
             "scaling": "strong" if args.global_nx else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (splitmix64 uniform[-1,1) RHS keyed by global index, seed %d)" % args.seed,
             "config": {"workload": name, "nx": nx, "ny": ny, "nz": nz, "nu_cfl": args.nu, "eps": args.eps,
-                       "levels": args.levels, "coarse_sweeps": args.coarse_sweeps, "parallelism": f"y-strips x{world}" if world > 1 else "single GPU",
+                       "levels": args.levels, "coarse_sweeps": args.coarse_sweeps, "boundary": args.boundary, "parallelism": f"y-strips x{world}" if world > 1 else "single GPU",
                        "l2": "vectors 1 GiB/GPU >> 126 MB L2 (no flush needed)"},
             "roofline": roof,
             "cpu_baseline": cpu,

@@ -12,6 +12,15 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 echo "launch list exit $?" >> gpurun_out/ncu_launch_$TAG.log
 timeout 300 python scripts/profile_kernels.py > gpurun_out/prof_plain_$TAG.log 2>&1 && \
 timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_line|k_residual_restrict|k_prolong" -c ${NCU_COUNT:-12} \
+    -k regex:"k_line" -c ${NCU_COUNT:-12} \
     -o gpurun_out/prof_$TAG python scripts/profile_kernels.py > gpurun_out/ncu_full_$TAG.log 2>&1
 echo "full capture exit $?" >> gpurun_out/ncu_full_$TAG.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_prolong" -c 4 \
+    -o gpurun_out/profp_$TAG python scripts/profile_kernels.py > gpurun_out/ncu_fullp_$TAG.log 2>&1
+echo "prolong capture exit $?" >> gpurun_out/ncu_fullp_$TAG.log
+# raw metric exports travel back; reports only when small (gpurun copies <= 64 MiB)
+for r in prof profp; do
+  [ -f gpurun_out/${r}_$TAG.ncu-rep ] || continue
+  ncu -i gpurun_out/${r}_$TAG.ncu-rep --page raw --csv > gpurun_out/${r}_${TAG}_raw.csv 2>/dev/null
+  [ -n "$KEEP_REP" ] || rm -f gpurun_out/${r}_$TAG.ncu-rep
+done

@@ -12,7 +12,11 @@ MODES = {0: "apply", 1: "residual", 2: "precondition", 3: "smooth", 4: "cg_direc
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """Rows of `ncu -i rep --page raw --csv` (or of an exported .csv of that page)."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     return rows[0], rows[1], rows[2:]
 
