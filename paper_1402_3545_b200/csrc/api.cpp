@@ -62,6 +62,7 @@ struct tpmg_ctx {
     // solver run-ahead: device flags per iteration, their pinned host copies, events
     int* d_flags = nullptr;
     int* h_flags = nullptr;
+    int* dh_flags = nullptr;            // device view of h_flags (mapped pinned memory)
     int flags_cap = 0;
     const int* skip = nullptr;  // predicate put into every launch while set
     cudaEvent_t ev_it[8] = {};
@@ -802,6 +803,7 @@ tpmg_status ensure_flags(tpmg_ctx* ctx, int n)
         ctx->h_flags = nullptr;
         CUDA_TRY(ctx, cudaMalloc((void**)&ctx->d_flags, sizeof(int) * n));
         CUDA_TRY(ctx, cudaMallocHost((void**)&ctx->h_flags, sizeof(int) * n));
+        CUDA_TRY(ctx, cudaHostGetDevicePointer((void**)&ctx->dh_flags, ctx->h_flags, 0));
         ctx->flags_cap = n;
     }
     for (auto& e : ctx->ev_it)
@@ -811,9 +813,9 @@ tpmg_status ensure_flags(tpmg_ctx* ctx, int n)
 }
 
 // Copy flag[m] to the host ring and record its event.
+// The check kernel stored flags[m] into the mapped pinned h_flags too; the event marks it.
 tpmg_status post_flag(tpmg_ctx* ctx, int m)
 {
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags + m, ctx->d_flags + m, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_it[m & 7], ctx->stream));
     return TPMG_OK;
 }
@@ -901,7 +903,8 @@ tpmg_status solve_mg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
             bind_fine(ctx, u, f);
             TRY(mg_smooth(ctx, ctx->L, norms + n));
             TRY(allreduce(ctx, norms + n, 1));
-            CUDA_TRY(ctx, launch_mg_check(launcher(ctx), norms + n, ctx->d_scal, n, eps, max_iter, ctx->d_flags));
+            CUDA_TRY(ctx, launch_mg_check(launcher(ctx), norms + n, ctx->d_scal, n, eps, max_iter, ctx->d_flags,
+                                          ctx->dh_flags));
             TRY(post_flag(ctx, n));
             ctx->skip = ctx->d_flags + n;
             if (n < max_iter) {                   // cycle n+1 (skipped on the device once flags[n] != 0)
@@ -1059,7 +1062,7 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
             TRY(run_line(ctx, MODE_CGPREC, a));
             TRY(allreduce(ctx, ctx->d_scal + S_RR(m), 2));
         }
-        CUDA_TRY(ctx, launch_cg_check(launcher(ctx), ctx->d_scal, m, eps, ctx->d_flags));
+        CUDA_TRY(ctx, launch_cg_check(launcher(ctx), ctx->d_scal, m, eps, ctx->d_flags, ctx->dh_flags));
         TRY(post_flag(ctx, m));
         enq = m;
         cur ^= 1;

@@ -646,7 +646,16 @@ __global__ void __launch_bounds__(256) k_halo_push(const HaloPush hp, int64_t n)
 
 // Convergence test of PCG iteration m on the device: ||r_m|| / ||r_0|| < eps
 // (eqn:epsilonTolerance), breakdown when <p, A p> <= 0 or <r, M^-1 r> <= 0.
-__global__ void k_cg_check(const double* scal, int m, double eps, int* flags)
+// The host reads the flag from pinned memory after an event behind the check kernel:
+// a system-scope store instead of a 4-byte copy in the stream (no copy-engine bubble).
+__device__ __forceinline__ void publish_flag(int* hflags, int m, int code)
+{
+    if (!hflags) return;
+    *reinterpret_cast<volatile int*>(hflags + m) = code;
+    __threadfence_system();
+}
+
+__global__ void k_cg_check(const double* scal, int m, double eps, int* flags, int* hflags)
 {
     const int prev = (m >= 1) ? flags[m - 1] : 0;
     int code = prev;
@@ -658,10 +667,12 @@ __global__ void k_cg_check(const double* scal, int m, double eps, int* flags)
         else if (!(zeta > 0.0)) code = 2;
     }
     flags[m] = code;
+    publish_flag(hflags, m, code);
 }
 
 // Convergence test of MG cycle n: ||f - A u_n|| / ||r_0|| < eps, or the cycle limit.
-__global__ void k_mg_check(const double* norm2, const double* r0_2, int n, double eps, int max_iter, int* flags)
+__global__ void k_mg_check(const double* norm2, const double* r0_2, int n, double eps, int max_iter, int* flags,
+                           int* hflags)
 {
     const int prev = (n >= 1) ? flags[n - 1] : 0;
     int code = prev;
@@ -672,6 +683,7 @@ __global__ void k_mg_check(const double* norm2, const double* r0_2, int n, doubl
         else if (n >= max_iter) code = 4;
     }
     flags[n] = code;
+    publish_flag(hflags, n, code);
 }
 
 }  // namespace
@@ -707,17 +719,17 @@ cudaError_t launch_halo_push(const Launcher& ln, const HaloPush& hp)
     return cudaGetLastError();
 }
 
-cudaError_t launch_cg_check(const Launcher& ln, const double* scal, int m, double eps, int* flags)
+cudaError_t launch_cg_check(const Launcher& ln, const double* scal, int m, double eps, int* flags, int* hflags)
 {
-    k_cg_check<<<1, 1, 0, ln.stream>>>(scal, m, eps, flags);
+    k_cg_check<<<1, 1, 0, ln.stream>>>(scal, m, eps, flags, hflags);
     if (ln.launch_counter) ++*ln.launch_counter;
     return cudaGetLastError();
 }
 
 cudaError_t launch_mg_check(const Launcher& ln, const double* norm2, const double* r0_2, int n, double eps,
-                            int max_iter, int* flags)
+                            int max_iter, int* flags, int* hflags)
 {
-    k_mg_check<<<1, 1, 0, ln.stream>>>(norm2, r0_2, n, eps, max_iter, flags);
+    k_mg_check<<<1, 1, 0, ln.stream>>>(norm2, r0_2, n, eps, max_iter, flags, hflags);
     if (ln.launch_counter) ++*ln.launch_counter;
     return cudaGetLastError();
 }

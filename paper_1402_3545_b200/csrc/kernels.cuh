@@ -197,10 +197,10 @@ cudaError_t launch_cg_halo(const Launcher& ln, double* out_lo, const double* z_l
 // Flag codes: 0 continue, 1 converged, 2 breakdown, 3 NaN, 4 iteration limit.
 // CG iteration m (m >= 1): scal[3m] = sigma, scal[3m+1] = ||r||^2, scal[3m+2] = zeta; m = 0 is the
 // setup (scal[1] = ||r_0||^2, scal[2] = zeta_0).  flags[m] = flags[m-1] if set, else the test.
-cudaError_t launch_cg_check(const Launcher& ln, const double* scal, int m, double eps, int* flags);
+cudaError_t launch_cg_check(const Launcher& ln, const double* scal, int m, double eps, int* flags, int* hflags);
 // MG cycle n: norm2 = ||f - A u_n||^2, r0_2 = ||r_0||^2.
 cudaError_t launch_mg_check(const Launcher& ln, const double* norm2, const double* r0_2, int n, double eps,
-                            int max_iter, int* flags);
+                            int max_iter, int* flags, int* hflags);
 // result = sum x*y over n elements (deterministic)
 cudaError_t launch_dot(const Launcher& ln, const double* x, const double* y, int64_t n,
                        ReduceSlot red);
