@@ -258,6 +258,11 @@ typedef enum {
  * their summed device time (ms) and the summed number of grid cells they
  * processed (fine cells for the transfer kernels). */
 tpmg_status tpmg_profile(tpmg_ctx *ctx, int32_t enable);
+/* Like tpmg_profile for the classes in mask (bit k = tpmg_kernel k) only; 0 stops.
+ * Each bracketed launch costs a timing-event pair on the stream (a few microseconds
+ * of serialisation), so a benchmark can time one class live and leave the others
+ * unbracketed. */
+tpmg_status tpmg_profile_mask(tpmg_ctx *ctx, uint32_t mask);
 tpmg_status tpmg_profile_read(tpmg_ctx *ctx, int32_t kernel, int64_t *launches, double *ms,
                               double *cells);
 

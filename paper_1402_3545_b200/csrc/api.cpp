@@ -101,7 +101,9 @@ struct tpmg_ctx {
     tpmg_stats stats{};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // profiling (tpmg_profile)
+    bool pdl = false;                   // programmatic dependent launches (TPMG_PDL=1)
     bool prof_on = false;
+    uint32_t prof_mask = 0;             // kernel classes bracketed with events (bit = tpmg_kernel)
     struct ProfRec { int cls; double cells; cudaEvent_t a, b; };
     std::vector<ProfRec> prof_pending;
     std::vector<cudaEvent_t> prof_pool;
@@ -161,6 +163,7 @@ Launcher launcher(tpmg_ctx* ctx)
     ln.num_sms = ctx->num_sms;
     ln.launch_counter = &ctx->stats.kernel_launches;
     ln.reserve_sms = ctx->cur_reserve;
+    ln.pdl = ctx->pdl;
     return ln;
 }
 
@@ -364,7 +367,7 @@ struct ProfScope {
     cudaEvent_t a = nullptr;
     ProfScope(tpmg_ctx* c, int k, double n) : ctx(c), cls(k), cells(n)
     {
-        if (ctx->prof_on) {
+        if (ctx->prof_on && ((ctx->prof_mask >> cls) & 1u)) {
             a = prof_event(ctx);
             cudaEventRecord(a, ctx->stream);
         }
@@ -1308,6 +1311,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->overlap = ov && ov[0] == '1';
         const char* rs = std::getenv("TPMG_RESERVE_SMS");
         if (rs) ctx->reserve_sms = std::max(0, std::atoi(rs));
+        const char* pd = std::getenv("TPMG_PDL");
+        ctx->pdl = pd && pd[0] == '1';
         const char* fp = std::getenv("TPMG_FUSE_PROLONG");
         ctx->fuse_prolong = fp && fp[0] == '1';
         const char* sd = std::getenv("TPMG_SYNC_DEBUG");
@@ -1606,7 +1611,13 @@ tpmg_status tpmg_stats_reset(tpmg_ctx* ctx)
 
 tpmg_status tpmg_profile(tpmg_ctx* ctx, int32_t enable)
 {
+    return tpmg_profile_mask(ctx, enable ? ((1u << TPMG_K_COUNT) - 1u) : 0u);
+}
+
+tpmg_status tpmg_profile_mask(tpmg_ctx* ctx, uint32_t mask)
+{
     if (!ctx) return TPMG_E_PARAM;
+    const bool enable = (mask & ((1u << TPMG_K_COUNT) - 1u)) != 0;
     if (enable) {
         TRY(prof_collect(ctx));
         for (int k = 0; k < TPMG_K_COUNT; ++k) {
@@ -1615,7 +1626,8 @@ tpmg_status tpmg_profile(tpmg_ctx* ctx, int32_t enable)
             ctx->prof_cells[k] = 0;
         }
     }
-    ctx->prof_on = enable != 0;
+    ctx->prof_on = enable;
+    ctx->prof_mask = mask;
     return TPMG_OK;
 }
 

@@ -10,6 +10,12 @@
 namespace tpmg {
 namespace dev {
 
+// Programmatic dependent launch (sm_90+): wait for the previous kernel in the stream to
+// complete and flush (a no-op when the kernel was launched without the attribute), and
+// allow the next kernel to be scheduled once every CTA of this one has started.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid)
 {
     unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));

@@ -145,7 +145,6 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     using G = Geom<NH, NP, TY>;
     constexpr int NT = G::NT;
 
-    if (a.skip && *a.skip) return;   // solver run-ahead: this iteration is not needed
     extern __shared__ __align__(128) double smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[NS];
     // TMA destinations must be 128-byte aligned: align the dynamic window explicitly
@@ -174,6 +173,11 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         }
     }
+
+    // prologue above (tables, barriers) overlaps the previous kernel's tail under PDL
+    pdl_wait();
+    pdl_trigger();
+    if (a.skip && *a.skip) return;   // solver run-ahead: this iteration is not needed
 
     double ratio = 0.0;
     if constexpr (MODE == MODE_CGDIR || MODE == MODE_CGPREC)
@@ -466,9 +470,7 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
     const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * part_rows(a.part, (int)((a.L.ny + TY - 1) / TY));
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, ln.num_sms - ln.reserve_sms) * per_sm);
     if (grid <= 0) return cudaSuccess;
-    kern<<<(unsigned)grid, TX * TY, smem, ln.stream>>>(a);
-    if (ln.launch_counter) ++*ln.launch_counter;
-    return cudaGetLastError();
+    return launch_kernel(ln, kern, dim3((unsigned)grid), dim3(TX * TY), smem, a);
 }
 
 template <int MODE, int TY>
@@ -490,6 +492,8 @@ cudaError_t launch_line_ty(const Launcher& ln, const LineArgs& a)
 __global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double* __restrict__ r,
                            double* __restrict__ fc)
 {
+    pdl_wait();
+    pdl_trigger();
     const int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int k = blockIdx.y;
     const int64_t J = blockIdx.z;
@@ -509,6 +513,8 @@ __global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double
 __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const LevelConst F, const HaloField uc,
                                                      double* __restrict__ uf, int lpt, const int* skip, int part)
 {
+    pdl_wait();
+    pdl_trigger();
     if (skip && *skip) return;
     const int64_t nxc = Cc.nx, nyc = Cc.ny;
     const int nz = Cc.nz;
@@ -588,6 +594,8 @@ __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const 
 __global__ void __launch_bounds__(256) k_dot(const double* __restrict__ x, const double* __restrict__ y,
                                              int64_t n, ReduceSlot red)
 {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double scratch[64];
     double acc[1] = {0.0};
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
@@ -598,6 +606,8 @@ __global__ void __launch_bounds__(256) k_dot(const double* __restrict__ x, const
 __global__ void __launch_bounds__(256) k_copy(double* __restrict__ dst, const double* __restrict__ src, int64_t n,
                                               const int* skip)
 {
+    pdl_wait();
+    pdl_trigger();
     if (skip && *skip) return;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
         dst[q] = src[q];
@@ -607,6 +617,8 @@ __global__ void __launch_bounds__(256) k_cg_halo(double* out_lo, const double* z
                                                  const double* z_hi, const double* p_hi, int64_t n, DevRatio r,
                                                  const int* skip)
 {
+    pdl_wait();
+    pdl_trigger();
     if (skip && *skip) return;
     const double beta = (r.num >= 0) ? r.s[r.num] / r.s[r.den] : 0.0;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
@@ -657,6 +669,8 @@ __device__ __forceinline__ void publish_flag(int* hflags, int m, int code)
 
 __global__ void k_cg_check(const double* scal, int m, double eps, int* flags, int* hflags)
 {
+    pdl_wait();
+    pdl_trigger();
     const int prev = (m >= 1) ? flags[m - 1] : 0;
     int code = prev;
     if (!prev) {
@@ -674,6 +688,8 @@ __global__ void k_cg_check(const double* scal, int m, double eps, int* flags, in
 __global__ void k_mg_check(const double* norm2, const double* r0_2, int n, double eps, int max_iter, int* flags,
                            int* hflags)
 {
+    pdl_wait();
+    pdl_trigger();
     const int prev = (n >= 1) ? flags[n - 1] : 0;
     int code = prev;
     if (!prev) {
@@ -692,9 +708,7 @@ cudaError_t launch_copy(const Launcher& ln, double* dst, const double* src, int6
 {
     if (n <= 0) return cudaSuccess;
     const int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)ln.num_sms * 8);
-    k_copy<<<(unsigned)grid, 256, 0, ln.stream>>>(dst, src, n, skip);
-    if (ln.launch_counter) ++*ln.launch_counter;
-    return cudaGetLastError();
+    return launch_kernel(ln, k_copy, dim3((unsigned)grid), dim3(256), 0, dst, src, n, skip);
 }
 
 cudaError_t launch_cg_halo(const Launcher& ln, double* out_lo, const double* z_lo, const double* p_lo, double* out_hi,
@@ -702,9 +716,7 @@ cudaError_t launch_cg_halo(const Launcher& ln, double* out_lo, const double* z_l
 {
     if (!out_lo && !out_hi) return cudaSuccess;
     const int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)ln.num_sms * 4);
-    k_cg_halo<<<(unsigned)grid, 256, 0, ln.stream>>>(out_lo, z_lo, p_lo, out_hi, z_hi, p_hi, n, beta, skip);
-    if (ln.launch_counter) ++*ln.launch_counter;
-    return cudaGetLastError();
+    return launch_kernel(ln, k_cg_halo, dim3((unsigned)grid), dim3(256), 0, out_lo, z_lo, p_lo, out_hi, z_hi, p_hi, n, beta, skip);
 }
 
 cudaError_t launch_halo_push(const Launcher& ln, const HaloPush& hp)
@@ -721,17 +733,13 @@ cudaError_t launch_halo_push(const Launcher& ln, const HaloPush& hp)
 
 cudaError_t launch_cg_check(const Launcher& ln, const double* scal, int m, double eps, int* flags, int* hflags)
 {
-    k_cg_check<<<1, 1, 0, ln.stream>>>(scal, m, eps, flags, hflags);
-    if (ln.launch_counter) ++*ln.launch_counter;
-    return cudaGetLastError();
+    return launch_kernel(ln, k_cg_check, dim3(1), dim3(1), 0, scal, m, eps, flags, hflags);
 }
 
 cudaError_t launch_mg_check(const Launcher& ln, const double* norm2, const double* r0_2, int n, double eps,
                             int max_iter, int* flags, int* hflags)
 {
-    k_mg_check<<<1, 1, 0, ln.stream>>>(norm2, r0_2, n, eps, max_iter, flags, hflags);
-    if (ln.launch_counter) ++*ln.launch_counter;
-    return cudaGetLastError();
+    return launch_kernel(ln, k_mg_check, dim3(1), dim3(1), 0, norm2, r0_2, n, eps, max_iter, flags, hflags);
 }
 
 int line_launch_rows(int mode, int nz, int nx, int use_tma, int ksplit_cfg)
@@ -777,9 +785,7 @@ cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const Le
 {
     dim3 block(64), grid((unsigned)((coarse.nx + 63) / 64), (unsigned)coarse.nz, (unsigned)coarse.ny);
     if (coarse.ny <= 0 || coarse.nx <= 0) return cudaSuccess;
-    k_restrict<<<grid, block, 0, ln.stream>>>(fine, coarse, r, fc);
-    if (ln.launch_counter) ++*ln.launch_counter;
-    return cudaGetLastError();
+    return launch_kernel(ln, k_restrict, dim3(grid), dim3(block), 0, fine, coarse, r, fc);
 }
 
 cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, const LevelConst& fine,
@@ -797,18 +803,14 @@ cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, con
     if (part == PART_INTERIOR) grid.y = (unsigned)((std::max<int64_t>(coarse.ny - 2, 0) + 3) / 4);
     if (part == PART_BOUNDARY) grid.y = 1;
     if (grid.y == 0) return cudaSuccess;
-    k_prolong_add<<<grid, block, 0, ln.stream>>>(coarse, fine, uc, uf, lpt, skip, part);
-    if (ln.launch_counter) ++*ln.launch_counter;
-    return cudaGetLastError();
+    return launch_kernel(ln, k_prolong_add, dim3(grid), dim3(block), 0, coarse, fine, uc, uf, lpt, skip, part);
 }
 
 cudaError_t launch_dot(const Launcher& ln, const double* x, const double* y, int64_t n, ReduceSlot red)
 {
     int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)ln.num_sms * 4);
     grid = std::max<int64_t>(grid, 1);
-    k_dot<<<(unsigned)grid, 256, 0, ln.stream>>>(x, y, n, red);
-    if (ln.launch_counter) ++*ln.launch_counter;
-    return cudaGetLastError();
+    return launch_kernel(ln, k_dot, dim3((unsigned)grid), dim3(256), 0, x, y, n, red);
 }
 
 }  // namespace tpmg

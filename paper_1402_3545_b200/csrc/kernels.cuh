@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <utility>
 
 namespace tpmg {
 
@@ -131,7 +132,31 @@ struct Launcher {
     int num_sms;
     int64_t* launch_counter;
     int reserve_sms;   // SMs left free (for NCCL kernels running concurrently)
+    bool pdl = false;  // programmatic dependent launch: overlap a kernel's launch and
+                       // prologue with the previous kernel's tail (griddepcontrol)
 };
+
+// Launch with the PDL attribute when ln.pdl.  Every kernel launched this way executes
+// griddepcontrol.wait (dev::pdl_wait) in every CTA before touching global data, so it
+// still observes all writes of the kernels before it.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_kernel(const Launcher& ln, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                          Args&&... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ln.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = ln.pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+    if (e == cudaSuccess && ln.launch_counter) ++*ln.launch_counter;
+    return e;
+}
 
 // Tile rows of the line kernel that will run for (mode, nz, nx) (TY of the chosen kernel).
 int line_launch_rows(int mode, int nz, int nx, int use_tma, int ksplit_cfg);

@@ -132,7 +132,6 @@ template <int MODE, int TY, int NSEG, int KB, int NS2>
 __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_constant__ LineArgs a,
                                                              const __grid_constant__ KTables T)
 {
-    if (a.skip && *a.skip) return;   // solver run-ahead: this iteration is not needed
     using G = KGeom<MODE, TY, KB>;
     constexpr int NT = 32 * TY * NSEG;
     constexpr int NCC = SL / KB;           // chunks per segment
@@ -160,6 +159,10 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
         for (int q = 0; q < NS2; ++q) mbar_init(&full_bar[q], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    // prologue above (tables, barriers) overlaps the previous kernel's tail under PDL
+    pdl_wait();
+    pdl_trigger();
+    if (a.skip && *a.skip) return;   // solver run-ahead: this iteration is not needed
     double acc[1] = {0.0};
 
     const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + TY - 1) / TY);
@@ -375,9 +378,7 @@ cudaError_t launch_k(const Launcher& ln, const LineArgs& a, const KTables& T)
     const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * part_rows(a.part, (int)((a.L.ny + TY - 1) / TY));
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, ln.num_sms - ln.reserve_sms) * per_sm);
     if (grid <= 0) return cudaSuccess;
-    kern<<<(unsigned)grid, 32 * TY * NSEG, smem, ln.stream>>>(a, T);
-    if (ln.launch_counter) ++*ln.launch_counter;
-    return cudaGetLastError();
+    return launch_kernel(ln, kern, dim3((unsigned)grid), dim3(32 * TY * NSEG), smem, a, T);
 }
 
 template <int MODE, int TY, int KB, int NS2>

@@ -73,6 +73,7 @@ _SIGS = {
     "tpmg_get_stats": ([_vp, _P(tpmg_stats)], C.c_int),
     "tpmg_stats_reset": ([_vp], C.c_int),
     "tpmg_profile": ([_vp, _i32], C.c_int),
+    "tpmg_profile_mask": ([_vp, C.c_uint32], C.c_int),
     "tpmg_profile_read": ([_vp, _i32, _P(_i64), _P(_d), _P(_d)], C.c_int),
     "tpmg_last_error": ([_vp], C.c_char_p),
 }
@@ -254,6 +255,10 @@ def tpmg_profile(ctx: int, enable: bool) -> None:
     _check(_lib.tpmg_profile(ctx, 1 if enable else 0), ctx)
 
 
+def tpmg_profile_mask(ctx: int, mask: int) -> None:
+    _check(_lib.tpmg_profile_mask(ctx, mask), ctx)
+
+
 def tpmg_profile_read(ctx: int, kernel: int):
     n, ms, cells = _i64(), _d(), _d()
     _check(_lib.tpmg_profile_read(ctx, kernel, C.byref(n), C.byref(ms), C.byref(cells)), ctx)
@@ -354,8 +359,12 @@ class Context:
     def stats_reset(self):
         tpmg_stats_reset(self.handle)
 
-    def profile(self, enable: bool):
-        tpmg_profile(self.handle, enable)
+    def profile(self, enable: bool, classes=None):
+        """Event-time every kernel class (enable), or only the named classes."""
+        if classes is None:
+            tpmg_profile(self.handle, enable)
+        else:
+            tpmg_profile_mask(self.handle, sum(1 << KERNEL_CLASSES.index(c) for c in classes) if enable else 0)
 
     def profile_read(self) -> dict:
         """{class name: (launches, ms, cells)} for every kernel class with launches."""
