@@ -468,6 +468,11 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
     if (e != cudaSuccess) return e;
     per_sm = std::max(per_sm, 1);
     const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * part_rows(a.part, (int)((a.L.ny + TY - 1) / TY));
+    // CG direction (two halo'd fields): on wide grids two CTAs per SM re-read the halo
+    // rows from HBM (2.1x the algorithmic reads at 4096 x 1024 x 128, ncu); one CTA per SM
+    // avoids it.  Measured (TB/s, 2 vs 1 CTA/SM): nx = 1024: 4.8-5.0 vs 4.7-4.8;
+    // nx = 2048: 4.0 vs 4.8; nx = 4096: 3.5 vs 4.7.
+    if (MODE == MODE_CGDIR && a.L.nx > 32 * TX) per_sm = 1;
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, ln.num_sms - ln.reserve_sms) * per_sm);
     if (grid <= 0) return cudaSuccess;
     return launch_kernel(ln, kern, dim3((unsigned)grid), dim3(TX * TY), smem, a);
