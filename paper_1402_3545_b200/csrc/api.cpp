@@ -84,6 +84,9 @@ struct tpmg_ctx {
         double** cur_hi = nullptr;
         int epoch = 0;
         size_t off_lo[2] = {0, 0}, off_hi[2] = {0, 0}, off_flags = 0;  // byte offsets in the pool
+        const double* pushed = nullptr; // buffer whose boundary rows a producer kernel pushed
+                                        // with epoch `epoch` (fused push, not yet waited for)
+        bool publish = false;           // a fused push awaits its publish_pushed()
     };
     std::vector<Chan> chans;
     void* halo_pool = nullptr;
@@ -102,6 +105,8 @@ struct tpmg_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // profiling (tpmg_profile)
     bool pdl = false;                   // programmatic dependent launches (TPMG_PDL=1)
+    bool halo_off = false;              // TPMG_HALO=off: skip halo exchanges (timing experiments)
+    bool fused_push = true;             // P2P: producers push their boundary rows (TPMG_FUSED_PUSH=0: off)
     bool prof_on = false;
     uint32_t prof_mask = 0;             // kernel classes bracketed with events (bit = tpmg_kernel)
     struct ProfRec { int cls; double cells; cudaEvent_t a, b; };
@@ -214,6 +219,7 @@ tpmg_status exchange_on(tpmg_ctx* ctx, cudaStream_t st, ncclComm_t comm, size_t 
 
 // ---- device-initiated halo exchange over NVLink (P2P mode)
 PFN_cuStreamWaitValue32_v11070 g_wait_value = nullptr;
+PFN_cuStreamWriteValue32_v11070 g_write_value = nullptr;
 
 bool stream_memops()
 {
@@ -225,8 +231,12 @@ bool stream_memops()
         if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
             g_wait_value = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
+        p = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_write_value = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p);
     }
-    return g_wait_value != nullptr;
+    return g_wait_value != nullptr && g_write_value != nullptr;
 }
 
 tpmg_status wait_value(tpmg_ctx* ctx, const void* addr, uint32_t v)
@@ -236,39 +246,117 @@ tpmg_status wait_value(tpmg_ctx* ctx, const void* addr, uint32_t v)
     return TPMG_OK;
 }
 
-// Channel c exchange, epoch E, buffer b = E & 1.  Flags (uint32) of channel c in every
-// rank's pool: [0] data from the lower neighbour, [1] data from the upper, [2] push ticket.
-//   push:  one kernel stores my row 0 into the lower neighbour's hi[b] slab and my row
-//          ny-1 into the upper neighbour's lo[b] slab (remote stores over NVLink); its last
-//          block fences (system scope) and writes E into both neighbours' data flags;
-//   wait:  stream memory operations wait until both neighbours' epoch-E data has arrived.
-// No acknowledgements are needed: a neighbour's epoch E-1 push is stream-ordered after its
-// kernels that read epoch E-2 (the slot b that epoch E overwrites), and I push epoch E
-// only after my stream saw its epoch E-1 data.  No kernel spins.
-tpmg_status exchange_p2p(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int c, const double* x)
+// Stream-ordered store of v to addr once all preceding work (and its memory traffic, the
+// default write-value fence) has completed.
+tpmg_status write_value(tpmg_ctx* ctx, void* addr, uint32_t v)
 {
-    const int E = ++ch.epoch;
+    CUresult r = g_write_value((CUstream)ctx->stream, (CUdeviceptr)addr, v, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) return fail(ctx, TPMG_E_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+    return TPMG_OK;
+}
+
+// Remote destinations of channel c's epoch-E rows: slot E & 1 of the neighbours' slabs.
+HaloPush push_desc(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int E)
+{
     const int b = E & 1;
-    const bool has_lo = ctx->rank > 0, has_hi = ctx->rank < ctx->nranks - 1;
-    char* mine = static_cast<char*>(ctx->halo_pool) + ch.off_flags;
-    (void)c;
     HaloPush hp{};
-    hp.src_first = x;
-    hp.src_last = x + (size_t)(ch.nyl - 1) * ch.plane;
     hp.n = (int64_t)ch.plane;
-    hp.dst_lo = has_lo ? reinterpret_cast<double*>(ctx->peer_pool[0] + ch.off_hi[b]) : nullptr;
-    hp.dst_hi = has_hi ? reinterpret_cast<double*>(ctx->peer_pool[1] + ch.off_lo[b]) : nullptr;
-    hp.flag_lo = has_lo ? reinterpret_cast<unsigned*>(ctx->peer_pool[0] + ch.off_flags + 1 * 4) : nullptr;  // its "from upper"
-    hp.flag_hi = has_hi ? reinterpret_cast<unsigned*>(ctx->peer_pool[1] + ch.off_flags + 0 * 4) : nullptr;  // its "from lower"
-    hp.ticket = reinterpret_cast<unsigned*>(mine + 2 * 4);
-    hp.epoch = (unsigned)E;
-    CUDA_TRY(ctx, launch_halo_push(launcher(ctx), hp));
-    if (has_lo) TRY(wait_value(ctx, mine + 0 * 4, (uint32_t)E));
-    if (has_hi) TRY(wait_value(ctx, mine + 1 * 4, (uint32_t)E));
-    *ch.cur_lo = ch.lo[b];
-    *ch.cur_hi = ch.hi[b];
+    hp.dst_lo = ctx->rank > 0 ? reinterpret_cast<double*>(ctx->peer_pool[0] + ch.off_hi[b]) : nullptr;
+    hp.dst_hi = ctx->rank < ctx->nranks - 1 ? reinterpret_cast<double*>(ctx->peer_pool[1] + ch.off_lo[b]) : nullptr;
+    return hp;
+}
+
+// Publish epoch E of channel ch to the neighbours: stream write-values into their flags
+// ("data from upper" of the lower neighbour, "data from lower" of the upper one), each
+// fenced after the preceding kernel's remote stores (CU_STREAM_WRITE_VALUE_DEFAULT).
+tpmg_status publish_epoch(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int E)
+{
+    if (ctx->rank > 0) TRY(write_value(ctx, ctx->peer_pool[0] + ch.off_flags + 1 * 4, (uint32_t)E));
+    if (ctx->rank < ctx->nranks - 1) TRY(write_value(ctx, ctx->peer_pool[1] + ch.off_flags + 0 * 4, (uint32_t)E));
+    return TPMG_OK;
+}
+
+// Wait until both neighbours' epoch-E rows of channel ch have arrived; point the
+// consumers at slot E & 1.
+tpmg_status wait_epoch(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int E)
+{
+    char* mine = static_cast<char*>(ctx->halo_pool) + ch.off_flags;
+    if (ctx->rank > 0) TRY(wait_value(ctx, mine + 0 * 4, (uint32_t)E));
+    if (ctx->rank < ctx->nranks - 1) TRY(wait_value(ctx, mine + 1 * 4, (uint32_t)E));
+    *ch.cur_lo = ch.lo[E & 1];
+    *ch.cur_hi = ch.hi[E & 1];
     ++ctx->stats.halo_exchanges;
     return TPMG_OK;
+}
+
+// Channel c exchange, epoch E, slot b = E & 1.  Flags (uint32) of channel c in every
+// rank's pool: [0] data from the lower neighbour, [1] data from the upper.
+//   push:    my row 0 goes into the lower neighbour's hi[b] slab and my row ny-1 into the
+//            upper neighbour's lo[b] slab, by remote stores over NVLink: either the
+//            producer kernel of x already did it (fused push, see fused_push) or one
+//            k_halo_push kernel does it now;
+//   publish: stream write-values store E into both neighbours' flags after that kernel;
+//   wait:    stream wait-values until both neighbours' epoch-E flags are set.
+// No acknowledgements are needed: a neighbour's epoch E-1 push is stream-ordered after its
+// kernels that read epoch E-2 (the slot b that epoch E overwrites), and I push epoch E
+// only after my stream saw its epoch E-1 data (every pushed epoch is waited for, in
+// order, before the next push).  No kernel spins.
+tpmg_status exchange_p2p(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int c, const double* x)
+{
+    (void)c;
+    if (ch.pushed) {
+        const bool mine = (ch.pushed == x);
+        ch.pushed = nullptr;
+        TRY(wait_epoch(ctx, ch, ch.epoch));
+        if (mine) return TPMG_OK;   // the producer already pushed x's boundary rows
+    }
+    const int E = ++ch.epoch;
+    HaloPush hp = push_desc(ctx, ch, E);
+    hp.src_first = x;
+    hp.src_last = x + (size_t)(ch.nyl - 1) * ch.plane;
+    CUDA_TRY(ctx, launch_halo_push(launcher(ctx), hp));
+    TRY(publish_epoch(ctx, ch, E));
+    return wait_epoch(ctx, ch, E);
+}
+
+// Fused push for a producer kernel about to write `out` (a field of channel c that will
+// be read with its halo next): returns the remote destinations to hand to the kernel
+// (empty when halos are not device-initiated); publish_pushed() follows the launch.  A
+// pending push of the channel is waited for first, so epochs stay in order.
+tpmg_status fused_push(tpmg_ctx* ctx, int c, const double* out, HaloPush* hp)
+{
+    *hp = HaloPush{};
+    if (ctx->nranks == 1 || !ctx->p2p || ctx->halo_off || !ctx->fused_push) return TPMG_OK;
+    tpmg_ctx::Chan& ch = ctx->chans[c];
+    if (ch.pushed) {
+        ch.pushed = nullptr;
+        TRY(wait_epoch(ctx, ch, ch.epoch));
+    }
+    const int E = ++ch.epoch;
+    *hp = push_desc(ctx, ch, E);
+    ch.pushed = out;
+    ch.publish = true;
+    return TPMG_OK;
+}
+
+// After the producer kernel of a fused push: publish its epoch.
+tpmg_status publish_pushed(tpmg_ctx* ctx, int c)
+{
+    if (ctx->nranks == 1 || c >= (int)ctx->chans.size()) return TPMG_OK;
+    tpmg_ctx::Chan& ch = ctx->chans[c];
+    if (!ch.publish) return TPMG_OK;
+    ch.publish = false;
+    return publish_epoch(ctx, ch, ch.epoch);
+}
+
+// A public call must not trust buffer identities from an earlier call (the caller may
+// have refilled or reallocated a buffer at the same address): pending fused pushes stay
+// pending (they are still waited for, in order) but never stand in for an exchange.
+const double* const kPendingOnly = reinterpret_cast<const double*>(alignof(double));
+void begin_call(tpmg_ctx* ctx)
+{
+    for (auto& ch : ctx->chans)
+        if (ch.pushed) ch.pushed = kPendingOnly;
 }
 
 // Fill the current halo slabs of channel c (a level, or the CG z channel) from the
@@ -276,6 +364,7 @@ tpmg_status exchange_p2p(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int c, const double*
 tpmg_status exchange_chan(tpmg_ctx* ctx, int c, const double* x)
 {
     if (ctx->nranks == 1) return TPMG_OK;
+    if (ctx->halo_off) return TPMG_OK;   // TPMG_HALO=off: timing experiments only (wrong results)
     tpmg_ctx::Chan& ch = ctx->chans[c];
     if (ctx->p2p) return exchange_p2p(ctx, ch, c, x);
     return exchange_on(ctx, ctx->stream, ctx->comm, ch.plane, ch.nyl, x, *ch.cur_lo, *ch.cur_hi);
@@ -577,7 +666,7 @@ tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
 // boundary launch (e.g. the CG p-halo update).
 template <typename PreBoundary>
 tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, LineArgs a, const double* x, double* lo, double* hi,
-                          PreBoundary pre_boundary)
+                          PreBoundary pre_boundary, const double* push_out = nullptr)
 {
     if (ctx->nranks == 1) {
         TRY(pre_boundary());
@@ -590,7 +679,9 @@ tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, LineArgs a, const 
         TRY(exchange(ctx, level, x));
         if (a.h0.base == x) a.h0 = halo_of(ctx, level, x);   // P2P: the current slab buffer alternates
         TRY(pre_boundary());
-        return run_line(ctx, mode, a);
+        if (push_out) TRY(fused_push(ctx, level, push_out, &a.push));   // after the input's exchange
+        TRY(run_line(ctx, mode, a));
+        return push_out ? publish_pushed(ctx, level) : TPMG_OK;
     }
     TRY(start_async_exchange(ctx, level, x, lo, hi));
     a.part = PART_INTERIOR;
@@ -605,10 +696,11 @@ tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, LineArgs a, const 
     return run_line(ctx, mode, a);
 }
 
-tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, const LineArgs& a, const double* x)
+tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, const LineArgs& a, const double* x,
+                          const double* push_out = nullptr)
 {
     LevelData& L = ctx->lv[level];
-    return run_line_halo(ctx, level, mode, a, x, L.slab_lo, L.slab_hi, [] { return TPMG_OK; });
+    return run_line_halo(ctx, level, mode, a, x, L.slab_lo, L.slab_hi, [] { return TPMG_OK; }, push_out);
 }
 
 // out = u + rho M^-1 (f - A u) (out-of-place), optional sum r^2 into result
@@ -620,7 +712,7 @@ tpmg_status smooth_once(tpmg_ctx* ctx, int level, const double* u, const double*
     a.q0 = f;
     a.out0 = out;
     a.red.result = result;
-    return run_line_halo(ctx, level, MODE_SMOOTH, a, u);
+    return run_line_halo(ctx, level, MODE_SMOOTH, a, u, /*push_out=*/out);   // out is read halo'd next
 }
 
 // ------------------------------------------------------------------ multigrid
@@ -658,7 +750,9 @@ tpmg_status mg_restrict_smooth(tpmg_ctx* ctx, int l)
     a.out0 = Cc.u[0];
     a.scale = ctx->p.rho;
     Cc.cur = 0;
-    return run_line(ctx, MODE_PREC, a);
+    TRY(fused_push(ctx, l, Cc.u[0], &a.push));   // u_c is read halo'd next (restriction / smooth)
+    TRY(run_line(ctx, MODE_PREC, a));
+    return publish_pushed(ctx, l);
 }
 
 tpmg_status mg_smooth(tpmg_ctx* ctx, int l, double* result = nullptr)
@@ -679,9 +773,11 @@ tpmg_status prolong_overlapped(tpmg_ctx* ctx, int lc_)
     if (ctx->nranks == 1 || !ctx->overlap || ctx->p2p || Cc.lc.ny < 3) {
         TRY(exchange(ctx, lc_, Cc.u[Cc.cur]));
         const HaloField uc2 = halo_of(ctx, lc_, Cc.u[Cc.cur]);   // current slabs after the exchange
+        HaloPush hp;
+        TRY(fused_push(ctx, lc_ + 1, F.u[F.cur], &hp));            // u_f is read halo'd by the post-smooth
         ProfScope ps(ctx, TPMG_K_PROLONG_ADD, cells);
-        CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc2, F.u[F.cur], ctx->skip));
-        return TPMG_OK;
+        CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc2, F.u[F.cur], ctx->skip, PART_ALL, &hp));
+        return publish_pushed(ctx, lc_ + 1);
     }
     TRY(start_async_exchange(ctx, lc_, Cc.u[Cc.cur], Cc.slab_lo, Cc.slab_hi));
     const double fb = 2.0 / (double)Cc.lc.ny;
@@ -998,7 +1094,9 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
         a.out1 = u;
         a.out2 = ctx->cg_z;
         a.red.result = ctx->d_scal + S_RR(0);
+        TRY(fused_push(ctx, l + 1, ctx->cg_z, &a.push));   // z is read halo'd by the direction kernel
         TRY(run_line(ctx, MODE_CGPREC, a));
+        TRY(publish_pushed(ctx, l + 1));
         TRY(allreduce(ctx, ctx->d_scal + S_RR(0), 2));
         TRY(fetch(ctx, ctx->d_scal + S_RR(0), 2));
     }
@@ -1062,7 +1160,9 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
             a.out2 = ctx->cg_z;
             a.ratio = DevRatio{ctx->d_scal, S_ZETA(m - 1), S_SIGMA(m)};
             a.red.result = ctx->d_scal + S_RR(m);
+            TRY(fused_push(ctx, l + 1, ctx->cg_z, &a.push));
             TRY(run_line(ctx, MODE_CGPREC, a));
+            TRY(publish_pushed(ctx, l + 1));
             TRY(allreduce(ctx, ctx->d_scal + S_RR(m), 2));
         }
         CUDA_TRY(ctx, launch_cg_check(launcher(ctx), ctx->d_scal, m, eps, ctx->d_flags, ctx->dh_flags));
@@ -1150,6 +1250,9 @@ tpmg_status halo_setup(tpmg_ctx* ctx)
         *ch.cur_hi = ch.hi[0];
     }
     const char* hm = std::getenv("TPMG_HALO");
+    ctx->halo_off = hm && std::strcmp(hm, "off") == 0;
+    const char* fpu = std::getenv("TPMG_FUSED_PUSH");
+    ctx->fused_push = !(fpu && fpu[0] == '0');
     ctx->p2p = !(hm && std::strcmp(hm, "nccl") == 0) && stream_memops();
     if (!ctx->p2p) return TPMG_OK;
     // exchange the pool handles
@@ -1464,6 +1567,7 @@ tpmg_status tpmg_local_box(const tpmg_ctx* cctx, int32_t level, int64_t* y0, int
 
 tpmg_status tpmg_apply(tpmg_ctx* ctx, int32_t level, const double* x, double* y)
 {
+    if (ctx) begin_call(ctx);
     TRY(check_level(ctx, level));
     if (!x || !y) return fail(ctx, TPMG_E_PARAM, "tpmg_apply: NULL vector");
     if (x == y) return fail(ctx, TPMG_E_SHAPE, "tpmg_apply: x and y must differ");
@@ -1476,6 +1580,7 @@ tpmg_status tpmg_apply(tpmg_ctx* ctx, int32_t level, const double* x, double* y)
 tpmg_status tpmg_residual(tpmg_ctx* ctx, int32_t level, const double* u, const double* f, double* r,
                           double* norm2)
 {
+    if (ctx) begin_call(ctx);
     TRY(check_level(ctx, level));
     if (!u || !f) return fail(ctx, TPMG_E_PARAM, "tpmg_residual: NULL vector");
     if (r == u) return fail(ctx, TPMG_E_SHAPE, "tpmg_residual: r must not alias u");
@@ -1497,6 +1602,7 @@ tpmg_status tpmg_residual(tpmg_ctx* ctx, int32_t level, const double* u, const d
 
 tpmg_status tpmg_precondition(tpmg_ctx* ctx, int32_t level, const double* r, double* z)
 {
+    if (ctx) begin_call(ctx);
     TRY(check_level(ctx, level));
     if (!r || !z) return fail(ctx, TPMG_E_PARAM, "tpmg_precondition: NULL vector");
     if (r == z) return fail(ctx, TPMG_E_SHAPE, "tpmg_precondition: r and z must differ");
@@ -1508,6 +1614,7 @@ tpmg_status tpmg_precondition(tpmg_ctx* ctx, int32_t level, const double* r, dou
 
 tpmg_status tpmg_smooth(tpmg_ctx* ctx, int32_t level, double* u, const double* f, int32_t sweeps)
 {
+    if (ctx) begin_call(ctx);
     TRY(check_level(ctx, level));
     if (!u || !f) return fail(ctx, TPMG_E_PARAM, "tpmg_smooth: NULL vector");
     if (sweeps < 0) return fail(ctx, TPMG_E_PARAM, "tpmg_smooth: sweeps < 0");
@@ -1527,6 +1634,7 @@ tpmg_status tpmg_smooth(tpmg_ctx* ctx, int32_t level, double* u, const double* f
 
 tpmg_status tpmg_restrict(tpmg_ctx* ctx, int32_t fine_level, const double* r_fine, double* f_coarse)
 {
+    if (ctx) begin_call(ctx);
     TRY(check_level(ctx, fine_level));
     if (fine_level < 2) return fail(ctx, TPMG_E_RANGE, "tpmg_restrict: fine_level %d < 2", fine_level);
     if (!r_fine || !f_coarse) return fail(ctx, TPMG_E_PARAM, "tpmg_restrict: NULL vector");
@@ -1537,6 +1645,7 @@ tpmg_status tpmg_restrict(tpmg_ctx* ctx, int32_t fine_level, const double* r_fin
 
 tpmg_status tpmg_prolong_add(tpmg_ctx* ctx, int32_t coarse_level, const double* u_coarse, double* u_fine)
 {
+    if (ctx) begin_call(ctx);
     TRY(check_level(ctx, coarse_level));
     if (coarse_level >= ctx->L) return fail(ctx, TPMG_E_RANGE, "tpmg_prolong_add: coarse_level %d >= L", coarse_level);
     if (!u_coarse || !u_fine) return fail(ctx, TPMG_E_PARAM, "tpmg_prolong_add: NULL vector");
@@ -1549,6 +1658,7 @@ tpmg_status tpmg_prolong_add(tpmg_ctx* ctx, int32_t coarse_level, const double* 
 
 tpmg_status tpmg_vcycle(tpmg_ctx* ctx, double* u, const double* f)
 {
+    if (ctx) begin_call(ctx);
     if (!ctx) return TPMG_E_PARAM;
     if (!u || !f) return fail(ctx, TPMG_E_PARAM, "tpmg_vcycle: NULL vector");
     if (u == f) return fail(ctx, TPMG_E_SHAPE, "tpmg_vcycle: u and f must differ");
@@ -1561,6 +1671,7 @@ tpmg_status tpmg_vcycle(tpmg_ctx* ctx, double* u, const double* f)
 tpmg_status tpmg_solve_mg(tpmg_ctx* ctx, const double* f, double* u, double eps, int32_t max_iter,
                           tpmg_result* res)
 {
+    if (ctx) begin_call(ctx);
     if (!ctx) return TPMG_E_PARAM;
     if (!u || !f) return fail(ctx, TPMG_E_PARAM, "tpmg_solve_mg: NULL vector");
     if (u == f) return fail(ctx, TPMG_E_SHAPE, "tpmg_solve_mg: u and f must differ");
@@ -1571,6 +1682,7 @@ tpmg_status tpmg_solve_mg(tpmg_ctx* ctx, const double* f, double* u, double eps,
 tpmg_status tpmg_solve_cg(tpmg_ctx* ctx, const double* f, double* u, double eps, int32_t max_iter,
                           tpmg_result* res)
 {
+    if (ctx) begin_call(ctx);
     if (!ctx) return TPMG_E_PARAM;
     if (!u || !f) return fail(ctx, TPMG_E_PARAM, "tpmg_solve_cg: NULL vector");
     if (u == f) return fail(ctx, TPMG_E_SHAPE, "tpmg_solve_cg: u and f must differ");
@@ -1581,6 +1693,7 @@ tpmg_status tpmg_solve_cg(tpmg_ctx* ctx, const double* f, double* u, double eps,
 tpmg_status tpmg_solve_host(tpmg_ctx* ctx, tpmg_solver solver, const double* f_host, double* u_host,
                             double eps, int32_t max_iter, tpmg_result* res)
 {
+    if (ctx) begin_call(ctx);
     if (!ctx) return TPMG_E_PARAM;
     if (!f_host || !u_host) return fail(ctx, TPMG_E_PARAM, "tpmg_solve_host: NULL buffer");
     const size_t n = ctx->lv[ctx->L].n();

@@ -16,6 +16,15 @@ namespace dev {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
+// ---- fused halo push (P2P mode): a producer kernel stores its strip-boundary output rows
+// straight into the neighbours' halo slabs over NVLink (the stream publishes the epoch).
+__device__ __forceinline__ void push_out(const HaloPush& p, int64_t j, int64_t ny, int64_t off, double x)
+{
+    if (j == 0 && p.dst_lo) p.dst_lo[off] = x;
+    if (j == ny - 1 && p.dst_hi) p.dst_hi[off] = x;
+}
+
+
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid)
 {
     unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));

@@ -199,7 +199,10 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 
     // producer cursor: next chunk to load
     int p_count = 0, p_ch = 0, p_slot = 0, p_tile = blockIdx.x;
-    int p_i0 = (p_tile % ntx) * TX, p_j0 = part_row(a.part, nty, p_tile / ntx) * TY;
+    const bool plo = a.push.dst_lo != nullptr, phi = a.push.dst_hi != nullptr;
+    const int nrows = part_rows(a.part, nty);
+    auto row_of = [&](int t) { return part_row(a.part, nty, push_row(t / ntx, nrows, plo, phi)); };
+    int p_i0 = (p_tile % ntx) * TX, p_j0 = row_of(p_tile) * TY;
     auto issue = [&]() {
         if (p_count < total) {
             double* st = stage + p_slot * G::STAGE;
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 p_ch = 0;
                 p_tile += gridDim.x;
                 p_i0 = (p_tile % ntx) * TX;
-                p_j0 = part_row(a.part, nty, p_tile / ntx) * TY;
+                p_j0 = row_of(p_tile) * TY;
             }
         }
         if constexpr (LOADER == 0) cp_async_commit();
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     auto tile_body = [&](auto bnd_t, int tl) {
         constexpr bool BND = decltype(bnd_t)::value;
         const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
-        const int64_t i0 = (int64_t)(tile % ntx) * TX, j0 = (int64_t)part_row(a.part, nty, tile / ntx) * TY;
+        const int64_t i0 = (int64_t)(tile % ntx) * TX, j0 = (int64_t)row_of(tile) * TY;
         const int64_t i = i0 + tx, j = j0 + ty;
         const bool valid = (i < nx) && (j < ny);
         const int64_t colbase = j * nx * (int64_t)nz + i;  // + k*nx
@@ -417,20 +420,26 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
                     x = fma(gm[q], x, gv[q]);
-                    if (valid) *op = x;
+                    if (valid) {
+                        *op = x;
+                        push_out(a.push, j, ny, (int64_t)(k - q) * nx + i, x);
+                    }
                     op -= nx;
                 }
             }
             for (; k >= 0; --k) {
                 x = fma(gim[k], x, gbuf[k * NT + tid]);
-                if (valid) *op = x;
+                if (valid) {
+                    *op = x;
+                    push_out(a.push, j, ny, (int64_t)k * nx + i, x);
+                }
                 op -= nx;
             }
         }
     };
     for (int tl = 0; tl < my_tiles; ++tl) {
         const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
-        if (tile_on_boundary(a.L, (int64_t)(tile % ntx) * TX, (int64_t)part_row(a.part, nty, tile / ntx) * TY, TX, TY))
+        if (tile_on_boundary(a.L, (int64_t)(tile % ntx) * TX, (int64_t)row_of(tile) * TY, TX, TY))
             tile_body(std::true_type{}, tl);
         else
             tile_body(std::false_type{}, tl);
@@ -515,12 +524,10 @@ __global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double
 // 402 us = 6.0 TB/s at 1024^2 x 128, was 531 us before the loads were batched).  The 3 x 3 coarse
 // neighbourhood is read through L1 (neighbouring threads share it); no integer
 // division in the loop.
-__global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const LevelConst F, const HaloField uc,
-                                                     double* __restrict__ uf, int lpt, const int* skip, int part)
+// The work of k_prolong_add; threads outside the grid return early (no barrier here).
+__device__ __forceinline__ void prolong_body(const LevelConst& Cc, const LevelConst& F, const HaloField& uc,
+                                             double* __restrict__ uf, int lpt, int part, const HaloPush& push)
 {
-    pdl_wait();
-    pdl_trigger();
-    if (skip && *skip) return;
     const int64_t nxc = Cc.nx, nyc = Cc.ny;
     const int nz = Cc.nz;
     const int64_t I = blockIdx.x * 32 + threadIdx.x;
@@ -591,10 +598,24 @@ __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const 
                 w.x = w.x + v0 / 16.0;
                 w.y = w.y + v1 / 16.0;
                 *reinterpret_cast<double2*>((b ? f1 : f0) + (int64_t)(k0 + q) * F.nx) = w;
+                const int64_t jf = 2 * J + b, off = (int64_t)(k0 + q) * F.nx + 2 * I;
+                if (jf == 0 && push.dst_lo) *reinterpret_cast<double2*>(push.dst_lo + off) = w;
+                if (jf == F.ny - 1 && push.dst_hi) *reinterpret_cast<double2*>(push.dst_hi + off) = w;
             }
         }
     }
 }
+
+__global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const LevelConst F, const HaloField uc,
+                                                     double* __restrict__ uf, int lpt, const int* skip, int part,
+                                                     const HaloPush push)
+{
+    pdl_wait();
+    pdl_trigger();
+    if (skip && *skip) return;
+    prolong_body(Cc, F, uc, uf, lpt, part, push);
+}
+
 
 __global__ void __launch_bounds__(256) k_dot(const double* __restrict__ x, const double* __restrict__ y,
                                              int64_t n, ReduceSlot red)
@@ -642,22 +663,6 @@ __global__ void __launch_bounds__(256) k_halo_push(const HaloPush hp, int64_t n)
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
         if (dl) dl[q] = sf[q];
         if (dh) dh[q] = sl[q];
-    }
-    // publish: every block's remote stores are fenced before its ticket; the last block
-    // writes the epoch into the neighbours' flags
-    __shared__ bool last;
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned t = atomicAdd(hp.ticket, 1u);
-        last = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (last && threadIdx.x == 0) {
-        __threadfence_system();
-        if (hp.flag_lo) asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(hp.flag_lo), "r"(hp.epoch) : "memory");
-        if (hp.flag_hi) asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(hp.flag_hi), "r"(hp.epoch) : "memory");
-        *hp.ticket = 0u;
     }
 }
 
@@ -794,7 +799,7 @@ cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const Le
 }
 
 cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, const LevelConst& fine,
-                               HaloField uc, double* uf, const int* skip, int part)
+                               HaloField uc, double* uf, const int* skip, int part, const HaloPush* push)
 {
     if (coarse.nx <= 0 || coarse.ny <= 0) return cudaSuccess;
     // levels per thread: enough threads to fill the GPU on the coarse levels
@@ -808,7 +813,8 @@ cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, con
     if (part == PART_INTERIOR) grid.y = (unsigned)((std::max<int64_t>(coarse.ny - 2, 0) + 3) / 4);
     if (part == PART_BOUNDARY) grid.y = 1;
     if (grid.y == 0) return cudaSuccess;
-    return launch_kernel(ln, k_prolong_add, dim3(grid), dim3(block), 0, coarse, fine, uc, uf, lpt, skip, part);
+    const HaloPush hp = push ? *push : HaloPush{};
+    return launch_kernel(ln, k_prolong_add, dim3(grid), dim3(block), 0, coarse, fine, uc, uf, lpt, skip, part, hp);
 }
 
 cudaError_t launch_dot(const Launcher& ln, const double* x, const double* y, int64_t n, ReduceSlot red)

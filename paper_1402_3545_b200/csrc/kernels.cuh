@@ -72,6 +72,16 @@ __host__ __device__ inline int part_row(int part, int nty, int idx)
     return part == PART_ALL ? idx : part == PART_INTERIOR ? idx + 1 : (idx == 0 ? 0 : nty - 1);
 }
 
+// Tile-row order of a launch that pushes its boundary rows to the neighbours (fused halo
+// push): the strip-boundary tile rows come first, so their remote stores drain while the
+// rest of the grid is computed.
+__host__ __device__ inline int push_row(int r, int nrows, bool lo, bool hi)
+{
+    if (nrows < 2 || !hi) return r;          // row 0 is first anyway
+    if (lo) return r == 0 ? 0 : (r == 1 ? nrows - 1 : r - 1);
+    return r == 0 ? nrows - 1 : r - 1;
+}
+
 // Scalar ratio read on the device: value = num_idx < 0 ? 0 : s[num]/s[den].
 struct DevRatio {
     const double* s;
@@ -109,6 +119,19 @@ constexpr int kTileX = 32;
 constexpr int kStageK = 8;
 constexpr int kSegK = 32;   // k-split kernel: levels per column segment
 
+// P2P halo exchange: dst_lo <- src_first (my row 0 into the lower neighbour's slab),
+// dst_hi <- src_last (my row ny-1 into the upper neighbour's); n doubles each, remote
+// stores over NVLink.  Carried by k_halo_push and by producer kernels (LineArgs::push,
+// k_prolong_add) that store their strip-boundary output rows into the neighbours' slabs
+// themselves (fused push; src_* unused).  The epoch flags are published by the stream
+// after the kernel (write-value with its memory fence), not by the kernel.
+struct HaloPush {
+    const double* src_first;
+    const double* src_last;
+    double* dst_lo;
+    double* dst_hi;
+    int64_t n;
+};
 struct LineArgs {
     LevelConst L;
     double rho;        // smoother relaxation (MODE_SMOOTH)
@@ -124,6 +147,7 @@ struct LineArgs {
     int use_tma;       // 1: loads by TMA (tma must be filled), 0: cp.async
     const int* skip;   // device flag: the kernel returns at once when *skip != 0 (solver run-ahead)
     int part;          // TilePart: which tile rows this launch covers
+    HaloPush push;     // fused halo push of the output (dst == nullptr: none)
     TmaMaps tma;
 };
 
@@ -190,28 +214,14 @@ cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const Line
 // f_c = 1/4 sum of the 2x2 fine children of r (plain restriction)
 cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const LevelConst& coarse,
                             const double* r, double* fc);
-// u_f += P u_c (bilinear, zero coarse ghosts)
+// u_f += P u_c (bilinear; coarse ghosts per the boundary reading); push: fused halo push
+// of the updated fine boundary rows (optional)
 cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse,
                                const LevelConst& fine, HaloField uc, double* uf, const int* skip = nullptr,
-                               int part = PART_ALL);
+                               int part = PART_ALL, const HaloPush* push = nullptr);
 // dst = src (n doubles) unless *skip
 cudaError_t launch_copy(const Launcher& ln, double* dst, const double* src, int64_t n, const int* skip);
 
-// P2P halo exchange: dst_lo <- src_first (my row 0 into the lower neighbour's slab),
-// dst_hi <- src_last (my row ny-1 into the upper neighbour's); n doubles each, remote
-// stores.  The last block to finish (ticket) fences at system scope and stores `epoch`
-// into the neighbours' data flags.
-struct HaloPush {
-    const double* src_first;
-    const double* src_last;
-    double* dst_lo;
-    double* dst_hi;
-    int64_t n;
-    unsigned* flag_lo;   // lower neighbour's "data from upper" flag (nullptr: no neighbour)
-    unsigned* flag_hi;   // upper neighbour's "data from lower" flag
-    unsigned* ticket;    // local completion counter (zero between launches)
-    unsigned epoch;
-};
 cudaError_t launch_halo_push(const Launcher& ln, const HaloPush& hp);
 
 // CG multi-GPU: p halo slabs updated locally, out = fma(beta, p, z) on each non-null slab.

@@ -166,7 +166,10 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     double acc[1] = {0.0};
 
     const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + TY - 1) / TY);
-    const int ntiles = ntx * part_rows(a.part, nty);
+    const int nrows = part_rows(a.part, nty);
+    const int ntiles = ntx * nrows;
+    const bool plo = a.push.dst_lo != nullptr, phi = a.push.dst_hi != nullptr;
+    auto row_of = [&](int t) { return part_row(a.part, nty, push_row(t / ntx, nrows, plo, phi)); };
     const int my_tiles = ((int)blockIdx.x < ntiles) ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
     const int total = my_tiles * NCC;
     __syncthreads();
@@ -176,8 +179,8 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     auto issue = [&]() {
         if (tid == 0 && p_count < total) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            tma_step<MODE, TY, KB, NSEG>(stage + p_slot * STG, a, (p_tile % ntx) * TX,
-                                         part_row(a.part, nty, p_tile / ntx) * TY, p_cc, &full_bar[p_slot]);
+            tma_step<MODE, TY, KB, NSEG>(stage + p_slot * STG, a, (p_tile % ntx) * TX, row_of(p_tile) * TY, p_cc,
+                                         &full_bar[p_slot]);
         }
         ++p_count;
         if (++p_slot == NS2) p_slot = 0;
@@ -198,7 +201,7 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     auto tile_body = [&](auto bnd_t, int tl) {
         constexpr bool BND = decltype(bnd_t)::value;
         const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
-        const int i0 = (tile % ntx) * TX, j0 = part_row(a.part, nty, tile / ntx) * TY;
+        const int i0 = (tile % ntx) * TX, j0 = row_of(tile) * TY;
         const int64_t i = i0 + lane, j = j0 + ty;
         const bool valid = (i < nx) && (j < ny);
         const double* ct = BND ? a.L.tab + (size_t)column_class(a.L, i, j) * kTabArrays * nz : tab;
@@ -336,7 +339,10 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
 #pragma unroll
             for (int q = 0; q < SL; ++q) {
                 const double x = fma(Qbw[kb + q], X, yv[q]);
-                if (valid) *op = x;
+                if (valid) {
+                    *op = x;
+                    push_out(a.push, j, ny, (int64_t)(kb + q) * nx + i, x);
+                }
                 op += nx;
             }
             // bnd is reused by the next tile only after its forward chunks (>= 1 __syncthreads)
@@ -344,7 +350,7 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     };
     for (int tl = 0; tl < my_tiles; ++tl) {
         const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
-        if (tile_on_boundary(a.L, (int64_t)(tile % ntx) * TX, (int64_t)part_row(a.part, nty, tile / ntx) * TY, TX, TY))
+        if (tile_on_boundary(a.L, (int64_t)(tile % ntx) * TX, (int64_t)row_of(tile) * TY, TX, TY))
             tile_body(std::true_type{}, tl);
         else
             tile_body(std::false_type{}, tl);
