@@ -106,7 +106,7 @@ struct tpmg_ctx {
     // profiling (tpmg_profile)
     bool pdl = false;                   // programmatic dependent launches (TPMG_PDL=1)
     bool halo_off = false;              // TPMG_HALO=off: skip halo exchanges (timing experiments)
-    bool fused_push = true;             // P2P: producers push their boundary rows (TPMG_FUSED_PUSH=0: off)
+    bool fused_push = false;            // P2P: producers push their boundary rows (TPMG_FUSED_PUSH=1)
     bool prof_on = false;
     uint32_t prof_mask = 0;             // kernel classes bracketed with events (bit = tpmg_kernel)
     struct ProfRec { int cls; double cells; cudaEvent_t a, b; };
@@ -1094,9 +1094,7 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
         a.out1 = u;
         a.out2 = ctx->cg_z;
         a.red.result = ctx->d_scal + S_RR(0);
-        TRY(fused_push(ctx, l + 1, ctx->cg_z, &a.push));   // z is read halo'd by the direction kernel
         TRY(run_line(ctx, MODE_CGPREC, a));
-        TRY(publish_pushed(ctx, l + 1));
         TRY(allreduce(ctx, ctx->d_scal + S_RR(0), 2));
         TRY(fetch(ctx, ctx->d_scal + S_RR(0), 2));
     }
@@ -1160,9 +1158,7 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
             a.out2 = ctx->cg_z;
             a.ratio = DevRatio{ctx->d_scal, S_ZETA(m - 1), S_SIGMA(m)};
             a.red.result = ctx->d_scal + S_RR(m);
-            TRY(fused_push(ctx, l + 1, ctx->cg_z, &a.push));
-            TRY(run_line(ctx, MODE_CGPREC, a));
-            TRY(publish_pushed(ctx, l + 1));
+            TRY(run_line(ctx, MODE_CGPREC, a));   // z's halo: push kernel (fused measured no faster)
             TRY(allreduce(ctx, ctx->d_scal + S_RR(m), 2));
         }
         CUDA_TRY(ctx, launch_cg_check(launcher(ctx), ctx->d_scal, m, eps, ctx->d_flags, ctx->dh_flags));
@@ -1252,7 +1248,7 @@ tpmg_status halo_setup(tpmg_ctx* ctx)
     const char* hm = std::getenv("TPMG_HALO");
     ctx->halo_off = hm && std::strcmp(hm, "off") == 0;
     const char* fpu = std::getenv("TPMG_FUSED_PUSH");
-    ctx->fused_push = !(fpu && fpu[0] == '0');
+    ctx->fused_push = fpu && fpu[0] == '1';   // measured no faster than the push kernel
     ctx->p2p = !(hm && std::strcmp(hm, "nccl") == 0) && stream_memops();
     if (!ctx->p2p) return TPMG_OK;
     // exchange the pool handles

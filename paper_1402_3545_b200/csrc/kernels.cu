@@ -420,20 +420,37 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
                     x = fma(gm[q], x, gv[q]);
-                    if (valid) {
-                        *op = x;
-                        push_out(a.push, j, ny, (int64_t)(k - q) * nx + i, x);
-                    }
+                    if (valid) *op = x;
                     op -= nx;
                 }
             }
             for (; k >= 0; --k) {
                 x = fma(gim[k], x, gbuf[k * NT + tid]);
-                if (valid) {
-                    *op = x;
-                    push_out(a.push, j, ny, (int64_t)k * nx + i, x);
-                }
+                if (valid) *op = x;
                 op -= nx;
+            }
+            // fused halo push: a strip-boundary row also goes to the neighbour's slab (read
+            // back from L1/L2, outside the recurrence loop)
+            if (valid && ((j == 0 && a.push.dst_lo) || (j == ny - 1 && a.push.dst_hi))) {
+                const double* src = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase;
+                double* dst = (j == 0 ? a.push.dst_lo : a.push.dst_hi) + i;
+                double* dst2 = (j == 0 && j == ny - 1) ? a.push.dst_hi : nullptr;   // a one-row strip
+                // batches of 16 independent loads: the copy is latency-, not bandwidth-bound
+                int kk = 0;
+                for (; kk + 16 <= nz; kk += 16) {
+                    double v[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) v[q] = src[(int64_t)(kk + q) * nx];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        dst[(int64_t)(kk + q) * nx] = v[q];
+                        if (dst2) dst2[(int64_t)(kk + q) * nx + i] = v[q];
+                    }
+                }
+                for (; kk < nz; ++kk) {
+                    dst[(int64_t)kk * nx] = src[(int64_t)kk * nx];
+                    if (dst2) dst2[(int64_t)kk * nx + i] = src[(int64_t)kk * nx];
+                }
             }
         }
     };
@@ -525,6 +542,7 @@ __global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double
 // neighbourhood is read through L1 (neighbouring threads share it); no integer
 // division in the loop.
 // The work of k_prolong_add; threads outside the grid return early (no barrier here).
+template <bool PUSH>
 __device__ __forceinline__ void prolong_body(const LevelConst& Cc, const LevelConst& F, const HaloField& uc,
                                              double* __restrict__ uf, int lpt, int part, const HaloPush& push)
 {
@@ -598,14 +616,18 @@ __device__ __forceinline__ void prolong_body(const LevelConst& Cc, const LevelCo
                 w.x = w.x + v0 / 16.0;
                 w.y = w.y + v1 / 16.0;
                 *reinterpret_cast<double2*>((b ? f1 : f0) + (int64_t)(k0 + q) * F.nx) = w;
-                const int64_t jf = 2 * J + b, off = (int64_t)(k0 + q) * F.nx + 2 * I;
-                if (jf == 0 && push.dst_lo) *reinterpret_cast<double2*>(push.dst_lo + off) = w;
-                if (jf == F.ny - 1 && push.dst_hi) *reinterpret_cast<double2*>(push.dst_hi + off) = w;
+                if constexpr (PUSH) {   // fused halo push of the fine strip-boundary rows
+                    const int64_t jf = 2 * J + b, off = (int64_t)(k0 + q) * F.nx + 2 * I;
+                    if (jf == 0 && push.dst_lo) *reinterpret_cast<double2*>(push.dst_lo + off) = w;
+                    if (jf == F.ny - 1 && push.dst_hi) *reinterpret_cast<double2*>(push.dst_hi + off) = w;
+                }
             }
         }
     }
+
 }
 
+template <bool PUSH>
 __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const LevelConst F, const HaloField uc,
                                                      double* __restrict__ uf, int lpt, const int* skip, int part,
                                                      const HaloPush push)
@@ -613,7 +635,7 @@ __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const 
     pdl_wait();
     pdl_trigger();
     if (skip && *skip) return;
-    prolong_body(Cc, F, uc, uf, lpt, part, push);
+    prolong_body<PUSH>(Cc, F, uc, uf, lpt, part, push);
 }
 
 
@@ -814,7 +836,9 @@ cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, con
     if (part == PART_BOUNDARY) grid.y = 1;
     if (grid.y == 0) return cudaSuccess;
     const HaloPush hp = push ? *push : HaloPush{};
-    return launch_kernel(ln, k_prolong_add, dim3(grid), dim3(block), 0, coarse, fine, uc, uf, lpt, skip, part, hp);
+    if (hp.dst_lo || hp.dst_hi)
+        return launch_kernel(ln, k_prolong_add<true>, dim3(grid), dim3(block), 0, coarse, fine, uc, uf, lpt, skip, part, hp);
+    return launch_kernel(ln, k_prolong_add<false>, dim3(grid), dim3(block), 0, coarse, fine, uc, uf, lpt, skip, part, hp);
 }
 
 cudaError_t launch_dot(const Launcher& ln, const double* x, const double* y, int64_t n, ReduceSlot red)

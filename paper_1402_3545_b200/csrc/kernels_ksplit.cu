@@ -128,7 +128,7 @@ __device__ __forceinline__ void tma_step(double* st, const LineArgs& a, int i0, 
     }
 }
 
-template <int MODE, int TY, int NSEG, int KB, int NS2>
+template <int MODE, int TY, int NSEG, int KB, int NS2, bool PUSH>
 __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_constant__ LineArgs a,
                                                              const __grid_constant__ KTables T)
 {
@@ -168,8 +168,10 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + TY - 1) / TY);
     const int nrows = part_rows(a.part, nty);
     const int ntiles = ntx * nrows;
-    const bool plo = a.push.dst_lo != nullptr, phi = a.push.dst_hi != nullptr;
-    auto row_of = [&](int t) { return part_row(a.part, nty, push_row(t / ntx, nrows, plo, phi)); };
+    const bool plo = PUSH && a.push.dst_lo != nullptr, phi = PUSH && a.push.dst_hi != nullptr;
+    auto row_of = [&](int t) {
+        return part_row(a.part, nty, PUSH ? push_row(t / ntx, nrows, plo, phi) : t / ntx);
+    };
     const int my_tiles = ((int)blockIdx.x < ntiles) ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
     const int total = my_tiles * NCC;
     __syncthreads();
@@ -341,7 +343,9 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
                 const double x = fma(Qbw[kb + q], X, yv[q]);
                 if (valid) {
                     *op = x;
-                    push_out(a.push, j, ny, (int64_t)(kb + q) * nx + i, x);
+                    // fused halo push (PUSH instantiation only): a strip-boundary row also
+                    // goes to the neighbour's slab over NVLink
+                    if constexpr (PUSH) push_out(a.push, j, ny, (int64_t)(kb + q) * nx + i, x);
                 }
                 op += nx;
             }
@@ -365,10 +369,10 @@ size_t ksmem(int nz)
     return (size_t)(NS2 * NSEG * G::SEGST + r16(6 * nz) + G::template bnd<NSEG>() + 64 + 16) * sizeof(double);
 }
 
-template <int MODE, int TY, int NSEG, int KB, int NS2>
-cudaError_t launch_k(const Launcher& ln, const LineArgs& a, const KTables& T)
+template <int MODE, int TY, int NSEG, int KB, int NS2, bool PUSH>
+cudaError_t launch_k_push(const Launcher& ln, const LineArgs& a, const KTables& T)
 {
-    auto kern = k_linek<MODE, TY, NSEG, KB, NS2>;
+    auto kern = k_linek<MODE, TY, NSEG, KB, NS2, PUSH>;
     const size_t smem = ksmem<MODE, TY, NSEG, KB, NS2>(a.L.nz);
     static size_t limit = 0;
     if (!limit) {
@@ -385,6 +389,16 @@ cudaError_t launch_k(const Launcher& ln, const LineArgs& a, const KTables& T)
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, ln.num_sms - ln.reserve_sms) * per_sm);
     if (grid <= 0) return cudaSuccess;
     return launch_kernel(ln, kern, dim3((unsigned)grid), dim3(32 * TY * NSEG), smem, a, T);
+}
+
+// The fused halo push (multi-GPU, P2P) has its own instantiation, so single-GPU launches
+// carry none of its code.  Only the smoother and the preconditioner push.
+template <int MODE, int TY, int NSEG, int KB, int NS2>
+cudaError_t launch_k(const Launcher& ln, const LineArgs& a, const KTables& T)
+{
+    if constexpr (MODE == MODE_SMOOTH || MODE == MODE_PREC)
+        if (a.push.dst_lo || a.push.dst_hi) return launch_k_push<MODE, TY, NSEG, KB, NS2, true>(ln, a, T);
+    return launch_k_push<MODE, TY, NSEG, KB, NS2, false>(ln, a, T);
 }
 
 template <int MODE, int TY, int KB, int NS2>
