@@ -232,3 +232,22 @@ def test_gpu_rhs_generator_matches_numpy():
     gpu.fill_rhs(t, 64, y0=8, seed=3)
     torch.cuda.synchronize()
     assert np.array_equal(t.cpu().numpy(), rhs_lambda(64, 24, 16, seed=3, y0=8))
+
+
+def test_profile_mask_times_only_selected_class():
+    """tpmg_profile_mask brackets only the chosen kernel classes with events."""
+    p = O.Params(nx=64, ny=64, nz=32)
+    ctx = ctx_for(p)
+    f = to_dev(rhs_zc(64, 64, 32, seed=3))
+    u = ctx.empty(p.L)
+    ctx.profile(True, classes=["cg_precondition"])
+    r = ctx.solve_cg(f, u)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    assert set(prof) == {"cg_precondition"}
+    assert prof["cg_precondition"][0] == r.iterations + 1      # setup + one per iteration
+    ctx.profile(True)
+    ctx.solve_cg(f, u)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    assert {"cg_precondition", "cg_direction"} <= set(prof)
