@@ -109,7 +109,7 @@ struct tpmg_ctx {
     bool fused_push = false;            // P2P: producers push their boundary rows (TPMG_FUSED_PUSH=1)
     bool prof_on = false;
     uint32_t prof_mask = 0;             // kernel classes bracketed with events (bit = tpmg_kernel)
-    struct ProfRec { int cls; double cells; cudaEvent_t a, b; };
+    struct ProfRec { int cls; double cells; cudaEvent_t a, b; const int* skip; };
     std::vector<ProfRec> prof_pending;
     std::vector<cudaEvent_t> prof_pool;
     // TMA descriptors, cached by (address, nx, nz, ny, box x, box rows)
@@ -466,21 +466,37 @@ struct ProfScope {
         if (a) {
             cudaEvent_t b = prof_event(ctx);
             cudaEventRecord(b, ctx->stream);
-            ctx->prof_pending.push_back({cls, cells, a, b});
+            ctx->prof_pending.push_back({cls, cells, a, b, ctx->skip});
         }
     }
 };
 
+// Fold the pending event pairs into the per-class totals.  Launches the solver's run-ahead
+// enqueued past convergence returned at once on the device (their skip flag was set):
+// they are dropped, so the totals count only launches that did the work.  Called before
+// the flags are reset (ensure_flags) and by tpmg_profile_read.
 tpmg_status prof_collect(tpmg_ctx* ctx)
 {
     if (ctx->prof_pending.empty()) return TPMG_OK;
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::vector<int> flags;
+    if (ctx->d_flags && ctx->flags_cap > 0) {
+        flags.resize(ctx->flags_cap);
+        CUDA_TRY(ctx, cudaMemcpy(flags.data(), ctx->d_flags, sizeof(int) * flags.size(), cudaMemcpyDeviceToHost));
+    }
     for (auto& r : ctx->prof_pending) {
-        float ms = 0;
-        CUDA_TRY(ctx, cudaEventElapsedTime(&ms, r.a, r.b));
-        ctx->prof_launches[r.cls] += 1;
-        ctx->prof_ms[r.cls] += ms;
-        ctx->prof_cells[r.cls] += r.cells;
+        bool skipped = false;
+        if (r.skip && !flags.empty()) {
+            const ptrdiff_t q = r.skip - ctx->d_flags;
+            skipped = q >= 0 && q < (ptrdiff_t)flags.size() && flags[q] != 0;
+        }
+        if (!skipped) {
+            float ms = 0;
+            CUDA_TRY(ctx, cudaEventElapsedTime(&ms, r.a, r.b));
+            ctx->prof_launches[r.cls] += 1;
+            ctx->prof_ms[r.cls] += ms;
+            ctx->prof_cells[r.cls] += r.cells;
+        }
         ctx->prof_pool.push_back(r.a);
         ctx->prof_pool.push_back(r.b);
     }
@@ -895,6 +911,7 @@ tpmg_status ensure_scal(tpmg_ctx* ctx, int n)
 
 tpmg_status ensure_flags(tpmg_ctx* ctx, int n)
 {
+    TRY(prof_collect(ctx));   // the pending profile records still refer to the old flags
     if (n > ctx->flags_cap) {
         if (ctx->d_flags) cudaFree(ctx->d_flags);
         if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
