@@ -105,6 +105,7 @@ struct tpmg_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // profiling (tpmg_profile)
     bool pdl = false;                   // programmatic dependent launches (TPMG_PDL=1)
+    bool ksplit_cg = false;             // k-split CG preconditioner (TPMG_KSPLIT_CG=1)
     bool halo_off = false;              // TPMG_HALO=off: skip halo exchanges (timing experiments)
     bool fused_push = false;            // P2P: producers push their boundary rows (TPMG_FUSED_PUSH=1)
     bool prof_on = false;
@@ -619,19 +620,32 @@ bool fill_tma_ksplit(tpmg_ctx* ctx, int mode, LineArgs& a)
     const int64_t nx = a.L.nx, ny = a.L.ny;
     const int nz = a.L.nz;
     const KsplitBoxes b = ksplit_boxes(mode, ctx->ksplit_cfg);
-    if (mode == MODE_SMOOTH || mode == MODE_RESTRICT || mode == MODE_SMOOTH_PROLONG)
+    if (mode == MODE_SMOOTH || mode == MODE_RESTRICT || mode == MODE_SMOOTH_PROLONG || mode == MODE_CGPREC)
         if (!ksplit_halo_maps(ctx, a.h0, nx, nz, ny, b.hx, b.ty + 2, b.depth, a.tma.h[0])) return false;
     if (mode == MODE_SMOOTH_PROLONG)
         if (!ksplit_halo_maps(ctx, a.h1, nx / 2, nz, ny / 2, b.hxc, b.ty / 2 + 2, b.depth, a.tma.h[1])) return false;
     if (!a.q0 || ((uintptr_t)a.q0 & 15)) return false;
     if (!tensor_map(ctx, a.q0, nx, nz, ny, kTileX, b.ty, &a.tma.q[0], b.kb)) return false;
+    if (mode == MODE_CGPREC) {   // u, the second plain input
+        if (!a.q1 || ((uintptr_t)a.q1 & 15)) return false;
+        if (!tensor_map(ctx, a.q1, nx, nz, ny, kTileX, b.ty, &a.tma.q[1], b.kb)) return false;
+    }
     a.use_tma = 1;
     return true;
 }
 
 bool ksplit_usable(tpmg_ctx* ctx, int mode, const LevelConst& lc)
 {
+    // the k-split CG preconditioner is opt-in (TPMG_KSPLIT_CG=1): measured 4% slower per CG
+    // iteration than the one-thread-per-column kernel at 1024^2 x 128
+    if (mode == MODE_CGPREC && !ctx->ksplit_cg) return false;
     return ctx->use_tma && ctx->ksplit_cfg >= 0 && ksplit_supported(mode, lc.nz, (int)lc.nx);
+}
+
+// Tile rows of the kernel run_line will launch for this mode and level.
+int launch_rows(tpmg_ctx* ctx, int mode, const LevelConst& lc)
+{
+    return ksplit_usable(ctx, mode, lc) ? ksplit_boxes(mode, ctx->ksplit_cfg).ty : line_tile_rows(mode, lc.nz);
 }
 
 // Fraction of the level's cells a launch covers (interior / boundary tile rows).
@@ -639,7 +653,7 @@ double part_cells(tpmg_ctx* ctx, int mode, const LineArgs& a)
 {
     const double all = level_cells(a.L);
     if (a.part == PART_ALL || a.L.ny <= 0) return all;
-    const int TY = line_launch_rows(mode, a.L.nz, (int)a.L.nx, ctx->use_tma ? 1 : 0, ctx->ksplit_cfg);
+    const int TY = launch_rows(ctx, mode, a.L);
     const int nty = (int)((a.L.ny + TY - 1) / TY);
     const double rows = (a.part == PART_INTERIOR) ? (double)(nty - 2) * TY : (double)a.L.ny - (double)(nty - 2) * TY;
     return all * rows / (double)a.L.ny;
@@ -689,7 +703,7 @@ tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, LineArgs a, const 
         return run_line(ctx, mode, a);
     }
     const LevelConst& lc = ctx->lv[level].lc;
-    const int TY = line_launch_rows(mode, lc.nz, (int)lc.nx, ctx->use_tma ? 1 : 0, ctx->ksplit_cfg);
+    const int TY = launch_rows(ctx, mode, lc);
     const int nty = (int)((lc.ny + TY - 1) / TY);
     if (!ctx->overlap || ctx->p2p || nty < 3) {
         TRY(exchange(ctx, level, x));
@@ -1427,6 +1441,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->overlap = ov && ov[0] == '1';
         const char* rs = std::getenv("TPMG_RESERVE_SMS");
         if (rs) ctx->reserve_sms = std::max(0, std::atoi(rs));
+        const char* kc = std::getenv("TPMG_KSPLIT_CG");
+        ctx->ksplit_cg = kc && kc[0] == '1';
         const char* pd = std::getenv("TPMG_PDL");
         ctx->pdl = pd && pd[0] == '1';
         const char* fp = std::getenv("TPMG_FUSE_PROLONG");

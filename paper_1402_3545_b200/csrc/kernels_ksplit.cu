@@ -57,7 +57,8 @@ __host__ __device__ constexpr int r16(int n) { return (n + 15) & ~15; }
 // and lets the fused prolongation form u + P u_c on the whole box, slab rows included.
 template <int MODE, int TY, int KB>
 struct KGeom {
-    static constexpr bool HALO = (MODE == MODE_SMOOTH || MODE == MODE_RESTRICT || MODE == MODE_SMOOTH_PROLONG);
+    static constexpr bool HALO = (MODE == MODE_SMOOTH || MODE == MODE_RESTRICT || MODE == MODE_SMOOTH_PROLONG ||
+                                  MODE == MODE_CGPREC);
     static constexpr bool PROL = (MODE == MODE_SMOOTH_PROLONG);
     static constexpr bool INPLACE = PROL || MODE == MODE_RESTRICT;  // aligned rows, slab rows in place
     static constexpr int HX = INPLACE ? TX + 8 : TX + 4;        // u box row width
@@ -67,10 +68,11 @@ struct KGeom {
     static constexpr int UBOX = HALO ? r16((TY + 2) * UROW) : 0;
     static constexpr int SROW = (HALO && !INPLACE) ? r16(UROW) : 0;  // one slab row slot
     static constexpr int FBOX = TY * KB * TX;
+    static constexpr int FBOX2 = (MODE == MODE_CGPREC) ? FBOX : 0;   // CG: u next to r
     static constexpr int CROWS = TY / 2 + 2;
     static constexpr int CROW = D * HXC;
     static constexpr int CBOX = PROL ? CROWS * CROW : 0;
-    static constexpr int SEGST = UBOX + 2 * SROW + FBOX + CBOX;  // doubles per segment per stage
+    static constexpr int SEGST = UBOX + 2 * SROW + FBOX + FBOX2 + CBOX;  // doubles per segment per stage
     static_assert(!INPLACE || ((UROW * 8) % 128 == 0 && (CROW * 8) % 128 == 0), "TMA row alignment");
     // exchange buffer: Thomas segment chaining [2][TY][NSEG][32], or (MODE_RESTRICT)
     // x-pair residual sums [2 (chunk parity)][TY][NSEG][KB][16]
@@ -102,7 +104,7 @@ __device__ __forceinline__ void tma_step(double* st, const LineArgs& a, int i0, 
 {
     using G = KGeom<MODE, TY, KB>;
     const int ny = (int)a.L.ny;
-    uint32_t bytes = NSEG * ((G::HALO ? (TY + 2) * G::UROW : 0) + G::FBOX + G::CBOX) * 8;
+    uint32_t bytes = NSEG * ((G::HALO ? (TY + 2) * G::UROW : 0) + G::FBOX + G::FBOX2 + G::CBOX) * 8;
     bool lo = false, hi = false;
     if constexpr (G::HALO && !G::INPLACE) {
         lo = a.tma.h[0].has_lo && j0 == 0;
@@ -125,6 +127,7 @@ __device__ __forceinline__ void tma_step(double* st, const LineArgs& a, int i0, 
             if (hi) tma_load_3d(seg + G::UBOX + G::SROW, &a.tma.h[0].hi, i0 - G::XO, k0 - 1, 0, bar);
         }
         tma_load_3d(seg + G::UBOX + 2 * G::SROW, &a.tma.q[0], i0, k0, j0, bar);
+        if constexpr (G::FBOX2 > 0) tma_load_3d(seg + G::UBOX + 2 * G::SROW + G::FBOX, &a.tma.q[1], i0, k0, j0, bar);
     }
 }
 
@@ -136,8 +139,10 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     constexpr int NT = 32 * TY * NSEG;
     constexpr int NCC = SL / KB;           // chunks per segment
     constexpr int STG = NSEG * G::SEGST;
-    constexpr bool NORM = (MODE == MODE_SMOOTH || MODE == MODE_SMOOTH_PROLONG);
+    constexpr bool CGP = (MODE == MODE_CGPREC);
+    constexpr bool NORM = (MODE == MODE_SMOOTH || MODE == MODE_SMOOTH_PROLONG || CGP);
     constexpr bool THOMAS = (MODE != MODE_RESTRICT);
+    constexpr int NR = CGP ? 2 : 1;   // CG: ||r||^2 and zeta = <r, M^-1 r>
 
     extern __shared__ __align__(128) double smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[NS2];
@@ -163,7 +168,13 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     pdl_wait();
     pdl_trigger();
     if (a.skip && *a.skip) return;   // solver run-ahead: this iteration is not needed
-    double acc[1] = {0.0};
+    double acc[NR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) acc[q] = 0.0;
+    // CG: alpha = zeta_{m-1} / sigma_m from the device scalars (written by earlier kernels)
+    double alpha = 0.0;
+    if constexpr (CGP)
+        if (a.ratio.num >= 0) alpha = a.ratio.s[a.ratio.num] / a.ratio.s[a.ratio.den];
 
     const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + TY - 1) / TY);
     const int nrows = part_rows(a.part, nty);
@@ -265,9 +276,24 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
                     const double uu = rc[(dd + 1) * HX];
                     const double S = (rc[dd * HX - 1] + rc[dd * HX + 1]) + (rs[dd * HX] + rn[dd * HX]);
                     const double Mu = fma(-gamma, ud + uu, diag[k] * uc);       // (M_T u)_k
-                    const double r = fma(c, S, fb[kk * TX]) - Mu;               // f - A u
-                    gv[kk] = fma(rho, r, Mu);            // g = (M - rho A) u + rho f  (one-pass smoother)
-                    rv[kk] = r;
+                    if constexpr (CGP) {
+                        // (Fused) Tridiag: r -= alpha A p, u += alpha p, then z = M^-1 r
+                        // (the box field is p, fb is r, fb + FBOX is u)
+                        const double Ap = fma(-c, S, Mu);
+                        const double rnew = fma(-alpha, Ap, fb[kk * TX]);
+                        const double unew = fma(alpha, uc, fb[G::FBOX + kk * TX]);
+                        if (valid) {
+                            const int64_t o = (j * nz + k) * nx + i;
+                            a.out0[o] = rnew;
+                            a.out1[o] = unew;
+                        }
+                        gv[kk] = rnew;
+                        rv[kk] = rnew;
+                    } else {
+                        const double r = fma(c, S, fb[kk * TX]) - Mu;           // f - A u
+                        gv[kk] = fma(rho, r, Mu);        // g = (M - rho A) u + rho f  (one-pass smoother)
+                        rv[kk] = r;
+                    }
                     ud = uc;
                     uc = uu;
                 }
@@ -324,7 +350,12 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
             // g'_k = (yhat_k + P_k Y) / m_k, then the local backward recurrence
             const int kb = s * SL;
 #pragma unroll
-            for (int q = 0; q < SL; ++q) yv[q] = fma(Pfw[kb + q], Y, yv[q]) * invm[kb + q];
+            for (int q = 0; q < SL; ++q) {
+                const double yt = fma(Pfw[kb + q], Y, yv[q]);   // y = L^-1 g
+                yv[q] = yt * invm[kb + q];                        // g' = D^-1 y
+                if constexpr (CGP)
+                    if (valid) acc[1] = fma(yv[q], yt, acc[1]);   // zeta = sum y_k g'_k [R22]
+            }
             double xh = 0.0;
 #pragma unroll
             for (int q = SL - 1; q >= 0; --q) {
@@ -337,7 +368,7 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
 #pragma unroll
             for (int q = NSEG - 1; q >= 1; --q)
                 if (q > s) X = fma(Qbw[q * SL], X, bB[q * 32]);
-            double* op = a.out0 + (j * nz + kb) * nx + i;
+            double* op = (CGP ? a.out2 : a.out0) + (j * nz + kb) * nx + i;
 #pragma unroll
             for (int q = 0; q < SL; ++q) {
                 const double x = fma(Qbw[kb + q], X, yv[q]);
@@ -359,7 +390,7 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
         else
             tile_body(std::false_type{}, tl);
     }
-    if (NORM && a.red.result != nullptr) grid_reduce<1>(a.red, acc, scratch);
+    if (NORM && a.red.result != nullptr) grid_reduce<NR>(a.red, acc, scratch);
 }
 
 template <int MODE, int TY, int NSEG, int KB, int NS2>
@@ -422,7 +453,8 @@ bool ksplit_supported(int mode, int nz, int nx)
 {
     // TMA row strides must be multiples of 16 bytes: even nx (and even coarse nx for the
     // fused prolongation)
-    return (mode == MODE_SMOOTH || mode == MODE_PREC || mode == MODE_RESTRICT || mode == MODE_SMOOTH_PROLONG) &&
+    return (mode == MODE_SMOOTH || mode == MODE_PREC || mode == MODE_RESTRICT || mode == MODE_SMOOTH_PROLONG ||
+            mode == MODE_CGPREC) &&
            nz % SL == 0 && nz <= kKsplitMaxNZ && (nz / SL == 1 || nz / SL == 2 || nz / SL == 4) && nx % 2 == 0 &&
            (mode != MODE_SMOOTH_PROLONG || nx % 4 == 0);
 }
@@ -450,6 +482,11 @@ cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const Line
         if (cfg == 1) return launch_k_nseg<MODE_PREC, 4, 4, 6>(ln, a, T);
         if (cfg == 2) return launch_k_nseg<MODE_PREC, 2, 4, 6>(ln, a, T);
         return launch_k_nseg<MODE_PREC, 2, 8, 4>(ln, a, T);
+    }
+    if (mode == MODE_CGPREC) {     // p box + r and u boxes: two stages fit at 4 x 4
+        if (cfg == 1) return launch_k_nseg<MODE_CGPREC, 4, 4, 2>(ln, a, T);
+        if (cfg == 2) return launch_k_nseg<MODE_CGPREC, 2, 4, 3>(ln, a, T);
+        return launch_k_nseg<MODE_CGPREC, 2, 8, 2>(ln, a, T);
     }
     if (mode == MODE_RESTRICT) {   // no Thomas: the exchange buffer replaces the chaining buffer
         if (cfg == 1) return launch_k_nseg<MODE_RESTRICT, 4, 4, 3>(ln, a, T);

@@ -251,3 +251,19 @@ def test_profile_mask_times_only_selected_class():
     prof = ctx.profile_read()
     ctx.profile(False)
     assert {"cg_precondition", "cg_direction"} <= set(prof)
+
+
+@pytest.mark.parametrize("p", [SOLVE_SHAPES[0], SOLVE_SHAPES[1], O.Params(nx=80, ny=48, nz=64, L=3)],
+                         ids=["32x32x16", "128x128x128", "80x48x64"])
+def test_cg_ksplit_preconditioner_opt_in(p, monkeypatch):
+    """TPMG_KSPLIT_CG=1: the CG preconditioner kernel in the k-split form (opt-in; the
+    one-thread-per-column kernel is the default) gives the oracle's solve."""
+    monkeypatch.setenv("TPMG_KSPLIT_CG", "1")
+    ctx = ctx_for(p)
+    f = rhs_zc(p.nx, p.ny, p.nz, seed=0)
+    u = ctx.empty(p.L)
+    res, ref = ctx.solve_cg(to_dev(f), u), O.solve_cg(p, f)
+    assert res.converged and abs(res.iterations - ref.iterations) <= 1
+    if res.iterations == ref.iterations:
+        assert rel_l2(to_host_zc(u), ref.u) < 1e-9
+        assert np.allclose(res.history, ref.history, rtol=1e-8)
