@@ -332,7 +332,8 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
                     const int k = s * SL + cc * KB + kk;
                     yprev = (cc == 0 && kk == 0) ? gv[kk] : fma(afw[k], yprev, gv[kk]);
                     yv[cc * KB + kk] = yprev;
-                    if constexpr (NORM) acc[0] = fma(rv[kk], rv[kk], acc[0]);
+                    if constexpr (NORM)
+                        if (valid) acc[0] = fma(rv[kk], rv[kk], acc[0]);   // phantom columns of ragged tiles excluded
                 }
                 __syncthreads();   // every warp is done with this slot
             }

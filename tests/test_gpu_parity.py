@@ -118,6 +118,8 @@ SOLVE_SHAPES = [
     O.Params(nx=128, ny=128, nz=128),
     O.Params(nx=128, ny=64, nz=32, nu_cfl=2.0),
     O.Params(nx=64, ny=64, nz=32, nu_cfl=10.0),
+    O.Params(nx=80, ny=48, nz=64, L=3),     # ragged x tiles (80 = 2.5 x 32): norms must skip phantom columns
+    O.Params(nx=48, ny=40, nz=32, L=3),     # ragged x and y tiles (40 rows = 10 x 4; 48 columns)
 ]
 
 
