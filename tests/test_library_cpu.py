@@ -93,3 +93,16 @@ def test_no_cpu_fallback_in_product_package():
             if fn.endswith((".py", ".cu", ".cpp", ".cuh", ".h")):
                 text = open(os.path.join(dirpath, fn)).read()
                 assert "oracle" not in text.replace("oracle/", "").lower() or fn == "build.py", fn
+
+
+def test_plain_c_client(T, tmp_path):
+    """The ABI is usable from plain C (no Python, no torch): compile tests/c/abi_host.c
+    against include/tpmg.h, link libtpmg.so, run its host-only checks."""
+    exe = str(tmp_path / "abi_host")
+    libdir = os.path.dirname(T.LIB_PATH)
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c", "abi_host.c"), "-L", libdir, "-ltpmg",
+                    "-Wl,-rpath," + libdir, "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "abi_host ok" in r.stdout
