@@ -312,7 +312,11 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 g = rn;
             }
             if constexpr (MODE == MODE_APPLY || MODE == MODE_RESID || MODE == MODE_CGDIR || MODE == MODE_CGPREC) {
-                if (ofw0) ofw0 += nx;
+                if constexpr (MODE == MODE_RESID) {   // the only mode whose out0 may be absent
+                    if (ofw0) ofw0 += nx;
+                } else {
+                    ofw0 += nx;
+                }
                 if constexpr (MODE == MODE_CGPREC) ofw1 += nx;
             }
             if constexpr (T::THOMAS) {
