@@ -60,3 +60,20 @@ def mode_face_zc(nx: int, ny: int, nz: int, p: int, q: int, r: int) -> np.ndarra
     sj = np.sin(q * np.pi * (np.arange(ny) + 0.5) / ny)
     ck = np.cos(r * np.pi * (np.arange(nz) + 0.5) / nz)
     return np.ascontiguousarray(sj[:, None, None] * si[None, :, None] * ck[None, None, :])
+
+
+def vertical_profiles(nz: int, seed: int = 0, coupling: float = 1.0):
+    """Seeded synthetic vertical profiles (a, b, c, d) of eqn:LocalMatrixStencil for a
+    non-uniform column (a stretched vertical grid / varying lambda and density): positive
+    interface couplings w_{k+1/2} in [0.25, 4] x `coupling` give b_k = -w_{k-1/2},
+    c_k = -w_{k+1/2} (zero at the ends: Neumann), a_k, d_k in [0.5, 2].  Pure input
+    generation (a splitmix64 stream), no solver arithmetic."""
+    u = (_mix(np.arange(4 * nz, dtype=np.uint64), seed) + 1.0) / 2.0   # [0, 1)
+    w = coupling * (0.25 + 3.75 * u[:nz])          # w[k] couples k and k+1 (w[nz-1] unused)
+    b = np.zeros(nz)
+    c = np.zeros(nz)
+    b[1:] = -w[:nz - 1]
+    c[:nz - 1] = -w[:nz - 1]
+    a = 0.5 + 1.5 * u[nz:2 * nz]
+    d = 0.5 + 1.5 * u[2 * nz:3 * nz]
+    return a, b, c, d

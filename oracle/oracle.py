@@ -39,7 +39,9 @@ class _Params(C.Structure):
     _fields_ = [("nx", C.c_long), ("ny", C.c_long), ("nz", C.c_int),
                 ("nu_cfl", C.c_double), ("H", C.c_double), ("lam", C.c_double),
                 ("L", C.c_int), ("pre", C.c_int), ("post", C.c_int),
-                ("coarse_sweeps", C.c_int), ("rho", C.c_double), ("boundary", C.c_int)]
+                ("coarse_sweeps", C.c_int), ("rho", C.c_double), ("boundary", C.c_int),
+                ("prof_a", C.POINTER(C.c_double)), ("prof_b", C.POINTER(C.c_double)),
+                ("prof_c", C.POINTER(C.c_double)), ("prof_d", C.POINTER(C.c_double))]
 
 
 @dataclass
@@ -58,10 +60,23 @@ class Params:
     coarse_sweeps: int = 2
     rho: float = 2.0 / 3.0
     boundary: int = 0   # horizontal Dirichlet reading: 0 ghost zero [R1], 1 face [R25]
+    profiles: tuple | None = None   # (a, b, c, d) vertical profiles; None: flat box [R2]
 
     def c(self) -> _Params:
+        ptrs = [None] * 4
+        if self.profiles is not None:
+            arrs = [np.ascontiguousarray(x, dtype=np.float64) for x in self.profiles]
+            assert all(a.shape == (self.nz,) for a in arrs)
+            self._keep = arrs   # the C struct points into these
+            ptrs = [a.ctypes.data_as(C.POINTER(C.c_double)) for a in arrs]
         return _Params(self.nx, self.ny, self.nz, self.nu_cfl, self.H, self.lam, self.L,
-                       self.pre, self.post, self.coarse_sweeps, self.rho, self.boundary)
+                       self.pre, self.post, self.coarse_sweeps, self.rho, self.boundary, *ptrs)
+
+    def flat_profiles(self) -> tuple:
+        """The flat-box profiles [R2] as arrays (a, b, c, d)."""
+        g = self.gamma()
+        k = np.arange(self.nz)
+        return (np.ones(self.nz), np.where(k > 0, -g, 0.0), np.where(k < self.nz - 1, -g, 0.0), np.ones(self.nz))
 
     def level_shape(self, level: int) -> tuple[int, int, int]:
         f = 1 << (self.L - level)

@@ -97,6 +97,11 @@ typedef struct {
     int coarse_sweeps;/* smoother iterations on the coarsest level (2) */
     double rho;       /* rho_relax = 2/3 */
     int boundary;     /* horizontal Dirichlet reading: 0 = ghost zero [R1], 1 = face [R25] */
+    /* vertical profiles a, b, c, d of eqn:LocalMatrixStencil, length nz, in the
+     * units of A (b, c include omega^2 lambda^2 / h_z^2, d multiplies alpha_{T,T'});
+     * NULL: the flat-box values [R2].  Requirements (a symmetric, diagonally dominant
+     * column block): b_0 = 0, c_{nz-1} = 0, b_{k+1} = c_k, a >= 0, b <= 0, c <= 0, d > 0. */
+    const double *prof_a, *prof_b, *prof_c, *prof_d;
 } or_params;
 
 /* Build the operator of level l (1 <= l <= L) by rediscretisation [R4]:
@@ -128,6 +133,23 @@ int or_op_init(const or_params *p, int l, or_op *op)
     op->c = (double *)malloc(sizeof(double) * p->nz);
     op->d = (double *)malloc(sizeof(double) * p->nz);
     if (!op->a || !op->b || !op->c || !op->d) return OR_E_OOM;
+    if (p->prof_a) {   /* general vertical profiles ("derived from the vertical
+                        * stiffness- and mass-matrices"; the same on every level) */
+        if (!p->prof_b || !p->prof_c || !p->prof_d) return OR_E_PARAM;
+        for (int k = 0; k < p->nz; ++k) {
+            if (!(p->prof_a[k] >= 0) || !(p->prof_b[k] <= 0) || !(p->prof_c[k] <= 0) || !(p->prof_d[k] > 0))
+                return OR_E_PARAM;
+            if (k + 1 < p->nz && p->prof_b[k + 1] != p->prof_c[k]) return OR_E_PARAM;
+        }
+        if (p->prof_b[0] != 0.0 || p->prof_c[p->nz - 1] != 0.0) return OR_E_PARAM;
+        for (int k = 0; k < p->nz; ++k) {
+            op->a[k] = p->prof_a[k];
+            op->b[k] = p->prof_b[k];
+            op->c[k] = p->prof_c[k];
+            op->d[k] = p->prof_d[k];
+        }
+        return OR_OK;
+    }
     for (int k = 0; k < p->nz; ++k) {
         op->a[k] = 1.0;
         op->d[k] = 1.0;
