@@ -231,6 +231,22 @@ tpmg_status tpmg_solve_host(tpmg_ctx *ctx, tpmg_solver solver, const double *f_h
                             double *u_host, double eps, int32_t max_iter,
                             tpmg_result *result);
 
+/* General vertical profiles a, b, c, d of eqn:LocalMatrixStencil ("derived
+ * from the vertical stiffness- and mass-matrices", the same for every column and level),
+ * e.g. a stretched vertical grid or height-dependent lambda / density:
+ *   A_T      = diag(a) - alpha_T diag(d) + tridiag(-(b+c), b, c),
+ *   A_{T,T'} = alpha_{T,T'} diag(d),   alpha_{T,T'} = -omega^2 / h_l^2 on level l,
+ * in the units of A (b, c include omega^2 lambda^2 / h_z^2; the flat box [R2] is a = d = 1,
+ * b_k = -gamma [k > 0], c_k = -gamma [k < nz-1]).  Host arrays of nz doubles, copied.
+ * Requirements (symmetric, diagonally dominant column blocks): b[0] = 0, c[nz-1] = 0,
+ * b[k+1] = c[k], a >= 0, b <= 0, c <= 0, d > 0, else TPMG_E_PARAM.  All NULL: back to the
+ * flat box.  Synchronises the context stream and rebuilds the per-level Thomas tables;
+ * applies to every later call.  COLLECTIVE in the sense that all ranks must pass the same
+ * profiles.  The fused prolongation and the k-split CG preconditioner options are flat-box
+ * only (the library falls back to the general kernels). */
+tpmg_status tpmg_set_profiles(tpmg_ctx *ctx, const double *a, const double *b, const double *c,
+                              const double *d);
+
 /* Counters (kernel launches etc.); tpmg_stats_reset zeroes them. */
 tpmg_status tpmg_get_stats(const tpmg_ctx *ctx, tpmg_stats *out);
 tpmg_status tpmg_stats_reset(tpmg_ctx *ctx);

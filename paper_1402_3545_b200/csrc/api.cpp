@@ -37,6 +37,7 @@ struct LevelData {
     int cur = 0;
     double* f = nullptr;                // MG right-hand side (coarse levels)
     KTables ktab{};                     // k-split tables (kernel parameter space)
+    double* d_prof = nullptr;           // general vertical profiles: [b_k][c_k][c_l d_k] (device)
     double* slab_lo = nullptr;          // halo rows j = -1 / j = ny for this level (nranks > 1)
     double* slab_hi = nullptr;
     size_t n() const { return (size_t)lc.nx * (size_t)lc.ny * (size_t)lc.nz; }
@@ -636,6 +637,8 @@ bool fill_tma_ksplit(tpmg_ctx* ctx, int mode, LineArgs& a)
 
 bool ksplit_usable(tpmg_ctx* ctx, int mode, const LevelConst& lc)
 {
+    // general vertical profiles: the k-split smoother / preconditioner / restriction only
+    if (lc.gen && (mode == MODE_SMOOTH_PROLONG || mode == MODE_CGPREC)) return false;
     // the k-split CG preconditioner is opt-in (TPMG_KSPLIT_CG=1): measured 4% slower per CG
     // iteration than the one-thread-per-column kernel at 1024^2 x 128
     if (mode == MODE_CGPREC && !ctx->ksplit_cg) return false;
@@ -848,7 +851,7 @@ tpmg_status vcycle_rec(tpmg_ctx* ctx, int l, bool skip_pre = false)
     HaloField uc = halo_of(ctx, l - 1, Cc.u[Cc.cur]);
     (void)uc;
     const bool fuse = p.post >= 1 && ctx->fuse_prolong && p.boundary == TPMG_BC_GHOST_ZERO &&
-                      ksplit_usable(ctx, MODE_SMOOTH_PROLONG, F.lc);   // fused form: zero coarse ghosts only
+                      ksplit_usable(ctx, MODE_SMOOTH_PROLONG, F.lc);   // fused form: zero coarse ghosts, flat box
     if (fuse) {
         TRY(exchange(ctx, l - 1, Cc.u[Cc.cur]));
         uc = halo_of(ctx, l - 1, Cc.u[Cc.cur]);
@@ -1324,6 +1327,7 @@ void ctx_free(tpmg_ctx* ctx)
     for (size_t l = 1; l < ctx->lv.size(); ++l) {
         LevelData& L = ctx->lv[l];
         cudaFree(L.d_tab);
+        cudaFree(L.d_prof);
         if ((int)l < ctx->L) { cudaFree(L.u[0]); cudaFree(L.f); }
         cudaFree(L.u[1]);
     }
@@ -1416,6 +1420,86 @@ tpmg_status tpmg_partition(const tpmg_params* params, int32_t rank, int32_t nran
     return TPMG_OK;
 }
 
+// Per-level tables of the column blocks M_T = A_T from the vertical profiles
+// (eqn:LocalMatrixStencil; prof == nullptr: the flat box [R2], a = d = 1,
+// b_k = -gamma [k > 0], c_k = -gamma [k < nz-1]).  Per level k:
+//   diag_k = a_k - b_k - c_k + (4 + nb) c_l d_k   (nb = boundary faces of the column class),
+//   m_k = diag_k - b_k c_{k-1} / m_{k-1}  (M = L D L^T, symmetric: b_k = c_{k-1}),
+//   1/m_k,  gim_k = -c_k / m_k (backward),  afw_k = -b_k / m_{k-1} (forward),
+//   and the k-split propagators over segments of kSegK levels:
+//   P_k = prod_{j = k_s..k} afw_j,  Q_k = prod_{j = k..k_e} gim_j.
+// One table set per column class (face Dirichlet [R25]: alpha_T = -(4 + nb) c); the
+// ghost-zero reading has class 0 only.  With general profiles the stencil also reads the
+// per-level couplings (b_k, c_k, c_l d_k) from LevelData::d_prof.
+tpmg_status build_tables(tpmg_ctx* ctx, const double* const* prof)
+{
+    const tpmg_params& p = ctx->p;
+    const int nz = p.nz;
+    const double gamma = ctx->lv[ctx->L].lc.gamma;
+    std::vector<double> a(nz), b(nz), c(nz), d(nz);
+    for (int k = 0; k < nz; ++k) {
+        a[k] = prof ? prof[0][k] : 1.0;
+        b[k] = prof ? prof[1][k] : (k > 0 ? -gamma : 0.0);
+        c[k] = prof ? prof[2][k] : (k < nz - 1 ? -gamma : 0.0);
+        d[k] = prof ? prof[3][k] : 1.0;
+    }
+    for (int l = 1; l <= ctx->L; ++l) {
+        LevelData& L = ctx->lv[l];
+        const double cl = L.lc.c;
+        const int ncls = (p.boundary == TPMG_BC_FACE) ? kBoundaryClasses : 1;
+        std::vector<double> tab(6 * (size_t)nz * ncls);
+        for (int cls = 0; cls < ncls; ++cls) {
+            double* t_diag = tab.data() + (size_t)cls * 6 * nz;
+            double* t_invm = t_diag + nz;
+            double* t_gim = t_invm + nz;
+            double* t_afw = t_gim + nz;
+            double* t_P = t_afw + nz;
+            double* t_Q = t_P + nz;
+            double mprev = 0.0;
+            for (int k = 0; k < nz; ++k) {
+                // flat box: 1 + (4 + nb) c + gamma ([k > 0] + [k < nz-1]), the same value
+                const double diag = prof ? a[k] - b[k] - c[k] + (4.0 + cls) * cl * d[k]
+                                         : 1.0 + (4.0 + cls) * cl + gamma * ((k > 0 ? 1.0 : 0.0) + (k < nz - 1 ? 1.0 : 0.0));
+                const double m = (k == 0) ? diag : diag - (-b[k]) * ((-c[k - 1]) / mprev);
+                if (m == 0.0 || !std::isfinite(m))
+                    return fail(ctx, TPMG_E_SINGULAR, "zero Thomas pivot at level %d, k = %d", l, k);
+                t_diag[k] = diag;
+                t_invm[k] = 1.0 / m;
+                t_gim[k] = (k < nz - 1) ? -c[k] / m : 0.0;
+                t_afw[k] = (k > 0) ? -b[k] / mprev : 0.0;
+                mprev = m;
+            }
+            for (int k0 = 0; k0 < nz; k0 += kSegK) {
+                const int k1 = std::min(nz, k0 + kSegK) - 1;
+                double pr = 1.0;
+                for (int k = k0; k <= k1; ++k) { pr *= t_afw[k]; t_P[k] = pr; }
+                pr = 1.0;
+                for (int k = k1; k >= k0; --k) { pr *= t_gim[k]; t_Q[k] = pr; }
+            }
+        }
+        if (nz <= kKsplitMaxNZ)
+            for (int q = 0; q < 6; ++q)
+                for (int k = 0; k < nz; ++k) L.ktab.t[q][k] = tab[(size_t)q * nz + k];
+        TRY(dev_alloc(ctx, &L.d_tab, tab.size()));
+        CUDA_TRY(ctx, cudaMemcpy(L.d_tab, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice));
+        L.lc.tab = L.d_tab;
+        // general profiles: per-level stencil couplings [b_k][c_k][c_l d_k]
+        L.lc.gen = prof ? 1 : 0;
+        if (prof) {
+            std::vector<double> pr(3 * (size_t)nz);
+            for (int k = 0; k < nz; ++k) {
+                pr[k] = b[k];
+                pr[nz + k] = c[k];
+                pr[2 * nz + k] = cl * d[k];
+            }
+            TRY(dev_alloc(ctx, &L.d_prof, pr.size()));
+            CUDA_TRY(ctx, cudaMemcpy(L.d_prof, pr.data(), sizeof(double) * pr.size(), cudaMemcpyHostToDevice));
+        }
+        L.lc.prof = prof ? L.d_prof : nullptr;
+    }
+    return TPMG_OK;
+}
+
 tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks, const void* id128,
                         int32_t device, void* cuda_stream, tpmg_ctx** out)
 {
@@ -1498,48 +1582,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         L.lc.bc = p.boundary;
         L.lc.bnd_lo = (rank == 0) ? 1 : 0;               // local row 0 / ny-1 on the physical boundary
         L.lc.bnd_hi = (rank == nranks - 1) ? 1 : 0;
-        // Thomas factors of the column block M_T = A_T, per level k:
-        //   diag_k, 1/m_k, b_k = gamma/m_k (backward), a_k = gamma/m_{k-1} (forward, L of M = L D L^T),
-        //   and the k-split propagators over segments of kSegK levels:
-        //   P_k = prod_{j = k_s..k} a_j,  Q_k = prod_{j = k..k_e} b_j.
-        // One table per column class: class nb = number of boundary faces of the column
-        // (face Dirichlet [R25]: alpha_T = -(4 + nb) c); ghost-zero Dirichlet has class 0 only.
-        const int nz = p.nz;
-        const int ncls = (p.boundary == TPMG_BC_FACE) ? kBoundaryClasses : 1;
-        std::vector<double> tab(6 * (size_t)nz * ncls);
-        for (int cls = 0; cls < ncls; ++cls) {
-            double* t_diag = tab.data() + (size_t)cls * 6 * nz;
-            double* t_invm = t_diag + nz;
-            double* t_gim = t_invm + nz;
-            double* t_afw = t_gim + nz;
-            double* t_P = t_afw + nz;
-            double* t_Q = t_P + nz;
-            double mprev = 0.0;
-            for (int k = 0; k < nz; ++k) {
-                const double diag = 1.0 + (4.0 + cls) * L.lc.c + gamma * ((k > 0 ? 1.0 : 0.0) + (k < nz - 1 ? 1.0 : 0.0));
-                const double m = (k == 0) ? diag : diag - gamma * (gamma / mprev);
-                if (m == 0.0 || !std::isfinite(m)) return bail(fail(ctx, TPMG_E_SINGULAR, "zero Thomas pivot at level %d, k = %d", l, k));
-                t_diag[k] = diag;
-                t_invm[k] = 1.0 / m;
-                t_gim[k] = (k < nz - 1) ? gamma / m : 0.0;
-                t_afw[k] = (k > 0) ? gamma / mprev : 0.0;
-                mprev = m;
-            }
-            for (int k0 = 0; k0 < nz; k0 += kSegK) {
-                const int k1 = std::min(nz, k0 + kSegK) - 1;
-                double pr = 1.0;
-                for (int k = k0; k <= k1; ++k) { pr *= t_afw[k]; t_P[k] = pr; }
-                pr = 1.0;
-                for (int k = k1; k >= k0; --k) { pr *= t_gim[k]; t_Q[k] = pr; }
-            }
-        }
-        if (nz <= kKsplitMaxNZ)
-            for (int q = 0; q < 6; ++q)
-                for (int k = 0; k < nz; ++k) L.ktab.t[q][k] = tab[(size_t)q * nz + k];
-        CREATE_TRY(dev_alloc(ctx, &L.d_tab, tab.size()));
-        CREATE_CUDA(cudaMemcpy(L.d_tab, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice));
-        L.lc.tab = L.d_tab;
     }
+    CREATE_TRY(build_tables(ctx, nullptr));
     if (nranks > 1) {
         ncclUniqueId id;
         std::memcpy(&id, id128, sizeof id);
@@ -1791,3 +1835,24 @@ const char* tpmg_last_error(const tpmg_ctx* ctx)
 }
 
 }  // extern "C"
+
+tpmg_status tpmg_set_profiles(tpmg_ctx* ctx, const double* a, const double* b, const double* c, const double* d)
+{
+    if (!ctx) return TPMG_E_PARAM;
+    const int nz = ctx->p.nz;
+    if (a || b || c || d) {
+        if (!a || !b || !c || !d) return fail(ctx, TPMG_E_PARAM, "tpmg_set_profiles: give all four profiles or none");
+        for (int k = 0; k < nz; ++k) {
+            if (!(a[k] >= 0) || !(b[k] <= 0) || !(c[k] <= 0) || !(d[k] > 0))
+                return fail(ctx, TPMG_E_PARAM, "tpmg_set_profiles: need a >= 0, b <= 0, c <= 0, d > 0 (k = %d)", k);
+            if (k + 1 < nz && b[k + 1] != c[k])
+                return fail(ctx, TPMG_E_PARAM, "tpmg_set_profiles: b[%d] != c[%d] (A must be symmetric)", k + 1, k);
+        }
+        if (b[0] != 0.0 || c[nz - 1] != 0.0)
+            return fail(ctx, TPMG_E_PARAM, "tpmg_set_profiles: b[0] and c[nz-1] must be 0 (no coupling outside the column)");
+        if (!ctx->use_tma) return fail(ctx, TPMG_E_PARAM, "tpmg_set_profiles: general profiles need the TMA loader");
+    }
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));   // queued kernels may still read the tables
+    const double* prof[4] = {a, b, c, d};
+    return build_tables(ctx, a ? prof : nullptr);
+}

@@ -137,7 +137,7 @@ __device__ __forceinline__ void tma_stage(double* st, const LineArgs& a, int64_t
 // mbarrier per stage.  The CTA walks its tiles (tile = blockIdx.x + t*gridDim.x)
 // as one global sequence of KB-level chunks, so the loads of the next tile's
 // first chunks overlap the current tile's backward sweep.
-template <int MODE, int TY, int LOADER>
+template <int MODE, int TY, int LOADER, bool GEN>
 __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArgs a)
 {
     using T = Traits<MODE>;
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     const double* diag_s = tab;
     const double* invm_s = tab + nz;
     const double* gim_s = tab + 2 * nz;
-    const double c = a.L.c, gamma = a.L.gamma;
+    const double c0 = a.L.c, gamma = a.L.gamma;
     if constexpr (LOADER == 1) {
         if (tid == 0) {
             for (int s = 0; s < NS; ++s) mbar_init(&full_bar[s], 1);
@@ -271,9 +271,19 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 
         // Complete level km (its upper neighbour up1 has arrived): stencil, the mode's
         // pointwise work and one Thomas forward-elimination step.
-        auto finalize = [&](double up1, double dgk, double imk, double* gslot, int rslot) {
-            const double vs = um1 + up1;
-            const double Mu = fma(-gamma, vs, dgk * u0);          // (M_T u)_k
+        auto finalize = [&](double up1, double dgk, double imk, double* gslot, int rslot, int km) {
+            // (M_T u)_k and the coefficient of the horizontal neighbour sum: -gamma and c in
+            // the flat box; b_k, c_k and c_l d_k with general profiles (GEN, warp-uniform
+            // cached loads)
+            double Mu, c, sk = -gamma;
+            if constexpr (GEN) {
+                sk = __ldg(a.L.prof + km);
+                Mu = fma(sk, um1, fma(__ldg(a.L.prof + nz + km), up1, dgk * u0));
+                c = __ldg(a.L.prof + 2 * nz + km);
+            } else {
+                Mu = fma(-gamma, um1 + up1, dgk * u0);
+                c = c0;
+            }
             double g = 0.0;
             if constexpr (MODE == MODE_APPLY) {
                 if (valid) *ofw0 = fma(-c, S0, Mu);                 // (A u)_k = (M_T u)_k - c sum(nbrs)
@@ -320,7 +330,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 if constexpr (MODE == MODE_CGPREC) ofw1 += nx;
             }
             if constexpr (T::THOMAS) {
-                const double y = fma(gamma, gprev, g);   // y = L^-1 g   (M = L D L^T)
+                const double y = fma(-sk, gprev, g);     // y = L^-1 g   (M = L D L^T; sub-diagonal s_k)
                 const double gp = y * imk;               // g'_k = (g_k - s_k g'_{k-1}) / m_k
                 *gslot = gp;
                 if constexpr (MODE == MODE_CGPREC)
@@ -362,7 +372,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             for (int kk = 0; kk < KB; ++kk) {
                 const int k = k0 + kk;
                 if (FULL || k < nz) {
-                    if (FULL || k > 0) finalize(ecv[kk], dg[kk], im[kk], gb + kk * NT, kk);
+                    if (FULL || k > 0) finalize(ecv[kk], dg[kk], im[kk], gb + kk * NT, kk, k - 1);
                     um1 = u0; u0 = ecv[kk]; S0 = Sv[kk]; qa = pav[kk]; qb = pbv[kk];
                 }
             }
@@ -378,7 +388,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             else
                 do_chunk(std::false_type{}, ch, st);
             if (ch == nch - 1)
-                finalize(0.0, diag[nz - 1], invm[nz - 1], gbuf + (nz - 1) * NT + tid, nz - ch * KB);
+                finalize(0.0, diag[nz - 1], invm[nz - 1], gbuf + (nz - 1) * NT + tid, nz - ch * KB, nz - 1);
             if constexpr (MODE == MODE_RESTRICT) {
                 // f_c(I, J, k) = 1/4 (x-pair sum of row 2J + x-pair sum of row 2J+1);
                 // this chunk completed levels ch*KB-1 .. ch*KB+KB-2 (and nz-1 if last), slot
@@ -481,11 +491,11 @@ size_t line_smem_bytes(int nz)
 
 constexpr size_t kMaxSmem = 227 * 1024 - 1024;  // leave room for static smem (barriers, flags)
 
-template <int MODE, int TY, int LOADER>
+template <int MODE, int TY, int LOADER, bool GEN>
 cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
 {
     const size_t smem = line_smem_bytes<MODE, TY>(a.L.nz);
-    auto kern = k_line<MODE, TY, LOADER>;
+    auto kern = k_line<MODE, TY, LOADER, GEN>;
     static size_t limit = 0;   // per instantiation
     if (!limit) {
         limit = dyn_smem_limit(kern);
@@ -511,7 +521,11 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
 template <int MODE, int TY>
 cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
 {
-    return a.use_tma ? launch_line_l<MODE, TY, 1>(ln, a) : launch_line_l<MODE, TY, 0>(ln, a);
+    if (a.L.gen) {   // general vertical profiles: TMA loader only
+        if (!a.use_tma) return cudaErrorNotSupported;
+        return launch_line_l<MODE, TY, 1, true>(ln, a);
+    }
+    return a.use_tma ? launch_line_l<MODE, TY, 1, false>(ln, a) : launch_line_l<MODE, TY, 0, false>(ln, a);
 }
 
 template <int MODE>

@@ -29,6 +29,8 @@ struct LevelConst {
     const double* tab;  // device: per column class [diag, invm, gim, afw, P, Q][nz] (Thomas factors of M_T)
     int32_t bc;         // tpmg_boundary: 0 ghost-zero [R1] (class 0 only), 1 face Dirichlet [R25]
     int32_t bnd_lo, bnd_hi;   // local row 0 / ny-1 lies on the physical boundary
+    int32_t gen;        // 1: general vertical profiles (stencil couplings from prof, not gamma / c)
+    const double* prof; // device, gen only: [b_k][c_k][c_l d_k], nz each
 };
 
 // Column classes of the face-Dirichlet reading: nb = number of boundary faces (0..4).

@@ -131,7 +131,7 @@ __device__ __forceinline__ void tma_step(double* st, const LineArgs& a, int i0, 
     }
 }
 
-template <int MODE, int TY, int NSEG, int KB, int NS2, bool PUSH>
+template <int MODE, int TY, int NSEG, int KB, int NS2, bool PUSH, bool GEN>
 __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_constant__ LineArgs a,
                                                              const __grid_constant__ KTables T)
 {
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     const int s = warp % NSEG, ty = warp / NSEG;
     // per-level tables, staged in shared memory (warp-uniform broadcast reads)
     for (int q = tid; q < 6 * nz; q += NT) tab[q] = T.t[q / nz][q % nz];   // interior class (0)
-    const double c = a.L.c, gamma = a.L.gamma, rho = a.rho, scale = a.scale;
+    const double c0 = a.L.c, gamma = a.L.gamma, rho = a.rho, scale = a.scale;
     if (tid == 0) {
         for (int q = 0; q < NS2; ++q) mbar_init(&full_bar[q], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -275,7 +275,13 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
                     const int k = s * SL + cc * KB + kk;
                     const double uu = rc[(dd + 1) * HX];
                     const double S = (rc[dd * HX - 1] + rc[dd * HX + 1]) + (rs[dd * HX] + rn[dd * HX]);
-                    const double Mu = fma(-gamma, ud + uu, diag[k] * uc);       // (M_T u)_k
+                    double Mu, c = c0;                                          // (M_T u)_k
+                    if constexpr (GEN) {   // general vertical profiles: b_k, c_k, c_l d_k
+                        Mu = fma(__ldg(a.L.prof + k), ud, fma(__ldg(a.L.prof + nz + k), uu, diag[k] * uc));
+                        c = __ldg(a.L.prof + 2 * nz + k);
+                    } else {
+                        Mu = fma(-gamma, ud + uu, diag[k] * uc);
+                    }
                     if constexpr (CGP) {
                         // (Fused) Tridiag: r -= alpha A p, u += alpha p, then z = M^-1 r
                         // (the box field is p, fb is r, fb + FBOX is u)
@@ -401,10 +407,10 @@ size_t ksmem(int nz)
     return (size_t)(NS2 * NSEG * G::SEGST + r16(6 * nz) + G::template bnd<NSEG>() + 64 + 16) * sizeof(double);
 }
 
-template <int MODE, int TY, int NSEG, int KB, int NS2, bool PUSH>
+template <int MODE, int TY, int NSEG, int KB, int NS2, bool PUSH, bool GEN = false>
 cudaError_t launch_k_push(const Launcher& ln, const LineArgs& a, const KTables& T)
 {
-    auto kern = k_linek<MODE, TY, NSEG, KB, NS2, PUSH>;
+    auto kern = k_linek<MODE, TY, NSEG, KB, NS2, PUSH, GEN>;
     const size_t smem = ksmem<MODE, TY, NSEG, KB, NS2>(a.L.nz);
     static size_t limit = 0;
     if (!limit) {
@@ -428,6 +434,15 @@ cudaError_t launch_k_push(const Launcher& ln, const LineArgs& a, const KTables& 
 template <int MODE, int TY, int NSEG, int KB, int NS2>
 cudaError_t launch_k(const Launcher& ln, const LineArgs& a, const KTables& T)
 {
+    if constexpr (MODE == MODE_SMOOTH || MODE == MODE_RESTRICT) {
+        if (a.L.gen) {   // general vertical profiles: the stencil's couplings per level
+            if constexpr (MODE == MODE_SMOOTH)
+                if (a.push.dst_lo || a.push.dst_hi) return launch_k_push<MODE, TY, NSEG, KB, NS2, true, true>(ln, a, T);
+            return launch_k_push<MODE, TY, NSEG, KB, NS2, false, true>(ln, a, T);
+        }
+    } else if constexpr (MODE != MODE_PREC) {
+        if (a.L.gen) return cudaErrorNotSupported;   // fused prolongation / k-split CG: flat box only
+    }
     if constexpr (MODE == MODE_SMOOTH || MODE == MODE_PREC)
         if (a.push.dst_lo || a.push.dst_hi) return launch_k_push<MODE, TY, NSEG, KB, NS2, true>(ln, a, T);
     return launch_k_push<MODE, TY, NSEG, KB, NS2, false>(ln, a, T);

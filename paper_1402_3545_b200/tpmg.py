@@ -74,6 +74,7 @@ _SIGS = {
     "tpmg_stats_reset": ([_vp], C.c_int),
     "tpmg_profile": ([_vp, _i32], C.c_int),
     "tpmg_profile_mask": ([_vp, C.c_uint32], C.c_int),
+    "tpmg_set_profiles": ([_vp, _P(_d), _P(_d), _P(_d), _P(_d)], C.c_int),
     "tpmg_profile_read": ([_vp, _i32, _P(_i64), _P(_d), _P(_d)], C.c_int),
     "tpmg_last_error": ([_vp], C.c_char_p),
 }
@@ -255,6 +256,17 @@ def tpmg_profile(ctx: int, enable: bool) -> None:
     _check(_lib.tpmg_profile(ctx, 1 if enable else 0), ctx)
 
 
+def tpmg_set_profiles(ctx: int, a=None, b=None, c=None, d=None) -> None:
+    """General vertical profiles (host float64 arrays of nz), or all None for the flat box."""
+    if a is None:
+        _check(_lib.tpmg_set_profiles(ctx, None, None, None, None), ctx)
+        return
+    import numpy as np
+    arrs = [np.ascontiguousarray(x, dtype=np.float64) for x in (a, b, c, d)]
+    ptrs = [x.ctypes.data_as(_P(_d)) for x in arrs]
+    _check(_lib.tpmg_set_profiles(ctx, *ptrs), ctx)
+
+
 def tpmg_profile_mask(ctx: int, mask: int) -> None:
     _check(_lib.tpmg_profile_mask(ctx, mask), ctx)
 
@@ -358,6 +370,9 @@ class Context:
 
     def stats_reset(self):
         tpmg_stats_reset(self.handle)
+
+    def set_profiles(self, a=None, b=None, c=None, d=None):
+        tpmg_set_profiles(self.handle, a, b, c, d)
 
     def profile(self, enable: bool, classes=None):
         """Event-time every kernel class (enable), or only the named classes."""

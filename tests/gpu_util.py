@@ -32,7 +32,10 @@ def ctx_for(p: O.Params, device: int = 0, loader: str | None = None):
     params = T.make_params(p.nx, p.ny, nz=p.nz, nu_cfl=p.nu_cfl, H=p.H, lam=p.lam, levels=p.L,
                            pre=p.pre, post=p.post, coarse_sweeps=p.coarse_sweeps, rho=p.rho,
                            boundary=p.boundary)
-    return T.Context(params, device=device)
+    ctx = T.Context(params, device=device)
+    if getattr(p, "profiles", None) is not None:
+        ctx.set_profiles(*p.profiles)
+    return ctx
 
 
 def to_dev(x_zc: np.ndarray):
