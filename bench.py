@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--coarse-sweeps", type=int, default=2, help="smoother sweeps on the coarsest level (P:456)")
     ap.add_argument("--boundary", type=int, default=0, choices=[0, 1],
                     help="horizontal Dirichlet reading: 0 ghost zero [R1], 1 face [R25] (sec:Robustness runs)")
+    ap.add_argument("--profiles", type=int, default=-1,
+                    help="general vertical profiles (inputs.vertical_profiles with this seed, couplings of "
+                         "the flat box's size); -1: flat box")
     ap.add_argument("--global-nx", type=int, default=0,
                     help="strong scaling: a fixed global nx x nx x nz grid split into y-strips (4096 = configs[4])")
     return ap.parse_args()
@@ -148,7 +151,20 @@ def measured_peak():
 
 # ---------------------------------------------------------------------------- oracle legs
 
-def oracle_sample(nx, nz, nu, rows, seed, threads=None, levels=5, coarse_sweeps=2, boundary=0):
+def bench_profiles(args):
+    """--profiles: synthetic non-uniform column (inputs.vertical_profiles) with couplings of
+    the size of the flat box's gamma = omega^2 lambda^2 / h_z^2 at this grid."""
+    if args.profiles < 0:
+        return None
+    from inputs import vertical_profiles
+    nx = args.global_nx or args.per_gpu_nx
+    h = 1.0 / nx
+    omega = 0.5 * args.nu * h
+    gamma = omega * omega / (0.01 / args.nz) ** 2
+    return vertical_profiles(args.nz, args.profiles, gamma)
+
+
+def oracle_sample(nx, nz, nu, rows, seed, threads=None, levels=5, coarse_sweeps=2, boundary=0, profiles=None):
     """Time the CPU oracle (as it stands) on a y-strip of `rows` rows of the workload:
     one MG V-cycle (solve_mg, max_iter=1: norm + V-cycle + residual) and one PCG
     iteration (solve_cg, max_iter=1: setup preconditioner + one iteration)."""
@@ -156,7 +172,8 @@ def oracle_sample(nx, nz, nu, rows, seed, threads=None, levels=5, coarse_sweeps=
     from inputs import rhs_zc
     if threads:
         O.set_threads(threads)
-    p = O.Params(nx=nx, ny=rows, nz=nz, nu_cfl=nu, L=levels, coarse_sweeps=coarse_sweeps, boundary=boundary)
+    p = O.Params(nx=nx, ny=rows, nz=nz, nu_cfl=nu, L=levels, coarse_sweeps=coarse_sweeps, boundary=boundary,
+                 profiles=profiles)
     f = rhs_zc(nx, rows, nz, seed=seed)
     t0 = time.perf_counter()
     O.solve_mg(p, f, eps=1e-30, max_iter=1)
@@ -177,13 +194,15 @@ def run_reference(args):
     it_mg, it_cg = 9, 51  # iteration counts of the oracle at 128^2 x 128 (tests/test_oracle_pins)
     for _ in range(args.warmup):
         oracle_sample(nx, args.nz, args.nu, rows, args.seed, levels=args.levels,
-                     coarse_sweeps=args.coarse_sweeps, boundary=args.boundary)
+                     coarse_sweeps=args.coarse_sweeps, boundary=args.boundary,
+                     profiles=bench_profiles(args))
     t = 0.0
     wall = 0.0
     for _ in range(args.steps):
         w0 = time.perf_counter()
         a, b, cores = oracle_sample(nx, args.nz, args.nu, rows, args.seed, levels=args.levels,
-                     coarse_sweeps=args.coarse_sweeps, boundary=args.boundary)
+                     coarse_sweeps=args.coarse_sweeps, boundary=args.boundary,
+                     profiles=bench_profiles(args))
         wall += time.perf_counter() - w0
         t += scale * (it_mg * a + it_cg * b)
     N = nx * ny * args.nz
@@ -234,6 +253,9 @@ def main():
     params = T.make_params(nx, ny, nz=nz, nu_cfl=args.nu, levels=args.levels, coarse_sweeps=args.coarse_sweeps,
                            boundary=args.boundary)
     ctx = T.Context(params, rank=rank, nranks=world, id128=id128, device=local, stream=stream)
+    prof = bench_profiles(args)
+    if prof is not None:
+        ctx.set_profiles(*prof)
     shape = ctx.shape(args.levels)
     f = torch.empty(shape, dtype=torch.float64, device=f"cuda:{local}")
     u = torch.empty_like(f)
@@ -358,7 +380,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rows = max(128, 1 << (args.levels - 1))
         a, b, cores = oracle_sample(nx, nz, args.nu, rows, args.seed, levels=args.levels,
-                                       coarse_sweeps=args.coarse_sweeps, boundary=args.boundary)
+                                       coarse_sweeps=args.coarse_sweeps, boundary=args.boundary,
+                     profiles=bench_profiles(args))
         scale = ny / rows
         it_mg = its[0].iterations if its[0] else 0
         it_cg = its[1].iterations if its[1] else 0
@@ -375,7 +398,9 @@ def main():
             "scaling": "strong" if args.global_nx else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (splitmix64 uniform[-1,1) RHS keyed by global index, seed %d)" % args.seed,
             "config": {"workload": name, "nx": nx, "ny": ny, "nz": nz, "nu_cfl": args.nu, "eps": args.eps,
-                       "levels": args.levels, "coarse_sweeps": args.coarse_sweeps, "boundary": args.boundary, "parallelism": f"y-strips x{world}" if world > 1 else "single GPU",
+                       "levels": args.levels, "coarse_sweeps": args.coarse_sweeps, "boundary": args.boundary,
+                       "vertical_profiles": "flat box" if args.profiles < 0 else f"synthetic seed {args.profiles}",
+                       "parallelism": f"y-strips x{world}" if world > 1 else "single GPU",
                        "l2": "vectors 1 GiB/GPU >> 126 MB L2 (no flush needed)"},
             "roofline": roof,
             "cpu_baseline": cpu,

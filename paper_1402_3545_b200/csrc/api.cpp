@@ -568,7 +568,7 @@ void fill_tma(tpmg_ctx* ctx, int mode, LineArgs& a)
     const int64_t nx = a.L.nx, ny = a.L.ny;
     const int nz = a.L.nz;
     if (nx % 2) return;
-    const int TY = line_tile_rows(mode, nz);
+    const int TY = line_tile_rows(mode, nz, a.L.gen);
     int nh, np;
     mode_fields(mode, &nh, &np);
     const HaloField* H[2] = {&a.h0, &a.h1};
@@ -648,7 +648,7 @@ bool ksplit_usable(tpmg_ctx* ctx, int mode, const LevelConst& lc)
 // Tile rows of the kernel run_line will launch for this mode and level.
 int launch_rows(tpmg_ctx* ctx, int mode, const LevelConst& lc)
 {
-    return ksplit_usable(ctx, mode, lc) ? ksplit_boxes(mode, ctx->ksplit_cfg).ty : line_tile_rows(mode, lc.nz);
+    return ksplit_usable(ctx, mode, lc) ? ksplit_boxes(mode, ctx->ksplit_cfg).ty : line_tile_rows(mode, lc.nz, lc.gen);
 }
 
 // Fraction of the level's cells a launch covers (interior / boundary tile rows).
@@ -1851,6 +1851,7 @@ tpmg_status tpmg_set_profiles(tpmg_ctx* ctx, const double* a, const double* b, c
         if (b[0] != 0.0 || c[nz - 1] != 0.0)
             return fail(ctx, TPMG_E_PARAM, "tpmg_set_profiles: b[0] and c[nz-1] must be 0 (no coupling outside the column)");
         if (!ctx->use_tma) return fail(ctx, TPMG_E_PARAM, "tpmg_set_profiles: general profiles need the TMA loader");
+        if (!line_gen_fits(nz)) return fail(ctx, TPMG_E_SHAPE, "tpmg_set_profiles: nz = %d too large for general profiles", nz);
     }
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));   // queued kernels may still read the tables
     const double* prof[4] = {a, b, c, d};

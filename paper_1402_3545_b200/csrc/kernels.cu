@@ -154,7 +154,8 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     const int64_t nx = a.L.nx, ny = a.L.ny;
     const int tabn = (3 * nz + 15) & ~15;    // keep the stages 128-byte aligned
     double* tab = smem;                      // diag[nz], invm[nz], gim[nz]
-    double* stage = smem + tabn;             // NS stages
+    double* ptab = smem + tabn;              // GEN: b_k[nz], c_k[nz], c_l d_k[nz]
+    double* stage = ptab + (GEN ? tabn : 0); // NS stages
     double* gbuf = stage + NS * G::STAGE;    // g'[nz][NT] (Thomas modes)
     // MODE_RESTRICT: x-pair sums [2][TY][KB+1][TX/2] (a chunk completes up to KB+1 levels)
     constexpr int RS = KB + 1;
@@ -163,6 +164,8 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     for (int q = tid; q < 3 * nz; q += NT) tab[q] = a.L.tab[q];   // interior class (0)
+    if constexpr (GEN)
+        for (int q = tid; q < 3 * nz; q += NT) ptab[q] = a.L.prof[q];
     const double* diag_s = tab;
     const double* invm_s = tab + nz;
     const double* gim_s = tab + 2 * nz;
@@ -273,13 +276,12 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
         // pointwise work and one Thomas forward-elimination step.
         auto finalize = [&](double up1, double dgk, double imk, double* gslot, int rslot, int km) {
             // (M_T u)_k and the coefficient of the horizontal neighbour sum: -gamma and c in
-            // the flat box; b_k, c_k and c_l d_k with general profiles (GEN, warp-uniform
-            // cached loads)
+            // the flat box; b_k, c_k and c_l d_k with general profiles (GEN, shared memory)
             double Mu, c, sk = -gamma;
             if constexpr (GEN) {
-                sk = __ldg(a.L.prof + km);
-                Mu = fma(sk, um1, fma(__ldg(a.L.prof + nz + km), up1, dgk * u0));
-                c = __ldg(a.L.prof + 2 * nz + km);
+                sk = ptab[km];
+                Mu = fma(sk, um1, fma(ptab[nz + km], up1, dgk * u0));
+                c = ptab[2 * nz + km];
             } else {
                 Mu = fma(-gamma, um1 + up1, dgk * u0);
                 c = c0;
@@ -480,12 +482,12 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 }
 
 template <int MODE, int TY>
-size_t line_smem_bytes(int nz)
+size_t line_smem_bytes(int nz, int gen = 0)
 {
     using T = Traits<MODE>;
     using G = Geom<T::NH, T::NP, TY>;
-    size_t d = ((3 * nz + 15) & ~15) + (size_t)NS * G::STAGE + (T::THOMAS ? (size_t)nz * G::NT : 0) + 64 + 16 +
-               (MODE == MODE_RESTRICT ? 2 * TY * (KB + 1) * (TX / 2) : 0);
+    size_t d = ((3 * nz + 15) & ~15) + (gen ? ((3 * nz + 15) & ~15) : 0) + (size_t)NS * G::STAGE +
+               (T::THOMAS ? (size_t)nz * G::NT : 0) + 64 + 16 + (MODE == MODE_RESTRICT ? 2 * TY * (KB + 1) * (TX / 2) : 0);
     return d * sizeof(double);
 }
 
@@ -494,7 +496,7 @@ constexpr size_t kMaxSmem = 227 * 1024 - 1024;  // leave room for static smem (b
 template <int MODE, int TY, int LOADER, bool GEN>
 cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
 {
-    const size_t smem = line_smem_bytes<MODE, TY>(a.L.nz);
+    const size_t smem = line_smem_bytes<MODE, TY>(a.L.nz, GEN ? 1 : 0);
     auto kern = k_line<MODE, TY, LOADER, GEN>;
     static size_t limit = 0;   // per instantiation
     if (!limit) {
@@ -531,8 +533,8 @@ cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
 template <int MODE>
 cudaError_t launch_line_ty(const Launcher& ln, const LineArgs& a)
 {
-    if (line_smem_bytes<MODE, 4>(a.L.nz) <= kMaxSmem) return launch_line_t<MODE, 4>(ln, a);
-    if (line_smem_bytes<MODE, 2>(a.L.nz) <= kMaxSmem) return launch_line_t<MODE, 2>(ln, a);
+    if (line_smem_bytes<MODE, 4>(a.L.nz, a.L.gen) <= kMaxSmem) return launch_line_t<MODE, 4>(ln, a);
+    if (line_smem_bytes<MODE, 2>(a.L.nz, a.L.gen) <= kMaxSmem) return launch_line_t<MODE, 2>(ln, a);
     return launch_line_t<MODE, 1>(ln, a);
 }
 
@@ -795,15 +797,17 @@ cudaError_t launch_mg_check(const Launcher& ln, const double* norm2, const doubl
 int line_launch_rows(int mode, int nz, int nx, int use_tma, int ksplit_cfg)
 {
     if (use_tma && ksplit_cfg >= 0 && ksplit_supported(mode, nz, nx)) return ksplit_boxes(mode, ksplit_cfg).ty;
-    return line_tile_rows(mode, nz);
+    return line_tile_rows(mode, nz, 0);
 }
 
-int line_tile_rows(int mode, int nz)
+bool line_gen_fits(int nz) { return line_smem_bytes<MODE_CGPREC, 1>(nz, 1) <= kMaxSmem; }
+
+int line_tile_rows(int mode, int nz, int gen)
 {
     switch (mode) {
-    case MODE_PREC: return line_smem_bytes<MODE_PREC, 4>(nz) <= kMaxSmem ? 4 : line_smem_bytes<MODE_PREC, 2>(nz) <= kMaxSmem ? 2 : 1;
-    case MODE_SMOOTH: return line_smem_bytes<MODE_SMOOTH, 4>(nz) <= kMaxSmem ? 4 : line_smem_bytes<MODE_SMOOTH, 2>(nz) <= kMaxSmem ? 2 : 1;
-    case MODE_CGPREC: return line_smem_bytes<MODE_CGPREC, 4>(nz) <= kMaxSmem ? 4 : line_smem_bytes<MODE_CGPREC, 2>(nz) <= kMaxSmem ? 2 : 1;
+    case MODE_PREC: return line_smem_bytes<MODE_PREC, 4>(nz, gen) <= kMaxSmem ? 4 : line_smem_bytes<MODE_PREC, 2>(nz, gen) <= kMaxSmem ? 2 : 1;
+    case MODE_SMOOTH: return line_smem_bytes<MODE_SMOOTH, 4>(nz, gen) <= kMaxSmem ? 4 : line_smem_bytes<MODE_SMOOTH, 2>(nz, gen) <= kMaxSmem ? 2 : 1;
+    case MODE_CGPREC: return line_smem_bytes<MODE_CGPREC, 4>(nz, gen) <= kMaxSmem ? 4 : line_smem_bytes<MODE_CGPREC, 2>(nz, gen) <= kMaxSmem ? 2 : 1;
     default: return 4;
     }
 }

@@ -189,7 +189,8 @@ int line_launch_rows(int mode, int nz, int nx, int use_tma, int ksplit_cfg);
 
 cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a);
 // Tile rows TY the launcher uses for `mode` at this nz (the TMA boxes depend on it).
-int line_tile_rows(int mode, int nz);
+int line_tile_rows(int mode, int nz, int gen = 0);   // gen: general vertical profiles
+bool line_gen_fits(int nz);   // the line kernels' on-chip buffers fit nz with general profiles
 // Largest nz the on-chip Thomas buffer supports.
 int line_max_nz();
 
