@@ -32,9 +32,14 @@ obj = [T.tpmg_nccl_id() if rank == 0 else None]
 dist.broadcast_object_list(obj, src=0)
 nx, ny, nz, L = 64, 64 * world, 16, 5
 BC = int(os.environ.get("TPMG_TEST_BOUNDARY", "0"))   # 1: face Dirichlet [R25]
-P = O.Params(nx=nx, ny=ny, nz=nz, L=L, boundary=BC)
+PROF_SEED = int(os.environ.get("TPMG_TEST_PROFILES", "-1"))   # >= 0: general vertical profiles
+from inputs import vertical_profiles
+PROF = vertical_profiles(nz, PROF_SEED, 300.0) if PROF_SEED >= 0 else None
+P = O.Params(nx=nx, ny=ny, nz=nz, L=L, boundary=BC, profiles=PROF)
 ctx = T.Context(T.make_params(nx, ny, nz=nz, levels=L, boundary=BC), rank=rank, nranks=world, id128=obj[0],
                 device=local)
+if PROF is not None:
+    ctx.set_profiles(*PROF)
 
 
 def strip(x_zc, level):
