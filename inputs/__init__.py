@@ -6,4 +6,4 @@ Lambda index) and the separable Fourier modes
 used to build manufactured fields.  Both the numpy version here and the CUDA
 version in ``splitmix_gpu.cu`` produce bit-identical values.
 """
-from .splitmix import rhs_lambda, rhs_zc, mode_zc, mode_face_zc, vertical_profiles, GOLDEN  # noqa: F401
+from .splitmix import rhs_lambda, rhs_zc, mode_zc, mode_face_zc, vertical_profiles, horizontal_fields, GOLDEN  # noqa: F401

@@ -77,3 +77,34 @@ def vertical_profiles(nz: int, seed: int = 0, coupling: float = 1.0):
     a = 0.5 + 1.5 * u[nz:2 * nz]
     d = 0.5 + 1.5 * u[2 * nz:3 * nz]
     return a, b, c, d
+
+
+def horizontal_fields(nx: int, ny: int, c: float, seed: int = 0, kind: str = "random"):
+    """Seeded synthetic per-column fields of eqn:LocalMatrixStencil (P:255: |T|, alpha_{T,T'}
+    "different for each horizontal grid cell T"), on the finest level:
+    area [ny, nx] = |T|, ax [ny, nx+1] and ay [ny+1, nx] = alpha_{T,T'} of the x- and y-faces
+    (face i of row j lies between columns i-1 and i; faces 0 and nx are boundary faces).
+
+    kind = "random": |T| in [0.5, 2], alpha = -c x [0.25, 4] independently per cell/face
+    (the hardest case for the tests); "smooth": O(1) smooth variations ("geometric
+    factors arising from the spherical geometry will modify this estimate by factors of
+    O(1)"): |T| = 1 + 0.4 sin(2 pi x) sin(2 pi y) and alpha = -c (1 + 0.5 cos(...)) at the
+    face centres.  Pure input generation, no solver arithmetic."""
+    if kind == "random":
+        n_a, n_x, n_y = nx * ny, (nx + 1) * ny, nx * (ny + 1)
+        u = (_mix(np.arange(n_a + n_x + n_y, dtype=np.uint64), seed + 7919) + 1.0) / 2.0   # [0, 1)
+        area = (0.5 + 1.5 * u[:n_a]).reshape(ny, nx)
+        ax = (-c * (0.25 + 3.75 * u[n_a:n_a + n_x])).reshape(ny, nx + 1)
+        ay = (-c * (0.25 + 3.75 * u[n_a + n_x:])).reshape(ny + 1, nx)
+        return area, ax, ay
+    if kind != "smooth":
+        raise ValueError(kind)
+    xc = (np.arange(nx) + 0.5) / nx
+    yc = (np.arange(ny) + 0.5) / ny
+    xf = np.arange(nx + 1) / nx
+    yf = np.arange(ny + 1) / ny
+    ph = 0.1 * seed
+    area = 1.0 + 0.4 * np.sin(2 * np.pi * (yc[:, None] + ph)) * np.sin(2 * np.pi * xc[None, :])
+    ax = -c * (1.0 + 0.5 * np.cos(np.pi * (xf[None, :] + yc[:, None] + ph)))
+    ay = -c * (1.0 + 0.5 * np.cos(np.pi * (xc[None, :] - yf[:, None] + ph)))
+    return area, ax, ay

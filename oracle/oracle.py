@@ -41,7 +41,9 @@ class _Params(C.Structure):
                 ("L", C.c_int), ("pre", C.c_int), ("post", C.c_int),
                 ("coarse_sweeps", C.c_int), ("rho", C.c_double), ("boundary", C.c_int),
                 ("prof_a", C.POINTER(C.c_double)), ("prof_b", C.POINTER(C.c_double)),
-                ("prof_c", C.POINTER(C.c_double)), ("prof_d", C.POINTER(C.c_double))]
+                ("prof_c", C.POINTER(C.c_double)), ("prof_d", C.POINTER(C.c_double)),
+                ("field_area", C.POINTER(C.c_double)), ("field_ax", C.POINTER(C.c_double)),
+                ("field_ay", C.POINTER(C.c_double))]
 
 
 @dataclass
@@ -61,16 +63,34 @@ class Params:
     rho: float = 2.0 / 3.0
     boundary: int = 0   # horizontal Dirichlet reading: 0 ghost zero [R1], 1 face [R25]
     profiles: tuple | None = None   # (a, b, c, d) vertical profiles; None: flat box [R2]
+    # (area [ny, nx], ax [ny, nx+1], ay [ny+1, nx]) per-column |T| and face alpha_{T,T'} of the
+    # finest level; None: the flat box.  Coarser levels: reading [R26].
+    fields: tuple | None = None
 
     def c(self) -> _Params:
         ptrs = [None] * 4
+        fptrs = [None] * 3
+        keep = []
         if self.profiles is not None:
             arrs = [np.ascontiguousarray(x, dtype=np.float64) for x in self.profiles]
             assert all(a.shape == (self.nz,) for a in arrs)
-            self._keep = arrs   # the C struct points into these
+            keep += arrs
             ptrs = [a.ctypes.data_as(C.POINTER(C.c_double)) for a in arrs]
+        if self.fields is not None:
+            shapes = [(self.ny, self.nx), (self.ny, self.nx + 1), (self.ny + 1, self.nx)]
+            arrs = [np.ascontiguousarray(x, dtype=np.float64) for x in self.fields]
+            assert [a.shape for a in arrs] == shapes, [a.shape for a in arrs]
+            keep += arrs
+            fptrs = [a.ctypes.data_as(C.POINTER(C.c_double)) for a in arrs]
+        self._keep = keep   # the C struct points into these
         return _Params(self.nx, self.ny, self.nz, self.nu_cfl, self.H, self.lam, self.L,
-                       self.pre, self.post, self.coarse_sweeps, self.rho, self.boundary, *ptrs)
+                       self.pre, self.post, self.coarse_sweeps, self.rho, self.boundary, *ptrs, *fptrs)
+
+    def flat_fields(self) -> tuple:
+        """The flat box as per-column fields: |T| = 1, alpha_{T,T'} = -c_h on every face."""
+        c = self.c_h()
+        return (np.ones((self.ny, self.nx)), np.full((self.ny, self.nx + 1), -c),
+                np.full((self.ny + 1, self.nx), -c))
 
     def flat_profiles(self) -> tuple:
         """The flat-box profiles [R2] as arrays (a, b, c, d)."""
@@ -125,6 +145,7 @@ def lib():
                             C.POINTER(C.c_int), _dp, C.c_int],
             "or_solve_cg": [P, _dp, _dp, C.c_double, C.c_int, C.POINTER(C.c_int),
                             C.POINTER(C.c_int), _dp, C.c_int],
+            "or_api_level_fields": [P, C.c_int, _dp, _dp, _dp],
             "or_api_num_threads": [],
             "or_api_set_threads": [C.c_int],
         }
@@ -294,6 +315,14 @@ def solve_mg(p: Params, f, eps: float = 1e-5, max_iter: int = 50) -> SolveResult
 def solve_cg(p: Params, f, eps: float = 1e-5, max_iter: int = 1000) -> SolveResult:
     """Line-preconditioned CG, textbook recurrences [R10]."""
     return _solve(lib().or_solve_cg, p, f, eps, max_iter)
+
+
+def level_fields(p: Params, level: int):
+    """(area, ax, ay) of `level` by reading [R26] (block mean of |T|, 8^-s face sums)."""
+    ny, nx, _ = p.level_shape(level)
+    area = np.empty((ny, nx)); ax = np.empty((ny, nx + 1)); ay = np.empty((ny + 1, nx))
+    _check(lib().or_api_level_fields(C.byref(p.c()), level, area, ax, ay), "level_fields")
+    return area, ax, ay
 
 
 def num_threads() -> int:

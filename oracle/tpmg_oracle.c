@@ -67,6 +67,15 @@ typedef struct {
     double alpha_T;   /* alpha_T of an interior column */
     int boundary;     /* 0: ghost-zero Dirichlet [R1]; 1: face Dirichlet [R25] */
     double *a, *b, *c, *d; /* vertical profiles, length nz */
+    /* per-column horizontal fields of this level ("|T|, alpha_{T,T'} and alpha_T are
+     * different for each horizontal grid cell T (and depend on the multigrid level)"), or NULL
+     * for the flat box (the scalars above):
+     *   fa[j*nx + i]      = |T| of column (i,j)
+     *   fx[j*(nx+1) + i]  = alpha_{T,T'} of the x-face between columns (i-1,j) and (i,j),
+     *                       i = 0..nx (faces 0 and nx lie on the boundary)
+     *   fy[j*nx + i]      = alpha_{T,T'} of the y-face between columns (i,j-1) and (i,j),
+     *                       j = 0..ny (faces 0 and ny lie on the boundary) */
+    double *fa, *fx, *fy;
 } or_op;
 
 /* alpha_T of column (i,j) ("alpha_T ... different for each horizontal grid cell").
@@ -75,6 +84,20 @@ typedef struct {
  * omega^2 (0 - u_T)/(h/2), i.e. 2 alpha_{T,T'} per boundary face. */
 static inline double or_alpha_T(const or_op *op, long i, long j)
 {
+    if (op->fa) {   /* per-column fields: alpha_T = sum over the 4 faces of alpha_{T,T'} [R1];
+                     * [R25] counts a boundary face twice */
+        const long nx = op->nx, ny = op->ny;
+        double w = op->fx[j * (nx + 1) + i], e = op->fx[j * (nx + 1) + i + 1];
+        double s = op->fy[j * nx + i], n = op->fy[(j + 1) * nx + i];
+        double aT = w + e + s + n;
+        if (op->boundary) {
+            if (i == 0) aT += w;
+            if (i == nx - 1) aT += e;
+            if (j == 0) aT += s;
+            if (j == ny - 1) aT += n;
+        }
+        return aT;
+    }
     if (!op->boundary) return op->alpha_T;
     int nb = (i == 0) + (i == op->nx - 1) + (j == 0) + (j == op->ny - 1);
     return op->alpha_T + (double)nb * op->alpha_TT;
@@ -102,13 +125,66 @@ typedef struct {
      * NULL: the flat-box values [R2].  Requirements (a symmetric, diagonally dominant
      * column block): b_0 = 0, c_{nz-1} = 0, b_{k+1} = c_k, a >= 0, b <= 0, c <= 0, d > 0. */
     const double *prof_a, *prof_b, *prof_c, *prof_d;
+    /* per-column horizontal fields of the FINEST level, or NULL for the flat box:
+     * field_area[ny][nx] = |T| > 0, field_ax[ny][nx+1] and field_ay[ny+1][nx] = alpha_{T,T'}
+     * <= 0 of the x- and y-faces (layout of or_op.fa/fx/fy, global indices).  Coarser
+     * levels follow reading [R26] (or_op_init). */
+    const double *field_area, *field_ax, *field_ay;
 } or_params;
+
+/* Per-column fields of level l from the finest level's (reading [R26]): with
+ * s = L - l and F = 2^s fine columns per coarse column and direction,
+ *   |T|_l(I,J)        = (1/F^2) sum of |T|_L over the F x F fine columns of (I,J)
+ *                       (the mean: |T| is normalised, the flat box has |T| = 1 on every level),
+ *   alpha_l(x-face I) = 8^-s  sum of alpha_L over the F fine x-faces on that face
+ *   alpha_l(y-face J) = 8^-s  sum of alpha_L over the F fine y-faces on that face.
+ * One level down, a face has 2 fine faces: the mean coefficient (1/2), times the
+ * normalised-area ratio of the rediscretisation (1/4) [R4]; so constant fields |T| = 1,
+ * alpha = -omega^2/h^2 give exactly the flat box's alpha_{T,T'} = -omega^2/h_l^2. */
+static int or_fields_init(const or_params *p, int l, or_op *op)
+{
+    const long F = 1L << (p->L - l), nxf = p->nx, nx = p->nx / F, ny = p->ny / F;
+    if (!p->field_ax || !p->field_ay) return OR_E_PARAM;
+    for (long q = 0; q < nxf * p->ny; ++q)
+        if (!(p->field_area[q] > 0) || !isfinite(p->field_area[q])) return OR_E_PARAM;
+    for (long q = 0; q < (nxf + 1) * p->ny; ++q)
+        if (!(p->field_ax[q] <= 0) || !isfinite(p->field_ax[q])) return OR_E_PARAM;
+    for (long q = 0; q < nxf * (p->ny + 1); ++q)
+        if (!(p->field_ay[q] <= 0) || !isfinite(p->field_ay[q])) return OR_E_PARAM;
+    double scale = 1.0;
+    for (int s = 0; s < p->L - l; ++s) scale /= 8.0;
+    op->fa = (double *)malloc(sizeof(double) * (size_t)(nx * ny));
+    op->fx = (double *)malloc(sizeof(double) * (size_t)((nx + 1) * ny));
+    op->fy = (double *)malloc(sizeof(double) * (size_t)(nx * (ny + 1)));
+    if (!op->fa || !op->fx || !op->fy) return OR_E_OOM;
+    for (long J = 0; J < ny; ++J)
+        for (long I = 0; I < nx; ++I) {
+            double sum = 0.0;
+            for (long b = 0; b < F; ++b)
+                for (long a = 0; a < F; ++a) sum += p->field_area[(J * F + b) * nxf + I * F + a];
+            op->fa[J * nx + I] = sum / (double)(F * F);
+        }
+    for (long J = 0; J < ny; ++J)
+        for (long I = 0; I <= nx; ++I) {
+            double sum = 0.0;
+            for (long b = 0; b < F; ++b) sum += p->field_ax[(J * F + b) * (nxf + 1) + I * F];
+            op->fx[J * (nx + 1) + I] = sum * scale;
+        }
+    for (long J = 0; J <= ny; ++J)
+        for (long I = 0; I < nx; ++I) {
+            double sum = 0.0;
+            for (long a = 0; a < F; ++a) sum += p->field_ay[(J * F) * nxf + I * F + a];
+            op->fy[J * nx + I] = sum * scale;
+        }
+    return OR_OK;
+}
 
 /* Build the operator of level l (1 <= l <= L) by rediscretisation [R4]:
  * the horizontal mesh width on level l is h_l = h * 2^(L-l) (horizontal-only
  * semicoarsening); omega, lambda and h_z are the same on every level. */
 int or_op_init(const or_params *p, int l, or_op *op)
 {
+    memset(op, 0, sizeof(*op));   /* or_op_free is safe after any early return */
     if (p->nx <= 0 || p->ny <= 0 || p->nz <= 0 || p->L <= 0 || l < 1 || l > p->L)
         return OR_E_PARAM;
     if (!(p->nu_cfl > 0) || !(p->H > 0) || !(p->lambda > 0)) return OR_E_PARAM;
@@ -132,7 +208,12 @@ int or_op_init(const or_params *p, int l, or_op *op)
     op->b = (double *)malloc(sizeof(double) * p->nz);
     op->c = (double *)malloc(sizeof(double) * p->nz);
     op->d = (double *)malloc(sizeof(double) * p->nz);
+    op->fa = op->fx = op->fy = NULL;
     if (!op->a || !op->b || !op->c || !op->d) return OR_E_OOM;
+    if (p->field_area) {
+        int st = or_fields_init(p, l, op);
+        if (st != OR_OK) return st;
+    }
     if (p->prof_a) {   /* general vertical profiles ("derived from the vertical
                         * stiffness- and mass-matrices"; the same on every level) */
         if (!p->prof_b || !p->prof_c || !p->prof_d) return OR_E_PARAM;
@@ -162,7 +243,9 @@ int or_op_init(const or_params *p, int l, or_op *op)
 void or_op_free(or_op *op)
 {
     free(op->a); free(op->b); free(op->c); free(op->d);
+    free(op->fa); free(op->fx); free(op->fy);
     op->a = op->b = op->c = op->d = NULL;
+    op->fa = op->fx = op->fy = NULL;
 }
 
 /* ------------------------------------------------------------------------ */
@@ -173,20 +256,31 @@ void or_apply_col(const or_op *op, const double *x, long i, long j, double *ycol
 {
     const int nz = op->nz;
     const int has_w = i > 0, has_e = i < op->nx - 1, has_s = j > 0, has_n = j < op->ny - 1;
+    const double area = op->fa ? op->fa[j * op->nx + i] : op->area;
     for (int k = 0; k < nz; ++k) {
         double xk = x[ZC(op, i, j, k)];
         /* A_T x^(T) */
-        double y = op->area * op->a[k] * xk - or_alpha_T(op, i, j) * op->d[k] * xk
-                 + op->area * (-(op->b[k] + op->c[k])) * xk;
-        if (k > 0) y += op->area * op->b[k] * x[ZC(op, i, j, k - 1)];
-        if (k < nz - 1) y += op->area * op->c[k] * x[ZC(op, i, j, k + 1)];
+        double y = area * op->a[k] * xk - or_alpha_T(op, i, j) * op->d[k] * xk
+                 + area * (-(op->b[k] + op->c[k])) * xk;
+        if (k > 0) y += area * op->b[k] * x[ZC(op, i, j, k - 1)];
+        if (k < nz - 1) y += area * op->c[k] * x[ZC(op, i, j, k + 1)];
         /* sum_{T'} A_{T,T'} x^(T') */
-        double nb = 0.0;
-        if (has_w) nb += x[ZC(op, i - 1, j, k)];
-        if (has_e) nb += x[ZC(op, i + 1, j, k)];
-        if (has_s) nb += x[ZC(op, i, j - 1, k)];
-        if (has_n) nb += x[ZC(op, i, j + 1, k)];
-        y += op->alpha_TT * op->d[k] * nb;
+        if (op->fa) {   /* per-face alpha_{T,T'} */
+            const long nx = op->nx;
+            double nb = 0.0;
+            if (has_w) nb += op->fx[j * (nx + 1) + i] * x[ZC(op, i - 1, j, k)];
+            if (has_e) nb += op->fx[j * (nx + 1) + i + 1] * x[ZC(op, i + 1, j, k)];
+            if (has_s) nb += op->fy[j * nx + i] * x[ZC(op, i, j - 1, k)];
+            if (has_n) nb += op->fy[(j + 1) * nx + i] * x[ZC(op, i, j + 1, k)];
+            y += op->d[k] * nb;
+        } else {
+            double nb = 0.0;
+            if (has_w) nb += x[ZC(op, i - 1, j, k)];
+            if (has_e) nb += x[ZC(op, i + 1, j, k)];
+            if (has_s) nb += x[ZC(op, i, j - 1, k)];
+            if (has_n) nb += x[ZC(op, i, j + 1, k)];
+            y += op->alpha_TT * op->d[k] * nb;
+        }
         ycol[k] = y;
     }
 }
@@ -248,11 +342,12 @@ int or_thomas(int n, const double *s, const double *dg, const double *t, const d
 static void or_block_diagonals(const or_op *op, long i, long j, double *s, double *dg, double *t)
 {
     const double alpha_T = or_alpha_T(op, i, j);
+    const double area = op->fa ? op->fa[j * op->nx + i] : op->area;
     for (int k = 0; k < op->nz; ++k) {
-        s[k] = op->area * op->b[k];
-        t[k] = op->area * op->c[k];
-        dg[k] = op->area * op->a[k] - alpha_T * op->d[k]
-              + op->area * (-(op->b[k] + op->c[k]));
+        s[k] = area * op->b[k];
+        t[k] = area * op->c[k];
+        dg[k] = area * op->a[k] - alpha_T * op->d[k]
+              + area * (-(op->b[k] + op->c[k]));
     }
 }
 
@@ -666,6 +761,22 @@ int or_api_thomas(int n, const double *s, const double *dg, const double *t, con
     if (!work) return OR_E_OOM;
     int st = or_thomas(n, s, dg, t, g, x, work);
     free(work);
+    return st;
+}
+
+/* Per-column fields of level l (reading [R26]); area[ny_l*nx_l], ax[ny_l*(nx_l+1)],
+ * ay[(ny_l+1)*nx_l].  OR_E_PARAM when the parameters carry no fields. */
+int or_api_level_fields(const or_params *p, int l, double *area, double *ax, double *ay)
+{
+    or_op op;
+    int st = or_op_init(p, l, &op);
+    if (st == OR_OK && !op.fa) st = OR_E_PARAM;
+    if (st == OR_OK) {
+        memcpy(area, op.fa, sizeof(double) * (size_t)(op.nx * op.ny));
+        memcpy(ax, op.fx, sizeof(double) * (size_t)((op.nx + 1) * op.ny));
+        memcpy(ay, op.fy, sizeof(double) * (size_t)(op.nx * (op.ny + 1)));
+    }
+    or_op_free(&op);
     return st;
 }
 
