@@ -247,6 +247,29 @@ tpmg_status tpmg_solve_host(tpmg_ctx *ctx, tpmg_solver solver, const double *f_h
 tpmg_status tpmg_set_profiles(tpmg_ctx *ctx, const double *a, const double *b, const double *c,
                               const double *d);
 
+/* Per-column horizontal fields of eqn:LocalMatrixStencil: "the coefficients
+ * alpha_{T,T'} and alpha_T are different for each horizontal grid cell T (and depend on the
+ * multigrid level)", with |T| the (normalised) cell size:
+ *   A_T      = |T| diag(a) - alpha_T diag(d) + |T| tridiag(-(b+c), b, c),
+ *   A_{T,T'} = alpha_{T,T'} diag(d),   alpha_T = sum of the column's 4 face alpha_{T,T'} [R1]
+ *   (the face-Dirichlet reading [R25] counts a boundary face twice).
+ * HOST arrays over the GLOBAL finest level (every rank passes the same arrays; each takes its
+ * strip), row-major, copied:
+ *   area[ny][nx]    |T| > 0 of column (i, j);
+ *   ax[ny][nx+1]    alpha_{T,T'} <= 0 of the x-face between columns (i-1, j) and (i, j);
+ *                   faces 0 and nx are boundary faces (they enter alpha_T only);
+ *   ay[ny+1][nx]    alpha_{T,T'} <= 0 of the y-face between columns (i, j-1) and (i, j).
+ * The flat box is area = 1, ax = ay = -omega^2/h^2.  Coarse levels follow reading [R26]
+ * (DESIGN.md): |T| averages the 2x2 children, a coarse face alpha is 1/8 of the sum of the
+ * two fine faces on it (flat fields reproduce the rediscretisation [R4] exactly).  Works
+ * with the vertical profiles of tpmg_set_profiles (either order).  All NULL: back to
+ * the uniform coefficients.  Errors: TPMG_E_PARAM (missing array, |T| <= 0, alpha > 0, non-
+ * finite values, cp.async loader), TPMG_E_SHAPE (nz too large for the on-chip per-column
+ * Thomas buffers).  Synchronises the context stream.  With fields every line kernel runs the
+ * one-thread-per-column form, which computes each column's Thomas pivots on the fly
+ * (the k-split and fused-prolongation options fall back). */
+tpmg_status tpmg_set_fields(tpmg_ctx *ctx, const double *area, const double *ax, const double *ay);
+
 /* Counters (kernel launches etc.); tpmg_stats_reset zeroes them. */
 tpmg_status tpmg_get_stats(const tpmg_ctx *ctx, tpmg_stats *out);
 tpmg_status tpmg_stats_reset(tpmg_ctx *ctx);

@@ -38,6 +38,8 @@ struct LevelData {
     double* f = nullptr;                // MG right-hand side (coarse levels)
     KTables ktab{};                     // k-split tables (kernel parameter space)
     double* d_prof = nullptr;           // general vertical profiles: [b_k][c_k][c_l d_k] (device)
+    double* d_fprof = nullptr;          // with per-column fields: [a_k-b_k-c_k][b_k][c_k][d_k] (device)
+    double* d_fld = nullptr;            // per-column fields, LevelConst::fld layout (device)
     double* slab_lo = nullptr;          // halo rows j = -1 / j = ny for this level (nranks > 1)
     double* slab_hi = nullptr;
     size_t n() const { return (size_t)lc.nx * (size_t)lc.ny * (size_t)lc.nz; }
@@ -54,6 +56,9 @@ struct tpmg_ctx {
     int L = 0;
     int64_t ny_loc = 0, y0 = 0;
     std::vector<LevelData> lv;  // index 1..L
+    std::vector<double> prof_abcd;   // the vertical profiles a, b, c, d in use (4 nz; set by build_tables)
+    bool fields = false;             // per-column horizontal fields set (tpmg_set_fields)
+    bool gen_profiles = false;       // general vertical profiles set (tpmg_set_profiles)
     // reductions
     double* d_partials = nullptr;
     unsigned* d_ticket = nullptr;
@@ -639,6 +644,8 @@ bool ksplit_usable(tpmg_ctx* ctx, int mode, const LevelConst& lc)
 {
     // general vertical profiles: the k-split smoother / preconditioner / restriction only
     if (lc.gen && (mode == MODE_SMOOTH_PROLONG || mode == MODE_CGPREC)) return false;
+    // per-column fields: the one-thread-per-column kernel only (per-column pivots)
+    if (lc.gen == 2) return false;
     // the k-split CG preconditioner is opt-in (TPMG_KSPLIT_CG=1): measured 4% slower per CG
     // iteration than the one-thread-per-column kernel at 1024^2 x 128
     if (mode == MODE_CGPREC && !ctx->ksplit_cg) return false;
@@ -1328,6 +1335,8 @@ void ctx_free(tpmg_ctx* ctx)
         LevelData& L = ctx->lv[l];
         cudaFree(L.d_tab);
         cudaFree(L.d_prof);
+        cudaFree(L.d_fprof);
+        cudaFree(L.d_fld);
         if ((int)l < ctx->L) { cudaFree(L.u[0]); cudaFree(L.f); }
         cudaFree(L.u[1]);
     }
@@ -1431,6 +1440,30 @@ tpmg_status tpmg_partition(const tpmg_params* params, int32_t rank, int32_t nran
 // One table set per column class (face Dirichlet [R25]: alpha_T = -(4 + nb) c); the
 // ghost-zero reading has class 0 only.  With general profiles the stencil also reads the
 // per-level couplings (b_k, c_k, c_l d_k) from LevelData::d_prof.
+// With per-column fields the line kernels take the profiles raw, [a_k-b_k-c_k][b_k][c_k][d_k]
+// (the same on every level), and the level's fields; lc.gen = 2.
+tpmg_status fields_profile_tables(tpmg_ctx* ctx)
+{
+    const int nz = ctx->p.nz;
+    const double* a = ctx->prof_abcd.data();
+    std::vector<double> t(4 * (size_t)nz);
+    for (int k = 0; k < nz; ++k) {
+        t[k] = a[k] - a[nz + k] - a[2 * nz + k];
+        t[nz + k] = a[nz + k];
+        t[2 * nz + k] = a[2 * nz + k];
+        t[3 * nz + k] = a[3 * nz + k];
+    }
+    for (int l = 1; l <= ctx->L; ++l) {
+        LevelData& L = ctx->lv[l];
+        TRY(dev_alloc(ctx, &L.d_fprof, t.size()));
+        CUDA_TRY(ctx, cudaMemcpy(L.d_fprof, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice));
+        L.lc.prof = L.d_fprof;
+        L.lc.fld = L.d_fld;
+        L.lc.gen = 2;
+    }
+    return TPMG_OK;
+}
+
 tpmg_status build_tables(tpmg_ctx* ctx, const double* const* prof)
 {
     const tpmg_params& p = ctx->p;
@@ -1497,6 +1530,15 @@ tpmg_status build_tables(tpmg_ctx* ctx, const double* const* prof)
         }
         L.lc.prof = prof ? L.d_prof : nullptr;
     }
+    ctx->gen_profiles = prof != nullptr;
+    ctx->prof_abcd.resize(4 * (size_t)nz);
+    for (int k = 0; k < nz; ++k) {
+        ctx->prof_abcd[k] = a[k];
+        ctx->prof_abcd[nz + k] = b[k];
+        ctx->prof_abcd[2 * nz + k] = c[k];
+        ctx->prof_abcd[3 * nz + k] = d[k];
+    }
+    if (ctx->fields) TRY(fields_profile_tables(ctx));
     return TPMG_OK;
 }
 
@@ -1836,6 +1878,87 @@ const char* tpmg_last_error(const tpmg_ctx* ctx)
 
 }  // extern "C"
 
+// Per-column horizontal fields.  Coarse levels by reading [R26]: one level down,
+//   |T|_c(I,J)   = (|T|(2I,2J) + |T|(2I+1,2J) + |T|(2I,2J+1) + |T|(2I+1,2J+1)) / 4,
+//   alpha_c(x-face I of row J) = (alpha(x-face 2I of row 2J) + alpha(x-face 2I of row 2J+1)) / 8,
+//   alpha_c(y-face J of column I) = (alpha(y-face 2J of column 2I) + alpha(y-face 2J of column 2I+1)) / 8
+// (the mean face coefficient times the 1/4 of the rediscretisation [R4]).  alpha_T of a column is
+// the sum of its 4 face alphas [R1]; the face-Dirichlet reading [R25] counts a boundary face twice.
+tpmg_status tpmg_set_fields(tpmg_ctx* ctx, const double* area, const double* ax, const double* ay)
+{
+    if (!ctx) return TPMG_E_PARAM;
+    const int64_t nx = ctx->p.nx, ny = ctx->p.ny;
+    const int nz = ctx->p.nz;
+    if (!area && !ax && !ay) {
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        ctx->fields = false;
+        const double* prof[4] = {ctx->prof_abcd.data(), ctx->prof_abcd.data() + nz, ctx->prof_abcd.data() + 2 * nz,
+                                 ctx->prof_abcd.data() + 3 * nz};
+        const bool flat = !ctx->gen_profiles;
+        for (int l = 1; l <= ctx->L; ++l) ctx->lv[l].lc.fld = nullptr;
+        return build_tables(ctx, flat ? nullptr : prof);
+    }
+    if (!area || !ax || !ay) return fail(ctx, TPMG_E_PARAM, "tpmg_set_fields: give all three fields or none");
+    for (int64_t q = 0; q < nx * ny; ++q)
+        if (!(area[q] > 0) || !std::isfinite(area[q]))
+            return fail(ctx, TPMG_E_PARAM, "tpmg_set_fields: |T| must be positive and finite (column %lld)", (long long)q);
+    for (int64_t q = 0; q < (nx + 1) * ny; ++q)
+        if (!(ax[q] <= 0) || !std::isfinite(ax[q]))
+            return fail(ctx, TPMG_E_PARAM, "tpmg_set_fields: x-face alpha must be <= 0 and finite (face %lld)", (long long)q);
+    for (int64_t q = 0; q < nx * (ny + 1); ++q)
+        if (!(ay[q] <= 0) || !std::isfinite(ay[q]))
+            return fail(ctx, TPMG_E_PARAM, "tpmg_set_fields: y-face alpha must be <= 0 and finite (face %lld)", (long long)q);
+    if (!ctx->use_tma) return fail(ctx, TPMG_E_PARAM, "tpmg_set_fields: per-column fields need the TMA loader");
+    if (!line_gen_fits(nz, 2)) return fail(ctx, TPMG_E_SHAPE, "tpmg_set_fields: nz = %d too large for per-column fields", nz);
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));   // queued kernels may still read the fields
+    // global fields of the current level, finest first
+    std::vector<double> A(area, area + nx * ny), X(ax, ax + (nx + 1) * ny), Y(ay, ay + nx * (ny + 1));
+    int64_t gx = nx, gy = ny;
+    const bool face = ctx->p.boundary == TPMG_BC_FACE;
+    for (int l = ctx->L; l >= 1; --l) {
+        LevelData& L = ctx->lv[l];
+        const int64_t lnx = L.lc.nx, lny = L.lc.ny, y0 = ctx->y0 >> (ctx->L - l), ncol = lnx * lny;
+        std::vector<double> F(6 * (size_t)ncol);
+        for (int64_t j = 0; j < lny; ++j)
+            for (int64_t i = 0; i < lnx; ++i) {
+                const int64_t J = y0 + j, c = j * lnx + i;
+                const double w = X[J * (gx + 1) + i], e = X[J * (gx + 1) + i + 1];
+                const double s = Y[J * gx + i], n = Y[(J + 1) * gx + i];
+                double aT = (w + e) + (s + n);
+                if (face) aT += (i == 0 ? w : 0.0) + (i == gx - 1 ? e : 0.0) + (J == 0 ? s : 0.0) + (J == gy - 1 ? n : 0.0);
+                F[c] = A[J * gx + i];
+                F[ncol + c] = aT;
+                F[2 * ncol + c] = w;
+                F[3 * ncol + c] = e;
+                F[4 * ncol + c] = s;
+                F[5 * ncol + c] = n;
+            }
+        TRY(dev_alloc(ctx, &L.d_fld, F.size()));
+        CUDA_TRY(ctx, cudaMemcpy(L.d_fld, F.data(), sizeof(double) * F.size(), cudaMemcpyHostToDevice));
+        if (l > 1) {   // [R26] one level down
+            const int64_t cx = gx / 2, cy = gy / 2;
+            std::vector<double> Ac(cx * cy), Xc((cx + 1) * cy), Yc(cx * (cy + 1));
+            for (int64_t J = 0; J < cy; ++J)
+                for (int64_t I = 0; I < cx; ++I)
+                    Ac[J * cx + I] = 0.25 * ((A[(2 * J) * gx + 2 * I] + A[(2 * J) * gx + 2 * I + 1]) +
+                                             (A[(2 * J + 1) * gx + 2 * I] + A[(2 * J + 1) * gx + 2 * I + 1]));
+            for (int64_t J = 0; J < cy; ++J)
+                for (int64_t I = 0; I <= cx; ++I)
+                    Xc[J * (cx + 1) + I] = 0.125 * (X[(2 * J) * (gx + 1) + 2 * I] + X[(2 * J + 1) * (gx + 1) + 2 * I]);
+            for (int64_t J = 0; J <= cy; ++J)
+                for (int64_t I = 0; I < cx; ++I)
+                    Yc[J * cx + I] = 0.125 * (Y[(2 * J) * gx + 2 * I] + Y[(2 * J) * gx + 2 * I + 1]);
+            A.swap(Ac);
+            X.swap(Xc);
+            Y.swap(Yc);
+            gx = cx;
+            gy = cy;
+        }
+    }
+    ctx->fields = true;
+    return fields_profile_tables(ctx);
+}
+
 tpmg_status tpmg_set_profiles(tpmg_ctx* ctx, const double* a, const double* b, const double* c, const double* d)
 {
     if (!ctx) return TPMG_E_PARAM;
@@ -1852,6 +1975,8 @@ tpmg_status tpmg_set_profiles(tpmg_ctx* ctx, const double* a, const double* b, c
             return fail(ctx, TPMG_E_PARAM, "tpmg_set_profiles: b[0] and c[nz-1] must be 0 (no coupling outside the column)");
         if (!ctx->use_tma) return fail(ctx, TPMG_E_PARAM, "tpmg_set_profiles: general profiles need the TMA loader");
         if (!line_gen_fits(nz)) return fail(ctx, TPMG_E_SHAPE, "tpmg_set_profiles: nz = %d too large for general profiles", nz);
+        if (ctx->fields && !line_gen_fits(nz, 2))
+            return fail(ctx, TPMG_E_SHAPE, "tpmg_set_profiles: nz = %d too large for per-column fields", nz);
     }
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));   // queued kernels may still read the tables
     const double* prof[4] = {a, b, c, d};

@@ -137,7 +137,12 @@ __device__ __forceinline__ void tma_stage(double* st, const LineArgs& a, int64_t
 // mbarrier per stage.  The CTA walks its tiles (tile = blockIdx.x + t*gridDim.x)
 // as one global sequence of KB-level chunks, so the loads of the next tile's
 // first chunks overlap the current tile's backward sweep.
-template <int MODE, int TY, int LOADER, bool GEN>
+// GEN: 0 flat box, 1 general vertical profiles, 2 per-column horizontal fields (|T|, alpha_T
+// and the 4 face alpha_{T,T'} of every column; profiles a, b, c, d as well).  With
+// fields the Thomas factors differ from column to column: the forward sweep computes the
+// pivot m_k of its own column (one division per cell) and keeps -t'_k = -t_k/m_k next to g'_k
+// in shared memory (16 * nz bytes per column).
+template <int MODE, int TY, int LOADER, int GEN>
 __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArgs a)
 {
     using T = Traits<MODE>;
@@ -153,19 +158,21 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     const int nz = a.L.nz;
     const int64_t nx = a.L.nx, ny = a.L.ny;
     const int tabn = (3 * nz + 15) & ~15;    // keep the stages 128-byte aligned
+    const int ptn = (GEN == 2) ? ((4 * nz + 15) & ~15) : tabn;
     double* tab = smem;                      // diag[nz], invm[nz], gim[nz]
-    double* ptab = smem + tabn;              // GEN: b_k[nz], c_k[nz], c_l d_k[nz]
-    double* stage = ptab + (GEN ? tabn : 0); // NS stages
-    double* gbuf = stage + NS * G::STAGE;    // g'[nz][NT] (Thomas modes)
+    double* ptab = smem + tabn;              // GEN 1: b_k, c_k, c_l d_k; GEN 2: a_k-b_k-c_k, b_k, c_k, d_k
+    double* stage = ptab + (GEN ? ptn : 0);  // NS stages
+    double* gbuf = stage + NS * G::STAGE;    // g'[nz][NT] (Thomas modes); GEN 2: then -t'[nz][NT]
+    constexpr int NBUF = (GEN == 2) ? 2 : 1;
     // MODE_RESTRICT: x-pair sums [2][TY][KB+1][TX/2] (a chunk completes up to KB+1 levels)
     constexpr int RS = KB + 1;
-    double* rbuf = gbuf + (T::THOMAS ? nz * NT : 0);
+    double* rbuf = gbuf + (T::THOMAS ? NBUF * nz * NT : 0);
     double* scratch = rbuf + (MODE == MODE_RESTRICT ? 2 * TY * RS * (TX / 2) : 0);  // reduction scratch
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     for (int q = tid; q < 3 * nz; q += NT) tab[q] = a.L.tab[q];   // interior class (0)
-    if constexpr (GEN)
-        for (int q = tid; q < 3 * nz; q += NT) ptab[q] = a.L.prof[q];
+    if constexpr (GEN != 0)
+        for (int q = tid; q < (GEN == 2 ? 4 : 3) * nz; q += NT) ptab[q] = a.L.prof[q];
     const double* diag_s = tab;
     const double* invm_s = tab + nz;
     const double* gim_s = tab + 2 * nz;
@@ -263,6 +270,21 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
         const double* diag = BND ? ctab : diag_s;
         const double* invm = BND ? ctab + nz : invm_s;
         const double* gim = BND ? ctab + 2 * nz : gim_s;
+        // GEN 2: this column's |T|, alpha_T and face alpha_{T,T'} (W, E, S, N), fields SoA
+        // [6][ny][nx] (a phantom column of a ragged tile gets |T| = 1 and no couplings)
+        double fT = 1.0, faT = 0.0, fw = 0.0, fe = 0.0, fs = 0.0, fn = 0.0, tprev = 0.0;
+        if constexpr (GEN == 2) {
+            if (valid) {
+                const int64_t ncol = nx * ny, cc = j * nx + i;
+                const double* F = a.L.fld + cc;
+                fT = __ldg(F);
+                faT = __ldg(F + ncol);
+                fw = __ldg(F + 2 * ncol);
+                fe = __ldg(F + 3 * ncol);
+                fs = __ldg(F + 4 * ncol);
+                fn = __ldg(F + 5 * ncol);
+            }
+        }
 
         // rolling state for the k-lag: values at level km = k-1 and km-1
         double um1 = 0.0, u0 = 0.0, S0 = 0.0, qa = 0.0, qb = 0.0, gprev = 0.0;
@@ -277,8 +299,15 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
         auto finalize = [&](double up1, double dgk, double imk, double* gslot, int rslot, int km) {
             // (M_T u)_k and the coefficient of the horizontal neighbour sum: -gamma and c in
             // the flat box; b_k, c_k and c_l d_k with general profiles (GEN, shared memory)
-            double Mu, c, sk = -gamma;
-            if constexpr (GEN) {
+            double Mu, c, sk = -gamma, tk = 0.0;
+            if constexpr (GEN == 2) {
+                // A_T = |T| (diag(a) + tridiag(-(b+c), b, c)) - alpha_T diag(d)
+                sk = fT * ptab[nz + km];
+                tk = fT * ptab[2 * nz + km];
+                dgk = fma(fT, ptab[km], -faT * ptab[3 * nz + km]);
+                Mu = fma(sk, um1, fma(tk, up1, dgk * u0));
+                c = -ptab[3 * nz + km];   // A u = M_T u + d_k sum_T' alpha_TT' u_T'
+            } else if constexpr (GEN == 1) {
                 sk = ptab[km];
                 Mu = fma(sk, um1, fma(ptab[nz + km], up1, dgk * u0));
                 c = ptab[2 * nz + km];
@@ -332,6 +361,12 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 if constexpr (MODE == MODE_CGPREC) ofw1 += nx;
             }
             if constexpr (T::THOMAS) {
+                if constexpr (GEN == 2) {
+                    // this column's pivot: m_k = diag_k - s_k t'_{k-1}, t'_k = t_k / m_k
+                    imk = 1.0 / fma(-sk, tprev, dgk);
+                    tprev = tk * imk;
+                    gslot[nz * NT] = -tprev;
+                }
                 const double y = fma(-sk, gprev, g);     // y = L^-1 g   (M = L D L^T; sub-diagonal s_k)
                 const double gp = y * imk;               // g'_k = (g_k - s_k g'_{k-1}) / m_k
                 *gslot = gp;
@@ -355,11 +390,18 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 if constexpr (NH >= 1) {
                     const double* h = hp + kk * G::HX;
                     ecv[kk] = h[0];
-                    Sv[kk] = (h[-1] + h[1]) + (h[-G::HALO_ROW] + h[G::HALO_ROW]);
+                    // neighbour sum; GEN 2: weighted by the face alpha_{T,T'}
+                    auto nsum = [&](const double* q) {
+                        if constexpr (GEN == 2)
+                            return fma(fw, q[-1], fe * q[1]) + fma(fs, q[-G::HALO_ROW], fn * q[G::HALO_ROW]);
+                        else
+                            return (q[-1] + q[1]) + (q[-G::HALO_ROW] + q[G::HALO_ROW]);
+                    };
+                    Sv[kk] = nsum(h);
                     if constexpr (MODE == MODE_CGDIR) {
                         const double* p = h + G::HY * G::HALO_ROW;  // field 1 = p_old
                         ecv[kk] = fma(ratio, p[0], ecv[kk]);
-                        Sv[kk] = fma(ratio, (p[-1] + p[1]) + (p[-G::HALO_ROW] + p[G::HALO_ROW]), Sv[kk]);
+                        Sv[kk] = fma(ratio, nsum(p), Sv[kk]);
                     }
                 }
                 if constexpr (NP >= 1) pav[kk] = pp[kk * TX];
@@ -431,7 +473,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
                     gv[q] = gq[(KB - 1 - q) * NT];
-                    gm[q] = mq[KB - 1 - q];
+                    gm[q] = (GEN == 2) ? gq[nz * NT + (KB - 1 - q) * NT] : mq[KB - 1 - q];
                 }
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
@@ -441,7 +483,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 }
             }
             for (; k >= 0; --k) {
-                x = fma(gim[k], x, gbuf[k * NT + tid]);
+                x = fma((GEN == 2) ? gbuf[(nz + k) * NT + tid] : gim[k], x, gbuf[k * NT + tid]);
                 if (valid) *op = x;
                 op -= nx;
             }
@@ -472,7 +514,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     };
     for (int tl = 0; tl < my_tiles; ++tl) {
         const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
-        if (tile_on_boundary(a.L, (int64_t)(tile % ntx) * TX, (int64_t)row_of(tile) * TY, TX, TY))
+        if (GEN != 2 && tile_on_boundary(a.L, (int64_t)(tile % ntx) * TX, (int64_t)row_of(tile) * TY, TX, TY))
             tile_body(std::true_type{}, tl);
         else
             tile_body(std::false_type{}, tl);
@@ -486,17 +528,18 @@ size_t line_smem_bytes(int nz, int gen = 0)
 {
     using T = Traits<MODE>;
     using G = Geom<T::NH, T::NP, TY>;
-    size_t d = ((3 * nz + 15) & ~15) + (gen ? ((3 * nz + 15) & ~15) : 0) + (size_t)NS * G::STAGE +
-               (T::THOMAS ? (size_t)nz * G::NT : 0) + 64 + 16 + (MODE == MODE_RESTRICT ? 2 * TY * (KB + 1) * (TX / 2) : 0);
+    size_t d = ((3 * nz + 15) & ~15) + (gen == 2 ? ((4 * nz + 15) & ~15) : gen ? ((3 * nz + 15) & ~15) : 0) +
+               (size_t)NS * G::STAGE + (T::THOMAS ? (size_t)(gen == 2 ? 2 : 1) * nz * G::NT : 0) + 64 + 16 +
+               (MODE == MODE_RESTRICT ? 2 * TY * (KB + 1) * (TX / 2) : 0);
     return d * sizeof(double);
 }
 
 constexpr size_t kMaxSmem = 227 * 1024 - 1024;  // leave room for static smem (barriers, flags)
 
-template <int MODE, int TY, int LOADER, bool GEN>
+template <int MODE, int TY, int LOADER, int GEN>
 cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
 {
-    const size_t smem = line_smem_bytes<MODE, TY>(a.L.nz, GEN ? 1 : 0);
+    const size_t smem = line_smem_bytes<MODE, TY>(a.L.nz, GEN);
     auto kern = k_line<MODE, TY, LOADER, GEN>;
     static size_t limit = 0;   // per instantiation
     if (!limit) {
@@ -523,11 +566,11 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
 template <int MODE, int TY>
 cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
 {
-    if (a.L.gen) {   // general vertical profiles: TMA loader only
+    if (a.L.gen) {   // general vertical profiles / per-column fields: TMA loader only
         if (!a.use_tma) return cudaErrorNotSupported;
-        return launch_line_l<MODE, TY, 1, true>(ln, a);
+        return a.L.gen == 2 ? launch_line_l<MODE, TY, 1, 2>(ln, a) : launch_line_l<MODE, TY, 1, 1>(ln, a);
     }
-    return a.use_tma ? launch_line_l<MODE, TY, 1, false>(ln, a) : launch_line_l<MODE, TY, 0, false>(ln, a);
+    return a.use_tma ? launch_line_l<MODE, TY, 1, 0>(ln, a) : launch_line_l<MODE, TY, 0, 0>(ln, a);
 }
 
 template <int MODE>
@@ -800,7 +843,7 @@ int line_launch_rows(int mode, int nz, int nx, int use_tma, int ksplit_cfg)
     return line_tile_rows(mode, nz, 0);
 }
 
-bool line_gen_fits(int nz) { return line_smem_bytes<MODE_CGPREC, 1>(nz, 1) <= kMaxSmem; }
+bool line_gen_fits(int nz, int gen) { return line_smem_bytes<MODE_CGPREC, 1>(nz, gen) <= kMaxSmem; }
 
 int line_tile_rows(int mode, int nz, int gen)
 {

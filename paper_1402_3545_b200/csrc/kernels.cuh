@@ -29,8 +29,13 @@ struct LevelConst {
     const double* tab;  // device: per column class [diag, invm, gim, afw, P, Q][nz] (Thomas factors of M_T)
     int32_t bc;         // tpmg_boundary: 0 ghost-zero [R1] (class 0 only), 1 face Dirichlet [R25]
     int32_t bnd_lo, bnd_hi;   // local row 0 / ny-1 lies on the physical boundary
-    int32_t gen;        // 1: general vertical profiles (stencil couplings from prof, not gamma / c)
-    const double* prof; // device, gen only: [b_k][c_k][c_l d_k], nz each
+    int32_t gen;        // 1: general vertical profiles (stencil couplings from prof, not gamma / c);
+                        // 2: per-column horizontal fields (fld) with the profiles a, b, c, d
+    const double* prof; // device, gen 1: [b_k][c_k][c_l d_k]; gen 2: [a_k-b_k-c_k][b_k][c_k][d_k];
+                        // nz each
+    const double* fld;  // device, gen 2: [|T|][alpha_T][alpha_W][alpha_E][alpha_S][alpha_N], each
+                        // [ny][nx] over the local columns ("different for each horizontal
+                        // grid cell T (and depend on the multigrid level)")
 };
 
 // Column classes of the face-Dirichlet reading: nb = number of boundary faces (0..4).
@@ -190,7 +195,7 @@ int line_launch_rows(int mode, int nz, int nx, int use_tma, int ksplit_cfg);
 cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a);
 // Tile rows TY the launcher uses for `mode` at this nz (the TMA boxes depend on it).
 int line_tile_rows(int mode, int nz, int gen = 0);   // gen: general vertical profiles
-bool line_gen_fits(int nz);   // the line kernels' on-chip buffers fit nz with general profiles
+bool line_gen_fits(int nz, int gen = 1);   // the line kernels' on-chip buffers fit nz (gen 1: profiles, 2: fields)
 // Largest nz the on-chip Thomas buffer supports.
 int line_max_nz();
 

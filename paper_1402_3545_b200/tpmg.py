@@ -75,6 +75,7 @@ _SIGS = {
     "tpmg_profile": ([_vp, _i32], C.c_int),
     "tpmg_profile_mask": ([_vp, C.c_uint32], C.c_int),
     "tpmg_set_profiles": ([_vp, _P(_d), _P(_d), _P(_d), _P(_d)], C.c_int),
+    "tpmg_set_fields": ([_vp, _P(_d), _P(_d), _P(_d)], C.c_int),
     "tpmg_profile_read": ([_vp, _i32, _P(_i64), _P(_d), _P(_d)], C.c_int),
     "tpmg_last_error": ([_vp], C.c_char_p),
 }
@@ -267,6 +268,21 @@ def tpmg_set_profiles(ctx: int, a=None, b=None, c=None, d=None) -> None:
     _check(_lib.tpmg_set_profiles(ctx, *ptrs), ctx)
 
 
+def tpmg_set_fields(ctx: int, area=None, ax=None, ay=None) -> None:
+    """Per-column fields |T| [ny, nx], x-face alpha [ny, nx+1], y-face alpha [ny+1, nx] of the
+    global finest level (host float64), or all None for the uniform coefficients."""
+    if area is None:
+        _check(_lib.tpmg_set_fields(ctx, None, None, None), ctx)
+        return
+    import numpy as np
+    arrs = [np.ascontiguousarray(x, dtype=np.float64) for x in (area, ax, ay)]
+    ny, nx = arrs[0].shape
+    if arrs[1].shape != (ny, nx + 1) or arrs[2].shape != (ny + 1, nx):
+        raise ValueError(f"field shapes {[a.shape for a in arrs]} do not match [ny, nx], [ny, nx+1], [ny+1, nx]")
+    ptrs = [x.ctypes.data_as(_P(_d)) for x in arrs]
+    _check(_lib.tpmg_set_fields(ctx, *ptrs), ctx)
+
+
 def tpmg_profile_mask(ctx: int, mask: int) -> None:
     _check(_lib.tpmg_profile_mask(ctx, mask), ctx)
 
@@ -373,6 +389,9 @@ class Context:
 
     def set_profiles(self, a=None, b=None, c=None, d=None):
         tpmg_set_profiles(self.handle, a, b, c, d)
+
+    def set_fields(self, area=None, ax=None, ay=None):
+        tpmg_set_fields(self.handle, area, ax, ay)
 
     def profile(self, enable: bool, classes=None):
         """Event-time every kernel class (enable), or only the named classes."""

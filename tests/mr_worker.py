@@ -23,6 +23,8 @@ failures = []
 
 
 def check(name, got, want, tol):
+    if os.environ.get("TPMG_TEST_FIELDS", "-1") != "-1":
+        tol = max(tol, 2e-10)   # random fields: kappa(M_T) ~ 1e5 (tests/test_gpu_parity_fields.py tol)
     err = np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-300)
     if not err < tol:
         failures.append(f"rank {rank}: {name} rel err {err:.3e} >= {tol}")
@@ -35,11 +37,17 @@ BC = int(os.environ.get("TPMG_TEST_BOUNDARY", "0"))   # 1: face Dirichlet [R25]
 PROF_SEED = int(os.environ.get("TPMG_TEST_PROFILES", "-1"))   # >= 0: general vertical profiles
 from inputs import vertical_profiles
 PROF = vertical_profiles(nz, PROF_SEED, 300.0) if PROF_SEED >= 0 else None
-P = O.Params(nx=nx, ny=ny, nz=nz, L=L, boundary=BC, profiles=PROF)
+FIELD_SEED = int(os.environ.get("TPMG_TEST_FIELDS", "-1"))   # >= 0: per-column fields (tpmg_set_fields)
+from inputs import horizontal_fields
+FIELDS = (horizontal_fields(nx, ny, O.Params(nx=nx, ny=ny, nz=nz, L=L).c_h(), FIELD_SEED)
+          if FIELD_SEED >= 0 else None)
+P = O.Params(nx=nx, ny=ny, nz=nz, L=L, boundary=BC, profiles=PROF, fields=FIELDS)
 ctx = T.Context(T.make_params(nx, ny, nz=nz, levels=L, boundary=BC), rank=rank, nranks=world, id128=obj[0],
                 device=local)
 if PROF is not None:
     ctx.set_profiles(*PROF)
+if FIELDS is not None:
+    ctx.set_fields(*FIELDS)
 
 
 def strip(x_zc, level):
