@@ -64,6 +64,9 @@ def parse():
     ap.add_argument("--profiles", type=int, default=-1,
                     help="general vertical profiles (inputs.vertical_profiles with this seed, couplings of "
                          "the flat box's size); -1: flat box")
+    ap.add_argument("--fields", choices=["none", "random", "smooth"], default="none",
+                    help="per-column horizontal fields |T|, alpha_TT' (inputs.horizontal_fields, seed 1; "
+                         "tpmg_set_fields): none = uniform coefficients")
     ap.add_argument("--global-nx", type=int, default=0,
                     help="strong scaling: a fixed global nx x nx x nz grid split into y-strips (4096 = configs[4])")
     return ap.parse_args()
@@ -164,7 +167,21 @@ def bench_profiles(args):
     return vertical_profiles(args.nz, args.profiles, gamma)
 
 
-def oracle_sample(nx, nz, nu, rows, seed, threads=None, levels=5, coarse_sweeps=2, boundary=0, profiles=None):
+def bench_fields(args, nx, ny):
+    """--fields: seeded per-column fields (inputs.horizontal_fields) of the global grid, alpha of
+    the size of the flat box's c_h = nu^2/4."""
+    if args.fields == "none":
+        return None
+    from inputs import horizontal_fields
+    return horizontal_fields(nx, ny, args.nu * args.nu / 4.0, 1, args.fields)
+
+
+def strip_fields(fields, rows):
+    return None if fields is None else (fields[0][:rows], fields[1][:rows], fields[2][:rows + 1])
+
+
+def oracle_sample(nx, nz, nu, rows, seed, threads=None, levels=5, coarse_sweeps=2, boundary=0, profiles=None,
+                  fields=None):
     """Time the CPU oracle (as it stands) on a y-strip of `rows` rows of the workload:
     one MG V-cycle (solve_mg, max_iter=1: norm + V-cycle + residual) and one PCG
     iteration (solve_cg, max_iter=1: setup preconditioner + one iteration)."""
@@ -173,7 +190,7 @@ def oracle_sample(nx, nz, nu, rows, seed, threads=None, levels=5, coarse_sweeps=
     if threads:
         O.set_threads(threads)
     p = O.Params(nx=nx, ny=rows, nz=nz, nu_cfl=nu, L=levels, coarse_sweeps=coarse_sweeps, boundary=boundary,
-                 profiles=profiles)
+                 profiles=profiles, fields=fields)
     f = rhs_zc(nx, rows, nz, seed=seed)
     t0 = time.perf_counter()
     O.solve_mg(p, f, eps=1e-30, max_iter=1)
@@ -192,17 +209,18 @@ def run_reference(args):
     rows = max(32, 1 << (args.levels - 1))
     scale = ny / rows
     it_mg, it_cg = 9, 51  # iteration counts of the oracle at 128^2 x 128 (tests/test_oracle_pins)
+    flds = strip_fields(bench_fields(args, nx, ny), rows)
     for _ in range(args.warmup):
         oracle_sample(nx, args.nz, args.nu, rows, args.seed, levels=args.levels,
                      coarse_sweeps=args.coarse_sweeps, boundary=args.boundary,
-                     profiles=bench_profiles(args))
+                     profiles=bench_profiles(args), fields=flds)
     t = 0.0
     wall = 0.0
     for _ in range(args.steps):
         w0 = time.perf_counter()
         a, b, cores = oracle_sample(nx, args.nz, args.nu, rows, args.seed, levels=args.levels,
                      coarse_sweeps=args.coarse_sweeps, boundary=args.boundary,
-                     profiles=bench_profiles(args))
+                     profiles=bench_profiles(args), fields=flds)
         wall += time.perf_counter() - w0
         t += scale * (it_mg * a + it_cg * b)
     N = nx * ny * args.nz
@@ -256,6 +274,9 @@ def main():
     prof = bench_profiles(args)
     if prof is not None:
         ctx.set_profiles(*prof)
+    flds = bench_fields(args, nx, ny)
+    if flds is not None:
+        ctx.set_fields(*flds)
     shape = ctx.shape(args.levels)
     f = torch.empty(shape, dtype=torch.float64, device=f"cuda:{local}")
     u = torch.empty_like(f)
@@ -389,7 +410,7 @@ def main():
         rows = max(128, 1 << (args.levels - 1))
         a, b, cores = oracle_sample(nx, nz, args.nu, rows, args.seed, levels=args.levels,
                                        coarse_sweeps=args.coarse_sweeps, boundary=args.boundary,
-                     profiles=bench_profiles(args))
+                     profiles=bench_profiles(args), fields=strip_fields(flds, rows))
         scale = ny / rows
         it_mg = its[0].iterations if its[0] else 0
         it_cg = its[1].iterations if its[1] else 0
@@ -408,6 +429,7 @@ def main():
             "config": {"workload": name, "nx": nx, "ny": ny, "nz": nz, "nu_cfl": args.nu, "eps": args.eps,
                        "levels": args.levels, "coarse_sweeps": args.coarse_sweeps, "boundary": args.boundary,
                        "vertical_profiles": "flat box" if args.profiles < 0 else f"synthetic seed {args.profiles}",
+                       "horizontal_fields": "uniform" if args.fields == "none" else f"{args.fields} seed 1",
                        "parallelism": f"y-strips x{world}" if world > 1 else "single GPU",
                        "l2": "vectors 1 GiB/GPU >> 126 MB L2 (no flush needed)"},
             "roofline": roof,

@@ -140,8 +140,12 @@ __device__ __forceinline__ void tma_stage(double* st, const LineArgs& a, int64_t
 // GEN: 0 flat box, 1 general vertical profiles, 2 per-column horizontal fields (|T|, alpha_T
 // and the 4 face alpha_{T,T'} of every column; profiles a, b, c, d as well).  With
 // fields the Thomas factors differ from column to column: the forward sweep computes the
-// pivot m_k of its own column (one division per cell) and keeps -t'_k = -t_k/m_k next to g'_k
-// in shared memory (16 * nz bytes per column).
+// pivots of its own column through the leading principal minors, p_k = diag_k p_{k-1} -
+// s_k t_{k-1} p_{k-2}, m_k = p_k / p_{k-1} (a linear recurrence: one FMA per level on the
+// dependency chain, the division 1/m_k = p_{k-1}/p_k off it), renormalised at every KB-th level
+// to (p_{k-1}, p_{k-2}) = (m_{k-1}, 1), and checkpoints m_{k-1} there next to g'_k in shared
+// memory ((nz + nz/KB) * 8 bytes per column).  The backward sweep recomputes each chunk's
+// pivots from its checkpoint with the same arithmetic instead of keeping all nz on chip.
 template <int MODE, int TY, int LOADER, int GEN>
 __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArgs a)
 {
@@ -162,11 +166,12 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     double* tab = smem;                      // diag[nz], invm[nz], gim[nz]
     double* ptab = smem + tabn;              // GEN 1: b_k, c_k, c_l d_k; GEN 2: a_k-b_k-c_k, b_k, c_k, d_k
     double* stage = ptab + (GEN ? ptn : 0);  // NS stages
-    double* gbuf = stage + NS * G::STAGE;    // g'[nz][NT] (Thomas modes); GEN 2: then -t'[nz][NT]
-    constexpr int NBUF = (GEN == 2) ? 2 : 1;
+    double* gbuf = stage + NS * G::STAGE;    // g'[nz][NT] (Thomas modes)
+    const int nck = (nz + KB - 1) / KB;
+    double* cbuf = gbuf + nz * NT;           // GEN 2: t'_{c KB - 1}[nck][NT], the pivot checkpoints
     // MODE_RESTRICT: x-pair sums [2][TY][KB+1][TX/2] (a chunk completes up to KB+1 levels)
     constexpr int RS = KB + 1;
-    double* rbuf = gbuf + (T::THOMAS ? NBUF * nz * NT : 0);
+    double* rbuf = gbuf + (T::THOMAS ? (nz + (GEN == 2 ? nck : 0)) * NT : 0);
     double* scratch = rbuf + (MODE == MODE_RESTRICT ? 2 * TY * RS * (TX / 2) : 0);  // reduction scratch
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
@@ -272,7 +277,20 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
         const double* gim = BND ? ctab + 2 * nz : gim_s;
         // GEN 2: this column's |T|, alpha_T and face alpha_{T,T'} (W, E, S, N), fields SoA
         // [6][ny][nx] (a phantom column of a ragged tile gets |T| = 1 and no couplings)
-        double fT = 1.0, faT = 0.0, fw = 0.0, fe = 0.0, fs = 0.0, fn = 0.0, tprev = 0.0;
+        double fT = 1.0, faT = 0.0, fw = 0.0, fe = 0.0, fs = 0.0, fn = 0.0;
+        double pm1 = 1.0, pm2 = 0.0, tkm1 = 0.0;   // GEN 2 pivot state: p_{k-1}, p_{k-2}, t_{k-1}
+        // GEN 2: one step of the minor recurrence at level k, returns 1/m_k (S:267's pivot)
+        auto pivot_step = [&](int k, double& p1, double& p2, double& t1) {
+            const double sk = fT * ptab[nz + k];
+            const double tk = fT * ptab[2 * nz + k];
+            const double dgk = fma(fT, ptab[k], -faT * ptab[3 * nz + k]);
+            const double p = fma(dgk, p1, -(sk * t1) * p2);
+            const double im = p1 / p;
+            p2 = p1;
+            p1 = p;
+            t1 = tk;
+            return im;
+        };
         if constexpr (GEN == 2) {
             if (valid) {
                 const int64_t ncol = nx * ny, cc = j * nx + i;
@@ -363,9 +381,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             if constexpr (T::THOMAS) {
                 if constexpr (GEN == 2) {
                     // this column's pivot: m_k = diag_k - s_k t'_{k-1}, t'_k = t_k / m_k
-                    imk = 1.0 / fma(-sk, tprev, dgk);
-                    tprev = tk * imk;
-                    gslot[nz * NT] = -tprev;
+                    imk = pivot_step(km, pm1, pm2, tkm1);
                 }
                 const double y = fma(-sk, gprev, g);     // y = L^-1 g   (M = L D L^T; sub-diagonal s_k)
                 const double gp = y * imk;               // g'_k = (g_k - s_k g'_{k-1}) / m_k
@@ -417,6 +433,13 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 const int k = k0 + kk;
                 if (FULL || k < nz) {
                     if (FULL || k > 0) finalize(ecv[kk], dg[kk], im[kk], gb + kk * NT, kk, k - 1);
+                    if constexpr (GEN == 2 && T::THOMAS)
+                        if (kk == 0 && ch > 0) {   // renormalise and checkpoint m_{k0-1}
+                            const double m = pm1 / pm2;
+                            pm1 = m;
+                            pm2 = 1.0;
+                            cbuf[ch * NT + tid] = m;
+                        }
                     um1 = u0; u0 = ecv[kk]; S0 = Sv[kk]; qa = pav[kk]; qb = pbv[kk];
                 }
             }
@@ -460,7 +483,36 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             }
         }
 
-        if constexpr (T::THOMAS) {
+        if constexpr (T::THOMAS && GEN == 2) {
+            // backward substitution per KB-level chunk: the chunk's t'_k recomputed from its
+            // checkpoint with the forward sweep's arithmetic, then x_k = g'_k - t'_k x_{k+1}
+            double* obase = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase;
+            double x = 0.0;
+            for (int c = nck - 1; c >= 0; --c) {
+                const int kb0 = c * KB;
+                double p1 = c ? cbuf[c * NT + tid] : 1.0, p2 = c ? 1.0 : 0.0;
+                double t1 = c ? fT * ptab[2 * nz + kb0 - 1] : 0.0;
+                double tq[KB], gv[KB];
+#pragma unroll
+                for (int q = 0; q < KB; ++q) {
+                    const int k = kb0 + q;
+                    if (k < nz) {
+                        const double tk = fT * ptab[2 * nz + k];
+                        tq[q] = -(tk * pivot_step(k, p1, p2, t1));   // -t'_k = -t_k / m_k
+                        gv[q] = gbuf[k * NT + tid];
+                    }
+                }
+#pragma unroll
+                for (int q = KB - 1; q >= 0; --q) {
+                    const int k = kb0 + q;
+                    if (k < nz) {
+                        x = fma(tq[q], x, gv[q]);
+                        if (valid) obase[(int64_t)k * nx] = x;
+                    }
+                }
+            }
+        }
+        if constexpr (T::THOMAS && GEN != 2) {
             // backward substitution x_k = g'_k - t'_k x_{k+1}, KB levels per step with
             // the shared-memory loads issued ahead of the dependent FMA chain
             double* op = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase + (int64_t)(nz - 1) * nx;
@@ -473,7 +525,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
                     gv[q] = gq[(KB - 1 - q) * NT];
-                    gm[q] = (GEN == 2) ? gq[nz * NT + (KB - 1 - q) * NT] : mq[KB - 1 - q];
+                    gm[q] = mq[KB - 1 - q];
                 }
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
@@ -483,10 +535,12 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 }
             }
             for (; k >= 0; --k) {
-                x = fma((GEN == 2) ? gbuf[(nz + k) * NT + tid] : gim[k], x, gbuf[k * NT + tid]);
+                x = fma(gim[k], x, gbuf[k * NT + tid]);
                 if (valid) *op = x;
                 op -= nx;
             }
+        }
+        if constexpr (T::THOMAS) {
             // fused halo push: a strip-boundary row also goes to the neighbour's slab (read
             // back from L1/L2, outside the recurrence loop)
             if (valid && ((j == 0 && a.push.dst_lo) || (j == ny - 1 && a.push.dst_hi))) {
@@ -529,7 +583,7 @@ size_t line_smem_bytes(int nz, int gen = 0)
     using T = Traits<MODE>;
     using G = Geom<T::NH, T::NP, TY>;
     size_t d = ((3 * nz + 15) & ~15) + (gen == 2 ? ((4 * nz + 15) & ~15) : gen ? ((3 * nz + 15) & ~15) : 0) +
-               (size_t)NS * G::STAGE + (T::THOMAS ? (size_t)(gen == 2 ? 2 : 1) * nz * G::NT : 0) + 64 + 16 +
+               (size_t)NS * G::STAGE + (T::THOMAS ? (size_t)(nz + (gen == 2 ? (nz + KB - 1) / KB : 0)) * G::NT : 0) + 64 + 16 +
                (MODE == MODE_RESTRICT ? 2 * TY * (KB + 1) * (TX / 2) : 0);
     return d * sizeof(double);
 }
