@@ -32,7 +32,10 @@ using namespace dev;
 
 constexpr int TX = kTileX;  // columns per tile row (one warp, 256 B per row segment)
 constexpr int KB = kStageK; // vertical levels per pipeline stage
-constexpr int NS = 3;   // pipeline stages
+constexpr int kNS = 3;  // pipeline stages
+// the CG preconditioner with per-column fields keeps 4 tile rows (4 warps per SM) with 2 stages
+template <int MODE, int GEN>
+constexpr int stages() { return (GEN == 2 && MODE == MODE_CGPREC) ? 2 : kNS; }
 
 template <int MODE>
 struct Traits;
@@ -153,6 +156,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     constexpr int NH = T::NH, NP = T::NP, NR = T::NR;
     using G = Geom<NH, NP, TY>;
     constexpr int NT = G::NT;
+    constexpr int NS = stages<MODE, GEN>();
 
     extern __shared__ __align__(128) double smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[NS];
@@ -162,7 +166,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     const int nz = a.L.nz;
     const int64_t nx = a.L.nx, ny = a.L.ny;
     const int tabn = (3 * nz + 15) & ~15;    // keep the stages 128-byte aligned
-    const int ptn = (GEN == 2) ? ((4 * nz + 15) & ~15) : tabn;
+    const int ptn = (GEN >= 2) ? ((4 * nz + 15) & ~15) : tabn;
     double* tab = smem;                      // diag[nz], invm[nz], gim[nz]
     double* ptab = smem + tabn;              // GEN 1: b_k, c_k, c_l d_k; GEN 2: a_k-b_k-c_k, b_k, c_k, d_k
     double* stage = ptab + (GEN ? ptn : 0);  // NS stages
@@ -177,7 +181,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     for (int q = tid; q < 3 * nz; q += NT) tab[q] = a.L.tab[q];   // interior class (0)
     if constexpr (GEN != 0)
-        for (int q = tid; q < (GEN == 2 ? 4 : 3) * nz; q += NT) ptab[q] = a.L.prof[q];
+        for (int q = tid; q < (GEN >= 2 ? 4 : 3) * nz; q += NT) ptab[q] = a.L.prof[q];
     const double* diag_s = tab;
     const double* invm_s = tab + nz;
     const double* gim_s = tab + 2 * nz;
@@ -291,7 +295,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             t1 = tk;
             return im;
         };
-        if constexpr (GEN == 2) {
+        if constexpr (GEN >= 2) {
             if (valid) {
                 const int64_t ncol = nx * ny, cc = j * nx + i;
                 const double* F = a.L.fld + cc;
@@ -318,7 +322,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             // (M_T u)_k and the coefficient of the horizontal neighbour sum: -gamma and c in
             // the flat box; b_k, c_k and c_l d_k with general profiles (GEN, shared memory)
             double Mu, c, sk = -gamma, tk = 0.0;
-            if constexpr (GEN == 2) {
+            if constexpr (GEN >= 2) {
                 // A_T = |T| (diag(a) + tridiag(-(b+c), b, c)) - alpha_T diag(d)
                 sk = fT * ptab[nz + km];
                 tk = fT * ptab[2 * nz + km];
@@ -408,7 +412,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                     ecv[kk] = h[0];
                     // neighbour sum; GEN 2: weighted by the face alpha_{T,T'}
                     auto nsum = [&](const double* q) {
-                        if constexpr (GEN == 2)
+                        if constexpr (GEN >= 2)
                             return fma(fw, q[-1], fe * q[1]) + fma(fs, q[-G::HALO_ROW], fn * q[G::HALO_ROW]);
                         else
                             return (q[-1] + q[1]) + (q[-G::HALO_ROW] + q[G::HALO_ROW]);
@@ -427,12 +431,20 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             if constexpr (MODE == MODE_RESTRICT) rbuf_cur = rbuf + (gi & 1) * (TY * RS * (TX / 2));
             const double* dg = diag + (k0 - 1);      // level km = k0 - 1 + kk
             const double* im = invm + (k0 - 1);
+            double imv[KB];   // GEN 3: the column's tabulated 1/m_k of levels k0-1 .. k0+KB-2
+            if constexpr (GEN == 3 && T::THOMAS) {
+#pragma unroll
+                for (int kk = 0; kk < KB; ++kk) {
+                    const int km = k0 - 1 + kk;
+                    imv[kk] = (valid && km >= 0 && km < nz) ? __ldg(a.L.piv + colbase + (int64_t)km * nx) : 0.0;
+                }
+            }
             double* gb = gbuf + (k0 - 1) * NT + tid;
 #pragma unroll
             for (int kk = 0; kk < KB; ++kk) {
                 const int k = k0 + kk;
                 if (FULL || k < nz) {
-                    if (FULL || k > 0) finalize(ecv[kk], dg[kk], im[kk], gb + kk * NT, kk, k - 1);
+                    if (FULL || k > 0) finalize(ecv[kk], dg[kk], (GEN == 3 && T::THOMAS) ? imv[kk] : im[kk], gb + kk * NT, kk, k - 1);
                     if constexpr (GEN == 2 && T::THOMAS)
                         if (kk == 0 && ch > 0) {   // renormalise and checkpoint m_{k0-1}
                             const double m = pm1 / pm2;
@@ -455,7 +467,10 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             else
                 do_chunk(std::false_type{}, ch, st);
             if (ch == nch - 1)
-                finalize(0.0, diag[nz - 1], invm[nz - 1], gbuf + (nz - 1) * NT + tid, nz - ch * KB, nz - 1);
+                finalize(0.0, diag[nz - 1],
+                         (GEN == 3 && T::THOMAS) ? (valid ? __ldg(a.L.piv + colbase + (int64_t)(nz - 1) * nx) : 0.0)
+                                                 : invm[nz - 1],
+                         gbuf + (nz - 1) * NT + tid, nz - ch * KB, nz - 1);
             if constexpr (MODE == MODE_RESTRICT) {
                 // f_c(I, J, k) = 1/4 (x-pair sum of row 2J + x-pair sum of row 2J+1);
                 // this chunk completed levels ch*KB-1 .. ch*KB+KB-2 (and nz-1 if last), slot
@@ -512,7 +527,35 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 }
             }
         }
-        if constexpr (T::THOMAS && GEN != 2) {
+        if constexpr (T::THOMAS && GEN == 3) {
+            // backward substitution with the column's tabulated 1/m_k (k_field_pivots):
+            // x_k = g'_k - t'_k x_{k+1}, t'_k = t_k / m_k; the 1/m_k of a chunk are loaded first
+            double* obase = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase;
+            const double* pb = a.L.piv + colbase;
+            double x = 0.0;
+            for (int c = nck - 1; c >= 0; --c) {
+                const int kb0 = c * KB;
+                double gm[KB], gv[KB];
+#pragma unroll
+                for (int q = 0; q < KB; ++q) {
+                    const int k = kb0 + q;
+                    if (k < nz) {
+                        const double im = valid ? __ldg(pb + (int64_t)k * nx) : 0.0;
+                        gm[q] = -(fT * ptab[2 * nz + k]) * im;
+                        gv[q] = gbuf[k * NT + tid];
+                    }
+                }
+#pragma unroll
+                for (int q = KB - 1; q >= 0; --q) {
+                    const int k = kb0 + q;
+                    if (k < nz) {
+                        x = fma(gm[q], x, gv[q]);
+                        if (valid) obase[(int64_t)k * nx] = x;
+                    }
+                }
+            }
+        }
+        if constexpr (T::THOMAS && GEN < 2) {
             // backward substitution x_k = g'_k - t'_k x_{k+1}, KB levels per step with
             // the shared-memory loads issued ahead of the dependent FMA chain
             double* op = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase + (int64_t)(nz - 1) * nx;
@@ -568,7 +611,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     };
     for (int tl = 0; tl < my_tiles; ++tl) {
         const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
-        if (GEN != 2 && tile_on_boundary(a.L, (int64_t)(tile % ntx) * TX, (int64_t)row_of(tile) * TY, TX, TY))
+        if (GEN < 2 && tile_on_boundary(a.L, (int64_t)(tile % ntx) * TX, (int64_t)row_of(tile) * TY, TX, TY))
             tile_body(std::true_type{}, tl);
         else
             tile_body(std::false_type{}, tl);
@@ -582,8 +625,8 @@ size_t line_smem_bytes(int nz, int gen = 0)
 {
     using T = Traits<MODE>;
     using G = Geom<T::NH, T::NP, TY>;
-    size_t d = ((3 * nz + 15) & ~15) + (gen == 2 ? ((4 * nz + 15) & ~15) : gen ? ((3 * nz + 15) & ~15) : 0) +
-               (size_t)NS * G::STAGE + (T::THOMAS ? (size_t)(nz + (gen == 2 ? (nz + KB - 1) / KB : 0)) * G::NT : 0) + 64 + 16 +
+    size_t d = ((3 * nz + 15) & ~15) + (gen >= 2 ? ((4 * nz + 15) & ~15) : gen ? ((3 * nz + 15) & ~15) : 0) +
+               (size_t)(gen == 2 ? stages<MODE, 2>() : kNS) * G::STAGE + (T::THOMAS ? (size_t)(nz + (gen == 2 ? (nz + KB - 1) / KB : 0)) * G::NT : 0) + 64 + 16 +
                (MODE == MODE_RESTRICT ? 2 * TY * (KB + 1) * (TX / 2) : 0);
     return d * sizeof(double);
 }
@@ -622,7 +665,9 @@ cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
 {
     if (a.L.gen) {   // general vertical profiles / per-column fields: TMA loader only
         if (!a.use_tma) return cudaErrorNotSupported;
-        return a.L.gen == 2 ? launch_line_l<MODE, TY, 1, 2>(ln, a) : launch_line_l<MODE, TY, 1, 1>(ln, a);
+        // gen 3 (fields with tabulated pivots) differs from gen 2 only in the Thomas modes
+        if (a.L.gen == 3 && Traits<MODE>::THOMAS) return launch_line_l<MODE, TY, 1, 3>(ln, a);
+        return a.L.gen >= 2 ? launch_line_l<MODE, TY, 1, 2>(ln, a) : launch_line_l<MODE, TY, 1, 1>(ln, a);
     }
     return a.use_tma ? launch_line_l<MODE, TY, 1, 0>(ln, a) : launch_line_l<MODE, TY, 0, 0>(ln, a);
 }
@@ -636,6 +681,31 @@ cudaError_t launch_line_ty(const Launcher& ln, const LineArgs& a)
 }
 
 // ------------------------------------------------------------------ simple streaming kernels
+
+// Per-column Thomas pivots with per-column fields (setup, once per operator): 1/m_k of the
+// column block A_T = |T| (diag(a) + tridiag(-(b+c), b, c)) - alpha_T diag(d), textbook
+// recurrence m_0 = diag_0, m_k = diag_k - s_k t_{k-1} / m_{k-1}, stored in the
+// Lambda layout of the level (one thread per column, coalesced along x).
+__global__ void k_field_pivots(const LevelConst L, double* __restrict__ piv)
+{
+    pdl_wait();
+    pdl_trigger();
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, j = blockIdx.y;
+    if (i >= L.nx) return;
+    const int nz = L.nz;
+    const int64_t ncol = L.nx * L.ny, cc = j * L.nx + i;
+    const double fT = L.fld[cc], faT = L.fld[ncol + cc];
+    const double* pr = L.prof;
+    double* out = piv + j * L.nx * nz + i;
+    double tprev = 0.0;
+    for (int k = 0; k < nz; ++k) {
+        const double sk = fT * pr[nz + k], tk = fT * pr[2 * nz + k];
+        const double dg = fma(fT, pr[k], -faT * pr[3 * nz + k]);
+        const double im = 1.0 / fma(-sk, tprev, dg);
+        out[(int64_t)k * L.nx] = im;
+        tprev = tk * im;
+    }
+}
 
 __global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double* __restrict__ r,
                            double* __restrict__ fc)
@@ -929,6 +999,12 @@ cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a)
     case MODE_RESTRICT: return launch_line_t<MODE_RESTRICT, 4>(ln, a);
     default: return cudaErrorInvalidValue;
     }
+}
+
+cudaError_t launch_field_pivots(const Launcher& ln, const LevelConst& L, double* piv)
+{
+    if (L.nx <= 0 || L.ny <= 0) return cudaSuccess;
+    return launch_kernel(ln, k_field_pivots, dim3((unsigned)((L.nx + 127) / 128), (unsigned)L.ny), dim3(128), 0, L, piv);
 }
 
 cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const LevelConst& coarse,
