@@ -430,7 +430,6 @@ def main():
                        "levels": args.levels, "coarse_sweeps": args.coarse_sweeps, "boundary": args.boundary,
                        "vertical_profiles": "flat box" if args.profiles < 0 else f"synthetic seed {args.profiles}",
                        "horizontal_fields": "uniform" if args.fields == "none" else f"{args.fields} seed 1",
-                       **({"field_pivots": os.environ.get("TPMG_FIELD_PIVOTS", "table")} if args.fields != "none" else {}),
                        "parallelism": f"y-strips x{world}" if world > 1 else "single GPU",
                        "l2": "vectors 1 GiB/GPU >> 126 MB L2 (no flush needed)"},
             "roofline": roof,

@@ -40,7 +40,6 @@ struct LevelData {
     double* d_prof = nullptr;           // general vertical profiles: [b_k][c_k][c_l d_k] (device)
     double* d_fprof = nullptr;          // with per-column fields: [a_k-b_k-c_k][b_k][c_k][d_k] (device)
     double* d_fld = nullptr;            // per-column fields, LevelConst::fld layout (device)
-    double* d_piv = nullptr;            // per-column Thomas pivots 1/m_k (fields, tabulated mode)
     double* slab_lo = nullptr;          // halo rows j = -1 / j = ny for this level (nranks > 1)
     double* slab_hi = nullptr;
     size_t n() const { return (size_t)lc.nx * (size_t)lc.ny * (size_t)lc.nz; }
@@ -60,8 +59,6 @@ struct tpmg_ctx {
     std::vector<double> prof_abcd;   // the vertical profiles a, b, c, d in use (4 nz; set by build_tables)
     bool fields = false;             // per-column horizontal fields set (tpmg_set_fields)
     bool gen_profiles = false;       // general vertical profiles set (tpmg_set_profiles)
-    bool field_pivots_onchip = false;  // TPMG_FIELD_PIVOTS=onchip: recompute the per-column pivots
-                                       // in the line kernels instead of tabulating them (gen 2)
     // reductions
     double* d_partials = nullptr;
     unsigned* d_ticket = nullptr;
@@ -648,7 +645,7 @@ bool ksplit_usable(tpmg_ctx* ctx, int mode, const LevelConst& lc)
     // general vertical profiles: the k-split smoother / preconditioner / restriction only
     if (lc.gen && (mode == MODE_SMOOTH_PROLONG || mode == MODE_CGPREC)) return false;
     // per-column fields: the one-thread-per-column kernel only (per-column pivots)
-    if (lc.gen >= 2) return false;
+    if (lc.gen == 2) return false;
     // the k-split CG preconditioner is opt-in (TPMG_KSPLIT_CG=1): measured 4% slower per CG
     // iteration than the one-thread-per-column kernel at 1024^2 x 128
     if (mode == MODE_CGPREC && !ctx->ksplit_cg) return false;
@@ -1340,7 +1337,6 @@ void ctx_free(tpmg_ctx* ctx)
         cudaFree(L.d_prof);
         cudaFree(L.d_fprof);
         cudaFree(L.d_fld);
-        cudaFree(L.d_piv);
         if ((int)l < ctx->L) { cudaFree(L.u[0]); cudaFree(L.f); }
         cudaFree(L.u[1]);
     }
@@ -1464,15 +1460,7 @@ tpmg_status fields_profile_tables(tpmg_ctx* ctx)
         L.lc.prof = L.d_fprof;
         L.lc.fld = L.d_fld;
         L.lc.gen = 2;
-        L.lc.piv = nullptr;
-        if (!ctx->field_pivots_onchip) {   // tabulate 1/m_k per column once (gen 3)
-            TRY(dev_alloc(ctx, &L.d_piv, L.n()));
-            CUDA_TRY(ctx, launch_field_pivots(launcher(ctx), L.lc, L.d_piv));
-            L.lc.piv = L.d_piv;
-            L.lc.gen = 3;
-        }
     }
-    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     return TPMG_OK;
 }
 
@@ -1585,8 +1573,6 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->pdl = pd && pd[0] == '1';
         const char* fp = std::getenv("TPMG_FUSE_PROLONG");
         ctx->fuse_prolong = fp && fp[0] == '1';
-        const char* fpv = std::getenv("TPMG_FIELD_PIVOTS");
-        ctx->field_pivots_onchip = fpv && std::string(fpv) == "onchip";
         const char* sd = std::getenv("TPMG_SYNC_DEBUG");
         ctx->sync_debug = sd && sd[0] == '1';
     }
@@ -1909,7 +1895,7 @@ tpmg_status tpmg_set_fields(tpmg_ctx* ctx, const double* area, const double* ax,
         const double* prof[4] = {ctx->prof_abcd.data(), ctx->prof_abcd.data() + nz, ctx->prof_abcd.data() + 2 * nz,
                                  ctx->prof_abcd.data() + 3 * nz};
         const bool flat = !ctx->gen_profiles;
-        for (int l = 1; l <= ctx->L; ++l) ctx->lv[l].lc.fld = ctx->lv[l].lc.piv = nullptr;
+        for (int l = 1; l <= ctx->L; ++l) ctx->lv[l].lc.fld = nullptr;
         return build_tables(ctx, flat ? nullptr : prof);
     }
     if (!area || !ax || !ay) return fail(ctx, TPMG_E_PARAM, "tpmg_set_fields: give all three fields or none");

@@ -37,6 +37,19 @@ constexpr int kNS = 3;  // pipeline stages
 template <int MODE, int GEN>
 constexpr int stages() { return (GEN == 2 && MODE == MODE_CGPREC) ? 2 : kNS; }
 
+// 1/x for the per-column pivots: the approximate reciprocal (MUFU) refined by two Newton
+// steps (error ~2^-92 before rounding, i.e. correctly rounded up to an ulp) -- 5 instructions
+// instead of the IEEE division's subroutine, which made the fields kernels instruction-bound.
+__device__ __forceinline__ double rcp_nr(double x)
+{
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
 template <int MODE>
 struct Traits;
 template <> struct Traits<MODE_APPLY>  { static constexpr int NH = 1, NP = 0, THOMAS = 0, NR = 0; };
@@ -172,7 +185,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     double* stage = ptab + (GEN ? ptn : 0);  // NS stages
     double* gbuf = stage + NS * G::STAGE;    // g'[nz][NT] (Thomas modes)
     const int nck = (nz + KB - 1) / KB;
-    double* cbuf = gbuf + nz * NT;           // GEN 2: t'_{c KB - 1}[nck][NT], the pivot checkpoints
+    double* cbuf = gbuf + nz * NT;           // GEN 2: m_{c KB - 1}[nck][NT], the pivot checkpoints
     // MODE_RESTRICT: x-pair sums [2][TY][KB+1][TX/2] (a chunk completes up to KB+1 levels)
     constexpr int RS = KB + 1;
     double* rbuf = gbuf + (T::THOMAS ? (nz + (GEN == 2 ? nck : 0)) * NT : 0);
@@ -289,7 +302,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             const double tk = fT * ptab[2 * nz + k];
             const double dgk = fma(fT, ptab[k], -faT * ptab[3 * nz + k]);
             const double p = fma(dgk, p1, -(sk * t1) * p2);
-            const double im = p1 / p;
+            const double im = p1 * rcp_nr(p);
             p2 = p1;
             p1 = p;
             t1 = tk;
@@ -431,23 +444,15 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             if constexpr (MODE == MODE_RESTRICT) rbuf_cur = rbuf + (gi & 1) * (TY * RS * (TX / 2));
             const double* dg = diag + (k0 - 1);      // level km = k0 - 1 + kk
             const double* im = invm + (k0 - 1);
-            double imv[KB];   // GEN 3: the column's tabulated 1/m_k of levels k0-1 .. k0+KB-2
-            if constexpr (GEN == 3 && T::THOMAS) {
-#pragma unroll
-                for (int kk = 0; kk < KB; ++kk) {
-                    const int km = k0 - 1 + kk;
-                    imv[kk] = (valid && km >= 0 && km < nz) ? __ldg(a.L.piv + colbase + (int64_t)km * nx) : 0.0;
-                }
-            }
             double* gb = gbuf + (k0 - 1) * NT + tid;
 #pragma unroll
             for (int kk = 0; kk < KB; ++kk) {
                 const int k = k0 + kk;
                 if (FULL || k < nz) {
-                    if (FULL || k > 0) finalize(ecv[kk], dg[kk], (GEN == 3 && T::THOMAS) ? imv[kk] : im[kk], gb + kk * NT, kk, k - 1);
+                    if (FULL || k > 0) finalize(ecv[kk], dg[kk], im[kk], gb + kk * NT, kk, k - 1);
                     if constexpr (GEN == 2 && T::THOMAS)
                         if (kk == 0 && ch > 0) {   // renormalise and checkpoint m_{k0-1}
-                            const double m = pm1 / pm2;
+                            const double m = pm1 * rcp_nr(pm2);
                             pm1 = m;
                             pm2 = 1.0;
                             cbuf[ch * NT + tid] = m;
@@ -467,10 +472,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             else
                 do_chunk(std::false_type{}, ch, st);
             if (ch == nch - 1)
-                finalize(0.0, diag[nz - 1],
-                         (GEN == 3 && T::THOMAS) ? (valid ? __ldg(a.L.piv + colbase + (int64_t)(nz - 1) * nx) : 0.0)
-                                                 : invm[nz - 1],
-                         gbuf + (nz - 1) * NT + tid, nz - ch * KB, nz - 1);
+                finalize(0.0, diag[nz - 1], invm[nz - 1], gbuf + (nz - 1) * NT + tid, nz - ch * KB, nz - 1);
             if constexpr (MODE == MODE_RESTRICT) {
                 // f_c(I, J, k) = 1/4 (x-pair sum of row 2J + x-pair sum of row 2J+1);
                 // this chunk completed levels ch*KB-1 .. ch*KB+KB-2 (and nz-1 if last), slot
@@ -522,34 +524,6 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                     const int k = kb0 + q;
                     if (k < nz) {
                         x = fma(tq[q], x, gv[q]);
-                        if (valid) obase[(int64_t)k * nx] = x;
-                    }
-                }
-            }
-        }
-        if constexpr (T::THOMAS && GEN == 3) {
-            // backward substitution with the column's tabulated 1/m_k (k_field_pivots):
-            // x_k = g'_k - t'_k x_{k+1}, t'_k = t_k / m_k; the 1/m_k of a chunk are loaded first
-            double* obase = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase;
-            const double* pb = a.L.piv + colbase;
-            double x = 0.0;
-            for (int c = nck - 1; c >= 0; --c) {
-                const int kb0 = c * KB;
-                double gm[KB], gv[KB];
-#pragma unroll
-                for (int q = 0; q < KB; ++q) {
-                    const int k = kb0 + q;
-                    if (k < nz) {
-                        const double im = valid ? __ldg(pb + (int64_t)k * nx) : 0.0;
-                        gm[q] = -(fT * ptab[2 * nz + k]) * im;
-                        gv[q] = gbuf[k * NT + tid];
-                    }
-                }
-#pragma unroll
-                for (int q = KB - 1; q >= 0; --q) {
-                    const int k = kb0 + q;
-                    if (k < nz) {
-                        x = fma(gm[q], x, gv[q]);
                         if (valid) obase[(int64_t)k * nx] = x;
                     }
                 }
@@ -665,8 +639,6 @@ cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
 {
     if (a.L.gen) {   // general vertical profiles / per-column fields: TMA loader only
         if (!a.use_tma) return cudaErrorNotSupported;
-        // gen 3 (fields with tabulated pivots) differs from gen 2 only in the Thomas modes
-        if (a.L.gen == 3 && Traits<MODE>::THOMAS) return launch_line_l<MODE, TY, 1, 3>(ln, a);
         return a.L.gen >= 2 ? launch_line_l<MODE, TY, 1, 2>(ln, a) : launch_line_l<MODE, TY, 1, 1>(ln, a);
     }
     return a.use_tma ? launch_line_l<MODE, TY, 1, 0>(ln, a) : launch_line_l<MODE, TY, 0, 0>(ln, a);
@@ -681,31 +653,6 @@ cudaError_t launch_line_ty(const Launcher& ln, const LineArgs& a)
 }
 
 // ------------------------------------------------------------------ simple streaming kernels
-
-// Per-column Thomas pivots with per-column fields (setup, once per operator): 1/m_k of the
-// column block A_T = |T| (diag(a) + tridiag(-(b+c), b, c)) - alpha_T diag(d), textbook
-// recurrence m_0 = diag_0, m_k = diag_k - s_k t_{k-1} / m_{k-1}, stored in the
-// Lambda layout of the level (one thread per column, coalesced along x).
-__global__ void k_field_pivots(const LevelConst L, double* __restrict__ piv)
-{
-    pdl_wait();
-    pdl_trigger();
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, j = blockIdx.y;
-    if (i >= L.nx) return;
-    const int nz = L.nz;
-    const int64_t ncol = L.nx * L.ny, cc = j * L.nx + i;
-    const double fT = L.fld[cc], faT = L.fld[ncol + cc];
-    const double* pr = L.prof;
-    double* out = piv + j * L.nx * nz + i;
-    double tprev = 0.0;
-    for (int k = 0; k < nz; ++k) {
-        const double sk = fT * pr[nz + k], tk = fT * pr[2 * nz + k];
-        const double dg = fma(fT, pr[k], -faT * pr[3 * nz + k]);
-        const double im = 1.0 / fma(-sk, tprev, dg);
-        out[(int64_t)k * L.nx] = im;
-        tprev = tk * im;
-    }
-}
 
 __global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double* __restrict__ r,
                            double* __restrict__ fc)
@@ -999,12 +946,6 @@ cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a)
     case MODE_RESTRICT: return launch_line_t<MODE_RESTRICT, 4>(ln, a);
     default: return cudaErrorInvalidValue;
     }
-}
-
-cudaError_t launch_field_pivots(const Launcher& ln, const LevelConst& L, double* piv)
-{
-    if (L.nx <= 0 || L.ny <= 0) return cudaSuccess;
-    return launch_kernel(ln, k_field_pivots, dim3((unsigned)((L.nx + 127) / 128), (unsigned)L.ny), dim3(128), 0, L, piv);
 }
 
 cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const LevelConst& coarse,

@@ -30,15 +30,12 @@ struct LevelConst {
     int32_t bc;         // tpmg_boundary: 0 ghost-zero [R1] (class 0 only), 1 face Dirichlet [R25]
     int32_t bnd_lo, bnd_hi;   // local row 0 / ny-1 lies on the physical boundary
     int32_t gen;        // 1: general vertical profiles (stencil couplings from prof, not gamma / c);
-                        // 2: per-column horizontal fields (fld) with the profiles a, b, c, d,
-                        //    pivots recomputed on chip; 3: the same with tabulated pivots (piv)
+                        // 2: per-column horizontal fields (fld) with the profiles a, b, c, d
     const double* prof; // device, gen 1: [b_k][c_k][c_l d_k]; gen 2: [a_k-b_k-c_k][b_k][c_k][d_k];
                         // nz each
     const double* fld;  // device, gen 2: [|T|][alpha_T][alpha_W][alpha_E][alpha_S][alpha_N], each
                         // [ny][nx] over the local columns ("different for each horizontal
                         // grid cell T (and depend on the multigrid level)")
-    const double* piv;  // device, gen 3: the columns' Thomas pivots 1/m_k (Lambda layout, one
-                        // vector of the level; k_field_pivots)
 };
 
 // Column classes of the face-Dirichlet reading: nb = number of boundary faces (0..4).
@@ -222,8 +219,6 @@ bool ksplit_supported(int mode, int nz, int nx);
 KsplitBoxes ksplit_boxes(int mode, int cfg);
 cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const LineArgs& a, const KTables& T);
 
-// Per-column Thomas pivots 1/m_k with per-column fields (gen 3 setup), Lambda layout
-cudaError_t launch_field_pivots(const Launcher& ln, const LevelConst& L, double* piv);
 // f_c = 1/4 sum of the 2x2 fine children of r (plain restriction)
 cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const LevelConst& coarse,
                             const double* r, double* fc);

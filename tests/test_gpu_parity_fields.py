@@ -43,23 +43,15 @@ SHAPES = [
 IDS = ["32x32x16", "80x48x64-smooth", "64x32x40-prof", "256x256x128", "48x48x32-face"]
 
 
-def fctx(p, pivots="table"):
-    """pivots: "table" (default: per-column 1/m_k tabulated once by k_field_pivots) or
-    "onchip" (recomputed in the line kernels, TPMG_FIELD_PIVOTS=onchip; read at tpmg_create)."""
-    import os
-    os.environ.pop("TPMG_FIELD_PIVOTS", None)
-    if pivots == "onchip":
-        os.environ["TPMG_FIELD_PIVOTS"] = "onchip"
+def fctx(p):
     ctx = ctx_for(p)
-    os.environ.pop("TPMG_FIELD_PIVOTS", None)
     ctx.set_fields(*p.fields)
     return ctx
 
 
-@pytest.mark.parametrize("pivots", ["table", "onchip"])
 @pytest.mark.parametrize("p", SHAPES, ids=IDS)
-def test_fields_ops_all_levels(p, pivots):
-    ctx = fctx(p, pivots)
+def test_fields_ops_all_levels(p):
+    ctx = fctx(p)
     for level in range(1, p.L + 1):
         s = p.level_shape(level)
         x, f = rand(s, 1 + level), rand(s, 100 + level)
@@ -81,10 +73,9 @@ def test_fields_ops_all_levels(p, pivots):
             assert rel_l2(to_host_zc(du), O.smooth(p, x, f, level, sweeps)) < tol(p, level)
 
 
-@pytest.mark.parametrize("pivots", ["table", "onchip"])
 @pytest.mark.parametrize("p", SHAPES, ids=IDS)
-def test_fields_vcycle(p, pivots):
-    ctx = fctx(p, pivots)
+def test_fields_vcycle(p):
+    ctx = fctx(p)
     s = p.level_shape(p.L)
     u, f = rand(s, 5), rand(s, 6)
     du = to_dev(u)
@@ -95,9 +86,8 @@ def test_fields_vcycle(p, pivots):
 @pytest.mark.parametrize("solver", ["mg", "cg"])
 @pytest.mark.parametrize("p", [SHAPES[0], SHAPES[1], SHAPES[4], F(128, 128, 128, 5, 7, "smooth")],
                          ids=["32x32x16", "80x48x64-smooth", "48x48x32-face", "128x128x128-smooth"])
-@pytest.mark.parametrize("pivots", ["table", "onchip"])
-def test_fields_solve_parity(p, solver, pivots):
-    ctx = fctx(p, pivots)
+def test_fields_solve_parity(p, solver):
+    ctx = fctx(p)
     f = rhs_zc(p.nx, p.ny, p.nz, seed=0)
     u = ctx.empty(p.L)
     if solver == "mg":
