@@ -17,6 +17,9 @@ from inputs import gpu as G
 
 n = int(os.environ.get("PROF_N", "1024"))
 ctx = T.Context(T.make_params(n, n, nz=128))
+if os.environ.get("PROF_FIELDS"):   # per-column fields (tpmg_set_fields), e.g. PROF_FIELDS=smooth
+    from inputs import horizontal_fields
+    ctx.set_fields(*horizontal_fields(n, n, 8.4 * 8.4 / 4, 1, os.environ["PROF_FIELDS"]))
 f = ctx.empty(5)
 u = ctx.empty(5)
 G.fill_rhs(f, n, seed=0)
