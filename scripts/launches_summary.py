@@ -14,7 +14,7 @@ def load(path):
     for r in rows[hi + 1:]:
         if len(r) <= vi:
             continue
-        m = re.search(r"k_line<(\d+), (\d+), (\d+)>", r[ki]) or re.search(r"(k_\w+)", r[ki])
+        m = re.search(r"k_line\w*<[^>]*>", r[ki]) or re.search(r"(k_\w+)", r[ki])
         out.append((m.group(0) if m else r[ki][:40], r[gi], float(r[vi].replace(",", "")) / 1e3))
     return out
 
