@@ -35,7 +35,7 @@ constexpr int KB = kStageK; // vertical levels per pipeline stage
 constexpr int kNS = 3;  // pipeline stages
 // the CG preconditioner with per-column fields keeps 4 tile rows (4 warps per SM) with 2 stages
 template <int MODE, int GEN>
-constexpr int stages() { return (GEN == 2 && MODE == MODE_CGPREC) ? 2 : kNS; }
+__host__ __device__ constexpr int stages() { return (GEN == 2 && MODE == MODE_CGPREC) ? 2 : kNS; }
 
 // 1/x for the per-column pivots: the approximate reciprocal (MUFU) refined by two Newton
 // steps (error ~2^-92 before rounding, i.e. correctly rounded up to an ulp) -- 5 instructions
@@ -502,14 +502,14 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 
         if constexpr (T::THOMAS && GEN == 2) {
             // backward substitution per KB-level chunk: the chunk's t'_k recomputed from its
-            // checkpoint with the forward sweep's arithmetic, then x_k = g'_k - t'_k x_{k+1}
+            // checkpoint with the forward sweep's arithmetic, then x_k = g'_k - t'_k x_{k+1}.
+            // Software-pipelined: chunk c-1's pivots (independent of x) are recomputed in the
+            // same loop body as chunk c's x recurrence, so the two dependency chains overlap.
             double* obase = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase;
-            double x = 0.0;
-            for (int c = nck - 1; c >= 0; --c) {
+            auto recompute = [&](int c, double (&tq)[KB], double (&gv)[KB]) {
                 const int kb0 = c * KB;
                 double p1 = c ? cbuf[c * NT + tid] : 1.0, p2 = c ? 1.0 : 0.0;
                 double t1 = c ? fT * ptab[2 * nz + kb0 - 1] : 0.0;
-                double tq[KB], gv[KB];
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
                     const int k = kb0 + q;
@@ -519,6 +519,13 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                         gv[q] = gbuf[k * NT + tid];
                     }
                 }
+            };
+            double x = 0.0;
+            double tq[KB], gv[KB], tq2[KB], gv2[KB];
+            recompute(nck - 1, tq, gv);
+            for (int c = nck - 1; c >= 0; --c) {
+                if (c > 0) recompute(c - 1, tq2, gv2);
+                const int kb0 = c * KB;
 #pragma unroll
                 for (int q = KB - 1; q >= 0; --q) {
                     const int k = kb0 + q;
@@ -526,6 +533,11 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                         x = fma(tq[q], x, gv[q]);
                         if (valid) obase[(int64_t)k * nx] = x;
                     }
+                }
+#pragma unroll
+                for (int q = 0; q < KB; ++q) {
+                    tq[q] = tq2[q];
+                    gv[q] = gv2[q];
                 }
             }
         }
