@@ -231,6 +231,24 @@ tpmg_status tpmg_solve_host(tpmg_ctx *ctx, tpmg_solver solver, const double *f_h
                             double *u_host, double eps, int32_t max_iter,
                             tpmg_result *result);
 
+/* Layout conversion (the fields are z-contiguous on the host, "transposing the fields
+ * from a z-contiguous data format on the host to the x-contiguous format ... on the GPU").
+ * z-contiguous: idx = (j*nx + i)*nz + k (columns contiguous, the CPU ordering of P:59);
+ * Lambda: idx = (j*nz + k)*nx + i (eqn:MemoryMapSingleGPU).  Over the rank's local
+ * box of `level`; src and dst are DEVICE pointers of that many doubles, must not alias.
+ * Pure data movement (bit-exact).  Errors: TPMG_E_PARAM (direction, NULL, aliasing),
+ * TPMG_E_RANGE (level).  Asynchronous on the context stream. */
+typedef enum { TPMG_ZC_TO_LAMBDA = 0, TPMG_LAMBDA_TO_ZC = 1 } tpmg_layout_direction;
+tpmg_status tpmg_transpose(tpmg_ctx *ctx, int32_t level, int32_t direction, const double *src, double *dst);
+
+/* tpmg_solve_host with HOST buffers in the z-contiguous layout: the paper's "total solution
+ * time" path (tab:SingleGPUTiming's t_MemCpy+transpose): copy f in, transpose to
+ * Lambda on the device, solve, transpose u back, copy out.  Same arguments and errors as
+ * tpmg_solve_host.  COLLECTIVE. */
+tpmg_status tpmg_solve_host_zc(tpmg_ctx *ctx, tpmg_solver solver, const double *f_host,
+                               double *u_host, double eps, int32_t max_iter,
+                               tpmg_result *result);
+
 /* General vertical profiles a, b, c, d of eqn:LocalMatrixStencil ("derived
  * from the vertical stiffness- and mass-matrices", the same for every column and level),
  * e.g. a stretched vertical grid or height-dependent lambda / density:

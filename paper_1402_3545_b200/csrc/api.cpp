@@ -1823,6 +1823,43 @@ tpmg_status tpmg_solve_host(tpmg_ctx* ctx, tpmg_solver solver, const double* f_h
     return TPMG_OK;
 }
 
+tpmg_status tpmg_transpose(tpmg_ctx* ctx, int32_t level, int32_t direction, const double* src, double* dst)
+{
+    if (ctx) begin_call(ctx);
+    if (!ctx) return TPMG_E_PARAM;
+    TRY(check_level(ctx, level));
+    if (direction != TPMG_ZC_TO_LAMBDA && direction != TPMG_LAMBDA_TO_ZC)
+        return fail(ctx, TPMG_E_PARAM, "tpmg_transpose: direction must be TPMG_ZC_TO_LAMBDA or TPMG_LAMBDA_TO_ZC");
+    if (!src || !dst) return fail(ctx, TPMG_E_PARAM, "tpmg_transpose: NULL buffer");
+    if (src == dst) return fail(ctx, TPMG_E_PARAM, "tpmg_transpose: src and dst must not alias");
+    const LevelConst& L = ctx->lv[level].lc;
+    CUDA_TRY(ctx, launch_transpose(launcher(ctx), direction == TPMG_ZC_TO_LAMBDA, src, dst, L.nx, L.ny, L.nz));
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_solve_host_zc(tpmg_ctx* ctx, tpmg_solver solver, const double* f_host, double* u_host,
+                               double eps, int32_t max_iter, tpmg_result* res)
+{
+    if (ctx) begin_call(ctx);
+    if (!ctx) return TPMG_E_PARAM;
+    if (!f_host || !u_host) return fail(ctx, TPMG_E_PARAM, "tpmg_solve_host_zc: NULL buffer");
+    const LevelConst& L = ctx->lv[ctx->L].lc;
+    const size_t n = ctx->lv[ctx->L].n();
+    TRY(dev_alloc(ctx, &ctx->host_f, n));
+    TRY(dev_alloc(ctx, &ctx->host_u, n));
+    // host_u stages the z-contiguous f, host_f holds f in the Lambda layout; after the solve
+    // (u in host_u) host_f stages the z-contiguous u
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_u, f_host, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, launch_transpose(launcher(ctx), true, ctx->host_u, ctx->host_f, L.nx, L.ny, L.nz));
+    tpmg_status st = (solver == TPMG_SOLVER_MG) ? tpmg_solve_mg(ctx, ctx->host_f, ctx->host_u, eps, max_iter, res)
+                                                : tpmg_solve_cg(ctx, ctx->host_f, ctx->host_u, eps, max_iter, res);
+    if (st != TPMG_OK) return st;
+    CUDA_TRY(ctx, launch_transpose(launcher(ctx), false, ctx->host_u, ctx->host_f, L.nx, L.ny, L.nz));
+    CUDA_TRY(ctx, cudaMemcpyAsync(u_host, ctx->host_f, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return TPMG_OK;
+}
+
 tpmg_status tpmg_get_stats(const tpmg_ctx* ctx, tpmg_stats* out)
 {
     if (!ctx || !out) return TPMG_E_PARAM;

@@ -502,14 +502,16 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 
         if constexpr (T::THOMAS && GEN == 2) {
             // backward substitution per KB-level chunk: the chunk's t'_k recomputed from its
-            // checkpoint with the forward sweep's arithmetic, then x_k = g'_k - t'_k x_{k+1}.
-            // Software-pipelined: chunk c-1's pivots (independent of x) are recomputed in the
-            // same loop body as chunk c's x recurrence, so the two dependency chains overlap.
+            // checkpoint with the forward sweep's arithmetic, then x_k = g'_k - t'_k x_{k+1}
+            // (software-pipelining the next chunk's recompute into this loop measured slower:
+            // 1869 vs 1770 us for the fine-level smoother, more registers, same stalls)
             double* obase = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase;
-            auto recompute = [&](int c, double (&tq)[KB], double (&gv)[KB]) {
+            double x = 0.0;
+            for (int c = nck - 1; c >= 0; --c) {
                 const int kb0 = c * KB;
                 double p1 = c ? cbuf[c * NT + tid] : 1.0, p2 = c ? 1.0 : 0.0;
                 double t1 = c ? fT * ptab[2 * nz + kb0 - 1] : 0.0;
+                double tq[KB], gv[KB];
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
                     const int k = kb0 + q;
@@ -519,13 +521,6 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                         gv[q] = gbuf[k * NT + tid];
                     }
                 }
-            };
-            double x = 0.0;
-            double tq[KB], gv[KB], tq2[KB], gv2[KB];
-            recompute(nck - 1, tq, gv);
-            for (int c = nck - 1; c >= 0; --c) {
-                if (c > 0) recompute(c - 1, tq2, gv2);
-                const int kb0 = c * KB;
 #pragma unroll
                 for (int q = KB - 1; q >= 0; --q) {
                     const int k = kb0 + q;
@@ -533,11 +528,6 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                         x = fma(tq[q], x, gv[q]);
                         if (valid) obase[(int64_t)k * nx] = x;
                     }
-                }
-#pragma unroll
-                for (int q = 0; q < KB; ++q) {
-                    tq[q] = tq2[q];
-                    gv[q] = gv2[q];
                 }
             }
         }
@@ -958,6 +948,60 @@ cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a)
     case MODE_RESTRICT: return launch_line_t<MODE_RESTRICT, 4>(ln, a);
     default: return cudaErrorInvalidValue;
     }
+}
+
+// z-contiguous <-> Lambda layout ("transposing the fields from a z-contiguous data
+// format on the host to the x-contiguous format ... on the GPU", after Harris's tiled
+// transpose): for every row j the nx x nz block zc[j][i][k] is transposed to lam[j][k][i].
+// A 32 x 32 tile through shared memory (one padding column: no bank conflicts), both global
+// sides coalesced.  TO_LAMBDA: src zc, dst Lambda; else the reverse.
+template <bool TO_LAMBDA>
+__global__ void __launch_bounds__(256) k_transpose(const double* __restrict__ src, double* __restrict__ dst,
+                                                   int64_t nx, int nz)
+{
+    __shared__ double tile[32][33];
+    pdl_wait();
+    pdl_trigger();
+    const int64_t i0 = (int64_t)blockIdx.x * 32, j = blockIdx.z;
+    const int k0 = blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t slab = j * nx * (int64_t)nz;
+    if (TO_LAMBDA) {
+        // read: k fastest (zc), tile[i][k]
+        for (int r = ty; r < 32; r += 8) {
+            const int64_t i = i0 + r;
+            const int k = k0 + tx;
+            if (i < nx && k < nz) tile[r][tx] = src[slab + i * nz + k];
+        }
+        __syncthreads();
+        for (int r = ty; r < 32; r += 8) {
+            const int k = k0 + r;
+            const int64_t i = i0 + tx;
+            if (i < nx && k < nz) dst[slab + (int64_t)k * nx + i] = tile[tx][r];
+        }
+    } else {
+        // read: i fastest (Lambda), tile[k][i]
+        for (int r = ty; r < 32; r += 8) {
+            const int k = k0 + r;
+            const int64_t i = i0 + tx;
+            if (i < nx && k < nz) tile[r][tx] = src[slab + (int64_t)k * nx + i];
+        }
+        __syncthreads();
+        for (int r = ty; r < 32; r += 8) {
+            const int64_t i = i0 + r;
+            const int k = k0 + tx;
+            if (i < nx && k < nz) dst[slab + i * nz + k] = tile[tx][r];
+        }
+    }
+}
+
+cudaError_t launch_transpose(const Launcher& ln, bool to_lambda, const double* src, double* dst, int64_t nx,
+                             int64_t ny, int nz)
+{
+    if (nx <= 0 || ny <= 0 || nz <= 0) return cudaSuccess;
+    const dim3 grid((unsigned)((nx + 31) / 32), (unsigned)((nz + 31) / 32), (unsigned)ny), block(32, 8);
+    return to_lambda ? launch_kernel(ln, k_transpose<true>, grid, block, 0, src, dst, nx, nz)
+                     : launch_kernel(ln, k_transpose<false>, grid, block, 0, src, dst, nx, nz);
 }
 
 cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const LevelConst& coarse,

@@ -219,6 +219,9 @@ bool ksplit_supported(int mode, int nz, int nx);
 KsplitBoxes ksplit_boxes(int mode, int cfg);
 cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const LineArgs& a, const KTables& T);
 
+// z-contiguous (zc[j][i][k]) <-> Lambda (lam[j][k][i]) layout of an nx x ny x nz field
+cudaError_t launch_transpose(const Launcher& ln, bool to_lambda, const double* src, double* dst, int64_t nx,
+                             int64_t ny, int nz);
 // f_c = 1/4 sum of the 2x2 fine children of r (plain restriction)
 cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const LevelConst& coarse,
                             const double* r, double* fc);

@@ -70,6 +70,8 @@ _SIGS = {
     "tpmg_solve_mg": ([_vp, _vp, _vp, _d, _i32, _P(tpmg_result)], C.c_int),
     "tpmg_solve_cg": ([_vp, _vp, _vp, _d, _i32, _P(tpmg_result)], C.c_int),
     "tpmg_solve_host": ([_vp, C.c_int, _vp, _vp, _d, _i32, _P(tpmg_result)], C.c_int),
+    "tpmg_solve_host_zc": ([_vp, C.c_int, _vp, _vp, _d, _i32, _P(tpmg_result)], C.c_int),
+    "tpmg_transpose": ([_vp, _i32, _i32, _vp, _vp], C.c_int),
     "tpmg_get_stats": ([_vp, _P(tpmg_stats)], C.c_int),
     "tpmg_stats_reset": ([_vp], C.c_int),
     "tpmg_profile": ([_vp, _i32], C.c_int),
@@ -223,8 +225,22 @@ def tpmg_solve_cg(ctx: int, f, u, eps: float = 1e-5, max_iter: int = 1000) -> So
     return _to_py(res, hist)
 
 
+TPMG_ZC_TO_LAMBDA, TPMG_LAMBDA_TO_ZC = 0, 1
+
+
+def tpmg_transpose(ctx: int, level: int, direction: int, src, dst) -> None:
+    """z-contiguous <-> Lambda layout of a level's local box (device tensors)."""
+    _check(_lib.tpmg_transpose(ctx, level, direction, _ptr(src), _ptr(dst)), ctx)
+
+
+def tpmg_solve_host_zc(ctx: int, solver: int, f_host, u_host, eps: float = 1e-5,
+                       max_iter: int = 1000) -> SolveResult:
+    """tpmg_solve_host with z-contiguous host buffers (the paper's total-time path)."""
+    return tpmg_solve_host(ctx, solver, f_host, u_host, eps, max_iter, _fn="tpmg_solve_host_zc")
+
+
 def tpmg_solve_host(ctx: int, solver: int, f_host, u_host, eps: float = 1e-5,
-                    max_iter: int = 1000) -> SolveResult:
+                    max_iter: int = 1000, _fn: str = "tpmg_solve_host") -> SolveResult:
     """f_host / u_host: CPU torch tensors (pinned or pageable) or host addresses."""
     def hptr(x):
         if isinstance(x, int):
@@ -233,8 +249,8 @@ def tpmg_solve_host(ctx: int, solver: int, f_host, u_host, eps: float = 1e-5,
             raise ValueError("host buffers must be contiguous CPU tensors")
         return x.data_ptr()
     res, hist = _result(max_iter)
-    _check(_lib.tpmg_solve_host(ctx, solver, hptr(f_host), hptr(u_host), eps, max_iter,
-                                C.byref(res)), ctx)
+    _check(getattr(_lib, _fn)(ctx, solver, hptr(f_host), hptr(u_host), eps, max_iter,
+                              C.byref(res)), ctx)
     return _to_py(res, hist)
 
 
@@ -380,6 +396,12 @@ class Context:
 
     def solve_host(self, solver, f_host, u_host, eps=1e-5, max_iter=1000):
         return tpmg_solve_host(self.handle, solver, f_host, u_host, eps, max_iter)
+
+    def solve_host_zc(self, solver, f_host, u_host, eps=1e-5, max_iter=1000):
+        return tpmg_solve_host_zc(self.handle, solver, f_host, u_host, eps, max_iter)
+
+    def transpose(self, level, direction, src, dst):
+        tpmg_transpose(self.handle, level, direction, src, dst)
 
     def stats(self):
         return tpmg_get_stats(self.handle)
