@@ -404,6 +404,21 @@ def main():
         nbytes = fh.numel() * 8 * world
         e2e = {"value": solves * n_glob * args.steps / te, "unit": UNIT,
                "h2d_bytes_per_step": solves * nbytes, "d2h_bytes_per_step": solves * nbytes}
+        # the paper's "total solution time" (tab:SingleGPUTiming): z-contiguous host
+        # fields, H2D + transpose on the GPU + solve + transpose + D2H, one solve of each kind
+        fz = fh.view(shape).permute(0, 2, 1).contiguous().pin_memory()
+        uz = torch.empty_like(fz).pin_memory()
+        tz = {}
+        for name, sv, on in (("mg_ms", T.TPMG_SOLVER_MG, do_mg), ("cg_ms", T.TPMG_SOLVER_CG, do_cg)):
+            if not on:
+                continue
+            barrier()
+            t0 = time.perf_counter()
+            ctx.solve_host_zc(sv, fz, uz, eps=args.eps)
+            barrier()
+            tz[name] = 1e3 * (time.perf_counter() - t0)
+        e2e["total_solution_time_zc"] = dict(tz, note="wall ms per solve through tpmg_solve_host_zc: "
+                                             "z-contiguous host f in, transposes on the GPU, u out (P:427)")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
