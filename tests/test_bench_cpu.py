@@ -1,0 +1,43 @@
+"""bench.py contract on the host (no GPU): the reference arm's JSON line (the oracle timed
+on the host cores) and the product arm failing loudly without a GPU (no CPU
+fallback).  Tiny workload; the GPU arm's line is checked on the box (profiles/r1/*)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TINY = ["--per-gpu-nx", "64", "--nz", "16", "--steps", "1", "--warmup", "1"]
+
+
+def _run(args):
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, cwd=ROOT,
+                          capture_output=True, text=True, timeout=300)
+
+
+def test_reference_arm_json_line():
+    p = _run(["--impl", "reference"] + TINY)
+    assert p.returncode == 0, p.stderr
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    with open(os.path.join(ROOT, "BASELINE.json")) as fh:
+        metric = json.load(fh)["metric"]
+    assert d["impl"] == "reference" and d["metric"] == metric
+    assert d["value"] > 0 and d["higher_is_better"] is True and d["n_gpus"] == 1
+    assert (d["steps"], d["warmup"]) == (1, 1) and d["dtype"] == "f64"
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["value"] == d["value"] and cb["cores"] >= 1 and cb["sample"]
+    e = d["e2e"]
+    assert e["value"] == d["value"] and e["unit"] == d["unit"]
+    assert e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
+    assert (d["config"]["nx"], d["config"]["ny"], d["config"]["nz"]) == (64, 64, 16)
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU failure")
+def test_product_arm_fails_loudly_without_gpu():
+    p = _run(TINY)
+    assert p.returncode != 0
+    assert not [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
