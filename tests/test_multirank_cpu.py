@@ -133,3 +133,19 @@ def w_nccl_id_broadcast(rank, world):
 @pytest.mark.parametrize("fn", ["w_partition", "w_halo", "w_nccl_id_broadcast"])
 def test_world2_gloo(fn):
     _run(fn, 2)
+
+
+@pytest.mark.parametrize("nx,ny", [(1024, 8192), (2048, 16384), (4096, 4096)])
+def test_partition_world8_bench_shapes(nx, ny):
+    # The driver's N = 8 scaling run (bench.py workload(): weak 1024^2 / 2048^2 per GPU,
+    # strong 4096^2): every level splits into 8 contiguous y-strips covering the grid.
+    from paper_1402_3545_b200 import build
+    build.build()
+    from paper_1402_3545_b200 import tpmg as T
+    p = T.make_params(nx, ny, nz=128)
+    for level in range(1, 6):
+        boxes = [T.tpmg_partition(p, r, 8, level) for r in range(8)]
+        assert boxes[0][0] == 0 and all(n > 0 for _, n in boxes)
+        for (a0, an), (b0, _) in zip(boxes, boxes[1:]):
+            assert a0 + an == b0
+        assert boxes[-1][0] + boxes[-1][1] == ny >> (5 - level)
