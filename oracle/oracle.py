@@ -24,10 +24,15 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "tpmg_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# scripts/oracle_mutation.py points this at a deliberately broken build of the oracle to
+# show that the pins catch the mutation (the default is the real oracle)
+_LIB_OVERRIDE = os.environ.get("TPMG_ORACLE_LIB")
 
 
 def build(force: bool = False) -> str:
     """Compile the oracle (plain C, fp64, -ffp-contract=off, OpenMP over columns)."""
+    if _LIB_OVERRIDE:
+        return _LIB_OVERRIDE
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(
             ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fopenmp",
@@ -141,6 +146,7 @@ def lib():
             "or_api_prolong_add": [P, C.c_int, _dp, _dp],
             "or_api_thomas": [C.c_int, _dp, _dp, _dp, _dp, _dp],
             "or_vcycle": [P, _dp, _dp],
+            "or_api_vcycle_trace": [P, _dp, _dp, np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")],
             "or_solve_mg": [P, _dp, _dp, C.c_double, C.c_int, C.POINTER(C.c_int),
                             C.POINTER(C.c_int), _dp, C.c_int],
             "or_solve_cg": [P, _dp, _dp, C.c_double, C.c_int, C.POINTER(C.c_int),
@@ -287,6 +293,18 @@ def vcycle(p: Params, u, f):
     u = _arr(u, p.level_shape(p.L)).copy(); f = _arr(f, p.level_shape(p.L))
     _check(lib().or_vcycle(C.byref(p.c()), u, f), "vcycle")
     return u
+
+
+TRACE_KINDS = ("Smooth", "ResSmooth", "Residual", "Prolongate")   # tab:TimingBreakdownMultigrid rows
+
+
+def vcycle_trace(p: Params, u, f):
+    """One V-cycle plus its kernel-call trace: (u_new, counts) with counts[l][kind] the number
+    of calls of TRACE_KINDS[kind] on level l (l = 1 coarsest .. L finest; row 0 unused)."""
+    u = _arr(u, p.level_shape(p.L)).copy(); f = _arr(f, p.level_shape(p.L))
+    counts = np.zeros((p.L + 1, len(TRACE_KINDS)), dtype=np.int32)
+    _check(lib().or_api_vcycle_trace(C.byref(p.c()), u, f, counts), "vcycle_trace")
+    return u, counts
 
 
 @dataclass

@@ -528,9 +528,21 @@ static size_t or_size(const or_op *op)
     return (size_t)op->nx * (size_t)op->ny * (size_t)op->nz;
 }
 
+/* Kernel-call trace of the V-cycle (test instrumentation only, no arithmetic): when
+ * or_trace_counts is set, counts[OR_NK * l + kind] is incremented once per kernel of
+ * alg:VCycle that runs on level l, with the kernel names of
+ * tab:TimingBreakdownMultigrid. */
+enum { OR_K_SMOOTH = 0, OR_K_RESSMOOTH = 1, OR_K_RESIDUAL = 2, OR_K_PROLONGATE = 3, OR_NK = 4 };
+static int *or_trace_counts = NULL;
+static inline void or_trace(int l, int kind)
+{
+    if (or_trace_counts) or_trace_counts[OR_NK * l + kind] += 1;
+}
+
 /* In-place smoother on level l: u^(l) <- u + rho M^{-1}(f - A u). */
 static int or_mg_smooth(or_mg *mg, int l)
 {
+    or_trace(l, OR_K_SMOOTH);
     int st = or_smooth(&mg->op[l], mg->u[l], mg->f[l], mg->p.rho, mg->tmp[l]);
     memcpy(mg->u[l], mg->tmp[l], sizeof(double) * or_size(&mg->op[l]));
     return st;
@@ -540,6 +552,7 @@ static int or_mg_smooth(or_mg *mg, int l)
  * i.e. one smoother step from the zero initial guess of P:278. */
 static int or_mg_restrict_smooth(or_mg *mg, int l)
 {
+    or_trace(l, OR_K_RESSMOOTH);
     or_restrict(&mg->op[l + 1], &mg->op[l], mg->r[l + 1], mg->f[l]);
     int st = or_precondition(&mg->op[l], mg->f[l], mg->u[l]);
     size_t n = or_size(&mg->op[l]);
@@ -575,10 +588,12 @@ static int or_vcycle_rec(or_mg *mg, int l)
         for (int s = 1; s < mg->p.pre; ++s) st |= or_mg_smooth(mg, l);
     }
     /* Calculate residual */
+    or_trace(l, OR_K_RESIDUAL);
     or_residual(&mg->op[l], mg->u[l], mg->f[l], mg->r[l]);
     /* Recursive call */
     st |= or_vcycle_rec(mg, l - 1);
     /* Add prolongated coarse grid correction */
+    or_trace(l, OR_K_PROLONGATE);
     or_prolong_add(&mg->op[l - 1], &mg->op[l], mg->u[l - 1], mg->u[l]);
     /* Postsmoothing */
     for (int s = 0; s < mg->p.post; ++s) st |= or_mg_smooth(mg, l);
@@ -595,6 +610,18 @@ int or_vcycle(const or_params *p, double *u, const double *f)
     mg.f[p->L] = (double *)f;
     st = or_vcycle_rec(&mg, p->L);
     or_mg_free(&mg);
+    return st;
+}
+
+/* One V-cycle (as or_vcycle) with the kernel-call trace: counts has OR_NK * (L + 1)
+ * entries, zeroed here; counts[OR_NK * l + kind] = calls of `kind` on level l. */
+int or_api_vcycle_trace(const or_params *p, double *u, const double *f, int *counts)
+{
+    if (p->L < 1 || p->L > 32) return OR_E_PARAM;
+    memset(counts, 0, sizeof(int) * (size_t)(OR_NK * (p->L + 1)));
+    or_trace_counts = counts;
+    int st = or_vcycle(p, u, f);
+    or_trace_counts = NULL;
     return st;
 }
 
