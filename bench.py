@@ -181,65 +181,174 @@ def strip_fields(fields, rows):
 
 
 def oracle_sample(nx, nz, nu, rows, seed, threads=None, levels=5, coarse_sweeps=2, boundary=0, profiles=None,
-                  fields=None):
-    """Time the CPU oracle (as it stands) on a y-strip of `rows` rows of the workload:
-    one MG V-cycle (solve_mg, max_iter=1: norm + V-cycle + residual) and one PCG
-    iteration (solve_cg, max_iter=1: setup preconditioner + one iteration)."""
+                  fields=None, mg_iter=1, cg_iter=1, eps=1e-30, f=None):
+    """Time the CPU oracle (as it stands) on a y-strip of `rows` rows of the workload (rows =
+    ny: the whole grid): an MG solve of at most mg_iter V-cycles (r0 norm + cycles + residual
+    each) and a PCG solve of at most cg_iter iterations (setup + iterations).  Returns
+    (t_mg, t_cg, threads, mg_iterations, cg_iterations)."""
     from oracle import oracle as O
     from inputs import rhs_zc
     if threads:
         O.set_threads(threads)
     p = O.Params(nx=nx, ny=rows, nz=nz, nu_cfl=nu, L=levels, coarse_sweeps=coarse_sweeps, boundary=boundary,
                  profiles=profiles, fields=fields)
-    f = rhs_zc(nx, rows, nz, seed=seed)
+    if f is None:
+        f = rhs_zc(nx, rows, nz, seed=seed)
     t0 = time.perf_counter()
-    O.solve_mg(p, f, eps=1e-30, max_iter=1)
+    rm = O.solve_mg(p, f, eps=eps, max_iter=mg_iter) if mg_iter else None
     t1 = time.perf_counter()
-    O.solve_cg(p, f, eps=1e-30, max_iter=1)
+    rc = O.solve_cg(p, f, eps=eps, max_iter=cg_iter) if cg_iter else None
     t2 = time.perf_counter()
-    return t1 - t0, t2 - t1, O.num_threads()
+    return t1 - t0, t2 - t1, O.num_threads(), rm and rm.iterations, rc and rc.iterations
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_counts(args, nx, ny):
+    """Iterations of the ORACLE's own full MG and PCG solves of this workload to 1e-5
+    (tests/golden/oracle_iterations.json, written by scripts/oracle_iterations.py, which calls
+    only oracle/): (mg, cg, source) or None when the workload has no entry."""
+    key = (f"{nx}x{ny}x{args.nz}_nu{args.nu:g}_L{args.levels}_cs{args.coarse_sweeps}_bc{args.boundary}"
+           f"_seed{args.seed}")
+    if args.profiles >= 0 or args.fields != "none":
+        return None
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "oracle_iterations.json")) as fh:
+            rec = json.load(fh)[key]
+        return rec["mg"]["iterations"], rec["cg"]["iterations"], f"oracle full solves of {key} (tests/golden/oracle_iterations.json)"
+    except Exception:
+        return None
+
+
+def _counts(args, nx, ny, gpu_counts):
+    cnt = oracle_counts(args, nx, ny)
+    if cnt is not None:
+        return cnt
+    it_mg, it_cg = gpu_counts or (10, 54)
+    return it_mg, it_cg, "this run's GPU iteration counts (no oracle full-solve entry for this workload)"
+
+
+def oracle_step_sample(args, nx, ny, do_mg, do_cg, gpu_counts=None, rows_mg=64, rows_cg=32, threads=None):
+    """One bounded sample of the workload for the oracle: the oracle's own full iteration
+    counts of the workload (oracle_counts) run on y-strips of it -- an MG solve of exactly
+    it_mg V-cycles on nx x rows_mg and a PCG solve of exactly it_cg iterations on nx x rows_cg
+    (setup amortised as in the whole solve) -- each scaled by ny/rows in cells.  Returns
+    (value, extrapolated seconds per step, description)."""
+    it_mg, it_cg, src = _counts(args, nx, ny, gpu_counts)
+    t = 0.0
+    parts = []
+    cores = None
+    for on, rows, mg_iter, cg_iter, what in ((do_mg, rows_mg, it_mg, 0, "solve_mg"), (do_cg, rows_cg, 0, it_cg, "solve_cg")):
+        if not on:
+            continue
+        rows = min(rows, ny)
+        flds = strip_fields(bench_fields(args, nx, ny), rows)
+        a, b, cores, im, ic = oracle_sample(nx, args.nz, args.nu, rows, args.seed, threads=threads,
+                                            levels=args.levels, coarse_sweeps=args.coarse_sweeps,
+                                            boundary=args.boundary, profiles=bench_profiles(args), fields=flds,
+                                            mg_iter=mg_iter, cg_iter=cg_iter, eps=1e-300)
+        dt = a + b
+        t += dt * ny / rows
+        parts.append(f"{what} of exactly {im or ic} iterations on a {nx}x{rows}x{args.nz} y-strip: {dt:.3f} s "
+                     f"(x{ny / rows:g} in cells)")
+    solves = int(do_mg) + int(do_cg)
+    desc = {"cores": cores, "sample": "oracle " + "; ".join(parts) + f"; iteration counts: {src}"}
+    return solves * nx * ny * args.nz / t, t, desc
+
+
+def cpu_baseline_block(args, nx, ny, do_mg, do_cg, gpu_counts=None):
+    """cpu_baseline (rank 0, N = 1): the oracle as it stands on all host cores -- the whole MG
+    solve of the workload to eps MEASURED (its own iteration count), the PCG solve's full
+    iteration count run on a y-strip (oracle_step_sample) -- plus a one-thread sample and the
+    CPU model."""
+    from oracle import oracle as O
+    a = 0.0
+    it_mg = None
+    cores = O.num_threads()
+    if do_mg:
+        a, _, cores, it_mg, _ = oracle_sample(nx, args.nz, args.nu, ny, args.seed, levels=args.levels,
+                                              coarse_sweeps=args.coarse_sweeps, boundary=args.boundary,
+                                              profiles=bench_profiles(args), fields=bench_fields(args, nx, ny),
+                                              mg_iter=50, cg_iter=0, eps=args.eps)
+    t_cg, d_cg = 0.0, None
+    if do_cg:
+        _, t_cg, d_cg = oracle_step_sample(args, nx, ny, False, True, gpu_counts)
+    t = a + t_cg
+    solves = int(do_mg) + int(do_cg)
+    v_all = solves * nx * ny * args.nz / t
+    v_one, t_one, d_one = oracle_step_sample(args, nx, ny, do_mg, do_cg, gpu_counts, rows_mg=32, rows_cg=16,
+                                             threads=1)
+    O.set_threads(cores)   # restore
+    sample = []
+    if do_mg:
+        sample.append(f"oracle solve_mg to {args.eps:g} on the whole {nx}x{ny}x{args.nz} grid: {a:.2f} s, "
+                      f"{it_mg} V-cycles (measured)")
+    if do_cg:
+        sample.append(d_cg["sample"] + f" = {t_cg:.2f} s")
+    return {"value": v_all, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "method": "MG: whole solve measured; PCG: its full iteration count measured on a y-strip, x cells",
+            "cpu_model": cpu_model(), "host_threads": os.cpu_count(), "sample": "; ".join(sample),
+            "seconds_per_step": round(t, 2),
+            "one_thread": {"value": v_one, "unit": UNIT, "cores": 1, "seconds_per_step": round(t_one, 2),
+                           "sample": d_one["sample"]},
+            "speedup_all_cores_vs_one": round(v_all / v_one, 2)}
 
 
 def run_reference(args):
-    """--impl reference: the oracle, as it stands, on the host cores (rank 0 only)."""
+    """--impl reference: the oracle, as it stands, on the host cores (rank 0 only).  Each
+    step is one bounded sample of the workload (oracle_step_sample: the oracle's whole MG and
+    PCG iteration counts on y-strips)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     nx, ny, name = workload(args, world)
-    rows = max(32, 1 << (args.levels - 1))
-    scale = ny / rows
-    it_mg, it_cg = 9, 51  # iteration counts of the oracle at 128^2 x 128 (tests/test_oracle_pins)
-    flds = strip_fields(bench_fields(args, nx, ny), rows)
+    do_mg = args.solver in ("both", "mg")
+    do_cg = args.solver in ("both", "cg")
     for _ in range(args.warmup):
-        oracle_sample(nx, args.nz, args.nu, rows, args.seed, levels=args.levels,
-                     coarse_sweeps=args.coarse_sweeps, boundary=args.boundary,
-                     profiles=bench_profiles(args), fields=flds)
+        oracle_step_sample(args, nx, ny, do_mg, do_cg)
     t = 0.0
     wall = 0.0
+    desc = None
     for _ in range(args.steps):
         w0 = time.perf_counter()
-        a, b, cores = oracle_sample(nx, args.nz, args.nu, rows, args.seed, levels=args.levels,
-                     coarse_sweeps=args.coarse_sweeps, boundary=args.boundary,
-                     profiles=bench_profiles(args), fields=flds)
+        _, ts, desc = oracle_step_sample(args, nx, ny, do_mg, do_cg)
         wall += time.perf_counter() - w0
-        t += scale * (it_mg * a + it_cg * b)
-    N = nx * ny * args.nz
-    value = 2 * N * args.steps / t
-    sample = (f"per step: oracle MG solve with max_iter=1 (norm + 1 V-cycle + residual) and PCG solve "
-              f"with max_iter=1 (setup + 1 iteration) on a {nx}x{rows}x{args.nz} y-strip of the workload; "
-              f"scaled x{scale:g} in cells and x{it_mg}/x{it_cg} in iterations (oracle counts, size-independent P:421)")
+        t += ts
+    solves = int(do_mg) + int(do_cg)
+    value = solves * nx * ny * args.nz * args.steps / t
+    cpu = {"value": value, "unit": UNIT, "cores": desc["cores"], "kind": "oracle",
+           "method": "per step: the oracle's full iteration counts of the workload measured on y-strips, x cells",
+           "cpu_model": cpu_model(), "host_threads": os.cpu_count(),
+           "seconds_per_step": round(t / args.steps, 2), "sample": "per step: " + desc["sample"]}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
         "extrapolated_ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": "strong" if args.global_nx else "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (splitmix64 RHS, seed %d)" % args.seed,
-        "config": {"workload": name, "nx": nx, "ny": ny, "nz": args.nz, "nu_cfl": args.nu, "eps": args.eps,
-                   "levels": args.levels, "coarse_sweeps": args.coarse_sweeps, "boundary": args.boundary},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "data": "synthetic (splitmix64 uniform[-1,1) RHS keyed by global index, seed %d)" % args.seed,
+        "config": config_block(args, nx, ny, name, world),
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def config_block(args, nx, ny, name, world):
+    return {"workload": name, "nx": nx, "ny": ny, "nz": args.nz, "nu_cfl": args.nu, "eps": args.eps,
+            "levels": args.levels, "coarse_sweeps": args.coarse_sweeps, "boundary": args.boundary,
+            "solver": args.solver,
+            "vertical_profiles": "flat box" if args.profiles < 0 else f"synthetic seed {args.profiles}",
+            "horizontal_fields": "uniform" if args.fields == "none" else f"{args.fields} seed 1",
+            "parallelism": f"y-strips x{world}" if world > 1 else "single GPU",
+            "l2": "vectors 1 GiB/GPU >> 126 MB L2 (no flush needed)"}
 
 
 # ---------------------------------------------------------------------------- GPU arm
@@ -411,31 +520,21 @@ def main():
         fz = fh.view(shape).permute(0, 2, 1).contiguous().pin_memory()
         uz = torch.empty_like(fz).pin_memory()
         tz = {}
-        for name, sv, on in (("mg_ms", T.TPMG_SOLVER_MG, do_mg), ("cg_ms", T.TPMG_SOLVER_CG, do_cg)):
+        for key, sv, on in (("mg_ms", T.TPMG_SOLVER_MG, do_mg), ("cg_ms", T.TPMG_SOLVER_CG, do_cg)):
             if not on:
                 continue
             barrier()
             t0 = time.perf_counter()
             ctx.solve_host_zc(sv, fz, uz, eps=args.eps)
             barrier()
-            tz[name] = 1e3 * (time.perf_counter() - t0)
+            tz[key] = 1e3 * (time.perf_counter() - t0)
         e2e["total_solution_time_zc"] = dict(tz, note="wall ms per solve through tpmg_solve_host_zc: "
                                              "z-contiguous host f in, transposes on the GPU, u out (P:427)")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rows = max(128, 1 << (args.levels - 1))
-        a, b, cores = oracle_sample(nx, nz, args.nu, rows, args.seed, levels=args.levels,
-                                       coarse_sweeps=args.coarse_sweeps, boundary=args.boundary,
-                     profiles=bench_profiles(args), fields=strip_fields(flds, rows))
-        scale = ny / rows
-        it_mg = its[0].iterations if its[0] else 0
-        it_cg = its[1].iterations if its[1] else 0
-        t_est = scale * ((it_mg * a if do_mg else 0) + (it_cg * b if do_cg else 0))
-        cpu = {"value": solves * n_glob / t_est, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": (f"oracle MG solve max_iter=1 ({a:.2f} s) and PCG solve max_iter=1 ({b:.2f} s) on a "
-                          f"{nx}x{rows}x{nz} y-strip of the workload, scaled x{scale:g} in cells and by the "
-                          f"iteration counts of this run ({it_mg} V-cycles, {it_cg} CG iterations)")}
+        gpu_counts = (its[0].iterations if its[0] else 0, its[1].iterations if its[1] else 0)
+        cpu = cpu_baseline_block(args, nx, ny, do_mg, do_cg, gpu_counts)
 
     if rank == 0:
         line = {
@@ -443,12 +542,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if args.global_nx else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (splitmix64 uniform[-1,1) RHS keyed by global index, seed %d)" % args.seed,
-            "config": {"workload": name, "nx": nx, "ny": ny, "nz": nz, "nu_cfl": args.nu, "eps": args.eps,
-                       "levels": args.levels, "coarse_sweeps": args.coarse_sweeps, "boundary": args.boundary,
-                       "vertical_profiles": "flat box" if args.profiles < 0 else f"synthetic seed {args.profiles}",
-                       "horizontal_fields": "uniform" if args.fields == "none" else f"{args.fields} seed 1",
-                       "parallelism": f"y-strips x{world}" if world > 1 else "single GPU",
-                       "l2": "vectors 1 GiB/GPU >> 126 MB L2 (no flush needed)"},
+            "config": config_block(args, nx, ny, name, world),
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

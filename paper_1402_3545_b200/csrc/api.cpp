@@ -111,6 +111,7 @@ struct tpmg_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // profiling (tpmg_profile)
     bool pdl = false;                   // programmatic dependent launches (TPMG_PDL=1)
+    bool tmem = true;                   // Thomas g' of the column kernels in Tensor Memory (TPMG_TMEM=0: smem)
     bool ksplit_cg = false;             // k-split CG preconditioner (TPMG_KSPLIT_CG=1)
     bool halo_off = false;              // TPMG_HALO=off: skip halo exchanges (timing experiments)
     bool fused_push = false;            // P2P: producers push their boundary rows (TPMG_FUSED_PUSH=1)
@@ -176,6 +177,7 @@ Launcher launcher(tpmg_ctx* ctx)
     ln.launch_counter = &ctx->stats.kernel_launches;
     ln.reserve_sms = ctx->cur_reserve;
     ln.pdl = ctx->pdl;
+    ln.tmem = ctx->tmem;
     return ln;
 }
 
@@ -1575,6 +1577,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->fuse_prolong = fp && fp[0] == '1';
         const char* sd = std::getenv("TPMG_SYNC_DEBUG");
         ctx->sync_debug = sd && sd[0] == '1';
+        const char* tm = std::getenv("TPMG_TMEM");   // "0": g' of the column kernels in shared memory
+        ctx->tmem = !(tm && tm[0] == '0');
     }
     ctx->ny_loc = p.ny / nranks;
     ctx->y0 = (int64_t)rank * ctx->ny_loc;

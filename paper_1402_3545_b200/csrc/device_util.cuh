@@ -118,6 +118,64 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// ------------------------------------------------------------------ Tensor Memory (TMEM)
+// The line kernels use TMEM (512 columns x 128 lanes x 32 bit per SM) as per-thread scratch
+// for the Thomas intermediates g'_k: thread t of warp w owns lane 32 w + t, level k sits in
+// columns 2k, 2k+1 (lo, hi word of the double).  A warp may only touch its own 32-lane
+// quarter (warp w % 4), so the kernels that use it have 4 warps per CTA.  Allocation: one
+// warp, power of two >= 32 columns, address written to shared memory; the same warp frees.
+template <uint32_t NCOL>
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot)
+{
+    static_assert(NCOL >= 32 && NCOL <= 512 && (NCOL & (NCOL - 1)) == 0, "TMEM columns: power of two in [32, 512]");
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(slot)),
+                 "n"(NCOL)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+template <uint32_t NCOL>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr)
+{
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(NCOL) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+// one double into columns col, col+1 of this thread's lane (asynchronous; tmem_wait_st orders it)
+__device__ __forceinline__ void tmem_st_f64(uint32_t taddr, double v)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(taddr), "r"(__double2loint(v)),
+                 "r"(__double2hiint(v))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+// 8 doubles from columns col .. col+15 of this thread's lane; the wait is in the same asm
+// statement, so no use of the registers can be scheduled before the data has arrived
+__device__ __forceinline__ void tmem_ld_f64x8(uint32_t taddr, double (&v)[8])
+{
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __hiloint2double((int)r[2 * q + 1], (int)r[2 * q]);
+}
+__device__ __forceinline__ double tmem_ld_f64(uint32_t taddr)
+{
+    uint32_t lo, hi;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "=r"(lo), "=r"(hi)
+        : "r"(taddr)
+        : "memory");
+    return __hiloint2double((int)hi, (int)lo);
+}
+
 // Dynamic shared memory available to a kernel: the opt-in maximum minus its static smem.
 template <typename K>
 size_t dyn_smem_limit(K kern)

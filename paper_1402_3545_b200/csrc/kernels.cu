@@ -162,10 +162,16 @@ __device__ __forceinline__ void tma_stage(double* st, const LineArgs& a, int64_t
 // to (p_{k-1}, p_{k-2}) = (m_{k-1}, 1), and checkpoints m_{k-1} there next to g'_k in shared
 // memory ((nz + nz/KB) * 8 bytes per column).  The backward sweep recomputes each chunk's
 // pivots from its checkpoint with the same arithmetic instead of keeping all nz on chip.
-template <int MODE, int TY, int LOADER, int GEN>
+// TM: the Thomas intermediates g'_k live in Tensor Memory instead of shared memory (flat box,
+// 4 warps = the 4 TMEM lane quarters, nz <= 128): the 8*nz bytes per column of shared memory
+// that held one CTA per SM leave room for two, i.e. twice the warps to hide the recurrences'
+// latency; TMEM itself (256 columns = 128 levels per CTA) holds exactly two CTAs.
+constexpr uint32_t kTmemCols = 256;
+template <int MODE, int TY, int LOADER, int GEN, bool TM = false>
 __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArgs a)
 {
     using T = Traits<MODE>;
+    static_assert(!TM || (TY == 4 && GEN == 0 && T::THOMAS), "TMEM g' buffer: 4 warps, flat box, Thomas modes");
     constexpr int NH = T::NH, NP = T::NP, NR = T::NR;
     using G = Geom<NH, NP, TY>;
     constexpr int NT = G::NT;
@@ -188,7 +194,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     double* cbuf = gbuf + nz * NT;           // GEN 2: m_{c KB - 1}[nck][NT], the pivot checkpoints
     // MODE_RESTRICT: x-pair sums [2][TY][KB+1][TX/2] (a chunk completes up to KB+1 levels)
     constexpr int RS = KB + 1;
-    double* rbuf = gbuf + (T::THOMAS ? (nz + (GEN == 2 ? nck : 0)) * NT : 0);
+    double* rbuf = gbuf + ((T::THOMAS && !TM) ? (nz + (GEN == 2 ? nck : 0)) * NT : 0);
     double* scratch = rbuf + (MODE == MODE_RESTRICT ? 2 * TY * RS * (TX / 2) : 0);  // reduction scratch
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
@@ -227,7 +233,17 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     const int nch = (nz + KB - 1) / KB;
     const int my_tiles = ((int)blockIdx.x < ntiles) ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
     const int total = my_tiles * nch;
+    __shared__ uint32_t tmem_slot;
+    if constexpr (TM) {
+        if (ty == 0) tmem_alloc<kTmemCols>(&tmem_slot);
+        tmem_fence_before();
+    }
     __syncthreads();
+    uint32_t tbase = 0;   // TM: this warp's lane quarter, column 0
+    if constexpr (TM) {
+        tmem_fence_after();
+        tbase = tmem_slot + ((uint32_t)(ty * 32) << 16);
+    }
 
     // producer cursor: next chunk to load
     int p_count = 0, p_ch = 0, p_slot = 0, p_tile = blockIdx.x;
@@ -402,7 +418,10 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 }
                 const double y = fma(-sk, gprev, g);     // y = L^-1 g   (M = L D L^T; sub-diagonal s_k)
                 const double gp = y * imk;               // g'_k = (g_k - s_k g'_{k-1}) / m_k
-                *gslot = gp;
+                if constexpr (TM)
+                    tmem_st_f64(tbase + 2u * (uint32_t)km, gp);
+                else
+                    *gslot = gp;
                 if constexpr (MODE == MODE_CGPREC)
                     if (valid) acc[1] = fma(gp, y, acc[1]);   // <g, M^-1 g> = sum y_k^2 / m_k
                 gprev = gp;
@@ -537,13 +556,21 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             double* op = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase + (int64_t)(nz - 1) * nx;
             double x = 0.0;
             int k = nz - 1;
+            if constexpr (TM) tmem_wait_st();   // the forward sweep's g' stores have landed
             for (; k >= KB - 1; k -= KB) {
                 const double* gq = gbuf + (k - (KB - 1)) * NT + tid;   // levels k-KB+1 .. k
                 const double* mq = gim + (k - (KB - 1));
                 double gv[KB], gm[KB];
+                if constexpr (TM) {
+                    static_assert(KB == 8, "tmem_ld_f64x8 loads 8 levels");
+                    double g8[KB];
+                    tmem_ld_f64x8(tbase + 2u * (uint32_t)(k - (KB - 1)), g8);
+#pragma unroll
+                    for (int q = 0; q < KB; ++q) gv[q] = g8[KB - 1 - q];
+                }
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
-                    gv[q] = gq[(KB - 1 - q) * NT];
+                    if constexpr (!TM) gv[q] = gq[(KB - 1 - q) * NT];
                     gm[q] = mq[KB - 1 - q];
                 }
 #pragma unroll
@@ -554,7 +581,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 }
             }
             for (; k >= 0; --k) {
-                x = fma(gim[k], x, gbuf[k * NT + tid]);
+                x = fma(gim[k], x, TM ? tmem_ld_f64(tbase + 2u * (uint32_t)k) : gbuf[k * NT + tid]);
                 if (valid) *op = x;
                 op -= nx;
             }
@@ -593,27 +620,35 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             tile_body(std::false_type{}, tl);
     }
     if constexpr (LOADER == 0) cp_async_wait<0>();
+    if constexpr (TM) {   // every warp is done with its lanes; the allocating warp frees them
+        tmem_fence_before();
+        __syncthreads();
+        if (ty == 0) {
+            tmem_fence_after();
+            tmem_dealloc<kTmemCols>(tmem_slot);
+        }
+    }
     if (want_red) grid_reduce<NR>(a.red, acc, scratch);
 }
 
 template <int MODE, int TY>
-size_t line_smem_bytes(int nz, int gen = 0)
+size_t line_smem_bytes(int nz, int gen = 0, bool tm = false)
 {
     using T = Traits<MODE>;
     using G = Geom<T::NH, T::NP, TY>;
     size_t d = ((3 * nz + 15) & ~15) + (gen >= 2 ? ((4 * nz + 15) & ~15) : gen ? ((3 * nz + 15) & ~15) : 0) +
-               (size_t)(gen == 2 ? stages<MODE, 2>() : kNS) * G::STAGE + (T::THOMAS ? (size_t)(nz + (gen == 2 ? (nz + KB - 1) / KB : 0)) * G::NT : 0) + 64 + 16 +
+               (size_t)(gen == 2 ? stages<MODE, 2>() : kNS) * G::STAGE + ((T::THOMAS && !tm) ? (size_t)(nz + (gen == 2 ? (nz + KB - 1) / KB : 0)) * G::NT : 0) + 64 + 16 +
                (MODE == MODE_RESTRICT ? 2 * TY * (KB + 1) * (TX / 2) : 0);
     return d * sizeof(double);
 }
 
 constexpr size_t kMaxSmem = 227 * 1024 - 1024;  // leave room for static smem (barriers, flags)
 
-template <int MODE, int TY, int LOADER, int GEN>
+template <int MODE, int TY, int LOADER, int GEN, bool TM = false>
 cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
 {
-    const size_t smem = line_smem_bytes<MODE, TY>(a.L.nz, GEN);
-    auto kern = k_line<MODE, TY, LOADER, GEN>;
+    const size_t smem = line_smem_bytes<MODE, TY>(a.L.nz, GEN, TM);
+    auto kern = k_line<MODE, TY, LOADER, GEN, TM>;
     static size_t limit = 0;   // per instantiation
     if (!limit) {
         limit = dyn_smem_limit(kern);
@@ -625,6 +660,7 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TX * TY, smem);
     if (e != cudaSuccess) return e;
     per_sm = std::max(per_sm, 1);
+    if (TM) per_sm = std::min<int>(per_sm, 512 / kTmemCols);   // resident CTAs must all get their TMEM
     const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * part_rows(a.part, (int)((a.L.ny + TY - 1) / TY));
     // CG direction (two halo'd fields): on wide grids two CTAs per SM re-read the halo
     // rows from HBM (2.1x the algorithmic reads at 4096 x 1024 x 128, ncu); one CTA per SM
@@ -643,12 +679,15 @@ cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
         if (!a.use_tma) return cudaErrorNotSupported;
         return a.L.gen >= 2 ? launch_line_l<MODE, TY, 1, 2>(ln, a) : launch_line_l<MODE, TY, 1, 1>(ln, a);
     }
+    if constexpr (Traits<MODE>::THOMAS && TY == 4)   // g' in Tensor Memory (flat box, TMA loader)
+        if (ln.tmem && a.use_tma && a.L.nz <= (int)(kTmemCols / 2)) return launch_line_l<MODE, 4, 1, 0, true>(ln, a);
     return a.use_tma ? launch_line_l<MODE, TY, 1, 0>(ln, a) : launch_line_l<MODE, TY, 0, 0>(ln, a);
 }
 
 template <int MODE>
 cudaError_t launch_line_ty(const Launcher& ln, const LineArgs& a)
 {
+    if (ln.tmem && a.use_tma && !a.L.gen && a.L.nz <= (int)(kTmemCols / 2)) return launch_line_t<MODE, 4>(ln, a);
     if (line_smem_bytes<MODE, 4>(a.L.nz, a.L.gen) <= kMaxSmem) return launch_line_t<MODE, 4>(ln, a);
     if (line_smem_bytes<MODE, 2>(a.L.nz, a.L.gen) <= kMaxSmem) return launch_line_t<MODE, 2>(ln, a);
     return launch_line_t<MODE, 1>(ln, a);

@@ -165,6 +165,7 @@ struct Launcher {
     int reserve_sms;   // SMs left free (for NCCL kernels running concurrently)
     bool pdl = false;  // programmatic dependent launch: overlap a kernel's launch and
                        // prologue with the previous kernel's tail (griddepcontrol)
+    bool tmem = true;  // one-thread-per-column Thomas kernels keep g' in Tensor Memory (nz <= 128)
 };
 
 // Launch with the PDL attribute when ln.pdl.  Every kernel launched this way executes
