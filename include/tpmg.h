@@ -5,8 +5,8 @@
  * solvers for anisotropic PDEs on GPU clusters" (arXiv:1402.3545).
  *
  * Citations "P:n" are lines of the paper's text; equation and
- * algorithm names are the paper's LaTeX labels.  DESIGN.md lists every
- * reading of the paper the library makes ([R1]..[R20]).
+ * algorithm names are the paper's LaTeX labels.  DESIGN.md section 3 lists
+ * every reading of the paper the library makes ([R1]..[R26]).
  *
  * ----------------------------------------------------------------------------
  * Problem (flat-box instance of eqn:ModelEquation):
@@ -41,9 +41,9 @@
  * every rank with matching arguments; the others are rank-local.
  *
  * Ownership: the caller owns every vector and the tpmg_result.history array;
- * the library owns the context, halo slabs, multigrid and CG work vectors,
- * the NCCL communicator and CUDA graphs.  No caller pointer is retained after
- * a call returns.
+ * the library owns the context, halo slabs, multigrid and CG work vectors
+ * and the NCCL communicator.  No caller pointer is retained after a call
+ * returns.
  *
  * Streams: every call enqueues on the context stream (the one given to
  * tpmg_create, or tpmg_set_stream).  Single-operator calls return without
@@ -128,7 +128,10 @@ typedef struct {
     int64_t kernel_launches;   /* kernels launched by the library since creation / reset */
     int64_t halo_exchanges;    /* halo exchange calls (nranks > 1) */
     int64_t allreduces;        /* NCCL all-reduce calls (nranks > 1) */
-    int64_t graph_launches;    /* CUDA graph launches */
+    int64_t graph_launches;    /* CUDA graph launches (coarse-level V-cycle graphs) */
+    int64_t p2p_halo;          /* 1: halos by device-initiated NVLink stores (decided collectively at
+                                  create: every rank's neighbours reachable peer-to-peer on one host);
+                                  0: NCCL send/recv (or one rank) */
 } tpmg_stats;
 
 typedef struct tpmg_ctx tpmg_ctx;

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <unistd.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -112,6 +114,7 @@ struct tpmg_ctx {
     // profiling (tpmg_profile)
     bool pdl = false;                   // programmatic dependent launches (TPMG_PDL=1)
     bool tmem = true;                   // Thomas g' of the column kernels in Tensor Memory (TPMG_TMEM=0: smem)
+    int tm_ctas = 1;                    // their CTAs per SM (TPMG_TM_CTAS; r2c: 1 and 2 equal)
     bool ksplit_cg = false;             // k-split CG preconditioner (TPMG_KSPLIT_CG=1)
     bool halo_off = false;              // TPMG_HALO=off: skip halo exchanges (timing experiments)
     bool fused_push = false;            // P2P: producers push their boundary rows (TPMG_FUSED_PUSH=1)
@@ -178,6 +181,7 @@ Launcher launcher(tpmg_ctx* ctx)
     ln.reserve_sms = ctx->cur_reserve;
     ln.pdl = ctx->pdl;
     ln.tmem = ctx->tmem;
+    ln.tm_ctas = ctx->tm_ctas;
     return ln;
 }
 
@@ -1249,9 +1253,32 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
     return TPMG_OK;
 }
 
+// All ranks agree on a step's outcome: returns TPMG_OK on every rank only when `local` is OK
+// on every rank (an allreduce over ctx->comm), so that no rank enters the next collective
+// while another has bailed out (it would wait there forever).
+tpmg_status agree(tpmg_ctx* ctx, tpmg_status local)
+{
+    int* d = nullptr;
+    if (cudaMalloc((void**)&d, sizeof(int)) != cudaSuccess) return fail(ctx, TPMG_E_CUDA, "agree: cudaMalloc");
+    const int mine = (local == TPMG_OK) ? 0 : 1;
+    int any = 1;
+    bool ok = cudaMemcpy(d, &mine, sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
+              ncclAllReduce(d, d, 1, ncclInt32, ncclMax, ctx->comm, ctx->stream) == ncclSuccess &&
+              cudaStreamSynchronize(ctx->stream) == cudaSuccess &&
+              cudaMemcpy(&any, d, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess;
+    cudaFree(d);
+    if (local != TPMG_OK) return local;
+    if (!ok) return fail(ctx, TPMG_E_NCCL, "agree: allreduce of the step status failed");
+    if (any) return fail(ctx, TPMG_E_NCCL, "another rank failed in the same collective step");
+    return TPMG_OK;
+}
+
 // Halo channels and their pool (nranks > 1).  P2P mode (default): the pool is exported
-// with cudaIpcGetMemHandle, the handles are all-gathered over NCCL, and each rank maps its
-// two neighbours' pools; the exchanges then run as remote stores (exchange_p2p).
+// with cudaIpcGetMemHandle, the handles are all-gathered over NCCL together with each rank's
+// host name and GPU PCI bus id, and each rank maps its two neighbours' pools; the exchanges
+// then run as remote stores (exchange_p2p).  P2P is decided collectively: a rank whose
+// neighbour is on another host, cannot be reached peer-to-peer, or whose pool cannot be
+// mapped votes no, and then EVERY rank falls back to NCCL send/recv.
 tpmg_status halo_setup(tpmg_ctx* ctx)
 {
     const int L = ctx->L;
@@ -1274,8 +1301,10 @@ tpmg_status halo_setup(tpmg_ctx* ctx)
         ch.off_flags = take(4 * sizeof(uint32_t));
     }
     ctx->halo_pool_bytes = off;
-    CUDA_TRY(ctx, cudaMalloc(&ctx->halo_pool, off));
-    CUDA_TRY(ctx, cudaMemset(ctx->halo_pool, 0, off));
+    tpmg_status st = TPMG_OK;
+    if (cudaMalloc(&ctx->halo_pool, off) != cudaSuccess || cudaMemset(ctx->halo_pool, 0, off) != cudaSuccess)
+        st = fail(ctx, TPMG_E_CUDA, "halo pool: cudaMalloc/cudaMemset of %zu bytes", off);
+    TRY(agree(ctx, st));
     char* base = static_cast<char*>(ctx->halo_pool);
     for (int c = 1; c <= L + 1; ++c) {
         tpmg_ctx::Chan& ch = ctx->chans[c];
@@ -1292,29 +1321,72 @@ tpmg_status halo_setup(tpmg_ctx* ctx)
     ctx->halo_off = hm && std::strcmp(hm, "off") == 0;
     const char* fpu = std::getenv("TPMG_FUSED_PUSH");
     ctx->fused_push = fpu && fpu[0] == '1';   // measured no faster than the push kernel
+    // the environment and driver capabilities are the same on every rank of a job; the
+    // per-neighbour checks below are voted on
     ctx->p2p = !(hm && std::strcmp(hm, "nccl") == 0) && stream_memops();
     if (!ctx->p2p) return TPMG_OK;
-    // exchange the pool handles
-    cudaIpcMemHandle_t mine;
-    CUDA_TRY(ctx, cudaIpcGetMemHandle(&mine, ctx->halo_pool));
-    const size_t hb = sizeof(cudaIpcMemHandle_t);
-    char* d_all = nullptr;
-    CUDA_TRY(ctx, cudaMalloc((void**)&d_all, hb * ctx->nranks));
-    CUDA_TRY(ctx, cudaMemcpy(d_all + hb * ctx->rank, &mine, hb, cudaMemcpyHostToDevice));
-    NCCL_TRY(ctx, ncclAllGather(d_all + hb * ctx->rank, d_all, hb, ncclChar, ctx->comm, ctx->stream));
+    struct PeerRec {
+        cudaIpcMemHandle_t h;
+        char host[64];
+        char bus[32];
+        int ok;   // this rank could export its pool
+    };
+    PeerRec mine{};
+    mine.ok = cudaIpcGetMemHandle(&mine.h, ctx->halo_pool) == cudaSuccess &&
+              cudaDeviceGetPCIBusId(mine.bus, sizeof mine.bus, ctx->device) == cudaSuccess;
+    gethostname(mine.host, sizeof mine.host - 1);
+    cudaGetLastError();
+    const size_t hb = sizeof(PeerRec);
     std::vector<char> all(hb * ctx->nranks);
-    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    CUDA_TRY(ctx, cudaMemcpy(all.data(), d_all, all.size(), cudaMemcpyDeviceToHost));
-    cudaFree(d_all);
-    for (int side = 0; side < 2; ++side) {
+    {
+        char* d_all = nullptr;
+        CUDA_TRY(ctx, cudaMalloc((void**)&d_all, hb * ctx->nranks));
+        CUDA_TRY(ctx, cudaMemcpy(d_all + hb * ctx->rank, &mine, hb, cudaMemcpyHostToDevice));
+        NCCL_TRY(ctx, ncclAllGather(d_all + hb * ctx->rank, d_all, hb, ncclChar, ctx->comm, ctx->stream));
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        CUDA_TRY(ctx, cudaMemcpy(all.data(), d_all, all.size(), cudaMemcpyDeviceToHost));
+        cudaFree(d_all);
+    }
+    int vote = mine.ok ? 1 : 0;
+    for (int side = 0; side < 2 && vote; ++side) {
         const int nb = ctx->rank + (side == 0 ? -1 : 1);
         if (nb < 0 || nb >= ctx->nranks) continue;
-        cudaIpcMemHandle_t h;
-        std::memcpy(&h, all.data() + hb * nb, hb);
+        PeerRec r;
+        std::memcpy(&r, all.data() + hb * nb, hb);
+        int dev_nb = -1, can = 0;
+        if (!r.ok || std::strncmp(r.host, mine.host, sizeof r.host) != 0 ||
+            cudaDeviceGetByPCIBusId(&dev_nb, r.bus) != cudaSuccess || dev_nb == ctx->device ||
+            cudaDeviceCanAccessPeer(&can, ctx->device, dev_nb) != cudaSuccess || !can) {
+            vote = 0;
+            break;
+        }
         void* p = nullptr;
-        CUDA_TRY(ctx, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        if (cudaIpcOpenMemHandle(&p, r.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            vote = 0;
+            break;
+        }
         ctx->peer_pool[side] = static_cast<char*>(p);
     }
+    cudaGetLastError();   // a failed probe above must not stick to the next call
+    // collective decision: P2P only when every rank voted yes
+    {
+        int* d = nullptr;
+        int all_ok = 0;
+        CUDA_TRY(ctx, cudaMalloc((void**)&d, sizeof(int)));
+        CUDA_TRY(ctx, cudaMemcpy(d, &vote, sizeof(int), cudaMemcpyHostToDevice));
+        NCCL_TRY(ctx, ncclAllReduce(d, d, 1, ncclInt32, ncclMin, ctx->comm, ctx->stream));
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        CUDA_TRY(ctx, cudaMemcpy(&all_ok, d, sizeof(int), cudaMemcpyDeviceToHost));
+        cudaFree(d);
+        if (!all_ok) {
+            for (auto& pp : ctx->peer_pool) {
+                if (pp) cudaIpcCloseMemHandle(pp);
+                pp = nullptr;
+            }
+            ctx->p2p = false;
+        }
+    }
+    ctx->stats.p2p_halo = ctx->p2p ? 1 : 0;
     return TPMG_OK;
 }
 
@@ -1579,6 +1651,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->sync_debug = sd && sd[0] == '1';
         const char* tm = std::getenv("TPMG_TMEM");   // "0": g' of the column kernels in shared memory
         ctx->tmem = !(tm && tm[0] == '0');
+        const char* tc = std::getenv("TPMG_TM_CTAS");
+        if (tc) ctx->tm_ctas = std::max(1, std::min(2, std::atoi(tc)));
     }
     ctx->ny_loc = p.ny / nranks;
     ctx->y0 = (int64_t)rank * ctx->ny_loc;
@@ -1642,10 +1716,13 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         e = ncclCommSplit(ctx->comm, 0, rank, &ctx->comm_halo, &cfg);
         if (e != ncclSuccess) return bail(fail(ctx, TPMG_E_NCCL, "ncclCommSplit: %s", ncclGetErrorString(e)));
         int lo_prio = 0, hi_prio = 0;
-        CREATE_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
-        CREATE_CUDA(cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, hi_prio));
-        CREATE_CUDA(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
-        CREATE_CUDA(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
+        tpmg_status st = TPMG_OK;
+        if (cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio) != cudaSuccess ||
+            cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, hi_prio) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming) != cudaSuccess)
+            st = fail(ctx, TPMG_E_CUDA, "tpmg_create: halo stream / events");
+        CREATE_TRY(agree(ctx, st));   // no rank enters halo_setup's collectives alone
         CREATE_TRY(halo_setup(ctx));
     }
 #undef CREATE_TRY

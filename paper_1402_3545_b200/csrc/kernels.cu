@@ -654,13 +654,17 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
         limit = dyn_smem_limit(kern);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
         if (e != cudaSuccess) return e;
+        // the largest shared-memory carveout, so that the occupancy query below (and the first
+        // launch) sees every CTA that fits, not the default carveout's count
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
     }
     if (smem > limit) return cudaErrorInvalidConfiguration;
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TX * TY, smem);
     if (e != cudaSuccess) return e;
     per_sm = std::max(per_sm, 1);
-    if (TM) per_sm = std::min<int>(per_sm, 512 / kTmemCols);   // resident CTAs must all get their TMEM
+    if (TM) per_sm = std::min<int>(per_sm, std::min<int>(ln.tm_ctas, 512 / kTmemCols));   // resident CTAs must all get their TMEM
     const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * part_rows(a.part, (int)((a.L.ny + TY - 1) / TY));
     // CG direction (two halo'd fields): on wide grids two CTAs per SM re-read the halo
     // rows from HBM (2.1x the algorithmic reads at 4096 x 1024 x 128, ncu); one CTA per SM

@@ -166,6 +166,7 @@ struct Launcher {
     bool pdl = false;  // programmatic dependent launch: overlap a kernel's launch and
                        // prologue with the previous kernel's tail (griddepcontrol)
     bool tmem = true;  // one-thread-per-column Thomas kernels keep g' in Tensor Memory (nz <= 128)
+    int tm_ctas = 1;   // CTAs per SM of those kernels (TMEM holds 2; 1 and 2 measured equal warm, 1 keeps the p halo rows in L2 cold)
 };
 
 // Launch with the PDL attribute when ln.pdl.  Every kernel launched this way executes

@@ -417,6 +417,10 @@ cudaError_t launch_k_push(const Launcher& ln, const LineArgs& a, const KTables& 
         limit = dyn_smem_limit(kern);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
         if (e != cudaSuccess) return e;
+        // the largest shared-memory carveout, so that the occupancy query below (and the first
+        // launch) sees every CTA that fits, not the default carveout's count
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
     }
     if (smem > limit) return cudaErrorInvalidConfiguration;
     int per_sm = 0;

@@ -46,7 +46,8 @@ class tpmg_result(C.Structure):
 
 class tpmg_stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("halo_exchanges", C.c_int64),
-                ("allreduces", C.c_int64), ("graph_launches", C.c_int64)]
+                ("allreduces", C.c_int64), ("graph_launches", C.c_int64),
+                ("p2p_halo", C.c_int64)]
 
 
 _vp, _i32, _i64, _d = C.c_void_p, C.c_int32, C.c_int64, C.c_double
@@ -93,18 +94,50 @@ class TpmgError(RuntimeError):
         super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 10 else status}: {msg}")
 
 
-def _ptr(x):
-    """Device address of a torch tensor (checked) or an int."""
+_ctx_device: dict = {}   # context handle -> CUDA device index (set by tpmg_create)
+_ctx_levels: dict = {}   # context handle -> number of levels L
+
+
+def _level_numel(ctx, level) -> int:
+    _, nx, ny, nz = tpmg_local_box(ctx, level)
+    return nx * ny * nz
+
+
+def _ptr(x, ctx=None, level=None, what="vector"):
+    """Device address of a torch tensor or an int (a raw address is passed unchecked).
+    A tensor must be a contiguous float64 CUDA tensor on the context's device with exactly
+    the cells of `level`'s local box (checked before the C library is called: an undersized
+    or host tensor would otherwise be read / written out of bounds by the kernels)."""
     if x is None:
         return None
     if isinstance(x, int):
         return x
     import torch
     if not isinstance(x, torch.Tensor):
-        raise TypeError(f"expected a torch tensor or an address, got {type(x)}")
+        raise TypeError(f"{what}: expected a torch tensor or an address, got {type(x)}")
     if x.dtype != torch.float64 or not x.is_contiguous():
-        raise ValueError("vectors must be contiguous float64 tensors (Lambda layout)")
+        raise ValueError(f"{what}: vectors must be contiguous float64 tensors (Lambda layout)")
+    if not x.is_cuda:
+        raise ValueError(f"{what}: expected a CUDA tensor, got one on {x.device}")
+    if ctx is not None and ctx in _ctx_device and x.device.index != _ctx_device[ctx]:
+        raise ValueError(f"{what}: tensor on cuda:{x.device.index}, context on cuda:{_ctx_device[ctx]}")
+    if ctx is not None and level is not None:
+        n = _level_numel(ctx, level)
+        if x.numel() != n:
+            raise ValueError(f"{what}: {x.numel()} elements, level {level}'s local box has {n}")
     return x.data_ptr()
+
+
+def _lv(ctx, level, lo=1, hi=0):
+    """`level` when it lies in [lo, L + hi] (size checks apply), else None: an out-of-range
+    level is left to the C library, which reports it (TPMG_E_RANGE)."""
+    L = _ctx_levels.get(ctx)
+    return level if L is not None and lo <= level <= L + hi else None
+
+
+def _fine(ctx) -> int:
+    """The finest level L of a context (recorded by tpmg_create)."""
+    return _ctx_levels[ctx]
 
 
 def _check(st: int, ctx=None):
@@ -142,10 +175,14 @@ def tpmg_create(params: tpmg_params, rank: int = 0, nranks: int = 1, id128: byte
     out = _vp()
     idbuf = C.create_string_buffer(id128, 128) if id128 is not None else None
     _check(_lib.tpmg_create(C.byref(params), rank, nranks, idbuf, device, cuda_stream, C.byref(out)))
+    _ctx_device[out.value] = device
+    _ctx_levels[out.value] = tpmg_params_levels(params)
     return out.value
 
 
 def tpmg_destroy(ctx: int) -> None:
+    _ctx_device.pop(ctx, None)
+    _ctx_levels.pop(ctx, None)
     _check(_lib.tpmg_destroy(ctx))
 
 
@@ -160,34 +197,37 @@ def tpmg_local_box(ctx: int, level: int):
 
 
 def tpmg_apply(ctx: int, level: int, x, y) -> None:
-    _check(_lib.tpmg_apply(ctx, level, _ptr(x), _ptr(y)), ctx)
+    _check(_lib.tpmg_apply(ctx, level, _ptr(x, ctx, _lv(ctx, level), "x"), _ptr(y, ctx, _lv(ctx, level), "y")), ctx)
 
 
 def tpmg_residual(ctx: int, level: int, u, f, r=None, want_norm2: bool = False):
     n2 = _d()
-    _check(_lib.tpmg_residual(ctx, level, _ptr(u), _ptr(f), _ptr(r),
+    _check(_lib.tpmg_residual(ctx, level, _ptr(u, ctx, _lv(ctx, level), "u"), _ptr(f, ctx, _lv(ctx, level), "f"), _ptr(r, ctx, _lv(ctx, level), "r"),
                               C.byref(n2) if want_norm2 else None), ctx)
     return n2.value if want_norm2 else None
 
 
 def tpmg_precondition(ctx: int, level: int, r, z) -> None:
-    _check(_lib.tpmg_precondition(ctx, level, _ptr(r), _ptr(z)), ctx)
+    _check(_lib.tpmg_precondition(ctx, level, _ptr(r, ctx, _lv(ctx, level), "r"), _ptr(z, ctx, _lv(ctx, level), "z")), ctx)
 
 
 def tpmg_smooth(ctx: int, level: int, u, f, sweeps: int = 1) -> None:
-    _check(_lib.tpmg_smooth(ctx, level, _ptr(u), _ptr(f), sweeps), ctx)
+    _check(_lib.tpmg_smooth(ctx, level, _ptr(u, ctx, _lv(ctx, level), "u"), _ptr(f, ctx, _lv(ctx, level), "f"), sweeps), ctx)
 
 
 def tpmg_restrict(ctx: int, fine_level: int, r_fine, f_coarse) -> None:
-    _check(_lib.tpmg_restrict(ctx, fine_level, _ptr(r_fine), _ptr(f_coarse)), ctx)
+    _check(_lib.tpmg_restrict(ctx, fine_level, _ptr(r_fine, ctx, _lv(ctx, fine_level, 2), "r_fine"),
+                              _ptr(f_coarse, ctx, _lv(ctx, fine_level, 2) and fine_level - 1, "f_coarse")), ctx)
 
 
 def tpmg_prolong_add(ctx: int, coarse_level: int, u_coarse, u_fine) -> None:
-    _check(_lib.tpmg_prolong_add(ctx, coarse_level, _ptr(u_coarse), _ptr(u_fine)), ctx)
+    _check(_lib.tpmg_prolong_add(ctx, coarse_level, _ptr(u_coarse, ctx, _lv(ctx, coarse_level, 1, -1), "u_coarse"),
+                                 _ptr(u_fine, ctx, _lv(ctx, coarse_level, 1, -1) and coarse_level + 1, "u_fine")), ctx)
 
 
 def tpmg_vcycle(ctx: int, u, f) -> None:
-    _check(_lib.tpmg_vcycle(ctx, _ptr(u), _ptr(f)), ctx)
+    L = _fine(ctx)
+    _check(_lib.tpmg_vcycle(ctx, _ptr(u, ctx, L, "u"), _ptr(f, ctx, L, "f")), ctx)
 
 
 @dataclass
@@ -215,13 +255,15 @@ def _to_py(res: tpmg_result, hist) -> SolveResult:
 
 def tpmg_solve_mg(ctx: int, f, u, eps: float = 1e-5, max_iter: int = 50) -> SolveResult:
     res, hist = _result(max_iter)
-    _check(_lib.tpmg_solve_mg(ctx, _ptr(f), _ptr(u), eps, max_iter, C.byref(res)), ctx)
+    L = _fine(ctx)
+    _check(_lib.tpmg_solve_mg(ctx, _ptr(f, ctx, L, "f"), _ptr(u, ctx, L, "u"), eps, max_iter, C.byref(res)), ctx)
     return _to_py(res, hist)
 
 
 def tpmg_solve_cg(ctx: int, f, u, eps: float = 1e-5, max_iter: int = 1000) -> SolveResult:
     res, hist = _result(max_iter)
-    _check(_lib.tpmg_solve_cg(ctx, _ptr(f), _ptr(u), eps, max_iter, C.byref(res)), ctx)
+    L = _fine(ctx)
+    _check(_lib.tpmg_solve_cg(ctx, _ptr(f, ctx, L, "f"), _ptr(u, ctx, L, "u"), eps, max_iter, C.byref(res)), ctx)
     return _to_py(res, hist)
 
 
@@ -230,7 +272,7 @@ TPMG_ZC_TO_LAMBDA, TPMG_LAMBDA_TO_ZC = 0, 1
 
 def tpmg_transpose(ctx: int, level: int, direction: int, src, dst) -> None:
     """z-contiguous <-> Lambda layout of a level's local box (device tensors)."""
-    _check(_lib.tpmg_transpose(ctx, level, direction, _ptr(src), _ptr(dst)), ctx)
+    _check(_lib.tpmg_transpose(ctx, level, direction, _ptr(src, ctx, _lv(ctx, level), "src"), _ptr(dst, ctx, _lv(ctx, level), "dst")), ctx)
 
 
 def tpmg_solve_host_zc(ctx: int, solver: int, f_host, u_host, eps: float = 1e-5,
@@ -241,12 +283,18 @@ def tpmg_solve_host_zc(ctx: int, solver: int, f_host, u_host, eps: float = 1e-5,
 
 def tpmg_solve_host(ctx: int, solver: int, f_host, u_host, eps: float = 1e-5,
                     max_iter: int = 1000, _fn: str = "tpmg_solve_host") -> SolveResult:
-    """f_host / u_host: CPU torch tensors (pinned or pageable) or host addresses."""
+    """f_host / u_host: CPU float64 torch tensors (pinned or pageable) with the local fine
+    box's cells, or host addresses (unchecked)."""
+    import torch
+    n = _level_numel(ctx, _fine(ctx))
+
     def hptr(x):
         if isinstance(x, int):
             return x
-        if x.device.type != "cpu" or not x.is_contiguous():
+        if not isinstance(x, torch.Tensor) or x.device.type != "cpu" or not x.is_contiguous():
             raise ValueError("host buffers must be contiguous CPU tensors")
+        if x.dtype != torch.float64 or x.numel() != n:
+            raise ValueError(f"host buffers must be float64 with {n} elements (got {x.dtype}, {x.numel()})")
         return x.data_ptr()
     res, hist = _result(max_iter)
     _check(getattr(_lib, _fn)(ctx, solver, hptr(f_host), hptr(u_host), eps, max_iter,

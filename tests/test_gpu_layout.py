@@ -32,10 +32,11 @@ def test_transpose_bit_exact(shape):
         ctx.transpose(level, T.TPMG_LAMBDA_TO_ZC, lam, back)
         torch.cuda.synchronize()
         assert np.array_equal(back.cpu().numpy(), x)
+    full = ctx.empty(L)
     with pytest.raises(T.TpmgError, match="TPMG_E_PARAM"):
-        ctx.transpose(L, T.TPMG_ZC_TO_LAMBDA, src, src)
+        ctx.transpose(L, T.TPMG_ZC_TO_LAMBDA, full, full)
     with pytest.raises(T.TpmgError, match="TPMG_E_PARAM"):
-        ctx.transpose(L, 7, src, lam)
+        ctx.transpose(L, 7, full, ctx.empty(L))
 
 
 @pytest.mark.parametrize("solver", ["mg", "cg"])
