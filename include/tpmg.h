@@ -132,6 +132,8 @@ typedef struct {
     int64_t p2p_halo;          /* 1: halos by device-initiated NVLink stores (decided collectively at
                                   create: every rank's neighbours reachable peer-to-peer on one host);
                                   0: NCCL send/recv (or one rank) */
+    int64_t p2p_allreduce;     /* 1: global sums by the device-initiated NVLink allreduce (P2P mode,
+                                  <= 8 ranks); 0: ncclAllReduce (TPMG_ALLREDUCE=nccl, or one rank) */
 } tpmg_stats;
 
 typedef struct tpmg_ctx tpmg_ctx;
@@ -290,6 +292,20 @@ tpmg_status tpmg_set_profiles(tpmg_ctx *ctx, const double *a, const double *b, c
  * one-thread-per-column form, which computes each column's Thomas pivots on the fly
  * (the k-split and fused-prolongation options fall back). */
 tpmg_status tpmg_set_fields(tpmg_ctx *ctx, const double *area, const double *ax, const double *ay);
+
+/* Halo-exchange primitives of the multi-rank path (y-strips with halo width 1),
+ * exposed so that the exchange kernels can be checked on a single GPU.  The solvers call the
+ * same kernels on the neighbours' IPC-mapped slabs (P2P mode).
+ * tpmg_halo_push: one launch of the push kernel -- dst_lo <- row 0 of src, dst_hi <- row
+ *   ny_l - 1 of src (each row a plane of nz * nx_l doubles of `level`, Lambda order); either
+ *   destination may be NULL (a physical boundary).  Device pointers, caller-owned; src must
+ *   not overlap a destination.  Rank-local, asynchronous on the context stream.
+ * tpmg_cg_halo: the CG direction kernel's local update of the p halo (the halo of
+ *   p = z + beta p_old without sending p): out = fma(beta, p, z) element by element on each
+ *   non-NULL triple of fine-level planes (nz * nx_L doubles).  Rank-local; synchronises. */
+tpmg_status tpmg_halo_push(tpmg_ctx *ctx, int32_t level, const double *src, double *dst_lo, double *dst_hi);
+tpmg_status tpmg_cg_halo(tpmg_ctx *ctx, double beta, double *out_lo, const double *z_lo, const double *p_lo,
+                         double *out_hi, const double *z_hi, const double *p_hi);
 
 /* Counters (kernel launches etc.); tpmg_stats_reset zeroes them. */
 tpmg_status tpmg_get_stats(const tpmg_ctx *ctx, tpmg_stats *out);

@@ -101,12 +101,18 @@ struct tpmg_ctx {
     size_t halo_pool_bytes = 0;
     bool p2p = false;                   // TPMG_HALO=nccl selects NCCL send/recv
     char* peer_pool[2] = {nullptr, nullptr};   // [0] lower neighbour's pool, [1] upper's (IPC-mapped)
+    std::vector<char*> peer_all;               // every rank's pool (IPC-mapped; mine at [rank])
+    bool p2p_reduce = false;                   // allreduces by k_allreduce_p2p (TPMG_ALLREDUCE=nccl: NCCL)
+    P2PReduce red{};                           // its slot / flag addresses
+    unsigned red_epoch = 0;
+    size_t off_red = 0, off_redflags = 0;      // byte offsets in the pool
     // overlap of halo exchanges with interior work (nranks > 1)
     ncclComm_t comm_halo = nullptr;     // halo traffic on its own communicator and stream
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
-    bool overlap = false;               // TPMG_OVERLAP=1 enables (measured slower at N=4: the split
-                                        // launches cost more than the NCCL latency they hide)
+    bool overlap = true;                // P2P halos: interior rows while the halo travels (TPMG_OVERLAP=0 off)
+    bool overlap_nccl = false;          // NCCL halos: TPMG_OVERLAP=1 (measured slower at N=4 in round 1:
+                                        // the split launches cost more than the NCCL latency they hide)
     int reserve_sms = 4;                // SMs left to NCCL while the interior runs
     int cur_reserve = 0;
     tpmg_stats stats{};
@@ -114,7 +120,8 @@ struct tpmg_ctx {
     // profiling (tpmg_profile)
     bool pdl = false;                   // programmatic dependent launches (TPMG_PDL=1)
     bool tmem = true;                   // Thomas g' of the column kernels in Tensor Memory (TPMG_TMEM=0: smem)
-    int tm_ctas = 1;                    // their CTAs per SM (TPMG_TM_CTAS; r2c: 1 and 2 equal)
+    int tm_ctas = 2;                    // their CTAs per SM (TPMG_TM_CTAS; r2c, r2f: 2 >= 1)
+    int tm_stages = 3;                  // their TMA ring depth (TPMG_TM_STAGES: 3, 4, 5)
     bool ksplit_cg = false;             // k-split CG preconditioner (TPMG_KSPLIT_CG=1)
     bool halo_off = false;              // TPMG_HALO=off: skip halo exchanges (timing experiments)
     bool fused_push = false;            // P2P: producers push their boundary rows (TPMG_FUSED_PUSH=1)
@@ -182,6 +189,7 @@ Launcher launcher(tpmg_ctx* ctx)
     ln.pdl = ctx->pdl;
     ln.tmem = ctx->tmem;
     ln.tm_ctas = ctx->tm_ctas;
+    ln.tm_stages = ctx->tm_stages;
     return ln;
 }
 
@@ -314,9 +322,12 @@ tpmg_status wait_epoch(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int E)
 // kernels that read epoch E-2 (the slot b that epoch E overwrites), and I push epoch E
 // only after my stream saw its epoch E-1 data (every pushed epoch is waited for, in
 // order, before the next push).  No kernel spins.
-tpmg_status exchange_p2p(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int c, const double* x)
+// First half of a P2P exchange: push x's boundary rows and publish the epoch, without
+// waiting for the neighbours' rows.  *E_out = the epoch to wait for (0: already waited, the
+// producer had pushed x itself).  Work that reads no halo row can run before p2p_finish.
+tpmg_status p2p_begin(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, const double* x, int* E_out)
 {
-    (void)c;
+    *E_out = 0;
     if (ch.pushed) {
         const bool mine = (ch.pushed == x);
         ch.pushed = nullptr;
@@ -329,7 +340,21 @@ tpmg_status exchange_p2p(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int c, const double*
     hp.src_last = x + (size_t)(ch.nyl - 1) * ch.plane;
     CUDA_TRY(ctx, launch_halo_push(launcher(ctx), hp));
     TRY(publish_epoch(ctx, ch, E));
-    return wait_epoch(ctx, ch, E);
+    *E_out = E;
+    return TPMG_OK;
+}
+
+tpmg_status p2p_finish(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int E)
+{
+    return E ? wait_epoch(ctx, ch, E) : TPMG_OK;
+}
+
+tpmg_status exchange_p2p(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int c, const double* x)
+{
+    (void)c;
+    int E = 0;
+    TRY(p2p_begin(ctx, ch, x, &E));
+    return p2p_finish(ctx, ch, E);
 }
 
 // Fused push for a producer kernel about to write `out` (a field of channel c that will
@@ -417,10 +442,18 @@ tpmg_status halo(tpmg_ctx* ctx, int level, const double* x, HaloField* out)
     return TPMG_OK;
 }
 
+// Global sum of n device doubles over the ranks, in place on the context stream:
+// device-initiated over NVLink (k_allreduce_p2p: the GPUs store their values into each
+// other's pools and wait on epoch flags, no host and no NCCL kernel) when the P2P pools are
+// mapped, else ncclAllReduce.
 tpmg_status allreduce(tpmg_ctx* ctx, double* d, int n)
 {
     if (ctx->nranks == 1) return TPMG_OK;
-    NCCL_TRY(ctx, ncclAllReduce(d, d, n, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    if (ctx->p2p_reduce && n <= 4) {
+        CUDA_TRY(ctx, launch_allreduce_p2p(launcher(ctx), d, n, ctx->red, ++ctx->red_epoch));
+    } else {
+        NCCL_TRY(ctx, ncclAllReduce(d, d, n, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    }
     ++ctx->stats.allreduces;
     return TPMG_OK;
 }
@@ -705,26 +738,47 @@ tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
     return TPMG_OK;
 }
 
-// A line kernel whose halo'd input x needs an exchange first.  With several ranks the
-// exchange runs on the halo stream while the interior tile rows (which read no halo
-// row) run, leaving reserve_sms SMs to NCCL; the boundary tile rows follow once the
-// halo has arrived.  pre_boundary (optional) runs between the exchange and the
-// boundary launch (e.g. the CG p-halo update).
+// A line kernel whose halo'd input x needs an exchange first (channel chan, default the
+// level's).  With several ranks the interior tile rows (which read no halo row) run while
+// the halo is in flight and the boundary tile rows follow once it has arrived:
+//   P2P (default): push x's boundary rows to the neighbours + publish the epoch, interior
+//     launch, stream wait for the neighbours' epoch, boundary launch;
+//   NCCL (TPMG_HALO=nccl with TPMG_OVERLAP=1): the exchange on the halo stream, leaving
+//     reserve_sms SMs to NCCL during the interior launch.
+// pre_boundary(a) (optional) runs between the halo's arrival and the boundary launch (e.g.
+// the CG p-halo update) and may refresh a's halo views.  TPMG_OVERLAP=0 (or a fused push of
+// the output) runs one launch after the exchange.
 template <typename PreBoundary>
 tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, LineArgs a, const double* x, double* lo, double* hi,
-                          PreBoundary pre_boundary, const double* push_out = nullptr)
+                          PreBoundary pre_boundary, const double* push_out = nullptr, int chan = -1)
 {
+    if (chan < 0) chan = level;
     if (ctx->nranks == 1) {
-        TRY(pre_boundary());
+        TRY(pre_boundary(a));
         return run_line(ctx, mode, a);
     }
     const LevelConst& lc = ctx->lv[level].lc;
     const int TY = launch_rows(ctx, mode, lc);
     const int nty = (int)((lc.ny + TY - 1) / TY);
-    if (!ctx->overlap || ctx->p2p || nty < 3) {
-        TRY(exchange(ctx, level, x));
-        if (a.h0.base == x) a.h0 = halo_of(ctx, level, x);   // P2P: the current slab buffer alternates
-        TRY(pre_boundary());
+    const bool fused_out = push_out && ctx->fused_push;
+    if (ctx->p2p && ctx->overlap && !ctx->halo_off && !fused_out && nty >= 3) {
+        tpmg_ctx::Chan& ch = ctx->chans[chan];
+        int E = 0;
+        TRY(p2p_begin(ctx, ch, x, &E));
+        a.part = PART_INTERIOR;
+        TRY(run_line(ctx, mode, a));
+        TRY(p2p_finish(ctx, ch, E));
+        if (a.h0.base == x) a.h0 = HaloField{x, ctx->rank > 0 ? *ch.cur_lo : nullptr,
+                                             ctx->rank < ctx->nranks - 1 ? *ch.cur_hi : nullptr};
+        TRY(pre_boundary(a));
+        a.part = PART_BOUNDARY;
+        a.red.accumulate = 1;
+        return run_line(ctx, mode, a);
+    }
+    if (!ctx->overlap_nccl || ctx->p2p || nty < 3) {
+        TRY(exchange_chan(ctx, chan, x));
+        if (a.h0.base == x && chan == level) a.h0 = halo_of(ctx, level, x);   // P2P: the current slab buffer alternates
+        TRY(pre_boundary(a));
         if (push_out) TRY(fused_push(ctx, level, push_out, &a.push));   // after the input's exchange
         TRY(run_line(ctx, mode, a));
         return push_out ? publish_pushed(ctx, level) : TPMG_OK;
@@ -736,7 +790,7 @@ tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, LineArgs a, const 
     ctx->cur_reserve = 0;
     TRY(st);
     TRY(finish_async_exchange(ctx));
-    TRY(pre_boundary());
+    TRY(pre_boundary(a));
     a.part = PART_BOUNDARY;
     a.red.accumulate = 1;
     return run_line(ctx, mode, a);
@@ -746,7 +800,7 @@ tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, const LineArgs& a,
                           const double* push_out = nullptr)
 {
     LevelData& L = ctx->lv[level];
-    return run_line_halo(ctx, level, mode, a, x, L.slab_lo, L.slab_hi, [] { return TPMG_OK; }, push_out);
+    return run_line_halo(ctx, level, mode, a, x, L.slab_lo, L.slab_hi, [](LineArgs&) { return TPMG_OK; }, push_out);
 }
 
 // out = u + rho M^-1 (f - A u) (out-of-place), optional sum r^2 into result
@@ -816,7 +870,23 @@ tpmg_status prolong_overlapped(tpmg_ctx* ctx, int lc_)
     LevelData& F = ctx->lv[lc_ + 1];
     const HaloField uc = halo_of(ctx, lc_, Cc.u[Cc.cur]);
     const double cells = level_cells(F.lc);
-    if (ctx->nranks == 1 || !ctx->overlap || ctx->p2p || Cc.lc.ny < 3) {
+    const double fb = Cc.lc.ny > 0 ? 2.0 / (double)Cc.lc.ny : 1.0;   // boundary coarse rows' share
+    if (ctx->nranks > 1 && ctx->p2p && ctx->overlap && !ctx->halo_off && !ctx->fused_push && Cc.lc.ny >= 3) {
+        // P2P overlap: interior coarse rows while the coarse halo rows travel
+        tpmg_ctx::Chan& ch = ctx->chans[lc_];
+        int E = 0;
+        TRY(p2p_begin(ctx, ch, Cc.u[Cc.cur], &E));
+        {
+            ProfScope ps(ctx, TPMG_K_PROLONG_ADD, cells * (1.0 - fb));
+            CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc, F.u[F.cur], ctx->skip, PART_INTERIOR));
+        }
+        TRY(p2p_finish(ctx, ch, E));
+        const HaloField uc2 = halo_of(ctx, lc_, Cc.u[Cc.cur]);
+        ProfScope ps(ctx, TPMG_K_PROLONG_ADD, cells * fb);
+        CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc2, F.u[F.cur], ctx->skip, PART_BOUNDARY));
+        return TPMG_OK;
+    }
+    if (ctx->nranks == 1 || !ctx->overlap_nccl || ctx->p2p || Cc.lc.ny < 3) {
         TRY(exchange(ctx, lc_, Cc.u[Cc.cur]));
         const HaloField uc2 = halo_of(ctx, lc_, Cc.u[Cc.cur]);   // current slabs after the exchange
         HaloPush hp;
@@ -826,7 +896,6 @@ tpmg_status prolong_overlapped(tpmg_ctx* ctx, int lc_)
         return publish_pushed(ctx, lc_ + 1);
     }
     TRY(start_async_exchange(ctx, lc_, Cc.u[Cc.cur], Cc.slab_lo, Cc.slab_hi));
-    const double fb = 2.0 / (double)Cc.lc.ny;
     {
         ProfScope ps(ctx, TPMG_K_PROLONG_ADD, cells * (1.0 - fb));
         CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc, F.u[F.cur], ctx->skip, PART_INTERIOR));
@@ -1172,14 +1241,8 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
         }
         // (Fused) direction kernel: p = z + beta p, sigma = <p, A p>.  Only z crosses NVLink;
         // the p halo is local: p_halo <- z_halo + beta p_halo (same fma as the neighbour's
-        // own rows).
-        if (ctx->nranks > 1) {
-            TRY(exchange_chan(ctx, l + 1, ctx->cg_z));
-            hz = HaloField{ctx->cg_z, has_lo ? ctx->cg_zlo : nullptr, has_hi ? ctx->cg_zhi : nullptr};
-            CUDA_TRY(ctx, launch_cg_halo(launcher(ctx), has_lo ? ctx->cg_plo[1 - cur] : nullptr, hz.lo, hp.lo,
-                                         has_hi ? ctx->cg_phi[1 - cur] : nullptr, hz.hi, hp.hi, (int64_t)plane, beta,
-                                         ctx->skip));
-        }
+        // own rows).  With several ranks the interior tile rows run while z's halo travels
+        // (run_line_halo); the p-halo update and the boundary rows follow its arrival.
         {
             LineArgs a = line_args(ctx, l);
             a.h0 = hz;
@@ -1187,7 +1250,16 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
             a.out0 = ctx->cg_p[1 - cur];
             a.ratio = beta;
             a.red.result = ctx->d_scal + S_SIGMA(m);
-            TRY(run_line(ctx, MODE_CGDIR, a));
+            auto p_halo = [&](LineArgs& b) -> tpmg_status {
+                if (ctx->nranks == 1) return TPMG_OK;
+                hz = HaloField{ctx->cg_z, has_lo ? ctx->cg_zlo : nullptr, has_hi ? ctx->cg_zhi : nullptr};
+                b.h0 = hz;   // the z slabs of this exchange's epoch
+                CUDA_TRY(ctx, launch_cg_halo(launcher(ctx), has_lo ? ctx->cg_plo[1 - cur] : nullptr, hz.lo, hp.lo,
+                                             has_hi ? ctx->cg_phi[1 - cur] : nullptr, hz.hi, hp.hi, (int64_t)plane,
+                                             beta, ctx->skip));
+                return TPMG_OK;
+            };
+            TRY(run_line_halo(ctx, l, MODE_CGDIR, a, ctx->cg_z, ctx->cg_zlo, ctx->cg_zhi, p_halo, nullptr, l + 1));
             TRY(allreduce(ctx, ctx->d_scal + S_SIGMA(m), 1));
         }
         HaloField hpn{ctx->cg_p[1 - cur], nullptr, nullptr};
@@ -1300,6 +1372,8 @@ tpmg_status halo_setup(tpmg_ctx* ctx)
         }
         ch.off_flags = take(4 * sizeof(uint32_t));
     }
+    ctx->off_red = take(sizeof(double) * 2 * kMaxP2PRanks * 4);
+    ctx->off_redflags = take(sizeof(unsigned) * kMaxP2PRanks);
     ctx->halo_pool_bytes = off;
     tpmg_status st = TPMG_OK;
     if (cudaMalloc(&ctx->halo_pool, off) != cudaSuccess || cudaMemset(ctx->halo_pool, 0, off) != cudaSuccess)
@@ -1347,16 +1421,19 @@ tpmg_status halo_setup(tpmg_ctx* ctx)
         CUDA_TRY(ctx, cudaMemcpy(all.data(), d_all, all.size(), cudaMemcpyDeviceToHost));
         cudaFree(d_all);
     }
+    // every rank's pool is mapped (the neighbours' carry the halos, all of them the
+    // allreduce slots); every peer must be on my host and reachable peer-to-peer
     int vote = mine.ok ? 1 : 0;
-    for (int side = 0; side < 2 && vote; ++side) {
-        const int nb = ctx->rank + (side == 0 ? -1 : 1);
-        if (nb < 0 || nb >= ctx->nranks) continue;
+    ctx->peer_all.assign(ctx->nranks, nullptr);
+    ctx->peer_all[ctx->rank] = static_cast<char*>(ctx->halo_pool);
+    for (int q = 0; q < ctx->nranks && vote; ++q) {
+        if (q == ctx->rank) continue;
         PeerRec r;
-        std::memcpy(&r, all.data() + hb * nb, hb);
-        int dev_nb = -1, can = 0;
+        std::memcpy(&r, all.data() + hb * q, hb);
+        int dev_q = -1, can = 0;
         if (!r.ok || std::strncmp(r.host, mine.host, sizeof r.host) != 0 ||
-            cudaDeviceGetByPCIBusId(&dev_nb, r.bus) != cudaSuccess || dev_nb == ctx->device ||
-            cudaDeviceCanAccessPeer(&can, ctx->device, dev_nb) != cudaSuccess || !can) {
+            cudaDeviceGetByPCIBusId(&dev_q, r.bus) != cudaSuccess || dev_q == ctx->device ||
+            cudaDeviceCanAccessPeer(&can, ctx->device, dev_q) != cudaSuccess || !can) {
             vote = 0;
             break;
         }
@@ -1365,7 +1442,11 @@ tpmg_status halo_setup(tpmg_ctx* ctx)
             vote = 0;
             break;
         }
-        ctx->peer_pool[side] = static_cast<char*>(p);
+        ctx->peer_all[q] = static_cast<char*>(p);
+    }
+    if (vote) {
+        ctx->peer_pool[0] = ctx->rank > 0 ? ctx->peer_all[ctx->rank - 1] : nullptr;
+        ctx->peer_pool[1] = ctx->rank < ctx->nranks - 1 ? ctx->peer_all[ctx->rank + 1] : nullptr;
     }
     cudaGetLastError();   // a failed probe above must not stick to the next call
     // collective decision: P2P only when every rank voted yes
@@ -1379,14 +1460,24 @@ tpmg_status halo_setup(tpmg_ctx* ctx)
         CUDA_TRY(ctx, cudaMemcpy(&all_ok, d, sizeof(int), cudaMemcpyDeviceToHost));
         cudaFree(d);
         if (!all_ok) {
-            for (auto& pp : ctx->peer_pool) {
-                if (pp) cudaIpcCloseMemHandle(pp);
-                pp = nullptr;
-            }
+            for (int q = 0; q < (int)ctx->peer_all.size(); ++q)
+                if (q != ctx->rank && ctx->peer_all[q]) cudaIpcCloseMemHandle(ctx->peer_all[q]);
+            ctx->peer_all.clear();
+            ctx->peer_pool[0] = ctx->peer_pool[1] = nullptr;
             ctx->p2p = false;
         }
     }
-    ctx->stats.p2p_halo = ctx->p2p ? 1 : 0;
+    // device-initiated allreduce over the mapped pools (TPMG_ALLREDUCE=nccl keeps NCCL)
+    const char* ar = std::getenv("TPMG_ALLREDUCE");
+    ctx->p2p_reduce = ctx->p2p && ctx->nranks <= kMaxP2PRanks && !(ar && std::strcmp(ar, "nccl") == 0);
+    if (ctx->p2p_reduce) {
+        ctx->red.me = ctx->rank;
+        ctx->red.nranks = ctx->nranks;
+        for (int q = 0; q < ctx->nranks; ++q) {
+            ctx->red.slots[q] = reinterpret_cast<double*>(ctx->peer_all[q] + ctx->off_red);
+            ctx->red.flags[q] = reinterpret_cast<unsigned*>(ctx->peer_all[q] + ctx->off_redflags);
+        }
+    }
     return TPMG_OK;
 }
 
@@ -1431,8 +1522,8 @@ void ctx_free(tpmg_ctx* ctx)
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     for (auto& r : ctx->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ctx->prof_pool) cudaEventDestroy(e);
-    for (auto pp : ctx->peer_pool)
-        if (pp) cudaIpcCloseMemHandle(pp);
+    for (int q = 0; q < (int)ctx->peer_all.size(); ++q)
+        if (q != ctx->rank && ctx->peer_all[q]) cudaIpcCloseMemHandle(ctx->peer_all[q]);
     cudaFree(ctx->halo_pool);
     if (ctx->comm_halo) ncclCommDestroy(ctx->comm_halo);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
@@ -1638,7 +1729,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         const char* ks = std::getenv("TPMG_KSPLIT");
         ctx->ksplit_cfg = !ks ? 1 : ks[0] == '0' ? -1 : ks[0] == '1' ? 0 : ks[0] == '3' ? 2 : 1;
         const char* ov = std::getenv("TPMG_OVERLAP");
-        ctx->overlap = ov && ov[0] == '1';
+        ctx->overlap = !(ov && ov[0] == '0');        // P2P transport: on by default
+        ctx->overlap_nccl = ov && ov[0] == '1';      // NCCL transport: opt-in
         const char* rs = std::getenv("TPMG_RESERVE_SMS");
         if (rs) ctx->reserve_sms = std::max(0, std::atoi(rs));
         const char* kc = std::getenv("TPMG_KSPLIT_CG");
@@ -1651,6 +1743,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->sync_debug = sd && sd[0] == '1';
         const char* tm = std::getenv("TPMG_TMEM");   // "0": g' of the column kernels in shared memory
         ctx->tmem = !(tm && tm[0] == '0');
+        const char* ts = std::getenv("TPMG_TM_STAGES");
+        if (ts) ctx->tm_stages = std::atoi(ts);
         const char* tc = std::getenv("TPMG_TM_CTAS");
         if (tc) ctx->tm_ctas = std::max(1, std::min(2, std::atoi(tc)));
     }
@@ -1918,6 +2012,43 @@ tpmg_status tpmg_transpose(tpmg_ctx* ctx, int32_t level, int32_t direction, cons
     return TPMG_OK;
 }
 
+tpmg_status tpmg_halo_push(tpmg_ctx* ctx, int32_t level, const double* src, double* dst_lo, double* dst_hi)
+{
+    if (ctx) begin_call(ctx);
+    if (!ctx) return TPMG_E_PARAM;
+    TRY(check_level(ctx, level));
+    if (!src) return fail(ctx, TPMG_E_PARAM, "tpmg_halo_push: NULL src");
+    const LevelData& L = ctx->lv[level];
+    const double* end = src + L.n();
+    for (const double* d : {static_cast<const double*>(dst_lo), static_cast<const double*>(dst_hi)})
+        if (d && d + L.plane() > src && d < end)
+            return fail(ctx, TPMG_E_PARAM, "tpmg_halo_push: a destination overlaps src");
+    HaloPush hp{src, src + (size_t)(L.lc.ny - 1) * L.plane(), dst_lo, dst_hi, (int64_t)L.plane()};
+    CUDA_TRY(ctx, launch_halo_push(launcher(ctx), hp));
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_cg_halo(tpmg_ctx* ctx, double beta, double* out_lo, const double* z_lo, const double* p_lo,
+                         double* out_hi, const double* z_hi, const double* p_hi)
+{
+    if (ctx) begin_call(ctx);
+    if (!ctx) return TPMG_E_PARAM;
+    if ((out_lo && (!z_lo || !p_lo)) || (out_hi && (!z_hi || !p_hi)))
+        return fail(ctx, TPMG_E_PARAM, "tpmg_cg_halo: an output plane needs its z and p planes");
+    // beta as the device ratio the kernel reads: s[0] / s[1] = beta / 1
+    double* d_beta = nullptr;
+    TRY(dev_alloc(ctx, &d_beta, 2));
+    const double hb[2] = {beta, 1.0};
+    cudaError_t e = cudaMemcpy(d_beta, hb, sizeof hb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = launch_cg_halo(launcher(ctx), out_lo, z_lo, p_lo, out_hi, z_hi, p_hi, (int64_t)ctx->lv[ctx->L].plane(),
+                           DevRatio{d_beta, 0, 1}, nullptr);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(d_beta);
+    if (e != cudaSuccess) return fail(ctx, TPMG_E_CUDA, "tpmg_cg_halo: %s", cudaGetErrorString(e));
+    return TPMG_OK;
+}
+
 tpmg_status tpmg_solve_host_zc(tpmg_ctx* ctx, tpmg_solver solver, const double* f_host, double* u_host,
                                double eps, int32_t max_iter, tpmg_result* res)
 {
@@ -1945,6 +2076,8 @@ tpmg_status tpmg_get_stats(const tpmg_ctx* ctx, tpmg_stats* out)
 {
     if (!ctx || !out) return TPMG_E_PARAM;
     *out = ctx->stats;
+    out->p2p_halo = ctx->p2p ? 1 : 0;
+    out->p2p_allreduce = ctx->p2p_reduce ? 1 : 0;
     return TPMG_OK;
 }
 

@@ -167,15 +167,16 @@ __device__ __forceinline__ void tma_stage(double* st, const LineArgs& a, int64_t
 // that held one CTA per SM leave room for two, i.e. twice the warps to hide the recurrences'
 // latency; TMEM itself (256 columns = 128 levels per CTA) holds exactly two CTAs.
 constexpr uint32_t kTmemCols = 256;
-template <int MODE, int TY, int LOADER, int GEN, bool TM = false>
+template <int MODE, int TY, int LOADER, int GEN, int TMS = 0>
 __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArgs a)
 {
     using T = Traits<MODE>;
+    constexpr bool TM = TMS > 0;   // TMS: pipeline stages of the TMEM form (the freed shared memory deepens it)
     static_assert(!TM || (TY == 4 && GEN == 0 && T::THOMAS), "TMEM g' buffer: 4 warps, flat box, Thomas modes");
     constexpr int NH = T::NH, NP = T::NP, NR = T::NR;
     using G = Geom<NH, NP, TY>;
     constexpr int NT = G::NT;
-    constexpr int NS = stages<MODE, GEN>();
+    constexpr int NS = TM ? TMS : stages<MODE, GEN>();
 
     extern __shared__ __align__(128) double smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[NS];
@@ -632,23 +633,25 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 }
 
 template <int MODE, int TY>
-size_t line_smem_bytes(int nz, int gen = 0, bool tm = false)
+size_t line_smem_bytes(int nz, int gen = 0, int tms = 0)
 {
     using T = Traits<MODE>;
     using G = Geom<T::NH, T::NP, TY>;
+    const bool tm = tms > 0;
     size_t d = ((3 * nz + 15) & ~15) + (gen >= 2 ? ((4 * nz + 15) & ~15) : gen ? ((3 * nz + 15) & ~15) : 0) +
-               (size_t)(gen == 2 ? stages<MODE, 2>() : kNS) * G::STAGE + ((T::THOMAS && !tm) ? (size_t)(nz + (gen == 2 ? (nz + KB - 1) / KB : 0)) * G::NT : 0) + 64 + 16 +
+               (size_t)(tm ? tms : gen == 2 ? stages<MODE, 2>() : kNS) * G::STAGE + ((T::THOMAS && !tm) ? (size_t)(nz + (gen == 2 ? (nz + KB - 1) / KB : 0)) * G::NT : 0) + 64 + 16 +
                (MODE == MODE_RESTRICT ? 2 * TY * (KB + 1) * (TX / 2) : 0);
     return d * sizeof(double);
 }
 
 constexpr size_t kMaxSmem = 227 * 1024 - 1024;  // leave room for static smem (barriers, flags)
 
-template <int MODE, int TY, int LOADER, int GEN, bool TM = false>
+template <int MODE, int TY, int LOADER, int GEN, int TMS = 0>
 cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
 {
-    const size_t smem = line_smem_bytes<MODE, TY>(a.L.nz, GEN, TM);
-    auto kern = k_line<MODE, TY, LOADER, GEN, TM>;
+    constexpr bool TM = TMS > 0;
+    const size_t smem = line_smem_bytes<MODE, TY>(a.L.nz, GEN, TMS);
+    auto kern = k_line<MODE, TY, LOADER, GEN, TMS>;
     static size_t limit = 0;   // per instantiation
     if (!limit) {
         limit = dyn_smem_limit(kern);
@@ -684,7 +687,16 @@ cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
         return a.L.gen >= 2 ? launch_line_l<MODE, TY, 1, 2>(ln, a) : launch_line_l<MODE, TY, 1, 1>(ln, a);
     }
     if constexpr (Traits<MODE>::THOMAS && TY == 4)   // g' in Tensor Memory (flat box, TMA loader)
-        if (ln.tmem && a.use_tma && a.L.nz <= (int)(kTmemCols / 2)) return launch_line_l<MODE, 4, 1, 0, true>(ln, a);
+        if (ln.tmem && a.use_tma && a.L.nz <= (int)(kTmemCols / 2)) {
+            // TMA ring depth (stages of 8 levels): the shared memory freed from g' would hold 7,
+            // but 7 measured 16% slower than 3 for CGPREC (r2e: 1.29 vs 1.11 ms); TPMG_TM_STAGES
+            // selects 3 (default), 4 or 5 for the CG preconditioner
+            if constexpr (MODE == MODE_CGPREC) {
+                if (ln.tm_stages == 4) return launch_line_l<MODE, 4, 1, 0, 4>(ln, a);
+                if (ln.tm_stages == 5) return launch_line_l<MODE, 4, 1, 0, 5>(ln, a);
+            }
+            return launch_line_l<MODE, 4, 1, 0, 3>(ln, a);
+        }
     return a.use_tma ? launch_line_l<MODE, TY, 1, 0>(ln, a) : launch_line_l<MODE, TY, 0, 0>(ln, a);
 }
 
@@ -867,6 +879,44 @@ __global__ void __launch_bounds__(256) k_halo_push(const HaloPush hp, int64_t n)
     }
 }
 
+__global__ void __launch_bounds__(32) k_allreduce_p2p(double* d, int n, const P2PReduce P, unsigned E)
+{
+    pdl_wait();
+    pdl_trigger();
+    const int t = threadIdx.x;
+    const int b = (int)(E & 1u);
+    if (t < n) {
+        const double v = d[t];
+        for (int r = 0; r < P.nranks; ++r) P.slots[r][(b * kMaxP2PRanks + P.me) * 4 + t] = v;   // NVLink stores
+    }
+    __threadfence_system();   // my values are visible everywhere before my flag is
+    __syncwarp();
+    if (t < P.nranks) asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(P.flags[t] + P.me), "r"(E) : "memory");
+    bool timed_out = false;
+    if (t < P.nranks) {
+        const unsigned* f = P.flags[P.me] + t;
+        uint64_t t0, now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            unsigned v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
+            if ((int)(v - E) >= 0) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if (now - t0 > 20000000000ull) { timed_out = true; break; }
+            __nanosleep(64);
+        }
+    }
+    timed_out = __any_sync(0xffffffffu, timed_out);
+    __syncwarp();
+    __threadfence_system();
+    if (t < n) {
+        double s = 0.0;
+        const volatile double* mine = P.slots[P.me] + b * kMaxP2PRanks * 4 + t;
+        for (int r = 0; r < P.nranks; ++r) s += mine[r * 4];   // rank order: identical on every rank
+        d[t] = timed_out ? __longlong_as_double(0x7ff8000000000000ll) : s;
+    }
+}
+
 // Convergence test of PCG iteration m on the device: ||r_m|| / ||r_0|| < eps
 // (eqn:epsilonTolerance), breakdown when <p, A p> <= 0 or <r, M^-1 r> <= 0.
 // The host reads the flag from pinned memory after an event behind the check kernel:
@@ -940,6 +990,12 @@ cudaError_t launch_halo_push(const Launcher& ln, const HaloPush& hp)
     else k_halo_push<double><<<grid, 256, 0, ln.stream>>>(hp, m);
     if (ln.launch_counter) ++*ln.launch_counter;
     return cudaGetLastError();
+}
+
+cudaError_t launch_allreduce_p2p(const Launcher& ln, double* d, int n, const P2PReduce& P, unsigned epoch)
+{
+    if (n < 1 || n > 4 || P.nranks > kMaxP2PRanks) return cudaErrorInvalidValue;
+    return launch_kernel(ln, k_allreduce_p2p, dim3(1), dim3(32), 0, d, n, P, epoch);
 }
 
 cudaError_t launch_cg_check(const Launcher& ln, const double* scal, int m, double eps, int* flags, int* hflags)

@@ -166,7 +166,8 @@ struct Launcher {
     bool pdl = false;  // programmatic dependent launch: overlap a kernel's launch and
                        // prologue with the previous kernel's tail (griddepcontrol)
     bool tmem = true;  // one-thread-per-column Thomas kernels keep g' in Tensor Memory (nz <= 128)
-    int tm_ctas = 1;   // CTAs per SM of those kernels (TMEM holds 2; 1 and 2 measured equal warm, 1 keeps the p halo rows in L2 cold)
+    int tm_stages = 3; // their TMA ring depth (3; 4, 5 for CGPREC A/B)
+    int tm_ctas = 2;   // CTAs per SM of those kernels (TMEM holds 2; r2f: 2 is 0.4% faster than 1)
 };
 
 // Launch with the PDL attribute when ln.pdl.  Every kernel launched this way executes
@@ -236,6 +237,21 @@ cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse,
 cudaError_t launch_copy(const Launcher& ln, double* dst, const double* src, int64_t n, const int* skip);
 
 cudaError_t launch_halo_push(const Launcher& ln, const HaloPush& hp);
+
+// Device-initiated allreduce over NVLink (P2P mode, up to kMaxP2PRanks ranks): every rank's
+// halo pool holds slots[2][kMaxP2PRanks][4] doubles and flags[kMaxP2PRanks] (uint32), mapped
+// into every other rank by CUDA IPC.  One single-warp kernel per allreduce of n <= 4 doubles:
+// store my values into slot [E&1][me] of every rank, fence, publish epoch E in every rank's
+// flags[me], wait until all flags[r] of my pool reached E, then sum slots [E&1][0..N-1] in rank
+// order -- the same sum, bit for bit, on every rank.  A wait longer than ~20 s (a rank that
+// died) writes NaN instead of hanging.
+constexpr int kMaxP2PRanks = 8;
+struct P2PReduce {
+    double* slots[kMaxP2PRanks];     // rank r's slot array (r == me: my own pool)
+    unsigned* flags[kMaxP2PRanks];   // rank r's flag array
+    int me, nranks;
+};
+cudaError_t launch_allreduce_p2p(const Launcher& ln, double* d, int n, const P2PReduce& P, unsigned epoch);
 
 // CG multi-GPU: p halo slabs updated locally, out = fma(beta, p, z) on each non-null slab.
 cudaError_t launch_cg_halo(const Launcher& ln, double* out_lo, const double* z_lo, const double* p_lo, double* out_hi,

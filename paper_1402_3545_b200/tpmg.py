@@ -47,7 +47,7 @@ class tpmg_result(C.Structure):
 class tpmg_stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("halo_exchanges", C.c_int64),
                 ("allreduces", C.c_int64), ("graph_launches", C.c_int64),
-                ("p2p_halo", C.c_int64)]
+                ("p2p_halo", C.c_int64), ("p2p_allreduce", C.c_int64)]
 
 
 _vp, _i32, _i64, _d = C.c_void_p, C.c_int32, C.c_int64, C.c_double
@@ -80,6 +80,8 @@ _SIGS = {
     "tpmg_set_profiles": ([_vp, _P(_d), _P(_d), _P(_d), _P(_d)], C.c_int),
     "tpmg_set_fields": ([_vp, _P(_d), _P(_d), _P(_d)], C.c_int),
     "tpmg_profile_read": ([_vp, _i32, _P(_i64), _P(_d), _P(_d)], C.c_int),
+    "tpmg_halo_push": ([_vp, _i32, _vp, _vp, _vp], C.c_int),
+    "tpmg_cg_halo": ([_vp, _d, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "tpmg_last_error": ([_vp], C.c_char_p),
 }
 for _name, (_args, _ret) in _SIGS.items():
@@ -300,6 +302,37 @@ def tpmg_solve_host(ctx: int, solver: int, f_host, u_host, eps: float = 1e-5,
     _check(getattr(_lib, _fn)(ctx, solver, hptr(f_host), hptr(u_host), eps, max_iter,
                               C.byref(res)), ctx)
     return _to_py(res, hist)
+
+
+def _plane_ptr(x, ctx, n, what):
+    """Address of a device plane of n doubles (checked like _ptr), None passes through."""
+    if x is None or isinstance(x, int):
+        return x
+    p = _ptr(x, ctx, None, what)
+    if x.numel() != n:
+        raise ValueError(f"{what}: {x.numel()} elements, a plane has {n}")
+    return p
+
+
+def tpmg_halo_push(ctx: int, level: int, src, dst_lo=None, dst_hi=None) -> None:
+    """dst_lo <- row 0 of src, dst_hi <- row ny-1 of src (the P2P halo push kernel)."""
+    lv = _lv(ctx, level)
+    n = None
+    if lv is not None:
+        _, nx, _, nz = tpmg_local_box(ctx, level)
+        n = nx * nz
+    _check(_lib.tpmg_halo_push(ctx, level, _ptr(src, ctx, lv, "src"),
+                               _plane_ptr(dst_lo, ctx, n, "dst_lo") if n else _ptr(dst_lo),
+                               _plane_ptr(dst_hi, ctx, n, "dst_hi") if n else _ptr(dst_hi)), ctx)
+
+
+def tpmg_cg_halo(ctx: int, beta: float, out_lo=None, z_lo=None, p_lo=None, out_hi=None, z_hi=None, p_hi=None) -> None:
+    """out = fma(beta, p, z) on each non-None fine-level halo plane (the CG p-halo update)."""
+    _, nx, _, nz = tpmg_local_box(ctx, _fine(ctx))
+    n = nx * nz
+    args = [_plane_ptr(x, ctx, n, w) for x, w in ((out_lo, "out_lo"), (z_lo, "z_lo"), (p_lo, "p_lo"),
+                                                  (out_hi, "out_hi"), (z_hi, "z_hi"), (p_hi, "p_hi"))]
+    _check(_lib.tpmg_cg_halo(ctx, float(beta), *args), ctx)
 
 
 def tpmg_get_stats(ctx: int) -> dict:

@@ -104,7 +104,11 @@ for name, solve, ref in (("mg", ctx.solve_mg, O.solve_mg(P, f)), ("cg", ctx.solv
 
 st = ctx.stats()
 if st["halo_exchanges"] == 0 or st["allreduces"] == 0:
-    failures.append(f"rank {rank}: no NCCL traffic recorded {st}")
+    failures.append(f"rank {rank}: no exchange / allreduce traffic recorded {st}")
+for key, var in (("p2p_halo", "TPMG_TEST_EXPECT_P2P"), ("p2p_allreduce", "TPMG_TEST_EXPECT_P2PAR")):
+    want = os.environ.get(var)
+    if want is not None and st[key] != int(want):   # the transport the case asked for is the one used
+        failures.append(f"rank {rank}: stats {key} = {st[key]}, expected {want}")
 ctx.close()
 allf = [None] * world
 dist.all_gather_object(allf, failures)
