@@ -122,6 +122,7 @@ struct tpmg_ctx {
     bool tmem = true;                   // Thomas g' of the column kernels in Tensor Memory (TPMG_TMEM=0: smem)
     int tm_ctas = 2;                    // their CTAs per SM (TPMG_TM_CTAS; r2c, r2f: 2 >= 1)
     int tm_stages = 3;                  // their TMA ring depth (TPMG_TM_STAGES: 3, 4, 5)
+    int prefetch = 0;                   // k_line: L2 prefetch chunks beyond the ring (TPMG_PREFETCH)
     bool ksplit_cg = false;             // k-split CG preconditioner (TPMG_KSPLIT_CG=1)
     bool halo_off = false;              // TPMG_HALO=off: skip halo exchanges (timing experiments)
     bool fused_push = false;            // P2P: producers push their boundary rows (TPMG_FUSED_PUSH=1)
@@ -349,6 +350,26 @@ tpmg_status p2p_finish(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int E)
     return E ? wait_epoch(ctx, ch, E) : TPMG_OK;
 }
 
+// x with the slabs of epoch E of channel ch (E = 0: the current slabs)
+HaloField halo_epoch_view(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, const double* x, int E)
+{
+    const bool lo = ctx->rank > 0, hi = ctx->rank < ctx->nranks - 1;
+    if (!E) return HaloField{x, lo ? *ch.cur_lo : nullptr, hi ? *ch.cur_hi : nullptr};
+    return HaloField{x, lo ? ch.lo[E & 1] : nullptr, hi ? ch.hi[E & 1] : nullptr};
+}
+
+// The in-kernel wait for epoch E of channel ch: my pool's flags [0] data from the lower
+// neighbour, [1] data from the upper one.
+HaloWait halo_wait_of(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int E)
+{
+    const unsigned* f = reinterpret_cast<const unsigned*>(static_cast<char*>(ctx->halo_pool) + ch.off_flags);
+    HaloWait w{};
+    w.flag[0] = ctx->rank > 0 ? f + 0 : nullptr;
+    w.flag[1] = ctx->rank < ctx->nranks - 1 ? f + 1 : nullptr;
+    w.epoch = (unsigned)E;
+    return w;
+}
+
 tpmg_status exchange_p2p(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int c, const double* x)
 {
     (void)c;
@@ -477,6 +498,7 @@ LineArgs line_args(tpmg_ctx* ctx, int level)
     a.ratio = DevRatio{nullptr, -1, -1};
     a.red = ReduceSlot{ctx->d_partials, ctx->d_ticket, nullptr, 0};
     a.skip = ctx->skip;
+    a.prefetch = ctx->prefetch;
     return a;
 }
 
@@ -762,18 +784,17 @@ tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, LineArgs a, const 
     const int nty = (int)((lc.ny + TY - 1) / TY);
     const bool fused_out = push_out && ctx->fused_push;
     if (ctx->p2p && ctx->overlap && !ctx->halo_off && !fused_out && nty >= 3) {
+        // ONE launch: its CTAs walk the interior tile rows first; the loader of a strip-
+        // boundary tile row waits in the kernel (ld.acquire.sys on my pool's epoch flag) for
+        // the neighbour's rows, which travel while the interior is computed
         tpmg_ctx::Chan& ch = ctx->chans[chan];
         int E = 0;
         TRY(p2p_begin(ctx, ch, x, &E));
-        a.part = PART_INTERIOR;
+        if (a.h0.base == x) a.h0 = halo_epoch_view(ctx, ch, x, E);
+        if (E) a.hw = halo_wait_of(ctx, ch, E);
         TRY(run_line(ctx, mode, a));
-        TRY(p2p_finish(ctx, ch, E));
-        if (a.h0.base == x) a.h0 = HaloField{x, ctx->rank > 0 ? *ch.cur_lo : nullptr,
-                                             ctx->rank < ctx->nranks - 1 ? *ch.cur_hi : nullptr};
-        TRY(pre_boundary(a));
-        a.part = PART_BOUNDARY;
-        a.red.accumulate = 1;
-        return run_line(ctx, mode, a);
+        TRY(p2p_finish(ctx, ch, E));   // stream order for the channel's next push (the kernel already waited)
+        return pre_boundary(a);
     }
     if (!ctx->overlap_nccl || ctx->p2p || nty < 3) {
         TRY(exchange_chan(ctx, chan, x));
@@ -872,19 +893,19 @@ tpmg_status prolong_overlapped(tpmg_ctx* ctx, int lc_)
     const double cells = level_cells(F.lc);
     const double fb = Cc.lc.ny > 0 ? 2.0 / (double)Cc.lc.ny : 1.0;   // boundary coarse rows' share
     if (ctx->nranks > 1 && ctx->p2p && ctx->overlap && !ctx->halo_off && !ctx->fused_push && Cc.lc.ny >= 3) {
-        // P2P overlap: interior coarse rows while the coarse halo rows travel
+        // P2P overlap in ONE launch: the blocks of the strip-boundary coarse rows go last and
+        // wait in the kernel for the coarse halo rows, which travel meanwhile
         tpmg_ctx::Chan& ch = ctx->chans[lc_];
         int E = 0;
         TRY(p2p_begin(ctx, ch, Cc.u[Cc.cur], &E));
+        const HaloField ucE = halo_epoch_view(ctx, ch, Cc.u[Cc.cur], E);
+        const HaloWait hw = halo_wait_of(ctx, ch, E);
         {
-            ProfScope ps(ctx, TPMG_K_PROLONG_ADD, cells * (1.0 - fb));
-            CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc, F.u[F.cur], ctx->skip, PART_INTERIOR));
+            ProfScope ps(ctx, TPMG_K_PROLONG_ADD, cells);
+            CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, ucE, F.u[F.cur], ctx->skip, PART_ALL, nullptr,
+                                             E ? &hw : nullptr));
         }
-        TRY(p2p_finish(ctx, ch, E));
-        const HaloField uc2 = halo_of(ctx, lc_, Cc.u[Cc.cur]);
-        ProfScope ps(ctx, TPMG_K_PROLONG_ADD, cells * fb);
-        CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, uc2, F.u[F.cur], ctx->skip, PART_BOUNDARY));
-        return TPMG_OK;
+        return p2p_finish(ctx, ch, E);
     }
     if (ctx->nranks == 1 || !ctx->overlap_nccl || ctx->p2p || Cc.lc.ny < 3) {
         TRY(exchange(ctx, lc_, Cc.u[Cc.cur]));
@@ -1743,6 +1764,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->sync_debug = sd && sd[0] == '1';
         const char* tm = std::getenv("TPMG_TMEM");   // "0": g' of the column kernels in shared memory
         ctx->tmem = !(tm && tm[0] == '0');
+        const char* pf = std::getenv("TPMG_PREFETCH");
+        if (pf) ctx->prefetch = std::max(0, std::min(8, std::atoi(pf)));
         const char* ts = std::getenv("TPMG_TM_STAGES");
         if (ts) ctx->tm_stages = std::atoi(ts);
         const char* tc = std::getenv("TPMG_TM_CTAS");

@@ -118,6 +118,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// L2 prefetch of a TMA box (no shared memory, no completion): the line kernels prefetch a few
+// chunks beyond their shared-memory ring so that the ring's loads hit L2
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int x, int y, int z)
+{
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y), "r"(z)
+                 : "memory");
+}
+
 // ------------------------------------------------------------------ Tensor Memory (TMEM)
 // The line kernels use TMEM (512 columns x 128 lanes x 32 bit per SM) as per-thread scratch
 // for the Thomas intermediates g'_k: thread t of warp w owns lane 32 w + t, level k sits in
@@ -174,6 +184,20 @@ __device__ __forceinline__ double tmem_ld_f64(uint32_t taddr)
         : "r"(taddr)
         : "memory");
     return __hiloint2double((int)hi, (int)lo);
+}
+
+// Wait until a halo epoch flag (written by a neighbour GPU's stream write-value into my
+// memory) reaches `epoch`; acquire at system scope, then order later TMA (async-proxy) reads
+// of the slab after it.
+__device__ __forceinline__ void halo_flag_wait(const unsigned* flag, unsigned epoch)
+{
+    for (;;) {
+        unsigned v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(flag) : "memory");
+        if ((int)(v - epoch) >= 0) break;
+        __nanosleep(32);
+    }
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
 
 // Dynamic shared memory available to a kernel: the opt-in maximum minus its static smem.

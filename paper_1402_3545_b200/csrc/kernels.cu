@@ -149,6 +149,18 @@ __device__ __forceinline__ void tma_stage(double* st, const LineArgs& a, int64_t
         tma_load_3d(st + G::PLAIN_BASE + f * TY * KB * TX, &a.tma.q[f], (int)i0, k0, (int)j0, bar);
 }
 
+// L2 prefetch of one stage's boxes (thread 0): the main boxes only (strip-boundary tiles
+// whose halo rows come from slabs are left to the ring's own loads).
+template <int NH, int NP, int TY>
+__device__ __forceinline__ void tma_prefetch_stage(const LineArgs& a, int64_t i0, int64_t j0, int k0)
+{
+    const int x0 = (int)i0 - 2;
+#pragma unroll
+    for (int f = 0; f < NH; ++f) tma_prefetch_3d(&a.tma.h[f].main, x0, k0, (int)j0 - 1);
+#pragma unroll
+    for (int f = 0; f < NP; ++f) tma_prefetch_3d(&a.tma.q[f], (int)i0, k0, (int)j0);
+}
+
 // The line kernel.  LOADER = 0: cp.async (all threads); 1: TMA (thread 0) with an
 // mbarrier per stage.  The CTA walks its tiles (tile = blockIdx.x + t*gridDim.x)
 // as one global sequence of KB-level chunks, so the loads of the next tile's
@@ -250,11 +262,37 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     int p_count = 0, p_ch = 0, p_slot = 0, p_tile = blockIdx.x;
     const bool plo = a.push.dst_lo != nullptr, phi = a.push.dst_hi != nullptr;
     const int nrows = part_rows(a.part, nty);
-    auto row_of = [&](int t) { return part_row(a.part, nty, push_row(t / ntx, nrows, plo, phi)); };
+    const bool hwait = a.hw.flag[0] || a.hw.flag[1];   // in-kernel halo wait: boundary rows last
+    auto row_of = [&](int t) {
+        return hwait ? boundary_last_row(t / ntx, nrows) : part_row(a.part, nty, push_row(t / ntx, nrows, plo, phi));
+    };
     int p_i0 = (p_tile % ntx) * TX, p_j0 = row_of(p_tile) * TY;
+    bool waited_lo = false, waited_hi = false;
+    // L2 prefetch cursor, a.prefetch chunks ahead of the ring's producer (TMA loader)
+    int f_count = 0, f_ch = 0, f_tile = blockIdx.x;
+    auto prefetch_next = [&]() {
+        if (f_count < total) {
+            if (tid == 0) tma_prefetch_stage<NH, NP, TY>(a, (int64_t)(f_tile % ntx) * TX, (int64_t)row_of(f_tile) * TY, f_ch * KB);
+            ++f_count;
+            if (++f_ch == nch) {
+                f_ch = 0;
+                f_tile += gridDim.x;
+            }
+        }
+    };
+    if constexpr (LOADER == 1)
+        if (a.prefetch > 0)
+            for (int q = 0; q < NS - 1 + a.prefetch; ++q) prefetch_next();
     auto issue = [&]() {
+        if constexpr (LOADER == 1)
+            if (a.prefetch > 0) prefetch_next();
         if (p_count < total) {
             double* st = stage + p_slot * G::STAGE;
+            if (hwait && p_ch == 0 && (LOADER == 0 || tid == 0)) {
+                // the first load of a tile row that reads a halo slab waits for its epoch
+                if (p_j0 == 0 && a.hw.flag[0] && !waited_lo) { halo_flag_wait(a.hw.flag[0], a.hw.epoch); waited_lo = true; }
+                if (p_j0 + TY >= ny && a.hw.flag[1] && !waited_hi) { halo_flag_wait(a.hw.flag[1], a.hw.epoch); waited_hi = true; }
+            }
             if constexpr (LOADER == 0) {
                 load_stage<NH, NP, TY>(st, a, p_i0, p_j0, p_ch * KB);
             } else {
@@ -735,18 +773,27 @@ __global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double
 // The work of k_prolong_add; threads outside the grid return early (no barrier here).
 template <bool PUSH>
 __device__ __forceinline__ void prolong_body(const LevelConst& Cc, const LevelConst& F, const HaloField& uc,
-                                             double* __restrict__ uf, int lpt, int part, const HaloPush& push)
+                                             double* __restrict__ uf, int lpt, int part, const HaloPush& push,
+                                             const HaloWait& hw)
 {
     const int64_t nxc = Cc.nx, nyc = Cc.ny;
     const int nz = Cc.nz;
     const int64_t I = blockIdx.x * 32 + threadIdx.x;
-    // PART_INTERIOR: coarse rows 1 .. nyc-2 (no halo row read); PART_BOUNDARY: rows 0, nyc-1
-    int64_t J = blockIdx.y * 4 + threadIdx.y;
+    // PART_INTERIOR: coarse rows 1 .. nyc-2 (no halo row read); PART_BOUNDARY: rows 0, nyc-1.
+    // In-kernel halo wait (hw): block row 0 (coarse rows 0..3) goes last, and the threads of
+    // coarse rows 0 / nyc-1 wait for the halo epoch before they read the slabs.
+    const bool hwait = hw.flag[0] || hw.flag[1];
+    const int by = hwait ? (int)((blockIdx.y + 1) % gridDim.y) : (int)blockIdx.y;
+    int64_t J = by * 4 + threadIdx.y;
     if (part == PART_INTERIOR) J += 1;
     else if (part == PART_BOUNDARY) J = (J == 0) ? 0 : ((J == 1 && nyc > 1) ? nyc - 1 : nyc);
     if (part == PART_INTERIOR && J >= nyc - 1) return;
     const int kbeg = blockIdx.z * lpt, kend = min(nz, kbeg + lpt);   // levels of this thread
     if (I >= nxc || J >= nyc) return;
+    if (hwait) {
+        if (J == 0 && hw.flag[0]) halo_flag_wait(hw.flag[0], hw.epoch);
+        if (J == nyc - 1 && hw.flag[1]) halo_flag_wait(hw.flag[1], hw.epoch);
+    }
     // coarse rows J-1, J, J+1 and columns I-1, I, I+1.  Ghosts outside the physical domain
     // are a factor times an in-domain value: 0 (zero coarse ghosts [R7]) or -1 (face
     // Dirichlet [R25]: the linear continuation through 0; a corner gets (-1)(-1) = +1), so
@@ -782,9 +829,11 @@ __device__ __forceinline__ void prolong_body(const LevelConst& Cc, const LevelCo
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
                 const double* r = rows[d] + (int64_t)k * nxc;
-                cc[q][d][0] = __ldg(r + iw);
-                cc[q][d][1] = __ldg(r + I);
-                cc[q][d][2] = __ldg(r + ie);
+                // plain loads, not ld.global.nc: with the in-kernel halo wait the slab rows are
+                // written (by the neighbour) while this kernel runs
+                cc[q][d][0] = r[iw];
+                cc[q][d][1] = r[I];
+                cc[q][d][2] = r[ie];
             }
         }
 #pragma unroll
@@ -821,12 +870,12 @@ __device__ __forceinline__ void prolong_body(const LevelConst& Cc, const LevelCo
 template <bool PUSH>
 __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const LevelConst F, const HaloField uc,
                                                      double* __restrict__ uf, int lpt, const int* skip, int part,
-                                                     const HaloPush push)
+                                                     const HaloPush push, const HaloWait hw)
 {
     pdl_wait();
     pdl_trigger();
     if (skip && *skip) return;
-    prolong_body<PUSH>(Cc, F, uc, uf, lpt, part, push);
+    prolong_body<PUSH>(Cc, F, uc, uf, lpt, part, push, hw);
 }
 
 
@@ -1112,7 +1161,8 @@ cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const Le
 }
 
 cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, const LevelConst& fine,
-                               HaloField uc, double* uf, const int* skip, int part, const HaloPush* push)
+                               HaloField uc, double* uf, const int* skip, int part, const HaloPush* push,
+                               const HaloWait* hw)
 {
     if (coarse.nx <= 0 || coarse.ny <= 0) return cudaSuccess;
     // levels per thread: enough threads to fill the GPU on the coarse levels
@@ -1127,9 +1177,10 @@ cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, con
     if (part == PART_BOUNDARY) grid.y = 1;
     if (grid.y == 0) return cudaSuccess;
     const HaloPush hp = push ? *push : HaloPush{};
+    const HaloWait w = hw ? *hw : HaloWait{};
     if (hp.dst_lo || hp.dst_hi)
-        return launch_kernel(ln, k_prolong_add<true>, dim3(grid), dim3(block), 0, coarse, fine, uc, uf, lpt, skip, part, hp);
-    return launch_kernel(ln, k_prolong_add<false>, dim3(grid), dim3(block), 0, coarse, fine, uc, uf, lpt, skip, part, hp);
+        return launch_kernel(ln, k_prolong_add<true>, dim3(grid), dim3(block), 0, coarse, fine, uc, uf, lpt, skip, part, hp, w);
+    return launch_kernel(ln, k_prolong_add<false>, dim3(grid), dim3(block), 0, coarse, fine, uc, uf, lpt, skip, part, hp, w);
 }
 
 cudaError_t launch_dot(const Launcher& ln, const double* x, const double* y, int64_t n, ReduceSlot red)

@@ -139,6 +139,22 @@ struct HaloPush {
     double* dst_hi;
     int64_t n;
 };
+// In-kernel halo wait (P2P overlap in ONE launch): flag[0] / flag[1] are my pool's epoch
+// flags "data from the lower / upper neighbour".  When set, the line kernels walk their
+// tile rows interior-first (boundary_last_row) and the loader waits (ld.acquire.sys)
+// until flag >= epoch before it loads a tile row that reads that halo slab, so the interior
+// rows run while the neighbours' rows are still on the way.  nullptr: no wait.
+struct HaloWait {
+    const unsigned* flag[2];
+    unsigned epoch;
+};
+// Tile-row order with the strip-boundary rows last (nrows >= 3): 1, 2, ..., nrows-2, 0, nrows-1.
+__host__ __device__ inline int boundary_last_row(int r, int nrows)
+{
+    if (nrows < 3) return r;
+    return r < nrows - 2 ? r + 1 : (r == nrows - 2 ? 0 : nrows - 1);
+}
+
 struct LineArgs {
     LevelConst L;
     double rho;        // smoother relaxation (MODE_SMOOTH)
@@ -155,6 +171,8 @@ struct LineArgs {
     const int* skip;   // device flag: the kernel returns at once when *skip != 0 (solver run-ahead)
     int part;          // TilePart: which tile rows this launch covers
     HaloPush push;     // fused halo push of the output (dst == nullptr: none)
+    HaloWait hw;       // in-kernel wait for the halo'd input's slabs (P2P overlap)
+    int prefetch;      // k_line, TMA: L2 prefetch (TMA bulk prefetch) this many chunks beyond the ring
     TmaMaps tma;
 };
 
@@ -232,7 +250,7 @@ cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const Le
 // of the updated fine boundary rows (optional)
 cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse,
                                const LevelConst& fine, HaloField uc, double* uf, const int* skip = nullptr,
-                               int part = PART_ALL, const HaloPush* push = nullptr);
+                               int part = PART_ALL, const HaloPush* push = nullptr, const HaloWait* hw = nullptr);
 // dst = src (n doubles) unless *skip
 cudaError_t launch_copy(const Launcher& ln, double* dst, const double* src, int64_t n, const int* skip);
 

@@ -180,7 +180,9 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     const int nrows = part_rows(a.part, nty);
     const int ntiles = ntx * nrows;
     const bool plo = PUSH && a.push.dst_lo != nullptr, phi = PUSH && a.push.dst_hi != nullptr;
+    const bool hwait = a.hw.flag[0] || a.hw.flag[1];   // in-kernel halo wait: boundary rows last
     auto row_of = [&](int t) {
+        if (hwait) return boundary_last_row(t / ntx, nrows);
         return part_row(a.part, nty, PUSH ? push_row(t / ntx, nrows, plo, phi) : t / ntx);
     };
     const int my_tiles = ((int)blockIdx.x < ntiles) ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
@@ -189,8 +191,14 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
 
     // producer (thread 0) and consumer cursors over the CTA's (tile, chunk) steps
     int p_count = 0, p_cc = 0, p_slot = 0, p_tile = blockIdx.x;
+    bool waited_lo = false, waited_hi = false;
     auto issue = [&]() {
         if (tid == 0 && p_count < total) {
+            if (hwait && p_cc == 0) {   // the first load of a tile row that reads a halo slab waits for its epoch
+                const int j0 = row_of(p_tile) * TY;
+                if (j0 == 0 && a.hw.flag[0] && !waited_lo) { halo_flag_wait(a.hw.flag[0], a.hw.epoch); waited_lo = true; }
+                if (j0 + TY >= ny && a.hw.flag[1] && !waited_hi) { halo_flag_wait(a.hw.flag[1], a.hw.epoch); waited_hi = true; }
+            }
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             tma_step<MODE, TY, KB, NSEG>(stage + p_slot * STG, a, (p_tile % ntx) * TX, row_of(p_tile) * TY, p_cc,
                                          &full_bar[p_slot]);

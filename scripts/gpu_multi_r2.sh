@@ -8,7 +8,7 @@ TAG=${TAG:-mr}
 N=$(nvidia-smi -L | wc -l)
 nvidia-smi topo -m > gpurun_out/topo_$TAG.txt 2>&1
 if [ -z "$SKIP_TESTS" ]; then
-  timeout 1800 python -m pytest tests/test_gpu_multirank.py tests/test_gpu_halo.py -m gpu -q -rs > gpurun_out/pytest_multirank_${N}gpu_$TAG.log 2>&1
+  timeout 1800 python -m pytest ${PYTEST_FILES:-tests/test_gpu_multirank.py tests/test_gpu_halo.py} -m gpu -q -rs > gpurun_out/pytest_multirank_${N}gpu_$TAG.log 2>&1
   echo "pytest exit $?" >> gpurun_out/pytest_multirank_${N}gpu_$TAG.log
 fi
 IFS=';' read -ra VS <<< "${VARIANTS:--;TPMG_OVERLAP=0;TPMG_ALLREDUCE=nccl;TPMG_HALO=nccl}"
