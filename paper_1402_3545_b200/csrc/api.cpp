@@ -122,7 +122,6 @@ struct tpmg_ctx {
     bool tmem = true;                   // Thomas g' of the column kernels in Tensor Memory (TPMG_TMEM=0: smem)
     int tm_ctas = 2;                    // their CTAs per SM (TPMG_TM_CTAS; r2c, r2f: 2 >= 1)
     int tm_stages = 3;                  // their TMA ring depth (TPMG_TM_STAGES: 3, 4, 5)
-    int prefetch = 0;                   // k_line: L2 prefetch chunks beyond the ring (TPMG_PREFETCH)
     bool ksplit_cg = false;             // k-split CG preconditioner (TPMG_KSPLIT_CG=1)
     bool halo_off = false;              // TPMG_HALO=off: skip halo exchanges (timing experiments)
     bool fused_push = false;            // P2P: producers push their boundary rows (TPMG_FUSED_PUSH=1)
@@ -498,7 +497,6 @@ LineArgs line_args(tpmg_ctx* ctx, int level)
     a.ratio = DevRatio{nullptr, -1, -1};
     a.red = ReduceSlot{ctx->d_partials, ctx->d_ticket, nullptr, 0};
     a.skip = ctx->skip;
-    a.prefetch = ctx->prefetch;
     return a;
 }
 
@@ -634,7 +632,7 @@ void fill_tma(tpmg_ctx* ctx, int mode, LineArgs& a)
     const int64_t nx = a.L.nx, ny = a.L.ny;
     const int nz = a.L.nz;
     if (nx % 2) return;
-    const int TY = line_tile_rows(mode, nz, a.L.gen);
+    const int TY = line_tile_rows(mode, nz, a.L.gen, ctx->tmem);
     int nh, np;
     mode_fields(mode, &nh, &np);
     const HaloField* H[2] = {&a.h0, &a.h1};
@@ -716,7 +714,8 @@ bool ksplit_usable(tpmg_ctx* ctx, int mode, const LevelConst& lc)
 // Tile rows of the kernel run_line will launch for this mode and level.
 int launch_rows(tpmg_ctx* ctx, int mode, const LevelConst& lc)
 {
-    return ksplit_usable(ctx, mode, lc) ? ksplit_boxes(mode, ctx->ksplit_cfg).ty : line_tile_rows(mode, lc.nz, lc.gen);
+    return ksplit_usable(ctx, mode, lc) ? ksplit_boxes(mode, ctx->ksplit_cfg).ty
+                                        : line_tile_rows(mode, lc.nz, lc.gen, ctx->tmem && ctx->use_tma);
 }
 
 // Fraction of the level's cells a launch covers (interior / boundary tile rows).
@@ -783,7 +782,9 @@ tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, LineArgs a, const 
     const int TY = launch_rows(ctx, mode, lc);
     const int nty = (int)((lc.ny + TY - 1) / TY);
     const bool fused_out = push_out && ctx->fused_push;
-    if (ctx->p2p && ctx->overlap && !ctx->halo_off && !fused_out && nty >= 3) {
+    const bool hw_ok = ksplit_usable(ctx, mode, lc) ? ksplit_halo_wait(mode, ctx->ksplit_cfg, lc.gen)
+                                                    : line_halo_wait(mode, lc.nz, lc.gen, ctx->use_tma, ctx->tmem);
+    if (ctx->p2p && ctx->overlap && !ctx->halo_off && !fused_out && nty >= 3 && hw_ok) {
         // ONE launch: its CTAs walk the interior tile rows first; the loader of a strip-
         // boundary tile row waits in the kernel (ld.acquire.sys on my pool's epoch flag) for
         // the neighbour's rows, which travel while the interior is computed
@@ -1764,8 +1765,6 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->sync_debug = sd && sd[0] == '1';
         const char* tm = std::getenv("TPMG_TMEM");   // "0": g' of the column kernels in shared memory
         ctx->tmem = !(tm && tm[0] == '0');
-        const char* pf = std::getenv("TPMG_PREFETCH");
-        if (pf) ctx->prefetch = std::max(0, std::min(8, std::atoi(pf)));
         const char* ts = std::getenv("TPMG_TM_STAGES");
         if (ts) ctx->tm_stages = std::atoi(ts);
         const char* tc = std::getenv("TPMG_TM_CTAS");

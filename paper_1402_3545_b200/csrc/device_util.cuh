@@ -118,16 +118,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-// L2 prefetch of a TMA box (no shared memory, no completion): the line kernels prefetch a few
-// chunks beyond their shared-memory ring so that the ring's loads hit L2
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int x, int y, int z)
-{
-    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"(x), "r"(y), "r"(z)
-                 : "memory");
-}
-
 // ------------------------------------------------------------------ Tensor Memory (TMEM)
 // The line kernels use TMEM (512 columns x 128 lanes x 32 bit per SM) as per-thread scratch
 // for the Thomas intermediates g'_k: thread t of warp w owns lane 32 w + t, level k sits in
@@ -173,6 +163,27 @@ __device__ __forceinline__ void tmem_ld_f64x8(uint32_t taddr, double (&v)[8])
         : "memory");
 #pragma unroll
     for (int q = 0; q < 8; ++q) v[q] = __hiloint2double((int)r[2 * q + 1], (int)r[2 * q]);
+}
+// Split form for software pipelining: issue the load of 16 columns now, wait later.  The wait
+// names the 16 destination registers as read-write operands, so the compiler cannot move
+// any use (or copy) of them above it.
+__device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t (&r)[16])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld16_wait(uint32_t (&r)[16])
+{
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+                 :
+                 : "memory");
 }
 __device__ __forceinline__ double tmem_ld_f64(uint32_t taddr)
 {

@@ -149,18 +149,6 @@ __device__ __forceinline__ void tma_stage(double* st, const LineArgs& a, int64_t
         tma_load_3d(st + G::PLAIN_BASE + f * TY * KB * TX, &a.tma.q[f], (int)i0, k0, (int)j0, bar);
 }
 
-// L2 prefetch of one stage's boxes (thread 0): the main boxes only (strip-boundary tiles
-// whose halo rows come from slabs are left to the ring's own loads).
-template <int NH, int NP, int TY>
-__device__ __forceinline__ void tma_prefetch_stage(const LineArgs& a, int64_t i0, int64_t j0, int k0)
-{
-    const int x0 = (int)i0 - 2;
-#pragma unroll
-    for (int f = 0; f < NH; ++f) tma_prefetch_3d(&a.tma.h[f].main, x0, k0, (int)j0 - 1);
-#pragma unroll
-    for (int f = 0; f < NP; ++f) tma_prefetch_3d(&a.tma.q[f], (int)i0, k0, (int)j0);
-}
-
 // The line kernel.  LOADER = 0: cp.async (all threads); 1: TMA (thread 0) with an
 // mbarrier per stage.  The CTA walks its tiles (tile = blockIdx.x + t*gridDim.x)
 // as one global sequence of KB-level chunks, so the loads of the next tile's
@@ -179,12 +167,13 @@ __device__ __forceinline__ void tma_prefetch_stage(const LineArgs& a, int64_t i0
 // that held one CTA per SM leave room for two, i.e. twice the warps to hide the recurrences'
 // latency; TMEM itself (256 columns = 128 levels per CTA) holds exactly two CTAs.
 constexpr uint32_t kTmemCols = 256;
-template <int MODE, int TY, int LOADER, int GEN, int TMS = 0>
+// HW: the in-kernel halo wait of the P2P overlap (LineArgs::hw), a separate instantiation
+template <int MODE, int TY, int LOADER, int GEN, int TMS = 0, bool HW = false>
 __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArgs a)
 {
     using T = Traits<MODE>;
     constexpr bool TM = TMS > 0;   // TMS: pipeline stages of the TMEM form (the freed shared memory deepens it)
-    static_assert(!TM || (TY == 4 && GEN == 0 && T::THOMAS), "TMEM g' buffer: 4 warps, flat box, Thomas modes");
+    static_assert(!TM || (TY == 4 && T::THOMAS), "TMEM g' buffer: 4 warps (the 4 TMEM lane quarters), Thomas modes");
     constexpr int NH = T::NH, NP = T::NP, NR = T::NR;
     using G = Geom<NH, NP, TY>;
     constexpr int NT = G::NT;
@@ -204,10 +193,10 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     double* stage = ptab + (GEN ? ptn : 0);  // NS stages
     double* gbuf = stage + NS * G::STAGE;    // g'[nz][NT] (Thomas modes)
     const int nck = (nz + KB - 1) / KB;
-    double* cbuf = gbuf + nz * NT;           // GEN 2: m_{c KB - 1}[nck][NT], the pivot checkpoints
+    double* cbuf = gbuf + (TM ? 0 : nz * NT);           // GEN 2: m_{c KB - 1}[nck][NT], the pivot checkpoints
     // MODE_RESTRICT: x-pair sums [2][TY][KB+1][TX/2] (a chunk completes up to KB+1 levels)
     constexpr int RS = KB + 1;
-    double* rbuf = gbuf + ((T::THOMAS && !TM) ? (nz + (GEN == 2 ? nck : 0)) * NT : 0);
+    double* rbuf = gbuf + (T::THOMAS ? ((TM ? 0 : nz) + (GEN == 2 ? nck : 0)) * NT : 0);
     double* scratch = rbuf + (MODE == MODE_RESTRICT ? 2 * TY * RS * (TX / 2) : 0);  // reduction scratch
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
@@ -262,36 +251,21 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     int p_count = 0, p_ch = 0, p_slot = 0, p_tile = blockIdx.x;
     const bool plo = a.push.dst_lo != nullptr, phi = a.push.dst_hi != nullptr;
     const int nrows = part_rows(a.part, nty);
-    const bool hwait = a.hw.flag[0] || a.hw.flag[1];   // in-kernel halo wait: boundary rows last
     auto row_of = [&](int t) {
-        return hwait ? boundary_last_row(t / ntx, nrows) : part_row(a.part, nty, push_row(t / ntx, nrows, plo, phi));
+        if constexpr (HW) return boundary_last_row(t / ntx, nrows);   // in-kernel halo wait: boundary rows last
+        return part_row(a.part, nty, push_row(t / ntx, nrows, plo, phi));
     };
     int p_i0 = (p_tile % ntx) * TX, p_j0 = row_of(p_tile) * TY;
     bool waited_lo = false, waited_hi = false;
-    // L2 prefetch cursor, a.prefetch chunks ahead of the ring's producer (TMA loader)
-    int f_count = 0, f_ch = 0, f_tile = blockIdx.x;
-    auto prefetch_next = [&]() {
-        if (f_count < total) {
-            if (tid == 0) tma_prefetch_stage<NH, NP, TY>(a, (int64_t)(f_tile % ntx) * TX, (int64_t)row_of(f_tile) * TY, f_ch * KB);
-            ++f_count;
-            if (++f_ch == nch) {
-                f_ch = 0;
-                f_tile += gridDim.x;
-            }
-        }
-    };
-    if constexpr (LOADER == 1)
-        if (a.prefetch > 0)
-            for (int q = 0; q < NS - 1 + a.prefetch; ++q) prefetch_next();
     auto issue = [&]() {
-        if constexpr (LOADER == 1)
-            if (a.prefetch > 0) prefetch_next();
         if (p_count < total) {
             double* st = stage + p_slot * G::STAGE;
-            if (hwait && p_ch == 0 && (LOADER == 0 || tid == 0)) {
-                // the first load of a tile row that reads a halo slab waits for its epoch
-                if (p_j0 == 0 && a.hw.flag[0] && !waited_lo) { halo_flag_wait(a.hw.flag[0], a.hw.epoch); waited_lo = true; }
-                if (p_j0 + TY >= ny && a.hw.flag[1] && !waited_hi) { halo_flag_wait(a.hw.flag[1], a.hw.epoch); waited_hi = true; }
+            if constexpr (HW) {
+                if (p_ch == 0 && (LOADER == 0 || tid == 0)) {
+                    // the first load of a tile row that reads a halo slab waits for its epoch
+                    if (p_j0 == 0 && a.hw.flag[0] && !waited_lo) { halo_flag_wait(a.hw.flag[0], a.hw.epoch); waited_lo = true; }
+                    if (p_j0 + TY >= ny && a.hw.flag[1] && !waited_hi) { halo_flag_wait(a.hw.flag[1], a.hw.epoch); waited_hi = true; }
+                }
             }
             if constexpr (LOADER == 0) {
                 load_stage<NH, NP, TY>(st, a, p_i0, p_j0, p_ch * KB);
@@ -565,18 +539,28 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             // 1869 vs 1770 us for the fine-level smoother, more registers, same stalls)
             double* obase = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase;
             double x = 0.0;
+            if constexpr (TM) tmem_wait_st();   // the forward sweep's g' stores have landed
             for (int c = nck - 1; c >= 0; --c) {
                 const int kb0 = c * KB;
                 double p1 = c ? cbuf[c * NT + tid] : 1.0, p2 = c ? 1.0 : 0.0;
                 double t1 = c ? fT * ptab[2 * nz + kb0 - 1] : 0.0;
                 double tq[KB], gv[KB];
+                if constexpr (TM) {   // g' of this chunk from Tensor Memory (warp-uniform loads)
+                    if (kb0 + KB <= nz) {
+                        tmem_ld_f64x8(tbase + 2u * (uint32_t)kb0, gv);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < KB; ++q)
+                            if (kb0 + q < nz) gv[q] = tmem_ld_f64(tbase + 2u * (uint32_t)(kb0 + q));
+                    }
+                }
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
                     const int k = kb0 + q;
                     if (k < nz) {
                         const double tk = fT * ptab[2 * nz + k];
                         tq[q] = -(tk * pivot_step(k, p1, p2, t1));   // -t'_k = -t_k / m_k
-                        gv[q] = gbuf[k * NT + tid];
+                        if constexpr (!TM) gv[q] = gbuf[k * NT + tid];
                     }
                 }
 #pragma unroll
@@ -595,17 +579,28 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             double* op = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase + (int64_t)(nz - 1) * nx;
             double x = 0.0;
             int k = nz - 1;
-            if constexpr (TM) tmem_wait_st();   // the forward sweep's g' stores have landed
+            // TM: the chunk's g' comes from Tensor Memory; the load of the next chunk is issued
+            // before this chunk's recurrence (software pipelining, one load in flight)
+            uint32_t tcur[16], tnxt[16];
+            if constexpr (TM) {
+                static_assert(KB == 8, "16 TMEM columns = 8 levels per chunk");
+                tmem_wait_st();   // the forward sweep's g' stores have landed
+                if (k >= KB - 1) {
+                    tmem_ld16_issue(tbase + 2u * (uint32_t)(k - (KB - 1)), tcur);
+                    tmem_ld16_wait(tcur);
+                }
+            }
             for (; k >= KB - 1; k -= KB) {
                 const double* gq = gbuf + (k - (KB - 1)) * NT + tid;   // levels k-KB+1 .. k
                 const double* mq = gim + (k - (KB - 1));
                 double gv[KB], gm[KB];
+                bool more = false;
                 if constexpr (TM) {
-                    static_assert(KB == 8, "tmem_ld_f64x8 loads 8 levels");
-                    double g8[KB];
-                    tmem_ld_f64x8(tbase + 2u * (uint32_t)(k - (KB - 1)), g8);
+                    more = k - KB >= KB - 1;
+                    if (more) tmem_ld16_issue(tbase + 2u * (uint32_t)(k - KB - (KB - 1)), tnxt);
 #pragma unroll
-                    for (int q = 0; q < KB; ++q) gv[q] = g8[KB - 1 - q];
+                    for (int q = 0; q < KB; ++q)
+                        gv[q] = __hiloint2double((int)tcur[2 * (KB - 1 - q) + 1], (int)tcur[2 * (KB - 1 - q)]);
                 }
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
@@ -617,6 +612,13 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                     x = fma(gm[q], x, gv[q]);
                     if (valid) *op = x;
                     op -= nx;
+                }
+                if constexpr (TM) {
+                    if (more) {
+                        tmem_ld16_wait(tnxt);
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) tcur[q] = tnxt[q];
+                    }
                 }
             }
             for (; k >= 0; --k) {
@@ -677,19 +679,19 @@ size_t line_smem_bytes(int nz, int gen = 0, int tms = 0)
     using G = Geom<T::NH, T::NP, TY>;
     const bool tm = tms > 0;
     size_t d = ((3 * nz + 15) & ~15) + (gen >= 2 ? ((4 * nz + 15) & ~15) : gen ? ((3 * nz + 15) & ~15) : 0) +
-               (size_t)(tm ? tms : gen == 2 ? stages<MODE, 2>() : kNS) * G::STAGE + ((T::THOMAS && !tm) ? (size_t)(nz + (gen == 2 ? (nz + KB - 1) / KB : 0)) * G::NT : 0) + 64 + 16 +
+               (size_t)(tm ? tms : gen == 2 ? stages<MODE, 2>() : kNS) * G::STAGE + (T::THOMAS ? (size_t)((tm ? 0 : nz) + (gen == 2 ? (nz + KB - 1) / KB : 0)) * G::NT : 0) + 64 + 16 +
                (MODE == MODE_RESTRICT ? 2 * TY * (KB + 1) * (TX / 2) : 0);
     return d * sizeof(double);
 }
 
 constexpr size_t kMaxSmem = 227 * 1024 - 1024;  // leave room for static smem (barriers, flags)
 
-template <int MODE, int TY, int LOADER, int GEN, int TMS = 0>
+template <int MODE, int TY, int LOADER, int GEN, int TMS = 0, bool HW = false>
 cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
 {
     constexpr bool TM = TMS > 0;
     const size_t smem = line_smem_bytes<MODE, TY>(a.L.nz, GEN, TMS);
-    auto kern = k_line<MODE, TY, LOADER, GEN, TMS>;
+    auto kern = k_line<MODE, TY, LOADER, GEN, TMS, HW>;
     static size_t limit = 0;   // per instantiation
     if (!limit) {
         limit = dyn_smem_limit(kern);
@@ -720,8 +722,21 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
 template <int MODE, int TY>
 cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
 {
+    if (a.hw.flag[0] || a.hw.flag[1]) {   // P2P overlap with the in-kernel halo wait (line_halo_wait())
+        if constexpr (TY == 4 && (MODE == MODE_CGDIR || MODE == MODE_RESTRICT))
+            if (!a.L.gen && a.use_tma) return launch_line_l<MODE, 4, 1, 0, 0, true>(ln, a);
+        if constexpr (TY == 4 && MODE == MODE_SMOOTH)
+            if (!a.L.gen && a.use_tma && ln.tmem && a.L.nz <= (int)(kTmemCols / 2))
+                return launch_line_l<MODE, 4, 1, 0, 3, true>(ln, a);
+        return cudaErrorNotSupported;
+    }
     if (a.L.gen) {   // general vertical profiles / per-column fields: TMA loader only
         if (!a.use_tma) return cudaErrorNotSupported;
+        if constexpr (Traits<MODE>::THOMAS && TY == 4)   // g' in Tensor Memory, 2 CTAs per SM
+            if (ln.tmem && a.L.nz <= (int)(kTmemCols / 2)) {
+                if (a.L.gen >= 2) return launch_line_l<MODE, 4, 1, 2, (MODE == MODE_CGPREC ? 2 : 3)>(ln, a);
+                return launch_line_l<MODE, 4, 1, 1, 3>(ln, a);
+            }
         return a.L.gen >= 2 ? launch_line_l<MODE, TY, 1, 2>(ln, a) : launch_line_l<MODE, TY, 1, 1>(ln, a);
     }
     if constexpr (Traits<MODE>::THOMAS && TY == 4)   // g' in Tensor Memory (flat box, TMA loader)
@@ -741,7 +756,7 @@ cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
 template <int MODE>
 cudaError_t launch_line_ty(const Launcher& ln, const LineArgs& a)
 {
-    if (ln.tmem && a.use_tma && !a.L.gen && a.L.nz <= (int)(kTmemCols / 2)) return launch_line_t<MODE, 4>(ln, a);
+    if (ln.tmem && a.use_tma && a.L.nz <= (int)(kTmemCols / 2)) return launch_line_t<MODE, 4>(ln, a);
     if (line_smem_bytes<MODE, 4>(a.L.nz, a.L.gen) <= kMaxSmem) return launch_line_t<MODE, 4>(ln, a);
     if (line_smem_bytes<MODE, 2>(a.L.nz, a.L.gen) <= kMaxSmem) return launch_line_t<MODE, 2>(ln, a);
     return launch_line_t<MODE, 1>(ln, a);
@@ -1058,6 +1073,13 @@ cudaError_t launch_mg_check(const Launcher& ln, const double* norm2, const doubl
     return launch_kernel(ln, k_mg_check, dim3(1), dim3(1), 0, norm2, r0_2, n, eps, max_iter, flags, hflags);
 }
 
+bool line_halo_wait(int mode, int nz, int gen, bool use_tma, bool tmem)
+{
+    if (gen || !use_tma) return false;
+    if (mode == MODE_CGDIR || mode == MODE_RESTRICT) return true;
+    return mode == MODE_SMOOTH && tmem && nz <= (int)(kTmemCols / 2);
+}
+
 int line_launch_rows(int mode, int nz, int nx, int use_tma, int ksplit_cfg)
 {
     if (use_tma && ksplit_cfg >= 0 && ksplit_supported(mode, nz, nx)) return ksplit_boxes(mode, ksplit_cfg).ty;
@@ -1066,8 +1088,10 @@ int line_launch_rows(int mode, int nz, int nx, int use_tma, int ksplit_cfg)
 
 bool line_gen_fits(int nz, int gen) { return line_smem_bytes<MODE_CGPREC, 1>(nz, gen) <= kMaxSmem; }
 
-int line_tile_rows(int mode, int nz, int gen)
+int line_tile_rows(int mode, int nz, int gen, bool tm)
 {
+    // the Tensor Memory form of the Thomas modes always runs 4 tile rows (the lane quarters)
+    if (tm && nz <= (int)(kTmemCols / 2) && (mode == MODE_PREC || mode == MODE_SMOOTH || mode == MODE_CGPREC)) return 4;
     switch (mode) {
     case MODE_PREC: return line_smem_bytes<MODE_PREC, 4>(nz, gen) <= kMaxSmem ? 4 : line_smem_bytes<MODE_PREC, 2>(nz, gen) <= kMaxSmem ? 2 : 1;
     case MODE_SMOOTH: return line_smem_bytes<MODE_SMOOTH, 4>(nz, gen) <= kMaxSmem ? 4 : line_smem_bytes<MODE_SMOOTH, 2>(nz, gen) <= kMaxSmem ? 2 : 1;

@@ -172,7 +172,6 @@ struct LineArgs {
     int part;          // TilePart: which tile rows this launch covers
     HaloPush push;     // fused halo push of the output (dst == nullptr: none)
     HaloWait hw;       // in-kernel wait for the halo'd input's slabs (P2P overlap)
-    int prefetch;      // k_line, TMA: L2 prefetch (TMA bulk prefetch) this many chunks beyond the ring
     TmaMaps tma;
 };
 
@@ -215,7 +214,7 @@ int line_launch_rows(int mode, int nz, int nx, int use_tma, int ksplit_cfg);
 
 cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a);
 // Tile rows TY the launcher uses for `mode` at this nz (the TMA boxes depend on it).
-int line_tile_rows(int mode, int nz, int gen = 0);   // gen: general vertical profiles
+int line_tile_rows(int mode, int nz, int gen = 0, bool tm = false);   // gen: vertical profiles / fields; tm: TMEM form
 bool line_gen_fits(int nz, int gen = 1);   // the line kernels' on-chip buffers fit nz (gen 1: profiles, 2: fields)
 // Largest nz the on-chip Thomas buffer supports.
 int line_max_nz();
@@ -237,6 +236,9 @@ struct KsplitBoxes {
     int xoc;     // coarse box starts at column i0/2 - xoc
 };
 bool ksplit_supported(int mode, int nz, int nx);
+// The launchers that have an in-kernel halo wait (LineArgs::hw) instantiation
+bool ksplit_halo_wait(int mode, int cfg, int gen);
+bool line_halo_wait(int mode, int nz, int gen, bool use_tma, bool tmem);
 KsplitBoxes ksplit_boxes(int mode, int cfg);
 cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const LineArgs& a, const KTables& T);
 

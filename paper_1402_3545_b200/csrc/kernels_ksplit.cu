@@ -131,7 +131,9 @@ __device__ __forceinline__ void tma_step(double* st, const LineArgs& a, int i0, 
     }
 }
 
-template <int MODE, int TY, int NSEG, int KB, int NS2, bool PUSH, bool GEN>
+// HW: the in-kernel halo wait of the P2P overlap (LineArgs::hw), a separate instantiation
+// so that the single-GPU kernels carry none of its code
+template <int MODE, int TY, int NSEG, int KB, int NS2, bool PUSH, bool GEN, bool HW = false>
 __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_constant__ LineArgs a,
                                                              const __grid_constant__ KTables T)
 {
@@ -180,9 +182,8 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     const int nrows = part_rows(a.part, nty);
     const int ntiles = ntx * nrows;
     const bool plo = PUSH && a.push.dst_lo != nullptr, phi = PUSH && a.push.dst_hi != nullptr;
-    const bool hwait = a.hw.flag[0] || a.hw.flag[1];   // in-kernel halo wait: boundary rows last
     auto row_of = [&](int t) {
-        if (hwait) return boundary_last_row(t / ntx, nrows);
+        if constexpr (HW) return boundary_last_row(t / ntx, nrows);   // in-kernel halo wait: boundary rows last
         return part_row(a.part, nty, PUSH ? push_row(t / ntx, nrows, plo, phi) : t / ntx);
     };
     const int my_tiles = ((int)blockIdx.x < ntiles) ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
@@ -194,10 +195,12 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     bool waited_lo = false, waited_hi = false;
     auto issue = [&]() {
         if (tid == 0 && p_count < total) {
-            if (hwait && p_cc == 0) {   // the first load of a tile row that reads a halo slab waits for its epoch
-                const int j0 = row_of(p_tile) * TY;
-                if (j0 == 0 && a.hw.flag[0] && !waited_lo) { halo_flag_wait(a.hw.flag[0], a.hw.epoch); waited_lo = true; }
-                if (j0 + TY >= ny && a.hw.flag[1] && !waited_hi) { halo_flag_wait(a.hw.flag[1], a.hw.epoch); waited_hi = true; }
+            if constexpr (HW) {
+                if (p_cc == 0) {   // the first load of a tile row that reads a halo slab waits for its epoch
+                    const int j0 = row_of(p_tile) * TY;
+                    if (j0 == 0 && a.hw.flag[0] && !waited_lo) { halo_flag_wait(a.hw.flag[0], a.hw.epoch); waited_lo = true; }
+                    if (j0 + TY >= ny && a.hw.flag[1] && !waited_hi) { halo_flag_wait(a.hw.flag[1], a.hw.epoch); waited_hi = true; }
+                }
             }
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             tma_step<MODE, TY, KB, NSEG>(stage + p_slot * STG, a, (p_tile % ntx) * TX, row_of(p_tile) * TY, p_cc,
@@ -415,10 +418,10 @@ size_t ksmem(int nz)
     return (size_t)(NS2 * NSEG * G::SEGST + r16(6 * nz) + G::template bnd<NSEG>() + 64 + 16) * sizeof(double);
 }
 
-template <int MODE, int TY, int NSEG, int KB, int NS2, bool PUSH, bool GEN = false>
+template <int MODE, int TY, int NSEG, int KB, int NS2, bool PUSH, bool GEN = false, bool HW = false>
 cudaError_t launch_k_push(const Launcher& ln, const LineArgs& a, const KTables& T)
 {
-    auto kern = k_linek<MODE, TY, NSEG, KB, NS2, PUSH, GEN>;
+    auto kern = k_linek<MODE, TY, NSEG, KB, NS2, PUSH, GEN, HW>;
     const size_t smem = ksmem<MODE, TY, NSEG, KB, NS2>(a.L.nz);
     static size_t limit = 0;
     if (!limit) {
@@ -443,9 +446,15 @@ cudaError_t launch_k_push(const Launcher& ln, const LineArgs& a, const KTables& 
 
 // The fused halo push (multi-GPU, P2P) has its own instantiation, so single-GPU launches
 // carry none of its code.  Only the smoother and the preconditioner push.
-template <int MODE, int TY, int NSEG, int KB, int NS2>
+template <int MODE, int TY, int NSEG, int KB, int NS2, bool HWOK = false>
 cudaError_t launch_k(const Launcher& ln, const LineArgs& a, const KTables& T)
 {
+    if (a.hw.flag[0] || a.hw.flag[1]) {   // P2P overlap with the in-kernel halo wait
+        if constexpr (HWOK && (MODE == MODE_SMOOTH || MODE == MODE_RESTRICT))
+            if (!a.L.gen && !a.push.dst_lo && !a.push.dst_hi)
+                return launch_k_push<MODE, TY, NSEG, KB, NS2, false, false, true>(ln, a, T);
+        return cudaErrorNotSupported;   // the host checks ksplit_halo_wait() first
+    }
     if constexpr (MODE == MODE_SMOOTH || MODE == MODE_RESTRICT) {
         if (a.L.gen) {   // general vertical profiles: the stencil's couplings per level
             if constexpr (MODE == MODE_SMOOTH)
@@ -460,13 +469,13 @@ cudaError_t launch_k(const Launcher& ln, const LineArgs& a, const KTables& T)
     return launch_k_push<MODE, TY, NSEG, KB, NS2, false>(ln, a, T);
 }
 
-template <int MODE, int TY, int KB, int NS2>
+template <int MODE, int TY, int KB, int NS2, bool HWOK = false>
 cudaError_t launch_k_nseg(const Launcher& ln, const LineArgs& a, const KTables& T)
 {
     switch (a.L.nz / SL) {
-    case 1: return launch_k<MODE, TY, 1, KB, NS2>(ln, a, T);
-    case 2: return launch_k<MODE, TY, 2, KB, NS2>(ln, a, T);
-    case 4: return launch_k<MODE, TY, 4, KB, NS2>(ln, a, T);
+    case 1: return launch_k<MODE, TY, 1, KB, NS2, HWOK>(ln, a, T);
+    case 2: return launch_k<MODE, TY, 2, KB, NS2, HWOK>(ln, a, T);
+    case 4: return launch_k<MODE, TY, 4, KB, NS2, HWOK>(ln, a, T);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -476,6 +485,11 @@ struct Cfg { int ty, kb; };
 constexpr Cfg kCfg[3] = {{2, 8}, {4, 4}, {2, 4}};
 
 }  // namespace
+
+bool ksplit_halo_wait(int mode, int cfg, int gen)
+{
+    return (mode == MODE_SMOOTH || mode == MODE_RESTRICT) && cfg == 1 && gen == 0;
+}
 
 bool ksplit_supported(int mode, int nz, int nx)
 {
@@ -497,7 +511,7 @@ KsplitBoxes ksplit_boxes(int mode, int cfg)
 cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const LineArgs& a, const KTables& T)
 {
     if (mode == MODE_SMOOTH) {
-        if (cfg == 1) return launch_k_nseg<MODE_SMOOTH, 4, 4, 3>(ln, a, T);
+        if (cfg == 1) return launch_k_nseg<MODE_SMOOTH, 4, 4, 3, true>(ln, a, T);
         if (cfg == 2) return launch_k_nseg<MODE_SMOOTH, 2, 4, 3>(ln, a, T);
         return launch_k_nseg<MODE_SMOOTH, 2, 8, 2>(ln, a, T);
     }
@@ -517,7 +531,7 @@ cudaError_t launch_line_ksplit(const Launcher& ln, int mode, int cfg, const Line
         return launch_k_nseg<MODE_CGPREC, 2, 8, 2>(ln, a, T);
     }
     if (mode == MODE_RESTRICT) {   // no Thomas: the exchange buffer replaces the chaining buffer
-        if (cfg == 1) return launch_k_nseg<MODE_RESTRICT, 4, 4, 3>(ln, a, T);
+        if (cfg == 1) return launch_k_nseg<MODE_RESTRICT, 4, 4, 3, true>(ln, a, T);
         if (cfg == 2) return launch_k_nseg<MODE_RESTRICT, 2, 4, 3>(ln, a, T);
         return launch_k_nseg<MODE_RESTRICT, 2, 8, 2>(ln, a, T);
     }
