@@ -128,7 +128,8 @@ typedef struct {
     int64_t kernel_launches;   /* kernels launched by the library since creation / reset */
     int64_t halo_exchanges;    /* halo exchange calls (nranks > 1) */
     int64_t allreduces;        /* NCCL all-reduce calls (nranks > 1) */
-    int64_t graph_launches;    /* CUDA graph launches (coarse-level V-cycle graphs) */
+    int64_t graph_launches;    /* CUDA graph launches: always 0 (the solvers enqueue their kernels
+                                  directly, run-ahead on device flags) */
     int64_t p2p_halo;          /* 1: halos by device-initiated NVLink stores (decided collectively at
                                   create: every rank's neighbours reachable peer-to-peer on one host);
                                   0: NCCL send/recv (or one rank) */
@@ -171,7 +172,10 @@ tpmg_status tpmg_create(const tpmg_params *params, int32_t rank, int32_t nranks,
 /* Release everything the context owns.  Accepts NULL. COLLECTIVE if nranks > 1. */
 tpmg_status tpmg_destroy(tpmg_ctx *ctx);
 
-/* Replace the context stream (a cudaStream_t on the context's device). */
+/* Replace the context stream (a cudaStream_t on the context's device).  Work already
+ * enqueued on the old stream is ordered before everything enqueued on the new one (an event
+ * recorded on the old stream, waited for by the new): the two never race on the library's
+ * scratch, reduction slots or halo slabs. */
 tpmg_status tpmg_set_stream(tpmg_ctx *ctx, void *cuda_stream);
 
 /* Shape of level `level` on this rank: first owned global row y0, local

@@ -1860,7 +1860,18 @@ tpmg_status tpmg_destroy(tpmg_ctx* ctx)
 tpmg_status tpmg_set_stream(tpmg_ctx* ctx, void* s)
 {
     if (!ctx) return TPMG_E_PARAM;
-    ctx->stream = (cudaStream_t)s;
+    cudaStream_t ns = (cudaStream_t)s;
+    if (ns != ctx->stream) {
+        // order the new stream after everything on the old one (shared scratch, reduction
+        // tickets, halo slabs)
+        cudaEvent_t e = nullptr;
+        CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        cudaError_t r = cudaEventRecord(e, ctx->stream);
+        if (r == cudaSuccess) r = cudaStreamWaitEvent(ns, e, 0);
+        cudaEventDestroy(e);
+        if (r != cudaSuccess) return fail(ctx, TPMG_E_CUDA, "tpmg_set_stream: %s", cudaGetErrorString(r));
+    }
+    ctx->stream = ns;
     return TPMG_OK;
 }
 
