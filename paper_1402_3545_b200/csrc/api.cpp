@@ -42,6 +42,8 @@ struct LevelData {
     double* d_prof = nullptr;           // general vertical profiles: [b_k][c_k][c_l d_k] (device)
     double* d_fprof = nullptr;          // with per-column fields: [a_k-b_k-c_k][b_k][c_k][d_k] (device)
     double* d_fld = nullptr;            // per-column fields, LevelConst::fld layout (device)
+    double* d_im = nullptr;             // per-column fields: 1/m_k of every column's block (Lambda layout)
+    bool im_ok = false;                 // d_im is current
     double* slab_lo = nullptr;          // halo rows j = -1 / j = ny for this level (nranks > 1)
     double* slab_hi = nullptr;
     size_t n() const { return (size_t)lc.nx * (size_t)lc.ny * (size_t)lc.nz; }
@@ -122,6 +124,8 @@ struct tpmg_ctx {
     bool tmem = true;                   // Thomas g' of the column kernels in Tensor Memory (TPMG_TMEM=0: smem)
     int tm_ctas = 2;                    // their CTAs per SM (TPMG_TM_CTAS; r2c, r2f: 2 >= 1)
     int tm_stages = 3;                  // their TMA ring depth (TPMG_TM_STAGES: 3, 4, 5)
+    bool stream_out = false;            // k_line outputs by st.global.cs (TPMG_STREAM_OUT=1)
+    bool pivots = true;                 // per-column fields: precomputed pivots (TPMG_PIVOTS=0: off)
     bool ksplit_cg = false;             // k-split CG preconditioner (TPMG_KSPLIT_CG=1)
     bool halo_off = false;              // TPMG_HALO=off: skip halo exchanges (timing experiments)
     bool fused_push = false;            // P2P: producers push their boundary rows (TPMG_FUSED_PUSH=1)
@@ -497,6 +501,8 @@ LineArgs line_args(tpmg_ctx* ctx, int level)
     a.ratio = DevRatio{nullptr, -1, -1};
     a.red = ReduceSlot{ctx->d_partials, ctx->d_ticket, nullptr, 0};
     a.skip = ctx->skip;
+    a.stream_out = ctx->stream_out;
+    a.im = (ctx->lv[level].lc.gen >= 2 && ctx->lv[level].im_ok) ? ctx->lv[level].d_im : nullptr;
     return a;
 }
 
@@ -653,6 +659,10 @@ void fill_tma(tpmg_ctx* ctx, int mode, LineArgs& a)
         if (!Q[f] || !aligned(Q[f])) return;
         if (!tensor_map(ctx, Q[f], nx, nz, ny, kTileX, TY, &a.tma.q[f])) return;
     }
+    // the precomputed pivots of the Thomas modes travel as plain field np
+    const bool thomas = mode == MODE_PREC || mode == MODE_SMOOTH || mode == MODE_CGPREC;
+    if (thomas && a.im && (!aligned(a.im) || !tensor_map(ctx, a.im, nx, nz, ny, kTileX, TY, &a.tma.q[np]))) a.im = nullptr;
+    if (!thomas) a.im = nullptr;
     a.use_tma = 1;
 }
 
@@ -1524,6 +1534,7 @@ void ctx_free(tpmg_ctx* ctx)
         cudaFree(L.d_prof);
         cudaFree(L.d_fprof);
         cudaFree(L.d_fld);
+        cudaFree(L.d_im);
         if ((int)l < ctx->L) { cudaFree(L.u[0]); cudaFree(L.f); }
         cudaFree(L.u[1]);
     }
@@ -1647,6 +1658,18 @@ tpmg_status fields_profile_tables(tpmg_ctx* ctx)
         L.lc.prof = L.d_fprof;
         L.lc.fld = L.d_fld;
         L.lc.gen = 2;
+        L.im_ok = false;
+    }
+    // the Thomas pivots of every column, once per operator: the line kernels stream them with
+    // the data instead of running the pivot recurrence (TPMG_PIVOTS=0: recurrence on chip)
+    if (ctx->pivots && ctx->use_tma && ctx->tmem && nz <= 128) {
+        for (int l = 1; l <= ctx->L; ++l) {
+            LevelData& L = ctx->lv[l];
+            TRY(dev_alloc(ctx, &L.d_im, L.n()));
+            CUDA_TRY(ctx, launch_pivots(launcher(ctx), L.lc, L.d_im));
+            L.im_ok = true;
+        }
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     }
     return TPMG_OK;
 }
@@ -1765,6 +1788,10 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->sync_debug = sd && sd[0] == '1';
         const char* tm = std::getenv("TPMG_TMEM");   // "0": g' of the column kernels in shared memory
         ctx->tmem = !(tm && tm[0] == '0');
+        const char* pv = std::getenv("TPMG_PIVOTS");
+        ctx->pivots = !(pv && pv[0] == '0');
+        const char* so = std::getenv("TPMG_STREAM_OUT");
+        if (so) ctx->stream_out = so[0] == '1';
         const char* ts = std::getenv("TPMG_TM_STAGES");
         if (ts) ctx->tm_stages = std::atoi(ts);
         const char* tc = std::getenv("TPMG_TM_CTAS");
@@ -2179,7 +2206,10 @@ tpmg_status tpmg_set_fields(tpmg_ctx* ctx, const double* area, const double* ax,
         const double* prof[4] = {ctx->prof_abcd.data(), ctx->prof_abcd.data() + nz, ctx->prof_abcd.data() + 2 * nz,
                                  ctx->prof_abcd.data() + 3 * nz};
         const bool flat = !ctx->gen_profiles;
-        for (int l = 1; l <= ctx->L; ++l) ctx->lv[l].lc.fld = nullptr;
+        for (int l = 1; l <= ctx->L; ++l) {
+            ctx->lv[l].lc.fld = nullptr;
+            ctx->lv[l].im_ok = false;
+        }
         return build_tables(ctx, flat ? nullptr : prof);
     }
     if (!area || !ax || !ay) return fail(ctx, TPMG_E_PARAM, "tpmg_set_fields: give all three fields or none");

@@ -148,6 +148,30 @@ __device__ __forceinline__ void tmem_st_f64(uint32_t taddr, double v)
                  : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+// two doubles into columns col .. col+3 of this thread's lane
+__device__ __forceinline__ void tmem_st_f64x2(uint32_t taddr, double v0, double v1)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(taddr),
+                 "r"(__double2loint(v0)), "r"(__double2hiint(v0)), "r"(__double2loint(v1)), "r"(__double2hiint(v1))
+                 : "memory");
+}
+// 16 doubles from columns col .. col+31 of this thread's lane (wait in the same statement)
+__device__ __forceinline__ void tmem_ld_f64x16(uint32_t taddr, double (&v)[16])
+{
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = __hiloint2double((int)r[2 * q + 1], (int)r[2 * q]);
+}
 // 8 doubles from columns col .. col+15 of this thread's lane; the wait is in the same asm
 // statement, so no use of the registers can be scheduled before the data has arrived
 __device__ __forceinline__ void tmem_ld_f64x8(uint32_t taddr, double (&v)[8])
@@ -163,27 +187,6 @@ __device__ __forceinline__ void tmem_ld_f64x8(uint32_t taddr, double (&v)[8])
         : "memory");
 #pragma unroll
     for (int q = 0; q < 8; ++q) v[q] = __hiloint2double((int)r[2 * q + 1], (int)r[2 * q]);
-}
-// Split form for software pipelining: issue the load of 16 columns now, wait later.  The wait
-// names the 16 destination registers as read-write operands, so the compiler cannot move
-// any use (or copy) of them above it.
-__device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t (&r)[16])
-{
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15}, [%16];\n"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr)
-        : "memory");
-}
-__device__ __forceinline__ void tmem_ld16_wait(uint32_t (&r)[16])
-{
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
-                 :
-                 : "memory");
 }
 __device__ __forceinline__ double tmem_ld_f64(uint32_t taddr)
 {
@@ -209,6 +212,14 @@ __device__ __forceinline__ void halo_flag_wait(const unsigned* flag, unsigned ep
         __nanosleep(32);
     }
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+
+// The loader of tile row [j0, j0 + ty) waits for the halo slabs it reads (row -1: flag[0], row ny:
+// flag[1]); out of line, so the single-GPU hot loop carries no extra registers.
+static __device__ __noinline__ void halo_tile_wait(const HaloWait& hw, int j0, int ty, int ny)
+{
+    if (j0 == 0 && hw.flag[0]) halo_flag_wait(hw.flag[0], hw.epoch);
+    if (j0 + ty >= ny && hw.flag[1]) halo_flag_wait(hw.flag[1], hw.epoch);
 }
 
 // Dynamic shared memory available to a kernel: the opt-in maximum minus its static smem.

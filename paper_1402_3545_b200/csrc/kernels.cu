@@ -168,13 +168,19 @@ __device__ __forceinline__ void tma_stage(double* st, const LineArgs& a, int64_t
 // latency; TMEM itself (256 columns = 128 levels per CTA) holds exactly two CTAs.
 constexpr uint32_t kTmemCols = 256;
 // HW: the in-kernel halo wait of the P2P overlap (LineArgs::hw), a separate instantiation
+// GEN 3: per-column fields with the pivots precomputed (LineArgs::im): like GEN 2, but 1/m_k
+// arrives as one more plain field through the TMA ring and the Thomas sweeps run no pivot
+// recurrence; g'_k and 1/m_k both live in TMEM (4 columns per level, the whole TMEM of the SM).
 template <int MODE, int TY, int LOADER, int GEN, int TMS = 0, bool HW = false>
 __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArgs a)
 {
     using T = Traits<MODE>;
     constexpr bool TM = TMS > 0;   // TMS: pipeline stages of the TMEM form (the freed shared memory deepens it)
     static_assert(!TM || (TY == 4 && T::THOMAS), "TMEM g' buffer: 4 warps (the 4 TMEM lane quarters), Thomas modes");
-    constexpr int NH = T::NH, NP = T::NP, NR = T::NR;
+    static_assert(GEN != 3 || (TM && T::THOMAS), "precomputed pivots: TMEM form of the Thomas modes");
+    constexpr int NH = T::NH, NR = T::NR;
+    constexpr int NP = T::NP + (GEN == 3 ? 1 : 0);   // + the pivot field
+    constexpr uint32_t NCOL = (GEN == 3) ? 512u : kTmemCols;
     using G = Geom<NH, NP, TY>;
     constexpr int NT = G::NT;
     constexpr int NS = TM ? TMS : stages<MODE, GEN>();
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     const int nz = a.L.nz;
     const int64_t nx = a.L.nx, ny = a.L.ny;
     const int tabn = (3 * nz + 15) & ~15;    // keep the stages 128-byte aligned
-    const int ptn = (GEN >= 2) ? ((4 * nz + 15) & ~15) : tabn;
+    const int ptn = (GEN >= 2) ? ((4 * nz + 15) & ~15) : tabn;   // GEN 3 uses GEN 2's profile table
     double* tab = smem;                      // diag[nz], invm[nz], gim[nz]
     double* ptab = smem + tabn;              // GEN 1: b_k, c_k, c_l d_k; GEN 2: a_k-b_k-c_k, b_k, c_k, d_k
     double* stage = ptab + (GEN ? ptn : 0);  // NS stages
@@ -219,6 +225,13 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     pdl_trigger();
     if (a.skip && *a.skip) return;   // solver run-ahead: this iteration is not needed
 
+    // outputs that no later kernel reads soon can bypass L2 residency (st.global.cs) so the
+    // halo'd input's rows stay in L2 for the neighbouring tiles (LineArgs::stream_out)
+    const bool cs = a.stream_out != 0;
+    auto put = [cs](double* q, double v) {
+        if (cs) __stcs(q, v);
+        else *q = v;
+    };
     double ratio = 0.0;
     if constexpr (MODE == MODE_CGDIR || MODE == MODE_CGPREC)
         if (a.ratio.num >= 0) ratio = a.ratio.s[a.ratio.num] / a.ratio.s[a.ratio.den];
@@ -237,7 +250,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     const int total = my_tiles * nch;
     __shared__ uint32_t tmem_slot;
     if constexpr (TM) {
-        if (ty == 0) tmem_alloc<kTmemCols>(&tmem_slot);
+        if (ty == 0) tmem_alloc<NCOL>(&tmem_slot);
         tmem_fence_before();
     }
     __syncthreads();
@@ -256,17 +269,11 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
         return part_row(a.part, nty, push_row(t / ntx, nrows, plo, phi));
     };
     int p_i0 = (p_tile % ntx) * TX, p_j0 = row_of(p_tile) * TY;
-    bool waited_lo = false, waited_hi = false;
     auto issue = [&]() {
         if (p_count < total) {
             double* st = stage + p_slot * G::STAGE;
-            if constexpr (HW) {
-                if (p_ch == 0 && (LOADER == 0 || tid == 0)) {
-                    // the first load of a tile row that reads a halo slab waits for its epoch
-                    if (p_j0 == 0 && a.hw.flag[0] && !waited_lo) { halo_flag_wait(a.hw.flag[0], a.hw.epoch); waited_lo = true; }
-                    if (p_j0 + TY >= ny && a.hw.flag[1] && !waited_hi) { halo_flag_wait(a.hw.flag[1], a.hw.epoch); waited_hi = true; }
-                }
-            }
+            if constexpr (HW)   // the first load of a tile row that reads a halo slab waits for its epoch
+                if (p_ch == 0 && (LOADER == 0 || tid == 0)) halo_tile_wait(a.hw, (int)p_j0, TY, (int)ny);
             if constexpr (LOADER == 0) {
                 load_stage<NH, NP, TY>(st, a, p_i0, p_j0, p_ch * KB);
             } else {
@@ -351,7 +358,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
         }
 
         // rolling state for the k-lag: values at level km = k-1 and km-1
-        double um1 = 0.0, u0 = 0.0, S0 = 0.0, qa = 0.0, qb = 0.0, gprev = 0.0;
+        double um1 = 0.0, u0 = 0.0, S0 = 0.0, qa = 0.0, qb = 0.0, qc = 0.0, gprev = 0.0;   // qc: 1/m_k (GEN 3)
         double* rbuf_cur = rbuf;   // MODE_RESTRICT: buffer of the current chunk
         // forward-pass outputs of level km live at ofw0/ofw1 (advanced by nx per level)
         double* ofw0 = (MODE == MODE_APPLY || MODE == MODE_RESID || MODE == MODE_CGDIR || MODE == MODE_CGPREC) && a.out0
@@ -397,7 +404,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             } else if constexpr (MODE == MODE_CGDIR) {
                 const double Ap = fma(-c, S0, Mu);
                 if (valid) {
-                    *ofw0 = u0;
+                    put(ofw0, u0);
                     acc[0] = fma(u0, Ap, acc[0]);
                 }
             } else if constexpr (MODE == MODE_RESTRICT) {
@@ -410,8 +417,8 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 const double rn = fma(-ratio, Ap, qa);
                 const double un = fma(ratio, u0, qb);
                 if (valid) {
-                    *ofw0 = rn;
-                    *ofw1 = un;
+                    put(ofw0, rn);
+                    put(ofw1, un);
                     acc[0] = fma(rn, rn, acc[0]);
                 }
                 g = rn;
@@ -428,10 +435,14 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 if constexpr (GEN == 2) {
                     // this column's pivot: m_k = diag_k - s_k t'_{k-1}, t'_k = t_k / m_k
                     imk = pivot_step(km, pm1, pm2, tkm1);
+                } else if constexpr (GEN == 3) {
+                    imk = qc;   // this column's 1/m_k, precomputed (launch_pivots)
                 }
                 const double y = fma(-sk, gprev, g);     // y = L^-1 g   (M = L D L^T; sub-diagonal s_k)
                 const double gp = y * imk;               // g'_k = (g_k - s_k g'_{k-1}) / m_k
-                if constexpr (TM)
+                if constexpr (GEN == 3)
+                    tmem_st_f64x2(tbase + 4u * (uint32_t)km, gp, imk);   // the backward sweep needs both
+                else if constexpr (TM)
                     tmem_st_f64(tbase + 2u * (uint32_t)km, gp);
                 else
                     *gslot = gp;
@@ -446,12 +457,12 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
         auto do_chunk = [&](auto full_t, int ch, const double* st) {
             constexpr bool FULL = decltype(full_t)::value;
             const int k0 = ch * KB;
-            double ecv[KB], Sv[KB], pav[KB], pbv[KB];
+            double ecv[KB], Sv[KB], pav[KB], pbv[KB], pcv[KB];
             const double* hp = st + (ty + 1) * G::HALO_ROW + tx + 2;           // own column
             const double* pp = st + G::PLAIN_BASE + ty * (KB * TX) + tx;       // plain field 0
 #pragma unroll
             for (int kk = 0; kk < KB; ++kk) {
-                ecv[kk] = 0.0; Sv[kk] = 0.0; pav[kk] = 0.0; pbv[kk] = 0.0;
+                ecv[kk] = 0.0; Sv[kk] = 0.0; pav[kk] = 0.0; pbv[kk] = 0.0; pcv[kk] = 0.0;
                 if constexpr (NH >= 1) {
                     const double* h = hp + kk * G::HX;
                     ecv[kk] = h[0];
@@ -469,8 +480,9 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                         Sv[kk] = fma(ratio, nsum(p), Sv[kk]);
                     }
                 }
-                if constexpr (NP >= 1) pav[kk] = pp[kk * TX];
-                if constexpr (NP >= 2) pbv[kk] = pp[TY * KB * TX + kk * TX];
+                if constexpr (T::NP >= 1) pav[kk] = pp[kk * TX];
+                if constexpr (T::NP >= 2) pbv[kk] = pp[TY * KB * TX + kk * TX];
+                if constexpr (GEN == 3) pcv[kk] = pp[T::NP * TY * KB * TX + kk * TX];   // the pivot field
             }
             __syncthreads();   // slot gi % NS is free for chunk gi + NS
             if constexpr (MODE == MODE_RESTRICT) rbuf_cur = rbuf + (gi & 1) * (TY * RS * (TX / 2));
@@ -489,7 +501,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                             pm2 = 1.0;
                             cbuf[ch * NT + tid] = m;
                         }
-                    um1 = u0; u0 = ecv[kk]; S0 = Sv[kk]; qa = pav[kk]; qb = pbv[kk];
+                    um1 = u0; u0 = ecv[kk]; S0 = Sv[kk]; qa = pav[kk]; qb = pbv[kk]; qc = pcv[kk];
                 }
             }
         };
@@ -532,6 +544,43 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             }
         }
 
+        if constexpr (T::THOMAS && GEN == 3) {
+            // backward substitution x_k = g'_k - (t_k / m_k) x_{k+1}, 8 levels per TMEM load of
+            // (g'_k, 1/m_k) pairs
+            double* op = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase + (int64_t)(nz - 1) * nx;
+            double x = 0.0;
+            int k = nz - 1;
+            tmem_wait_st();   // the forward sweep's stores have landed
+            for (; k >= KB - 1; k -= KB) {
+                double v[2 * KB];   // v[2q] = g'_{k0+q}, v[2q+1] = 1/m_{k0+q}, k0 = k-KB+1
+                tmem_ld_f64x16(tbase + 4u * (uint32_t)(k - (KB - 1)), v);
+#pragma unroll
+                for (int q = KB - 1; q >= 0; --q) {
+                    const int kq = k - (KB - 1) + q;
+                    const double tp = fT * ptab[2 * nz + kq] * v[2 * q + 1];   // t'_k = t_k / m_k
+                    x = fma(-tp, x, v[2 * q]);
+                    if (valid) put(op, x);
+                    op -= nx;
+                }
+            }
+            for (; k >= 0; --k) {
+                double v2[2];
+                {
+                    uint32_t lo0, hi0, lo1, hi1;
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+                        "tcgen05.wait::ld.sync.aligned;\n"
+                        : "=r"(lo0), "=r"(hi0), "=r"(lo1), "=r"(hi1)
+                        : "r"(tbase + 4u * (uint32_t)k)
+                        : "memory");
+                    v2[0] = __hiloint2double((int)hi0, (int)lo0);
+                    v2[1] = __hiloint2double((int)hi1, (int)lo1);
+                }
+                x = fma(-(fT * ptab[2 * nz + k] * v2[1]), x, v2[0]);
+                if (valid) put(op, x);
+                op -= nx;
+            }
+        }
         if constexpr (T::THOMAS && GEN == 2) {
             // backward substitution per KB-level chunk: the chunk's t'_k recomputed from its
             // checkpoint with the forward sweep's arithmetic, then x_k = g'_k - t'_k x_{k+1}
@@ -579,28 +628,19 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             double* op = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase + (int64_t)(nz - 1) * nx;
             double x = 0.0;
             int k = nz - 1;
-            // TM: the chunk's g' comes from Tensor Memory; the load of the next chunk is issued
-            // before this chunk's recurrence (software pipelining, one load in flight)
-            uint32_t tcur[16], tnxt[16];
-            if constexpr (TM) {
-                static_assert(KB == 8, "16 TMEM columns = 8 levels per chunk");
-                tmem_wait_st();   // the forward sweep's g' stores have landed
-                if (k >= KB - 1) {
-                    tmem_ld16_issue(tbase + 2u * (uint32_t)(k - (KB - 1)), tcur);
-                    tmem_ld16_wait(tcur);
-                }
-            }
+            // TM: the chunk's g' comes from Tensor Memory, 8 levels per load (a software-pipelined
+            // form with the next chunk's load in flight measured the same, r2k, at 237 registers)
+            if constexpr (TM) tmem_wait_st();   // the forward sweep's g' stores have landed
             for (; k >= KB - 1; k -= KB) {
                 const double* gq = gbuf + (k - (KB - 1)) * NT + tid;   // levels k-KB+1 .. k
                 const double* mq = gim + (k - (KB - 1));
                 double gv[KB], gm[KB];
-                bool more = false;
                 if constexpr (TM) {
-                    more = k - KB >= KB - 1;
-                    if (more) tmem_ld16_issue(tbase + 2u * (uint32_t)(k - KB - (KB - 1)), tnxt);
+                    static_assert(KB == 8, "16 TMEM columns = 8 levels per chunk");
+                    double g8[KB];
+                    tmem_ld_f64x8(tbase + 2u * (uint32_t)(k - (KB - 1)), g8);
 #pragma unroll
-                    for (int q = 0; q < KB; ++q)
-                        gv[q] = __hiloint2double((int)tcur[2 * (KB - 1 - q) + 1], (int)tcur[2 * (KB - 1 - q)]);
+                    for (int q = 0; q < KB; ++q) gv[q] = g8[KB - 1 - q];
                 }
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
@@ -610,15 +650,8 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 #pragma unroll
                 for (int q = 0; q < KB; ++q) {
                     x = fma(gm[q], x, gv[q]);
-                    if (valid) *op = x;
+                    if (valid) put(op, x);
                     op -= nx;
-                }
-                if constexpr (TM) {
-                    if (more) {
-                        tmem_ld16_wait(tnxt);
-#pragma unroll
-                        for (int q = 0; q < 16; ++q) tcur[q] = tnxt[q];
-                    }
                 }
             }
             for (; k >= 0; --k) {
@@ -666,7 +699,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
         __syncthreads();
         if (ty == 0) {
             tmem_fence_after();
-            tmem_dealloc<kTmemCols>(tmem_slot);
+            tmem_dealloc<NCOL>(tmem_slot);
         }
     }
     if (want_red) grid_reduce<NR>(a.red, acc, scratch);
@@ -677,6 +710,9 @@ size_t line_smem_bytes(int nz, int gen = 0, int tms = 0)
 {
     using T = Traits<MODE>;
     using G = Geom<T::NH, T::NP, TY>;
+    using G3 = Geom<T::NH, T::NP + 1, TY>;   // GEN 3: + the pivot field
+    if (gen == 3)
+        return (size_t)(((3 * nz + 15) & ~15) + ((4 * nz + 15) & ~15) + (size_t)tms * G3::STAGE + 64 + 16) * sizeof(double);
     const bool tm = tms > 0;
     size_t d = ((3 * nz + 15) & ~15) + (gen >= 2 ? ((4 * nz + 15) & ~15) : gen ? ((3 * nz + 15) & ~15) : 0) +
                (size_t)(tm ? tms : gen == 2 ? stages<MODE, 2>() : kNS) * G::STAGE + (T::THOMAS ? (size_t)((tm ? 0 : nz) + (gen == 2 ? (nz + KB - 1) / KB : 0)) * G::NT : 0) + 64 + 16 +
@@ -708,6 +744,7 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
     if (e != cudaSuccess) return e;
     per_sm = std::max(per_sm, 1);
     if (TM) per_sm = std::min<int>(per_sm, std::min<int>(ln.tm_ctas, 512 / kTmemCols));   // resident CTAs must all get their TMEM
+    if (GEN == 3) per_sm = 1;   // 512 TMEM columns per CTA
     const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * part_rows(a.part, (int)((a.L.ny + TY - 1) / TY));
     // CG direction (two halo'd fields): on wide grids two CTAs per SM re-read the halo
     // rows from HBM (2.1x the algorithmic reads at 4096 x 1024 x 128, ncu); one CTA per SM
@@ -732,6 +769,9 @@ cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
     }
     if (a.L.gen) {   // general vertical profiles / per-column fields: TMA loader only
         if (!a.use_tma) return cudaErrorNotSupported;
+        if constexpr (Traits<MODE>::THOMAS && TY == 4)   // precomputed pivots streamed with the data
+            if (a.L.gen >= 2 && a.im && ln.tmem && a.L.nz <= (int)(kTmemCols / 2))
+                return launch_line_l<MODE, 4, 1, 3, 3>(ln, a);
         if constexpr (Traits<MODE>::THOMAS && TY == 4)   // g' in Tensor Memory, 2 CTAs per SM
             if (ln.tmem && a.L.nz <= (int)(kTmemCols / 2)) {
                 if (a.L.gen >= 2) return launch_line_l<MODE, 4, 1, 2, (MODE == MODE_CGPREC ? 2 : 3)>(ln, a);
@@ -893,6 +933,28 @@ __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const 
     prolong_body<PUSH>(Cc, F, uc, uf, lpt, part, push, hw);
 }
 
+
+// One thread per column (i, j): the Thomas pivots of its block M_T = |T| (diag(a) + tridiag(-(b+c),
+// b, c)) - alpha_T diag(d) (eqn:LocalMatrixStencil, the fields layout of LevelConst::fld and the
+// profile table [a-b-c][b][c][d]): m_0 = dg_0, m_k = dg_k - s_k t_{k-1} / m_{k-1}, stored as 1/m_k.
+__global__ void __launch_bounds__(128) k_pivots(const LevelConst L, double* __restrict__ im)
+{
+    const int64_t nx = L.nx, ny = L.ny;
+    const int nz = L.nz;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, j = blockIdx.y;
+    if (i >= nx || j >= ny) return;
+    const int64_t ncol = nx * ny, cc = j * nx + i;
+    const double fT = L.fld[cc], faT = L.fld[ncol + cc];
+    const double* pr = L.prof;   // [a-b-c][b][c][d], nz each
+    double m = 0.0, tprev = 0.0;
+    for (int k = 0; k < nz; ++k) {
+        const double sk = fT * pr[nz + k], tk = fT * pr[2 * nz + k];
+        const double dg = fma(fT, pr[k], -faT * pr[3 * nz + k]);
+        m = (k == 0) ? dg : dg - sk * tprev / m;
+        im[(j * nz + k) * nx + i] = 1.0 / m;
+        tprev = tk;
+    }
+}
 
 __global__ void __launch_bounds__(256) k_dot(const double* __restrict__ x, const double* __restrict__ y,
                                              int64_t n, ReduceSlot red)
@@ -1205,6 +1267,12 @@ cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse, con
     if (hp.dst_lo || hp.dst_hi)
         return launch_kernel(ln, k_prolong_add<true>, dim3(grid), dim3(block), 0, coarse, fine, uc, uf, lpt, skip, part, hp, w);
     return launch_kernel(ln, k_prolong_add<false>, dim3(grid), dim3(block), 0, coarse, fine, uc, uf, lpt, skip, part, hp, w);
+}
+
+cudaError_t launch_pivots(const Launcher& ln, const LevelConst& L, double* im)
+{
+    if (L.nx <= 0 || L.ny <= 0 || L.gen < 2 || !L.fld || !L.prof) return cudaErrorInvalidValue;
+    return launch_kernel(ln, k_pivots, dim3((unsigned)((L.nx + 127) / 128), (unsigned)L.ny), dim3(128), 0, L, im);
 }
 
 cudaError_t launch_dot(const Launcher& ln, const double* x, const double* y, int64_t n, ReduceSlot red)

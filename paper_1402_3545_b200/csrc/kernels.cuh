@@ -116,7 +116,7 @@ struct TmaHalo {
 };
 struct TmaMaps {
     TmaHalo h[2];
-    CUtensorMap q[2];
+    CUtensorMap q[3];   // plain inputs; q[NP] = the pivot field of the precomputed-pivot form
 };
 
 // Tile geometry of the line kernels: TX = 32 columns along x per tile row,
@@ -172,6 +172,10 @@ struct LineArgs {
     int part;          // TilePart: which tile rows this launch covers
     HaloPush push;     // fused halo push of the output (dst == nullptr: none)
     HaloWait hw;       // in-kernel wait for the halo'd input's slabs (P2P overlap)
+    int stream_out;    // k_line: outputs by streaming (evict-first) stores
+    const double* im;  // per-column fields: 1/m_k of every column's line block (Lambda layout, this
+                       // level), precomputed once per operator (launch_pivots); the Thomas modes then
+                       // stream it with the data instead of running the pivot recurrence
     TmaMaps tma;
 };
 
@@ -253,6 +257,10 @@ cudaError_t launch_restrict(const Launcher& ln, const LevelConst& fine, const Le
 cudaError_t launch_prolong_add(const Launcher& ln, const LevelConst& coarse,
                                const LevelConst& fine, HaloField uc, double* uf, const int* skip = nullptr,
                                int part = PART_ALL, const HaloPush* push = nullptr, const HaloWait* hw = nullptr);
+// Per-column fields: the Thomas pivots of every column's block M_T:
+// m_0 = dg_0, m_k = dg_k - s_k t_{k-1} / m_{k-1}; im[(j nz + k) nx + i] = 1 / m_k.  They depend
+// on the coefficients only, so they are computed once per operator (tpmg_set_fields).
+cudaError_t launch_pivots(const Launcher& ln, const LevelConst& L, double* im);
 // dst = src (n doubles) unless *skip
 cudaError_t launch_copy(const Launcher& ln, double* dst, const double* src, int64_t n, const int* skip);
 

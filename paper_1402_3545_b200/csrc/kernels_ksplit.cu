@@ -192,16 +192,11 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
 
     // producer (thread 0) and consumer cursors over the CTA's (tile, chunk) steps
     int p_count = 0, p_cc = 0, p_slot = 0, p_tile = blockIdx.x;
-    bool waited_lo = false, waited_hi = false;
     auto issue = [&]() {
         if (tid == 0 && p_count < total) {
-            if constexpr (HW) {
-                if (p_cc == 0) {   // the first load of a tile row that reads a halo slab waits for its epoch
-                    const int j0 = row_of(p_tile) * TY;
-                    if (j0 == 0 && a.hw.flag[0] && !waited_lo) { halo_flag_wait(a.hw.flag[0], a.hw.epoch); waited_lo = true; }
-                    if (j0 + TY >= ny && a.hw.flag[1] && !waited_hi) { halo_flag_wait(a.hw.flag[1], a.hw.epoch); waited_hi = true; }
-                }
-            }
+            if constexpr (HW)
+                if (p_cc == 0) halo_tile_wait(a.hw, row_of(p_tile) * TY, TY, (int)ny);   // a strip-boundary tile row
+                                                                                          // waits for the halo epoch
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             tma_step<MODE, TY, KB, NSEG>(stage + p_slot * STG, a, (p_tile % ntx) * TX, row_of(p_tile) * TY, p_cc,
                                          &full_bar[p_slot]);
