@@ -124,7 +124,6 @@ struct tpmg_ctx {
     bool tmem = true;                   // Thomas g' of the column kernels in Tensor Memory (TPMG_TMEM=0: smem)
     int tm_ctas = 2;                    // their CTAs per SM (TPMG_TM_CTAS; r2c, r2f: 2 >= 1)
     int tm_stages = 3;                  // their TMA ring depth (TPMG_TM_STAGES: 3, 4, 5)
-    bool stream_out = false;            // k_line outputs by st.global.cs (TPMG_STREAM_OUT=1)
     bool pivots = true;                 // per-column fields: precomputed pivots (TPMG_PIVOTS=0: off)
     bool ksplit_cg = false;             // k-split CG preconditioner (TPMG_KSPLIT_CG=1)
     bool halo_off = false;              // TPMG_HALO=off: skip halo exchanges (timing experiments)
@@ -133,6 +132,8 @@ struct tpmg_ctx {
     uint32_t prof_mask = 0;             // kernel classes bracketed with events (bit = tpmg_kernel)
     struct ProfRec { int cls; double cells; cudaEvent_t a, b; const int* skip; };
     std::vector<ProfRec> prof_pending;
+    bool prof_detail = false;           // TPMG_PROF_DETAIL=1: per-level breakdown on stderr at tpmg_destroy
+    std::map<std::pair<int, double>, std::pair<int64_t, double>> prof_by_size;
     std::vector<cudaEvent_t> prof_pool;
     // TMA descriptors, cached by (address, nx, nz, ny, box x, box rows)
     bool use_tma = true;
@@ -501,7 +502,6 @@ LineArgs line_args(tpmg_ctx* ctx, int level)
     a.ratio = DevRatio{nullptr, -1, -1};
     a.red = ReduceSlot{ctx->d_partials, ctx->d_ticket, nullptr, 0};
     a.skip = ctx->skip;
-    a.stream_out = ctx->stream_out;
     a.im = (ctx->lv[level].lc.gen >= 2 && ctx->lv[level].im_ok) ? ctx->lv[level].d_im : nullptr;
     return a;
 }
@@ -568,6 +568,11 @@ tpmg_status prof_collect(tpmg_ctx* ctx)
             ctx->prof_launches[r.cls] += 1;
             ctx->prof_ms[r.cls] += ms;
             ctx->prof_cells[r.cls] += r.cells;
+            if (ctx->prof_detail) {   // per (class, cells of the launch) = per level
+                auto& d = ctx->prof_by_size[std::make_pair(r.cls, r.cells)];
+                d.first += 1;
+                d.second += ms;
+            }
         }
         ctx->prof_pool.push_back(r.a);
         ctx->prof_pool.push_back(r.b);
@@ -1788,10 +1793,10 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->sync_debug = sd && sd[0] == '1';
         const char* tm = std::getenv("TPMG_TMEM");   // "0": g' of the column kernels in shared memory
         ctx->tmem = !(tm && tm[0] == '0');
+        const char* pdt = std::getenv("TPMG_PROF_DETAIL");
+        ctx->prof_detail = pdt && pdt[0] == '1';
         const char* pv = std::getenv("TPMG_PIVOTS");
         ctx->pivots = !(pv && pv[0] == '0');
-        const char* so = std::getenv("TPMG_STREAM_OUT");
-        if (so) ctx->stream_out = so[0] == '1';
         const char* ts = std::getenv("TPMG_TM_STAGES");
         if (ts) ctx->tm_stages = std::atoi(ts);
         const char* tc = std::getenv("TPMG_TM_CTAS");
@@ -1877,6 +1882,11 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
 tpmg_status tpmg_destroy(tpmg_ctx* ctx)
 {
     if (!ctx) return TPMG_OK;
+    if (ctx->prof_detail)
+        for (auto& kv : ctx->prof_by_size)
+            std::fprintf(stderr, "tpmg prof rank %d class %d cells %.0f launches %lld ms %.4f avg_us %.1f\n", ctx->rank,
+                         kv.first.first, kv.first.second, (long long)kv.second.first, kv.second.second,
+                         1e3 * kv.second.second / (double)std::max<int64_t>(kv.second.first, 1));
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream); else cudaDeviceSynchronize();
     ctx_free(ctx);

@@ -225,13 +225,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     pdl_trigger();
     if (a.skip && *a.skip) return;   // solver run-ahead: this iteration is not needed
 
-    // outputs that no later kernel reads soon can bypass L2 residency (st.global.cs) so the
-    // halo'd input's rows stay in L2 for the neighbouring tiles (LineArgs::stream_out)
-    const bool cs = a.stream_out != 0;
-    auto put = [cs](double* q, double v) {
-        if (cs) __stcs(q, v);
-        else *q = v;
-    };
+    auto put = [](double* q, double v) { *q = v; };   // (st.global.cs measured no different, r2o)
     double ratio = 0.0;
     if constexpr (MODE == MODE_CGDIR || MODE == MODE_CGPREC)
         if (a.ratio.num >= 0) ratio = a.ratio.s[a.ratio.num] / a.ratio.s[a.ratio.den];

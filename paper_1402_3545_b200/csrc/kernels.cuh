@@ -172,7 +172,6 @@ struct LineArgs {
     int part;          // TilePart: which tile rows this launch covers
     HaloPush push;     // fused halo push of the output (dst == nullptr: none)
     HaloWait hw;       // in-kernel wait for the halo'd input's slabs (P2P overlap)
-    int stream_out;    // k_line: outputs by streaming (evict-first) stores
     const double* im;  // per-column fields: 1/m_k of every column's line block (Lambda layout, this
                        // level), precomputed once per operator (launch_pivots); the Thomas modes then
                        // stream it with the data instead of running the pivot recurrence
