@@ -132,6 +132,7 @@ struct tpmg_ctx {
     uint32_t prof_mask = 0;             // kernel classes bracketed with events (bit = tpmg_kernel)
     struct ProfRec { int cls; double cells; cudaEvent_t a, b; const int* skip; };
     std::vector<ProfRec> prof_pending;
+    int dbg = 0;                        // LineArgs::dbg (timing experiments)
     bool prof_detail = false;           // TPMG_PROF_DETAIL=1: per-level breakdown on stderr at tpmg_destroy
     std::map<std::pair<int, double>, std::pair<int64_t, double>> prof_by_size;
     std::vector<cudaEvent_t> prof_pool;
@@ -502,6 +503,7 @@ LineArgs line_args(tpmg_ctx* ctx, int level)
     a.ratio = DevRatio{nullptr, -1, -1};
     a.red = ReduceSlot{ctx->d_partials, ctx->d_ticket, nullptr, 0};
     a.skip = ctx->skip;
+    a.dbg = ctx->dbg;
     a.im = (ctx->lv[level].lc.gen >= 2 && ctx->lv[level].im_ok) ? ctx->lv[level].d_im : nullptr;
     return a;
 }
@@ -692,6 +694,8 @@ bool ksplit_halo_maps(tpmg_ctx* ctx, const HaloField& hf, int64_t nx, int nz, in
     M.has_hi = hf.hi != nullptr;
     if (hf.lo && (!aligned(hf.lo) || !tensor_map(ctx, hf.lo, nx, nz, 1, bx, 1, &M.lo, depth))) return false;
     if (hf.hi && (!aligned(hf.hi) || !tensor_map(ctx, hf.hi, nx, nz, 1, bx, 1, &M.hi, depth))) return false;
+    M.has_m1 = 0;
+    if ((hf.lo || hf.hi) && rows > 2) M.has_m1 = tensor_map(ctx, hf.base, nx, nz, ny, bx, rows - 1, &M.m1, depth) ? 1 : 0;
     return true;
 }
 
@@ -1793,6 +1797,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->sync_debug = sd && sd[0] == '1';
         const char* tm = std::getenv("TPMG_TMEM");   // "0": g' of the column kernels in shared memory
         ctx->tmem = !(tm && tm[0] == '0');
+        const char* dpr = std::getenv("TPMG_DBG_PERROW");
+        ctx->dbg = (dpr && dpr[0] == '1') ? 1 : 0;
         const char* pdt = std::getenv("TPMG_PROF_DETAIL");
         ctx->prof_detail = pdt && pdt[0] == '1';
         const char* pv = std::getenv("TPMG_PIVOTS");

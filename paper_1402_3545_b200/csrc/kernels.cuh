@@ -112,7 +112,9 @@ enum LineMode : int {
 // and the halo slabs (rows j = -1 / j = ny) when present.
 struct TmaHalo {
     CUtensorMap main, row, lo, hi;
-    int has_lo, has_hi;
+    CUtensorMap m1;   // k-split in-place layout: the box minus one row (a strip-boundary tile loads
+                      // its in-domain rows with it and the slab row separately)
+    int has_lo, has_hi, has_m1;
 };
 struct TmaMaps {
     TmaHalo h[2];
@@ -172,6 +174,7 @@ struct LineArgs {
     int part;          // TilePart: which tile rows this launch covers
     HaloPush push;     // fused halo push of the output (dst == nullptr: none)
     HaloWait hw;       // in-kernel wait for the halo'd input's slabs (P2P overlap)
+    int dbg;           // debug experiments: bit 0 = k-split in-place boxes row by row (TPMG_DBG_PERROW)
     const double* im;  // per-column fields: 1/m_k of every column's line block (Lambda layout, this
                        // level), precomputed once per operator (launch_pivots); the Thomas modes then
                        // stream it with the data instead of running the pivot recurrence

@@ -83,11 +83,23 @@ struct KGeom {
 // Rows r0 .. r0+nrows-1 (local row index of the box's first row = jb) of a halo'd
 // field into dst: one box TMA when no row comes from a slab, else one TMA per row.
 __device__ __forceinline__ void tma_rows(double* dst, const TmaHalo& M, int rows, int rowst, int x, int k, int jb,
-                                         int nyl, uint64_t* bar)
+                                         int nyl, uint64_t* bar, bool force_rows = false)
 {
-    const bool per_row = (M.has_lo && jb < 0) || (M.has_hi && jb + rows - 1 >= nyl);
-    if (!per_row) {
+    const bool lo = M.has_lo && jb < 0, hi = M.has_hi && jb + rows - 1 >= nyl;
+    if (!force_rows && !lo && !hi) {
         tma_load_3d(dst, &M.main, x, k, jb, bar);
+        return;
+    }
+    // a strip-boundary tile: the in-domain rows as one box, the slab row by itself (row-by-row
+    // loads measured 4.5x slower per tile, and the kernel waits for its slowest CTA: r2r)
+    if (!force_rows && M.has_m1 && lo != hi) {
+        if (lo) {
+            tma_load_3d(dst, &M.lo, x, k, 0, bar);
+            tma_load_3d(dst + rowst, &M.m1, x, k, jb + 1, bar);
+        } else {
+            tma_load_3d(dst, &M.m1, x, k, jb, bar);
+            tma_load_3d(dst + (rows - 1) * rowst, &M.hi, x, k, 0, bar);
+        }
         return;
     }
     for (int r = 0; r < rows; ++r) {
@@ -117,7 +129,7 @@ __device__ __forceinline__ void tma_step(double* st, const LineArgs& a, int i0, 
         double* seg = st + s * G::SEGST;
         const int k0 = s * SL + cc * KB;
         if constexpr (G::INPLACE) {
-            tma_rows(seg, a.tma.h[0], TY + 2, G::UROW, i0 - G::XO, k0 - 1, j0 - 1, ny, bar);
+            tma_rows(seg, a.tma.h[0], TY + 2, G::UROW, i0 - G::XO, k0 - 1, j0 - 1, ny, bar, a.dbg & 1);
             if constexpr (G::PROL)
                 tma_rows(seg + G::UBOX + G::FBOX, a.tma.h[1], G::CROWS, G::CROW, i0 / 2 - XOC, k0 - 1, j0 / 2 - 1,
                          ny / 2, bar);
