@@ -661,6 +661,7 @@ void fill_tma(tpmg_ctx* ctx, int mode, LineArgs& a)
         M.has_hi = hf.hi != nullptr;
         if (hf.lo && (!aligned(hf.lo) || !tensor_map(ctx, hf.lo, nx, nz, 1, kTileX + 4, 1, &M.lo))) return;
         if (hf.hi && (!aligned(hf.hi) || !tensor_map(ctx, hf.hi, nx, nz, 1, kTileX + 4, 1, &M.hi))) return;
+        M.has_m1 = (hf.lo || hf.hi) && tensor_map(ctx, hf.base, nx, nz, ny, kTileX + 4, TY + 1, &M.m1) ? 1 : 0;
     }
     for (int f = 0; f < np; ++f) {
         if (!Q[f] || !aligned(Q[f])) return;

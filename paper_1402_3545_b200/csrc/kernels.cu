@@ -130,9 +130,19 @@ __device__ __forceinline__ void tma_stage(double* st, const LineArgs& a, int64_t
     for (int f = 0; f < NH; ++f) {
         const TmaHalo& M = a.tma.h[f];
         double* dst = st + f * G::HY * G::HALO_ROW;
-        const bool rows = (M.has_lo && j0 == 0) || (M.has_hi && j0 + TY >= ny);
-        if (!rows) {
+        const bool lo = M.has_lo && j0 == 0, hi = M.has_hi && j0 + TY >= ny;
+        if (!lo && !hi) {
             tma_load_3d(dst, &M.main, x0, k0, (int)j0 - 1, bar);
+        } else if (M.has_m1 && lo != hi && (lo || j0 + TY == ny)) {   // (a ragged last row: row by row)
+            // strip-boundary tile: the in-domain rows as one box, the slab row by itself (a
+            // row-by-row tile is several times slower and its CTA sets the kernel time)
+            if (lo) {
+                tma_load_3d(dst, &M.lo, x0, k0, 0, bar);
+                tma_load_3d(dst + G::HALO_ROW, &M.m1, x0, k0, (int)j0, bar);
+            } else {
+                tma_load_3d(dst, &M.m1, x0, k0, (int)j0 - 1, bar);
+                tma_load_3d(dst + (G::HY - 1) * G::HALO_ROW, &M.hi, x0, k0, 0, bar);
+            }
         } else {
             for (int r = 0; r < G::HY; ++r) {
                 const int64_t j = j0 - 1 + r;
@@ -259,7 +269,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     const bool plo = a.push.dst_lo != nullptr, phi = a.push.dst_hi != nullptr;
     const int nrows = part_rows(a.part, nty);
     auto row_of = [&](int t) {
-        if constexpr (HW) return boundary_last_row(t / ntx, nrows);   // in-kernel halo wait: boundary rows last
+        if constexpr (HW) return boundary_deferred_row(t / ntx, nrows, kHaloDefer);   // in-kernel halo wait
         return part_row(a.part, nty, push_row(t / ntx, nrows, plo, phi));
     };
     int p_i0 = (p_tile % ntx) * TX, p_j0 = row_of(p_tile) * TY;
@@ -829,10 +839,10 @@ __device__ __forceinline__ void prolong_body(const LevelConst& Cc, const LevelCo
     const int nz = Cc.nz;
     const int64_t I = blockIdx.x * 32 + threadIdx.x;
     // PART_INTERIOR: coarse rows 1 .. nyc-2 (no halo row read); PART_BOUNDARY: rows 0, nyc-1.
-    // In-kernel halo wait (hw): block row 0 (coarse rows 0..3) goes last, and the threads of
-    // coarse rows 0 / nyc-1 wait for the halo epoch before they read the slabs.
+    // In-kernel halo wait (hw): the block rows with coarse rows 0 / nyc-1 are deferred by a
+    // few block rows, and their threads wait for the halo epoch before they read the slabs.
     const bool hwait = hw.flag[0] || hw.flag[1];
-    const int by = hwait ? (int)((blockIdx.y + 1) % gridDim.y) : (int)blockIdx.y;
+    const int by = hwait ? boundary_deferred_row((int)blockIdx.y, (int)gridDim.y, kHaloDefer) : (int)blockIdx.y;
     int64_t J = by * 4 + threadIdx.y;
     if (part == PART_INTERIOR) J += 1;
     else if (part == PART_BOUNDARY) J = (J == 0) ? 0 : ((J == 1 && nyc > 1) ? nyc - 1 : nyc);

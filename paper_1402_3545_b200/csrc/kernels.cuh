@@ -143,19 +143,25 @@ struct HaloPush {
 };
 // In-kernel halo wait (P2P overlap in ONE launch): flag[0] / flag[1] are my pool's epoch
 // flags "data from the lower / upper neighbour".  When set, the line kernels walk their
-// tile rows interior-first (boundary_last_row) and the loader waits (ld.acquire.sys)
-// until flag >= epoch before it loads a tile row that reads that halo slab, so the interior
-// rows run while the neighbours' rows are still on the way.  nullptr: no wait.
+// tile rows with the strip-boundary rows deferred (boundary_deferred_row) and the loader
+// waits (ld.acquire.sys) until flag >= epoch before it loads a tile row that reads that halo
+// slab, so interior rows run while the neighbours' rows are still on the way.  nullptr: no
+// wait.
 struct HaloWait {
     const unsigned* flag[2];
     unsigned epoch;
 };
-// Tile-row order with the strip-boundary rows last (nrows >= 3): 1, 2, ..., nrows-2, 0, nrows-1.
-__host__ __device__ inline int boundary_last_row(int r, int nrows)
+// Tile-row order with the two strip-boundary rows deferred by d rows (nrows >= 3):
+// 1, ..., d, 0, nrows-1, d+1, ..., nrows-2.  A few µs of interior work cover the NVLink
+// push; deferring them to the very end (d = nrows-2) made them the kernel's tail (r2s:
+// +15% for the fine-level restriction).
+__host__ __device__ inline int boundary_deferred_row(int r, int nrows, int d)
 {
     if (nrows < 3) return r;
-    return r < nrows - 2 ? r + 1 : (r == nrows - 2 ? 0 : nrows - 1);
+    d = d < nrows - 2 ? d : nrows - 2;
+    return r < d ? r + 1 : (r == d ? 0 : (r == d + 1 ? nrows - 1 : r - 1));
 }
+constexpr int kHaloDefer = 8;   // tile rows of interior work before the boundary rows
 
 struct LineArgs {
     LevelConst L;

@@ -92,7 +92,7 @@ __device__ __forceinline__ void tma_rows(double* dst, const TmaHalo& M, int rows
     }
     // a strip-boundary tile: the in-domain rows as one box, the slab row by itself (row-by-row
     // loads measured 4.5x slower per tile, and the kernel waits for its slowest CTA: r2r)
-    if (!force_rows && M.has_m1 && lo != hi) {
+    if (!force_rows && M.has_m1 && lo != hi && (lo || jb + rows - 1 == nyl)) {   // (ragged last row: row by row)
         if (lo) {
             tma_load_3d(dst, &M.lo, x, k, 0, bar);
             tma_load_3d(dst + rowst, &M.m1, x, k, jb + 1, bar);
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     const int ntiles = ntx * nrows;
     const bool plo = PUSH && a.push.dst_lo != nullptr, phi = PUSH && a.push.dst_hi != nullptr;
     auto row_of = [&](int t) {
-        if constexpr (HW) return boundary_last_row(t / ntx, nrows);   // in-kernel halo wait: boundary rows last
+        if constexpr (HW) return boundary_deferred_row(t / ntx, nrows, kHaloDefer);   // in-kernel halo wait
         return part_row(a.part, nty, PUSH ? push_row(t / ntx, nrows, plo, phi) : t / ntx);
     };
     const int my_tiles = ((int)blockIdx.x < ntiles) ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
