@@ -113,6 +113,7 @@ struct tpmg_ctx {
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     bool overlap = true;                // P2P halos: interior rows while the halo travels (TPMG_OVERLAP=0 off)
+    bool overlap_cg = false;            // the CG direction kernel too (TPMG_OVERLAP_CG=1)
     bool overlap_nccl = false;          // NCCL halos: TPMG_OVERLAP=1 (measured slower at N=4 in round 1:
                                         // the split launches cost more than the NCCL latency they hide)
     int reserve_sms = 4;                // SMs left to NCCL while the interior runs
@@ -791,7 +792,8 @@ tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
 // the output) runs one launch after the exchange.
 template <typename PreBoundary>
 tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, LineArgs a, const double* x, double* lo, double* hi,
-                          PreBoundary pre_boundary, const double* push_out = nullptr, int chan = -1)
+                          PreBoundary pre_boundary, const double* push_out = nullptr, int chan = -1,
+                          bool overlap = true)
 {
     if (chan < 0) chan = level;
     if (ctx->nranks == 1) {
@@ -804,7 +806,7 @@ tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, LineArgs a, const 
     const bool fused_out = push_out && ctx->fused_push;
     const bool hw_ok = ksplit_usable(ctx, mode, lc) ? ksplit_halo_wait(mode, ctx->ksplit_cfg, lc.gen)
                                                     : line_halo_wait(mode, lc.nz, lc.gen, ctx->use_tma, ctx->tmem);
-    if (ctx->p2p && ctx->overlap && !ctx->halo_off && !fused_out && nty >= 3 && hw_ok) {
+    if (ctx->p2p && ctx->overlap && overlap && !ctx->halo_off && !fused_out && nty >= 3 && hw_ok) {
         // ONE launch: its CTAs walk the interior tile rows first; the loader of a strip-
         // boundary tile row waits in the kernel (ld.acquire.sys on my pool's epoch flag) for
         // the neighbour's rows, which travel while the interior is computed
@@ -1301,7 +1303,9 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
                                              beta, ctx->skip));
                 return TPMG_OK;
             };
-            TRY(run_line_halo(ctx, l, MODE_CGDIR, a, ctx->cg_z, ctx->cg_zlo, ctx->cg_zhi, p_halo, nullptr, l + 1));
+            // (the in-kernel overlap measured 2.5% slower per CG iteration at N = 2, r2t: opt-in)
+            TRY(run_line_halo(ctx, l, MODE_CGDIR, a, ctx->cg_z, ctx->cg_zlo, ctx->cg_zhi, p_halo, nullptr, l + 1,
+                              ctx->overlap_cg));
             TRY(allreduce(ctx, ctx->d_scal + S_SIGMA(m), 1));
         }
         HaloField hpn{ctx->cg_p[1 - cur], nullptr, nullptr};
@@ -1786,6 +1790,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         const char* ov = std::getenv("TPMG_OVERLAP");
         ctx->overlap = !(ov && ov[0] == '0');        // P2P transport: on by default
         ctx->overlap_nccl = ov && ov[0] == '1';      // NCCL transport: opt-in
+        const char* ovc = std::getenv("TPMG_OVERLAP_CG");
+        ctx->overlap_cg = ovc && ovc[0] == '1';
         const char* rs = std::getenv("TPMG_RESERVE_SMS");
         if (rs) ctx->reserve_sms = std::max(0, std::atoi(rs));
         const char* kc = std::getenv("TPMG_KSPLIT_CG");

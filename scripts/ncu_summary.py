@@ -57,9 +57,9 @@ def main(rep, traffic_json=None):
         if "k_prolong_add" in name:   # keep the largest (fine-level) launch
             if (rd + wr) * 1e9 > traffic["prolong_add"]["bytes"]:
                 traffic["prolong_add"] = {"bytes": (rd + wr) * 1e9, "time_ms": t, "grid": r[c["Grid Size"]]}
-        if m and (r[c["Grid Size"]].startswith("(148") or mode in (4, 6)):
+        if m:   # per class, the largest (fine-level) capture
             cls = MODES.get(mode)
-            if cls and cls not in traffic:
+            if cls and (cls not in traffic or (rd + wr) * 1e9 > traffic[cls]["bytes"]):
                 traffic[cls] = {"bytes": (rd + wr) * 1e9, "time_ms": t, "grid": r[c["Grid Size"]]}
     if traffic_json:
         json.dump(traffic, open(traffic_json, "w"), indent=1)

@@ -16,6 +16,7 @@ def ngpus():
 
 CASES = [  # (world, TPMG_OVERLAP, halo transport, boundary / coefficients)
     (2, "", "p2p", "0"),            # default: P2P halos overlapped with interior rows, NVLink allreduce
+    (2, "cg", "p2p", "0"),          # + the CG direction kernel overlapped (TPMG_OVERLAP_CG=1)
     (4, "", "p2p", "1"),
     (2, "0", "p2p", "0"),           # P2P without overlap
     (2, "", "p2p-ncclar", "0"),     # P2P halos, ncclAllReduce
@@ -49,7 +50,10 @@ def test_multirank_parity(world, overlap, halo, bc):
                TPMG_TEST_FIELDS="5" if flds else "-1",
                TPMG_FUSED_PUSH="1" if fused else "0")
     env.pop("TPMG_OVERLAP", None)
-    if overlap:
+    env.pop("TPMG_OVERLAP_CG", None)
+    if overlap == "cg":
+        env["TPMG_OVERLAP_CG"] = "1"
+    elif overlap:
         env["TPMG_OVERLAP"] = overlap
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 0, (r.stdout[-4000:], r.stderr[-4000:])
