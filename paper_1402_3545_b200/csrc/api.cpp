@@ -114,6 +114,8 @@ struct tpmg_ctx {
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     bool overlap = true;                // P2P halos: interior rows while the halo travels (TPMG_OVERLAP=0 off)
     bool overlap_cg = false;            // the CG direction kernel too (TPMG_OVERLAP_CG=1)
+    bool pair_u = false;                // CG: u updated every second iteration (TPMG_PAIR_U=1; r2v: PCG
+                                        // -4% time, but the two variants run at 0.86 of the copy peak)
     bool overlap_nccl = false;          // NCCL halos: TPMG_OVERLAP=1 (measured slower at N=4 in round 1:
                                         // the split launches cost more than the NCCL latency they hide)
     int reserve_sms = 4;                // SMs left to NCCL while the interior runs
@@ -123,7 +125,7 @@ struct tpmg_ctx {
     // profiling (tpmg_profile)
     bool pdl = false;                   // programmatic dependent launches (TPMG_PDL=1)
     bool tmem = true;                   // Thomas g' of the column kernels in Tensor Memory (TPMG_TMEM=0: smem)
-    int tm_ctas = 2;                    // their CTAs per SM (TPMG_TM_CTAS; r2c, r2f: 2 >= 1)
+    int tm_ctas = 1;                    // their CTAs per SM (TPMG_TM_CTAS; see kernels.cuh)
     int tm_stages = 3;                  // their TMA ring depth (TPMG_TM_STAGES: 3, 4, 5)
     bool pivots = true;                 // per-column fields: precomputed pivots (TPMG_PIVOTS=0: off)
     bool ksplit_cg = false;             // k-split CG preconditioner (TPMG_KSPLIT_CG=1)
@@ -632,7 +634,7 @@ bool tensor_map(tpmg_ctx* ctx, const double* base, int64_t nx, int nz, int64_t n
 
 void mode_fields(int mode, int* nh, int* np)
 {
-    static const int NH[8] = {1, 1, 0, 1, 2, 1, 1, 2}, NP[8] = {0, 1, 1, 1, 0, 2, 1, 1};
+    static const int NH[10] = {1, 1, 0, 1, 2, 1, 1, 2, 1, 1}, NP[10] = {0, 1, 1, 1, 0, 2, 1, 1, 1, 3};
     *nh = NH[mode];
     *np = NP[mode];
 }
@@ -650,7 +652,7 @@ void fill_tma(tpmg_ctx* ctx, int mode, LineArgs& a)
     int nh, np;
     mode_fields(mode, &nh, &np);
     const HaloField* H[2] = {&a.h0, &a.h1};
-    const double* Q[2] = {a.q0, a.q1};
+    const double* Q[3] = {a.q0, a.q1, a.q2};
     auto aligned = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
     for (int f = 0; f < nh; ++f) {
         TmaHalo& M = a.tma.h[f];
@@ -669,7 +671,7 @@ void fill_tma(tpmg_ctx* ctx, int mode, LineArgs& a)
         if (!tensor_map(ctx, Q[f], nx, nz, ny, kTileX, TY, &a.tma.q[f])) return;
     }
     // the precomputed pivots of the Thomas modes travel as plain field np
-    const bool thomas = mode == MODE_PREC || mode == MODE_SMOOTH || mode == MODE_CGPREC;
+    const bool thomas = mode == MODE_PREC || mode == MODE_SMOOTH || is_cgprec(mode);
     if (thomas && a.im && (!aligned(a.im) || !tensor_map(ctx, a.im, nx, nz, ny, kTileX, TY, &a.tma.q[np]))) a.im = nullptr;
     if (!thomas) a.im = nullptr;
     a.use_tma = 1;
@@ -724,6 +726,7 @@ bool ksplit_usable(tpmg_ctx* ctx, int mode, const LevelConst& lc)
 {
     // general vertical profiles: the k-split smoother / preconditioner / restriction only
     if (lc.gen && (mode == MODE_SMOOTH_PROLONG || mode == MODE_CGPREC)) return false;
+    if (mode == MODE_CGPREC_D || mode == MODE_CGPREC_P) return false;   // one-thread-per-column kernel only
     // per-column fields: the one-thread-per-column kernel only (per-column pivots)
     if (lc.gen == 2) return false;
     // the k-split CG preconditioner is opt-in (TPMG_KSPLIT_CG=1): measured 4% slower per CG
@@ -768,7 +771,11 @@ tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
     if (mode == MODE_SMOOTH_PROLONG) return fail(ctx, TPMG_E_PARAM, "fused prolongation-smooth needs the k-split kernel");
     a = a0;
     fill_tma(ctx, mode, a);
-    ProfScope ps(ctx, mode == MODE_RESTRICT ? TPMG_K_RESIDUAL_RESTRICT : mode, part_cells(ctx, mode, a));  // modes 0..5 = TPMG_K_0..5
+    // modes 0..5 = TPMG_K_0..5; the paired-u CG variants count as CG preconditioning with their
+    // own bytes expressed in units of MODE_CGPREC's 48 B per cell (32 and 56 B)
+    const int pcls = mode == MODE_RESTRICT ? TPMG_K_RESIDUAL_RESTRICT : is_cgprec(mode) ? TPMG_K_CG_PRECONDITION : mode;
+    const double pscale = mode == MODE_CGPREC_D ? 32.0 / 48.0 : mode == MODE_CGPREC_P ? 56.0 / 48.0 : 1.0;
+    ProfScope ps(ctx, pcls, part_cells(ctx, mode, a) * pscale);
     CUDA_TRY(ctx, launch_line(launcher(ctx), mode, a));
     if (ctx->sync_debug) {
         cudaError_t e = cudaStreamSynchronize(ctx->stream);
@@ -1312,7 +1319,10 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
         if (ctx->nranks > 1)
             hpn = HaloField{ctx->cg_p[1 - cur], has_lo ? ctx->cg_plo[1 - cur] : nullptr,
                             has_hi ? ctx->cg_phi[1 - cur] : nullptr};
-        // (Fused) preconditioner kernel: r -= alpha A p, u += alpha p, z = M^-1 r, ||r||^2, <r,z>
+        // (Fused) preconditioner kernel: r -= alpha A p, u += alpha p, z = M^-1 r, ||r||^2, <r,z>.
+        // Paired u updates (ctx->pair_u): odd iterations skip u, even ones add alpha_{m-1} p_{m-1}
+        // + alpha_m p_m (p_{m-1} is still in the other direction buffer): 68 instead of 72 B per
+        // cell per iteration; r, z and the sums -- the whole iteration -- are unchanged.
         {
             LineArgs a = line_args(ctx, l);
             a.h0 = hpn;
@@ -1323,7 +1333,17 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
             a.out2 = ctx->cg_z;
             a.ratio = DevRatio{ctx->d_scal, S_ZETA(m - 1), S_SIGMA(m)};
             a.red.result = ctx->d_scal + S_RR(m);
-            TRY(run_line(ctx, MODE_CGPREC, a));   // z's halo: push kernel (fused measured no faster)
+            int mode = MODE_CGPREC;
+            if (ctx->pair_u && (m & 1)) {
+                mode = MODE_CGPREC_D;
+                a.q1 = nullptr;
+                a.out1 = nullptr;
+            } else if (ctx->pair_u) {
+                mode = MODE_CGPREC_P;
+                a.q2 = ctx->cg_p[cur];   // p_{m-1}
+                a.ratio2 = DevRatio{ctx->d_scal, S_ZETA(m - 2), S_SIGMA(m - 1)};
+            }
+            TRY(run_line(ctx, mode, a));   // z's halo: push kernel (fused measured no faster)
             TRY(allreduce(ctx, ctx->d_scal + S_RR(m), 2));
         }
         CUDA_TRY(ctx, launch_cg_check(launcher(ctx), ctx->d_scal, m, eps, ctx->d_flags, ctx->dh_flags));
@@ -1356,6 +1376,11 @@ tpmg_status solve_cg_impl(tpmg_ctx* ctx, const double* f, double* u, double eps,
         }
         if (code == 3) return fail(ctx, TPMG_E_BREAKDOWN, "CG iteration %d: NaN residual", it);
         conv = (code == 1);
+    }
+    if (ctx->pair_u && (it & 1)) {
+        // the last iteration was odd: its step alpha_it p_it is still to be added to u
+        CUDA_TRY(ctx, launch_cg_halo(launcher(ctx), u, u, ctx->cg_p[it & 1], nullptr, nullptr, nullptr, (int64_t)n,
+                                     DevRatio{ctx->d_scal, S_ZETA(it - 1), S_SIGMA(it)}, nullptr));
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
     CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
@@ -1790,6 +1815,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         const char* ov = std::getenv("TPMG_OVERLAP");
         ctx->overlap = !(ov && ov[0] == '0');        // P2P transport: on by default
         ctx->overlap_nccl = ov && ov[0] == '1';      // NCCL transport: opt-in
+        const char* pu = std::getenv("TPMG_PAIR_U");
+        ctx->pair_u = pu && pu[0] == '1';
         const char* ovc = std::getenv("TPMG_OVERLAP_CG");
         ctx->overlap_cg = ovc && ovc[0] == '1';
         const char* rs = std::getenv("TPMG_RESERVE_SMS");

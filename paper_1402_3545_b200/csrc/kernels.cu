@@ -35,7 +35,7 @@ constexpr int KB = kStageK; // vertical levels per pipeline stage
 constexpr int kNS = 3;  // pipeline stages
 // the CG preconditioner with per-column fields keeps 4 tile rows (4 warps per SM) with 2 stages
 template <int MODE, int GEN>
-__host__ __device__ constexpr int stages() { return (GEN == 2 && MODE == MODE_CGPREC) ? 2 : kNS; }
+__host__ __device__ constexpr int stages() { return (GEN == 2 && is_cgprec(MODE)) ? 2 : kNS; }
 
 // 1/x for the per-column pivots: the approximate reciprocal (MUFU) refined by two Newton
 // steps (error ~2^-92 before rounding, i.e. correctly rounded up to an ulp) -- 5 instructions
@@ -59,6 +59,8 @@ template <> struct Traits<MODE_SMOOTH> { static constexpr int NH = 1, NP = 1, TH
 template <> struct Traits<MODE_CGDIR>  { static constexpr int NH = 2, NP = 0, THOMAS = 0, NR = 1; };
 template <> struct Traits<MODE_CGPREC> { static constexpr int NH = 1, NP = 2, THOMAS = 1, NR = 2; };
 template <> struct Traits<MODE_RESTRICT> { static constexpr int NH = 1, NP = 1, THOMAS = 0, NR = 0; };
+template <> struct Traits<MODE_CGPREC_D> { static constexpr int NH = 1, NP = 1, THOMAS = 1, NR = 2; };
+template <> struct Traits<MODE_CGPREC_P> { static constexpr int NH = 1, NP = 3, THOMAS = 1, NR = 2; };
 
 template <int NH, int NP, int TY>
 struct Geom {
@@ -104,7 +106,7 @@ __device__ __forceinline__ void load_stage(double* st, const LineArgs& a, int64_
             const int f = s2 / (TY * KB);
             const int rem = s2 - f * (TY * KB);
             const int r = rem / KB, kk = rem - (rem / KB) * KB;
-            const double* Q = (f == 0) ? a.q0 : a.q1;
+            const double* Q = (f == 0) ? a.q0 : (f == 1 ? a.q1 : a.q2);
             const int64_t j = j0 + r;
             const int k = k0 + kk;
             const bool rowok = (j < ny) && (k < nz);
@@ -236,9 +238,12 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     if (a.skip && *a.skip) return;   // solver run-ahead: this iteration is not needed
 
     auto put = [](double* q, double v) { *q = v; };   // (st.global.cs measured no different, r2o)
-    double ratio = 0.0;
-    if constexpr (MODE == MODE_CGDIR || MODE == MODE_CGPREC)
+    constexpr bool CGP = is_cgprec(MODE);
+    double ratio = 0.0, ratio2 = 0.0;
+    if constexpr (MODE == MODE_CGDIR || CGP)
         if (a.ratio.num >= 0) ratio = a.ratio.s[a.ratio.num] / a.ratio.s[a.ratio.den];
+    if constexpr (MODE == MODE_CGPREC_P)
+        if (a.ratio2.num >= 0) ratio2 = a.ratio2.s[a.ratio2.num] / a.ratio2.s[a.ratio2.den];
 
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
@@ -362,12 +367,12 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
         }
 
         // rolling state for the k-lag: values at level km = k-1 and km-1
-        double um1 = 0.0, u0 = 0.0, S0 = 0.0, qa = 0.0, qb = 0.0, qc = 0.0, gprev = 0.0;   // qc: 1/m_k (GEN 3)
+        double um1 = 0.0, u0 = 0.0, S0 = 0.0, qa = 0.0, qb = 0.0, qc = 0.0, qd = 0.0, gprev = 0.0;   // qc: 1/m_k (GEN 3), qd: p_prev
         double* rbuf_cur = rbuf;   // MODE_RESTRICT: buffer of the current chunk
         // forward-pass outputs of level km live at ofw0/ofw1 (advanced by nx per level)
-        double* ofw0 = (MODE == MODE_APPLY || MODE == MODE_RESID || MODE == MODE_CGDIR || MODE == MODE_CGPREC) && a.out0
+        double* ofw0 = (MODE == MODE_APPLY || MODE == MODE_RESID || MODE == MODE_CGDIR || CGP) && a.out0
                            ? a.out0 + colbase : nullptr;
-        double* ofw1 = (MODE == MODE_CGPREC) ? a.out1 + colbase : nullptr;
+        double* ofw1 = (MODE == MODE_CGPREC || MODE == MODE_CGPREC_P) ? a.out1 + colbase : nullptr;
 
         // Complete level km (its upper neighbour up1 has arrived): stencil, the mode's
         // pointwise work and one Thomas forward-elimination step.
@@ -416,24 +421,24 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 const double r = fma(c, S0, qa) - Mu;
                 const double rs = r + __shfl_xor_sync(0xffffffffu, r, 1);
                 if ((tx & 1) == 0) rbuf_cur[(ty * RS + rslot) * (TX / 2) + (tx >> 1)] = rs;
-            } else if constexpr (MODE == MODE_CGPREC) {
+            } else if constexpr (CGP) {
                 const double Ap = fma(-c, S0, Mu);
                 const double rn = fma(-ratio, Ap, qa);
-                const double un = fma(ratio, u0, qb);
                 if (valid) {
                     put(ofw0, rn);
-                    put(ofw1, un);
+                    if constexpr (MODE == MODE_CGPREC) put(ofw1, fma(ratio, u0, qb));
+                    if constexpr (MODE == MODE_CGPREC_P) put(ofw1, fma(ratio, u0, fma(ratio2, qd, qb)));
                     acc[0] = fma(rn, rn, acc[0]);
                 }
                 g = rn;
             }
-            if constexpr (MODE == MODE_APPLY || MODE == MODE_RESID || MODE == MODE_CGDIR || MODE == MODE_CGPREC) {
+            if constexpr (MODE == MODE_APPLY || MODE == MODE_RESID || MODE == MODE_CGDIR || CGP) {
                 if constexpr (MODE == MODE_RESID) {   // the only mode whose out0 may be absent
                     if (ofw0) ofw0 += nx;
                 } else {
                     ofw0 += nx;
                 }
-                if constexpr (MODE == MODE_CGPREC) ofw1 += nx;
+                if constexpr (MODE == MODE_CGPREC || MODE == MODE_CGPREC_P) ofw1 += nx;
             }
             if constexpr (T::THOMAS) {
                 if constexpr (GEN == 2) {
@@ -450,7 +455,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                     tmem_st_f64(tbase + 2u * (uint32_t)km, gp);
                 else
                     *gslot = gp;
-                if constexpr (MODE == MODE_CGPREC)
+                if constexpr (CGP)
                     if (valid) acc[1] = fma(gp, y, acc[1]);   // <g, M^-1 g> = sum y_k^2 / m_k
                 gprev = gp;
             }
@@ -461,12 +466,12 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
         auto do_chunk = [&](auto full_t, int ch, const double* st) {
             constexpr bool FULL = decltype(full_t)::value;
             const int k0 = ch * KB;
-            double ecv[KB], Sv[KB], pav[KB], pbv[KB], pcv[KB];
+            double ecv[KB], Sv[KB], pav[KB], pbv[KB], pcv[KB], pdv[KB];
             const double* hp = st + (ty + 1) * G::HALO_ROW + tx + 2;           // own column
             const double* pp = st + G::PLAIN_BASE + ty * (KB * TX) + tx;       // plain field 0
 #pragma unroll
             for (int kk = 0; kk < KB; ++kk) {
-                ecv[kk] = 0.0; Sv[kk] = 0.0; pav[kk] = 0.0; pbv[kk] = 0.0; pcv[kk] = 0.0;
+                ecv[kk] = 0.0; Sv[kk] = 0.0; pav[kk] = 0.0; pbv[kk] = 0.0; pcv[kk] = 0.0; pdv[kk] = 0.0;
                 if constexpr (NH >= 1) {
                     const double* h = hp + kk * G::HX;
                     ecv[kk] = h[0];
@@ -486,6 +491,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 }
                 if constexpr (T::NP >= 1) pav[kk] = pp[kk * TX];
                 if constexpr (T::NP >= 2) pbv[kk] = pp[TY * KB * TX + kk * TX];
+                if constexpr (T::NP >= 3) pdv[kk] = pp[2 * TY * KB * TX + kk * TX];   // MODE_CGPREC_P: p_prev
                 if constexpr (GEN == 3) pcv[kk] = pp[T::NP * TY * KB * TX + kk * TX];   // the pivot field
             }
             __syncthreads();   // slot gi % NS is free for chunk gi + NS
@@ -505,7 +511,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                             pm2 = 1.0;
                             cbuf[ch * NT + tid] = m;
                         }
-                    um1 = u0; u0 = ecv[kk]; S0 = Sv[kk]; qa = pav[kk]; qb = pbv[kk]; qc = pcv[kk];
+                    um1 = u0; u0 = ecv[kk]; S0 = Sv[kk]; qa = pav[kk]; qb = pbv[kk]; qc = pcv[kk]; qd = pdv[kk];
                 }
             }
         };
@@ -551,7 +557,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
         if constexpr (T::THOMAS && GEN == 3) {
             // backward substitution x_k = g'_k - (t_k / m_k) x_{k+1}, 8 levels per TMEM load of
             // (g'_k, 1/m_k) pairs
-            double* op = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase + (int64_t)(nz - 1) * nx;
+            double* op = (CGP ? a.out2 : a.out0) + colbase + (int64_t)(nz - 1) * nx;
             double x = 0.0;
             int k = nz - 1;
             tmem_wait_st();   // the forward sweep's stores have landed
@@ -590,7 +596,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             // checkpoint with the forward sweep's arithmetic, then x_k = g'_k - t'_k x_{k+1}
             // (software-pipelining the next chunk's recompute into this loop measured slower:
             // 1869 vs 1770 us for the fine-level smoother, more registers, same stalls)
-            double* obase = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase;
+            double* obase = (CGP ? a.out2 : a.out0) + colbase;
             double x = 0.0;
             if constexpr (TM) tmem_wait_st();   // the forward sweep's g' stores have landed
             for (int c = nck - 1; c >= 0; --c) {
@@ -629,7 +635,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
         if constexpr (T::THOMAS && GEN < 2) {
             // backward substitution x_k = g'_k - t'_k x_{k+1}, KB levels per step with
             // the shared-memory loads issued ahead of the dependent FMA chain
-            double* op = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase + (int64_t)(nz - 1) * nx;
+            double* op = (CGP ? a.out2 : a.out0) + colbase + (int64_t)(nz - 1) * nx;
             double x = 0.0;
             int k = nz - 1;
             // TM: the chunk's g' comes from Tensor Memory, 8 levels per load (a software-pipelined
@@ -668,7 +674,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             // fused halo push: a strip-boundary row also goes to the neighbour's slab (read
             // back from L1/L2, outside the recurrence loop)
             if (valid && ((j == 0 && a.push.dst_lo) || (j == ny - 1 && a.push.dst_hi))) {
-                const double* src = ((MODE == MODE_CGPREC) ? a.out2 : a.out0) + colbase;
+                const double* src = (CGP ? a.out2 : a.out0) + colbase;
                 double* dst = (j == 0 ? a.push.dst_lo : a.push.dst_hi) + i;
                 double* dst2 = (j == 0 && j == ny - 1) ? a.push.dst_hi : nullptr;   // a one-row strip
                 // batches of 16 independent loads: the copy is latency-, not bandwidth-bound
@@ -778,7 +784,7 @@ cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
                 return launch_line_l<MODE, 4, 1, 3, 3>(ln, a);
         if constexpr (Traits<MODE>::THOMAS && TY == 4)   // g' in Tensor Memory, 2 CTAs per SM
             if (ln.tmem && a.L.nz <= (int)(kTmemCols / 2)) {
-                if (a.L.gen >= 2) return launch_line_l<MODE, 4, 1, 2, (MODE == MODE_CGPREC ? 2 : 3)>(ln, a);
+                if (a.L.gen >= 2) return launch_line_l<MODE, 4, 1, 2, (is_cgprec(MODE) ? 2 : 3)>(ln, a);
                 return launch_line_l<MODE, 4, 1, 1, 3>(ln, a);
             }
         return a.L.gen >= 2 ? launch_line_l<MODE, TY, 1, 2>(ln, a) : launch_line_l<MODE, TY, 1, 1>(ln, a);
@@ -1157,11 +1163,13 @@ bool line_gen_fits(int nz, int gen) { return line_smem_bytes<MODE_CGPREC, 1>(nz,
 int line_tile_rows(int mode, int nz, int gen, bool tm)
 {
     // the Tensor Memory form of the Thomas modes always runs 4 tile rows (the lane quarters)
-    if (tm && nz <= (int)(kTmemCols / 2) && (mode == MODE_PREC || mode == MODE_SMOOTH || mode == MODE_CGPREC)) return 4;
+    if (tm && nz <= (int)(kTmemCols / 2) && (mode == MODE_PREC || mode == MODE_SMOOTH || is_cgprec(mode))) return 4;
     switch (mode) {
     case MODE_PREC: return line_smem_bytes<MODE_PREC, 4>(nz, gen) <= kMaxSmem ? 4 : line_smem_bytes<MODE_PREC, 2>(nz, gen) <= kMaxSmem ? 2 : 1;
     case MODE_SMOOTH: return line_smem_bytes<MODE_SMOOTH, 4>(nz, gen) <= kMaxSmem ? 4 : line_smem_bytes<MODE_SMOOTH, 2>(nz, gen) <= kMaxSmem ? 2 : 1;
     case MODE_CGPREC: return line_smem_bytes<MODE_CGPREC, 4>(nz, gen) <= kMaxSmem ? 4 : line_smem_bytes<MODE_CGPREC, 2>(nz, gen) <= kMaxSmem ? 2 : 1;
+    case MODE_CGPREC_D: return line_smem_bytes<MODE_CGPREC_D, 4>(nz, gen) <= kMaxSmem ? 4 : line_smem_bytes<MODE_CGPREC_D, 2>(nz, gen) <= kMaxSmem ? 2 : 1;
+    case MODE_CGPREC_P: return line_smem_bytes<MODE_CGPREC_P, 4>(nz, gen) <= kMaxSmem ? 4 : line_smem_bytes<MODE_CGPREC_P, 2>(nz, gen) <= kMaxSmem ? 2 : 1;
     default: return 4;
     }
 }
@@ -1183,6 +1191,8 @@ cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a)
     case MODE_SMOOTH: return launch_line_ty<MODE_SMOOTH>(ln, a);
     case MODE_CGDIR: return launch_line_t<MODE_CGDIR, 4>(ln, a);
     case MODE_CGPREC: return launch_line_ty<MODE_CGPREC>(ln, a);
+    case MODE_CGPREC_D: return launch_line_ty<MODE_CGPREC_D>(ln, a);
+    case MODE_CGPREC_P: return launch_line_ty<MODE_CGPREC_P>(ln, a);
     case MODE_RESTRICT: return launch_line_t<MODE_RESTRICT, 4>(ln, a);
     default: return cudaErrorInvalidValue;
     }

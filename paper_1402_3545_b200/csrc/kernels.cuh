@@ -106,7 +106,16 @@ enum LineMode : int {
     MODE_RESTRICT = 6,// out0 (coarse) = R (f - A u): fine residual restricted (halo: u; plain: f)
     MODE_SMOOTH_PROLONG = 7, // out0 = smooth(u + P u_c), sum r^2  (halo: u, coarse u_c; plain: f;
                              // k-split kernel only)
+    // CG preconditioner with the u update paired over two iterations (the level-1 BLAS
+    // fused into the two kernels): odd iterations leave u alone, even ones add both steps;
+    // r, z, the sums and hence the iteration are bit-identical to MODE_CGPREC's
+    MODE_CGPREC_D = 8,  // r -= alpha A p; z = M^-1 r; sums (no u)          (halo: p; plain: r)
+    MODE_CGPREC_P = 9,  // as MODE_CGPREC with u += alpha2 p_prev + alpha p  (halo: p; plain: r, u, p_prev)
 };
+__host__ __device__ constexpr bool is_cgprec(int mode)
+{
+    return mode == MODE_CGPREC || mode == MODE_CGPREC_D || mode == MODE_CGPREC_P;
+}
 
 // TMA descriptors of one halo'd field: the whole (TY+2)-row box, a one-row box,
 // and the halo slabs (rows j = -1 / j = ny) when present.
@@ -118,7 +127,7 @@ struct TmaHalo {
 };
 struct TmaMaps {
     TmaHalo h[2];
-    CUtensorMap q[3];   // plain inputs; q[NP] = the pivot field of the precomputed-pivot form
+    CUtensorMap q[4];   // plain inputs; q[NP] = the pivot field of the precomputed-pivot form
 };
 
 // Tile geometry of the line kernels: TX = 32 columns along x per tile row,
@@ -170,10 +179,12 @@ struct LineArgs {
     HaloField h0, h1;  // halo'd inputs
     const double* q0;  // plain inputs
     const double* q1;
+    const double* q2;  // MODE_CGPREC_P: p of the previous iteration
     double* out0;
     double* out1;
     double* out2;
     DevRatio ratio;    // beta (CGDIR) or alpha (CGPREC)
+    DevRatio ratio2;   // MODE_CGPREC_P: alpha of the previous iteration
     ReduceSlot red;    // result may be nullptr: no reduction
     int use_tma;       // 1: loads by TMA (tma must be filled), 0: cp.async
     const int* skip;   // device flag: the kernel returns at once when *skip != 0 (solver run-ahead)
@@ -196,7 +207,7 @@ struct Launcher {
                        // prologue with the previous kernel's tail (griddepcontrol)
     bool tmem = true;  // one-thread-per-column Thomas kernels keep g' in Tensor Memory (nz <= 128)
     int tm_stages = 3; // their TMA ring depth (3; 4, 5 for CGPREC A/B)
-    int tm_ctas = 2;   // CTAs per SM of those kernels (TMEM holds 2; r2f: 2 is 0.4% faster than 1)
+    int tm_ctas = 1;   // CTAs per SM of those kernels (TMEM holds 2; 1 and 2 measured equal: r2c, r2f, r2k, r2p; 1 keeps every CG variant on the same grid, so the reductions -- and the iteration -- are identical)
 };
 
 // Launch with the PDL attribute when ln.pdl.  Every kernel launched this way executes

@@ -142,11 +142,13 @@ def test_tmem_form_bit_identical_to_shared_memory_form(shape):
     for tm in ("1", "0"):
         os.environ["TPMG_TMEM"] = tm
         os.environ["TPMG_TM_CTAS"] = "1"
+        os.environ["TPMG_PAIR_U"] = "0"   # (the paired-u variants run other tile rows without TMEM)
         try:
             ctx = ctx_for(O.Params(nx=nx, ny=ny, nz=nz, L=L))
         finally:
             os.environ.pop("TPMG_TMEM")
             os.environ.pop("TPMG_TM_CTAS")
+            os.environ.pop("TPMG_PAIR_U")
         f = torch.from_numpy(np.random.default_rng(4).standard_normal(ctx.shape(L))).cuda()
         x = torch.empty_like(f)
         r = ctx.solve_cg(f, x, max_iter=12)
@@ -159,3 +161,29 @@ def test_tmem_form_bit_identical_to_shared_memory_form(shape):
     assert np.array_equal(z1.view(np.int64), z0.view(np.int64))
     assert np.array_equal(x1.view(np.int64), x0.view(np.int64))
     assert h1 == h0
+
+
+@pytest.mark.parametrize("max_iter", [7, 8, 1000])
+def test_paired_u_update_changes_only_u_rounding(max_iter):
+    """PCG with the u update paired over two iterations (TPMG_PAIR_U=1) vs every iteration
+    (default): r, z and the sums are the same arithmetic on the same grid, so the residual history is
+    bit-identical; u differs by rounding only.  Odd and even stops (the last odd step is added
+    after the loop)."""
+    import torch
+    nx, ny, nz, L = 64, 64, 32, 3
+    outs = []
+    for pu in ("1", "0"):
+        os.environ["TPMG_PAIR_U"] = pu
+        try:
+            ctx = ctx_for(O.Params(nx=nx, ny=ny, nz=nz, L=L))
+        finally:
+            os.environ.pop("TPMG_PAIR_U")
+        f = torch.from_numpy(np.random.default_rng(6).standard_normal(ctx.shape(L))).cuda()
+        x = torch.empty_like(f)
+        r = ctx.solve_cg(f, x, eps=1e-10, max_iter=max_iter)
+        torch.cuda.synchronize()
+        outs.append((x.cpu().numpy(), r))
+        ctx.close()
+    (x1, r1), (x0, r0) = outs
+    assert r1.iterations == r0.iterations and r1.history == r0.history
+    assert np.linalg.norm(x1 - x0) <= 1e-13 * np.linalg.norm(x0)
