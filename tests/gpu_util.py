@@ -54,3 +54,25 @@ def rel_l2(a, b) -> float:
     a = np.ravel(a); b = np.ravel(b)
     nb = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+
+
+COLF = 50.0   # per-column bar = COLF x the whole-field bar
+
+
+def col_err(a, b) -> float:
+    """Largest error of one vertical column (z-contiguous (ny, nx, nz) arrays), relative to the
+    RMS column norm of b: a wrong tile seam, boundary column or halo row changes a few columns,
+    which the whole-field rel-L2 dilutes by the number of columns (VERDICT r1 weak #9)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if a.ndim != 3:
+        return rel_l2(a, b)
+    d = np.linalg.norm(a - b, axis=2)
+    w = np.linalg.norm(b, axis=2)
+    scale = float(np.sqrt(np.mean(w * w)))
+    return float(d.max() / (scale if scale > 0 else 1.0))
+
+
+def close(got, want, t: float) -> bool:
+    """Whole-field rel-L2 < t AND every column within COLF * t (relative to the RMS column)."""
+    return rel_l2(got, want) < t and col_err(got, want) < COLF * t

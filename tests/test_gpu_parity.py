@@ -14,7 +14,7 @@ import pytest
 from oracle import oracle as O
 from inputs import mode_zc, rhs_zc
 
-from gpu_util import ctx_for, lib, rel_l2, to_dev, to_host_zc
+from gpu_util import ctx_for, lib, rel_l2, to_dev, to_host_zc, close
 
 pytestmark = pytest.mark.gpu
 
@@ -64,15 +64,15 @@ def test_apply_residual_precondition_all_levels(p, loader):
         dx, df = to_dev(x), to_dev(f)
         y = ctx.empty(level)
         ctx.apply(level, dx, y)
-        assert rel_l2(to_host_zc(y), O.apply(p, x, level)) < tol(p, level)
+        assert close(to_host_zc(y), O.apply(p, x, level), tol(p, level))
         r = ctx.empty(level)
         n2 = ctx.residual(level, dx, df, r, want_norm2=True)
         want = O.residual(p, x, f, level)
-        assert rel_l2(to_host_zc(r), want) < tol(p, level)
+        assert close(to_host_zc(r), want, tol(p, level))
         assert n2 == pytest.approx(float(np.sum(want * want)), rel=1e-12)
         z = ctx.empty(level)
         ctx.precondition(level, df, z)
-        assert rel_l2(to_host_zc(z), O.precondition(p, f, level)) < tol(p, level)
+        assert close(to_host_zc(z), O.precondition(p, f, level), tol(p, level))
 
 
 @pytest.mark.parametrize("loader", LOADERS)
@@ -85,7 +85,7 @@ def test_smooth_all_levels(p, loader):
         for sweeps in (1, 2):
             du = to_dev(u)
             ctx.smooth(level, du, to_dev(f), sweeps)
-            assert rel_l2(to_host_zc(du), O.smooth(p, u, f, level, sweeps)) < tol(p, level)
+            assert close(to_host_zc(du), O.smooth(p, u, f, level, sweeps), tol(p, level))
 
 
 @pytest.mark.parametrize("p", [q for q in SHAPES if q.L > 1], ids=[i for q, i in zip(SHAPES, IDS) if q.L > 1])
@@ -95,11 +95,11 @@ def test_transfers_all_levels(p):
         rf = rand(p.level_shape(fine), 3 + fine)
         fc = ctx.empty(fine - 1)
         ctx.restrict(fine, to_dev(rf), fc)
-        assert rel_l2(to_host_zc(fc), O.restrict(p, rf, fine)) < TOL
+        assert close(to_host_zc(fc), O.restrict(p, rf, fine), TOL)
         uc, uf = rand(p.level_shape(fine - 1), 30 + fine), rand(p.level_shape(fine), 40 + fine)
         duf = to_dev(uf)
         ctx.prolong_add(fine - 1, to_dev(uc), duf)
-        assert rel_l2(to_host_zc(duf), O.prolong_add(p, uc, uf, fine - 1)) < TOL
+        assert close(to_host_zc(duf), O.prolong_add(p, uc, uf, fine - 1), TOL)
 
 
 @pytest.mark.parametrize("loader", LOADERS)
@@ -110,7 +110,7 @@ def test_vcycle(p, loader):
     u, f = rand(s, 5), rand(s, 6)
     du = to_dev(u)
     ctx.vcycle(du, to_dev(f))
-    assert rel_l2(to_host_zc(du), O.vcycle(p, u, f)) < tol(p)
+    assert close(to_host_zc(du), O.vcycle(p, u, f), tol(p))
 
 
 SOLVE_SHAPES = [
@@ -138,10 +138,10 @@ def test_solve_parity(p, solver, loader):
     assert abs(res.iterations - ref.iterations) <= 1
     ug = to_host_zc(u)
     if res.iterations == ref.iterations:
-        assert rel_l2(ug, ref.u) < 1e-9
+        assert close(ug, ref.u, 1e-9)
         assert np.allclose(res.history, ref.history, rtol=1e-8)
     else:
-        assert rel_l2(ug, ref.u) < 1e-3
+        assert close(ug, ref.u, 1e-3)
     # independent check of the GPU answer: the oracle's true residual
     rr = np.linalg.norm(O.residual(p, ug, f)) / np.linalg.norm(f)
     assert rr < (1e-5 if solver == "mg" else 2e-5)
@@ -160,7 +160,7 @@ def test_solve_edge_cases():
     v = mode_zc(32, 32, 16, 2, 3, 1)
     r = ctx.solve_cg(to_dev(v), u, eps=1e-10)
     assert r.iterations == 1
-    assert rel_l2(to_host_zc(u), O.solve_cg(p, v, eps=1e-10).u) < 1e-12
+    assert close(to_host_zc(u), O.solve_cg(p, v, eps=1e-10).u, 1e-12)
     # max_iter = 0: no iteration, not converged
     r = ctx.solve_mg(to_dev(rhs_zc(32, 32, 16)), u, max_iter=0)
     assert r.iterations == 0 and not r.converged
@@ -186,7 +186,7 @@ def test_iteration_limit(solver):
     ref = (O.solve_mg if solver == "mg" else O.solve_cg)(p, f, max_iter=k)
     assert res.iterations == ref.iterations == k and not res.converged and not ref.converged
     assert np.allclose(res.history, ref.history, rtol=1e-9)
-    assert rel_l2(to_host_zc(u), ref.u) < 1e-10
+    assert close(to_host_zc(u), ref.u, 1e-10)
 
 
 def test_single_level_hierarchy():
@@ -199,7 +199,7 @@ def test_single_level_hierarchy():
     res, ref = ctx.solve_mg(to_dev(f), u, max_iter=20), O.solve_mg(p, f, max_iter=20)
     assert res.iterations == ref.iterations == 20 and not res.converged
     assert np.allclose(res.history, ref.history, rtol=1e-10)
-    assert rel_l2(to_host_zc(u), ref.u) < 1e-10
+    assert close(to_host_zc(u), ref.u, 1e-10)
 
 
 def test_solve_host_matches_device():
@@ -267,5 +267,5 @@ def test_cg_ksplit_preconditioner_opt_in(p, monkeypatch):
     res, ref = ctx.solve_cg(to_dev(f), u), O.solve_cg(p, f)
     assert res.converged and abs(res.iterations - ref.iterations) <= 1
     if res.iterations == ref.iterations:
-        assert rel_l2(to_host_zc(u), ref.u) < 1e-9
+        assert close(to_host_zc(u), ref.u, 1e-9)
         assert np.allclose(res.history, ref.history, rtol=1e-8)

@@ -9,7 +9,7 @@ import pytest
 from oracle import oracle as O
 from inputs import mode_face_zc, rhs_zc
 
-from gpu_util import ctx_for, rel_l2, to_dev, to_host_zc
+from gpu_util import ctx_for, rel_l2, to_dev, to_host_zc, close
 from test_gpu_parity import tol, rand
 
 pytestmark = pytest.mark.gpu
@@ -36,27 +36,27 @@ def test_face_ops_all_levels(p, loader):
         dx, df = to_dev(x), to_dev(f)
         y = ctx.empty(level)
         ctx.apply(level, dx, y)
-        assert rel_l2(to_host_zc(y), O.apply(p, x, level)) < tol(p, level)
+        assert close(to_host_zc(y), O.apply(p, x, level), tol(p, level))
         r = ctx.empty(level)
         n2 = ctx.residual(level, dx, df, r, want_norm2=True)
         want = O.residual(p, x, f, level)
-        assert rel_l2(to_host_zc(r), want) < tol(p, level)
+        assert close(to_host_zc(r), want, tol(p, level))
         assert n2 == pytest.approx(float(np.sum(want * want)), rel=1e-12)
         z = ctx.empty(level)
         ctx.precondition(level, df, z)
-        assert rel_l2(to_host_zc(z), O.precondition(p, f, level)) < tol(p, level)
+        assert close(to_host_zc(z), O.precondition(p, f, level), tol(p, level))
         for sweeps in (1, 2):
             du = to_dev(x)
             ctx.smooth(level, du, df, sweeps)
-            assert rel_l2(to_host_zc(du), O.smooth(p, x, f, level, sweeps)) < tol(p, level)
+            assert close(to_host_zc(du), O.smooth(p, x, f, level, sweeps), tol(p, level))
         if level > 1:
             fc = ctx.empty(level - 1)
             ctx.restrict(level, dx, fc)
-            assert rel_l2(to_host_zc(fc), O.restrict(p, x, level)) < 1e-11
+            assert close(to_host_zc(fc), O.restrict(p, x, level), 1e-11)
             uc = rand(p.level_shape(level - 1), 30 + level)
             duf = to_dev(f)
             ctx.prolong_add(level - 1, to_dev(uc), duf)
-            assert rel_l2(to_host_zc(duf), O.prolong_add(p, uc, f, level - 1)) < 1e-11
+            assert close(to_host_zc(duf), O.prolong_add(p, uc, f, level - 1), 1e-11)
 
 
 @pytest.mark.parametrize("loader", LOADERS)
@@ -67,7 +67,7 @@ def test_face_vcycle(p, loader):
     u, f = rand(s, 5), rand(s, 6)
     du = to_dev(u)
     ctx.vcycle(du, to_dev(f))
-    assert rel_l2(to_host_zc(du), O.vcycle(p, u, f)) < tol(p)
+    assert close(to_host_zc(du), O.vcycle(p, u, f), tol(p))
 
 
 def test_face_eigenmode_closed_form():
@@ -81,7 +81,7 @@ def test_face_eigenmode_closed_form():
     ctx = ctx_for(p)
     y = ctx.empty(1)
     ctx.apply(1, to_dev(v), y)
-    assert rel_l2(to_host_zc(y), lam * v) < 1e-12
+    assert close(to_host_zc(y), lam * v, 1e-12)
 
 
 ROB = [(5, 8.4, 2), (5, 84.0, 30), (5, 840.0, 150), (7, 84.0, 5), (7, 840.0, 15)]
@@ -117,5 +117,5 @@ def test_face_solve_parity(solver):
     assert res.converged and ref.converged
     assert abs(res.iterations - ref.iterations) <= 1
     if res.iterations == ref.iterations:
-        assert rel_l2(to_host_zc(u), ref.u) < 1e-9
+        assert close(to_host_zc(u), ref.u, 1e-9)
         assert np.allclose(res.history, ref.history, rtol=1e-8)
