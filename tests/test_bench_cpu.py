@@ -54,3 +54,21 @@ def test_reference_arm_two_ranks_rank0_only():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_oracle_counts_and_config_block():
+    """The oracle legs use the oracle's own iteration counts of C2 (tests/golden, written by
+    scripts/oracle_iterations.py) and name the same workload as the GPU arm (round-1 review:
+    the workload name was overwritten by a loop variable)."""
+    sys.path.insert(0, ROOT)
+    import argparse
+    import bench
+    args = argparse.Namespace(nz=128, nu=8.4, levels=5, coarse_sweeps=2, boundary=0, seed=0, profiles=-1,
+                              fields="none", eps=1e-5, solver="both", per_gpu_nx=1024, global_nx=0)
+    mg, cg, src = bench.oracle_counts(args, 1024, 1024)
+    assert (mg, cg) == (10, 54) and "oracle_iterations.json" in src
+    nx, ny, name = bench.workload(args, 1)
+    cfg = bench.config_block(args, nx, ny, name, 1)
+    assert cfg["workload"].startswith("C2") and (cfg["nx"], cfg["ny"], cfg["nz"]) == (1024, 1024, 128)
+    src_text = open(os.path.join(ROOT, "bench.py")).read()
+    assert "for name, sv, on in" not in src_text
