@@ -12,8 +12,11 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 if [ -z "$SKIP_TESTS" ]; then
   timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu_$TAG.log
 fi
-/usr/bin/time -f "wall %e s" timeout 900 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
-/usr/bin/time -f "wall %e s" timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
+t0=$SECONDS; timeout 900 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
+echo "wall $((SECONDS - t0)) s" >> gpurun_out/bench_ref_$TAG.err
+t0=$SECONDS; timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
+echo "wall $((SECONDS - t0)) s" >> gpurun_out/bench_$TAG.err
+[ -n "$SKIP_NCU" ] && exit 0
 BENCH="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 timeout 600 $BENCH > gpurun_out/bench_plain_$TAG.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
