@@ -145,6 +145,8 @@ struct tpmg_ctx {
     bool fuse_prolong = false; // TPMG_FUSE_PROLONG=1: prolongation fused into the post-smooth (k-split);
                                // off by default: measured slower (the in-smem u + P u_c pass
                                // costs more issue slots than the 16 B/cell it saves)
+    int ksplit_cfg_coarse = 0;   // k-split config on levels whose 4x4 tiles do not fill the SMs: 0 = 2x8
+                                 // (r2ac: 0.5% per V-cycle; TPMG_KSPLIT_COARSE=-1 keeps ksplit_cfg)
     int ksplit_cfg = 1;        // k-split config (TPMG_KSPLIT: "0" off, "1" 2x8/2 stages, "2" 4x4/3 stages
                                // (default), "3" 2x4/2 stages); -1 = off
     std::map<std::tuple<uintptr_t, int64_t, int, int64_t, int, int>, CUtensorMap> tmaps;
@@ -703,11 +705,22 @@ bool ksplit_halo_maps(tpmg_ctx* ctx, const HaloField& hf, int64_t nx, int nz, in
     return true;
 }
 
+// k-split configuration of a launch: the context's, or (TPMG_KSPLIT_COARSE=c) config c on the
+// coarse levels whose 4 x 4 tiles do not fill the SMs
+int ksplit_cfg_of(tpmg_ctx* ctx, const LevelConst& lc)
+{
+    if (ctx->ksplit_cfg_coarse >= 0) {
+        const int64_t tiles = ((lc.nx + kTileX - 1) / kTileX) * ((lc.ny + 3) / 4);
+        if (tiles < ctx->num_sms) return ctx->ksplit_cfg_coarse;
+    }
+    return ctx->ksplit_cfg;
+}
+
 bool fill_tma_ksplit(tpmg_ctx* ctx, int mode, LineArgs& a)
 {
     const int64_t nx = a.L.nx, ny = a.L.ny;
     const int nz = a.L.nz;
-    const KsplitBoxes b = ksplit_boxes(mode, ctx->ksplit_cfg);
+    const KsplitBoxes b = ksplit_boxes(mode, ksplit_cfg_of(ctx, a.L));
     if (mode == MODE_SMOOTH || mode == MODE_RESTRICT || mode == MODE_SMOOTH_PROLONG || mode == MODE_CGPREC)
         if (!ksplit_halo_maps(ctx, a.h0, nx, nz, ny, b.hx, b.ty + 2, b.depth, a.tma.h[0])) return false;
     if (mode == MODE_SMOOTH_PROLONG)
@@ -727,8 +740,9 @@ bool ksplit_usable(tpmg_ctx* ctx, int mode, const LevelConst& lc)
     // general vertical profiles: the k-split smoother / preconditioner / restriction only
     if (lc.gen && (mode == MODE_SMOOTH_PROLONG || mode == MODE_CGPREC)) return false;
     if (mode == MODE_CGPREC_D || mode == MODE_CGPREC_P) return false;   // one-thread-per-column kernel only
-    // per-column fields: the one-thread-per-column kernel only (per-column pivots)
-    if (lc.gen == 2) return false;
+    // per-column fields: the one-thread-per-column kernel (per-column pivots), except the
+    // residual->restriction, which has no Thomas solve
+    if (lc.gen == 2 && mode != MODE_RESTRICT) return false;
     // the k-split CG preconditioner is opt-in (TPMG_KSPLIT_CG=1): measured 4% slower per CG
     // iteration than the one-thread-per-column kernel at 1024^2 x 128
     if (mode == MODE_CGPREC && !ctx->ksplit_cg) return false;
@@ -738,7 +752,7 @@ bool ksplit_usable(tpmg_ctx* ctx, int mode, const LevelConst& lc)
 // Tile rows of the kernel run_line will launch for this mode and level.
 int launch_rows(tpmg_ctx* ctx, int mode, const LevelConst& lc)
 {
-    return ksplit_usable(ctx, mode, lc) ? ksplit_boxes(mode, ctx->ksplit_cfg).ty
+    return ksplit_usable(ctx, mode, lc) ? ksplit_boxes(mode, ksplit_cfg_of(ctx, lc)).ty
                                         : line_tile_rows(mode, lc.nz, lc.gen, ctx->tmem && ctx->use_tma);
 }
 
@@ -759,7 +773,7 @@ tpmg_status run_line(tpmg_ctx* ctx, int mode, const LineArgs& a0)
     if (ksplit_usable(ctx, mode, a.L) && fill_tma_ksplit(ctx, mode, a)) {
         ProfScope ps(ctx, mode == MODE_SMOOTH_PROLONG ? TPMG_K_SMOOTH_PROLONG : mode, part_cells(ctx, mode, a));
         const KTables& kt = ctx->lv[level_of(ctx, a.L)].ktab;
-        CUDA_TRY(ctx, launch_line_ksplit(launcher(ctx), mode, ctx->ksplit_cfg, a, kt));
+        CUDA_TRY(ctx, launch_line_ksplit(launcher(ctx), mode, ksplit_cfg_of(ctx, a.L), a, kt));
         if (ctx->sync_debug) {
             cudaError_t e = cudaStreamSynchronize(ctx->stream);
             if (e != cudaSuccess)
@@ -811,7 +825,7 @@ tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, LineArgs a, const 
     const int TY = launch_rows(ctx, mode, lc);
     const int nty = (int)((lc.ny + TY - 1) / TY);
     const bool fused_out = push_out && ctx->fused_push;
-    const bool hw_ok = ksplit_usable(ctx, mode, lc) ? ksplit_halo_wait(mode, ctx->ksplit_cfg, lc.gen)
+    const bool hw_ok = ksplit_usable(ctx, mode, lc) ? ksplit_halo_wait(mode, ksplit_cfg_of(ctx, lc), lc.gen)
                                                     : line_halo_wait(mode, lc.nz, lc.gen, ctx->use_tma, ctx->tmem);
     if (ctx->p2p && ctx->overlap && overlap && !ctx->halo_off && !fused_out && nty >= 3 && hw_ok) {
         // ONE launch: its CTAs walk the interior tile rows first; the loader of a strip-
@@ -1812,6 +1826,9 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->use_tma = !(ld && std::strcmp(ld, "cpasync") == 0);
         const char* ks = std::getenv("TPMG_KSPLIT");
         ctx->ksplit_cfg = !ks ? 1 : ks[0] == '0' ? -1 : ks[0] == '1' ? 0 : ks[0] == '3' ? 2 : 1;
+        const char* ksc = std::getenv("TPMG_KSPLIT_COARSE");   // "0" 2x8 / "2" 2x4 on unfilled levels
+        if (ksc) ctx->ksplit_cfg_coarse = std::max(-1, std::min(2, std::atoi(ksc)));
+        if (ctx->ksplit_cfg < 0) ctx->ksplit_cfg_coarse = -1;
         const char* ov = std::getenv("TPMG_OVERLAP");
         ctx->overlap = !(ov && ov[0] == '0');        // P2P transport: on by default
         ctx->overlap_nccl = ov && ov[0] == '1';      // NCCL transport: opt-in

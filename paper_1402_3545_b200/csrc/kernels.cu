@@ -836,7 +836,7 @@ __global__ void k_restrict(const LevelConst F, const LevelConst Cc, const double
 // neighbourhood is read through L1 (neighbouring threads share it); no integer
 // division in the loop.
 // The work of k_prolong_add; threads outside the grid return early (no barrier here).
-template <bool PUSH>
+template <bool PUSH, int PB>
 __device__ __forceinline__ void prolong_body(const LevelConst& Cc, const LevelConst& F, const HaloField& uc,
                                              double* __restrict__ uf, int lpt, int part, const HaloPush& push,
                                              const HaloWait& hw)
@@ -882,7 +882,6 @@ __device__ __forceinline__ void prolong_body(const LevelConst& Cc, const LevelCo
     double* f1 = f0 + fplane;                        // fine row 2J+1
     // PB levels per step: all loads of the step are issued before its stores (the fine
     // read-modify-write would otherwise serialise on memory latency level by level)
-    constexpr int PB = 2;
     for (int k0 = kbeg; k0 < kend; k0 += PB) {
         double2 fv[PB][2];
         double cc[PB][3][3];
@@ -932,7 +931,7 @@ __device__ __forceinline__ void prolong_body(const LevelConst& Cc, const LevelCo
 
 }
 
-template <bool PUSH>
+template <bool PUSH, int PB = 2>   // PB: levels per load batch (4 measured slower, r2ac)
 __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const LevelConst F, const HaloField uc,
                                                      double* __restrict__ uf, int lpt, const int* skip, int part,
                                                      const HaloPush push, const HaloWait hw)
@@ -940,7 +939,7 @@ __global__ void __launch_bounds__(128) k_prolong_add(const LevelConst Cc, const 
     pdl_wait();
     pdl_trigger();
     if (skip && *skip) return;
-    prolong_body<PUSH>(Cc, F, uc, uf, lpt, part, push, hw);
+    prolong_body<PUSH, PB>(Cc, F, uc, uf, lpt, part, push, hw);
 }
 
 
