@@ -240,6 +240,17 @@ tpmg_status tpmg_solve_host(tpmg_ctx *ctx, tpmg_solver solver, const double *f_h
                             double *u_host, double eps, int32_t max_iter,
                             tpmg_result *result);
 
+/* Both solvers on one host right-hand side -- the benchmark's step (an MG solve and a PCG
+ * solve of the same f, BASELINE.json): f is copied in ONCE, the MG solve runs into a device
+ * buffer, its solution's device->host copy runs on a separate copy stream while the PCG solve
+ * computes, then the PCG solution is copied out.  Host buffers as tpmg_solve_host (pinned for
+ * the overlap; pageable still works, without it); results for each solver (either may be
+ * NULL).  max_iter_mg / max_iter_cg as tpmg_solve_mg / tpmg_solve_cg.  COLLECTIVE; returns
+ * after both copies have completed. */
+tpmg_status tpmg_solve_host_pair(tpmg_ctx *ctx, const double *f_host, double *u_mg_host, double *u_cg_host,
+                                 double eps, int32_t max_iter_mg, int32_t max_iter_cg, tpmg_result *res_mg,
+                                 tpmg_result *res_cg);
+
 /* Layout conversion (the fields are z-contiguous on the host, "transposing the fields
  * from a z-contiguous data format on the host to the x-contiguous format ... on the GPU").
  * z-contiguous: idx = (j*nx + i)*nz + k (columns contiguous, the CPU ordering of P:59);

@@ -82,6 +82,9 @@ struct tpmg_ctx {
     double *cg_r = nullptr, *cg_z = nullptr, *cg_p[2] = {nullptr, nullptr};
     double *cg_zlo = nullptr, *cg_zhi = nullptr, *cg_plo[2] = {nullptr, nullptr}, *cg_phi[2] = {nullptr, nullptr};
     double *host_f = nullptr, *host_u = nullptr;  // device buffers for tpmg_solve_host
+    double* host_u2 = nullptr;                     // ... the second solution of tpmg_solve_host_pair
+    cudaStream_t copy_stream = nullptr;            // tpmg_solve_host_pair's overlapped device->host copy
+    cudaEvent_t ev_copy = nullptr;
     ncclComm_t comm = nullptr;
     // halo channels (nranks > 1): 1..L = levels, L+1 = CG z.  Each has double-buffered slabs
     // in one pool allocation; in P2P mode the neighbours write into them over NVLink.
@@ -740,9 +743,9 @@ bool ksplit_usable(tpmg_ctx* ctx, int mode, const LevelConst& lc)
     // general vertical profiles: the k-split smoother / preconditioner / restriction only
     if (lc.gen && (mode == MODE_SMOOTH_PROLONG || mode == MODE_CGPREC)) return false;
     if (mode == MODE_CGPREC_D || mode == MODE_CGPREC_P) return false;   // one-thread-per-column kernel only
-    // per-column fields: the one-thread-per-column kernel (per-column pivots), except the
-    // residual->restriction, which has no Thomas solve
-    if (lc.gen == 2 && mode != MODE_RESTRICT) return false;
+    // per-column fields: the one-thread-per-column kernel (per-column pivots; a k-split
+    // residual->restriction with the face-weighted stencil measured slower, r2ad: 703 vs 642 us)
+    if (lc.gen == 2) return false;
     // the k-split CG preconditioner is opt-in (TPMG_KSPLIT_CG=1): measured 4% slower per CG
     // iteration than the one-thread-per-column kernel at 1024^2 x 128
     if (mode == MODE_CGPREC && !ctx->ksplit_cg) return false;
@@ -1598,7 +1601,9 @@ void ctx_free(tpmg_ctx* ctx)
     cudaFree(ctx->cg_r); cudaFree(ctx->cg_z); cudaFree(ctx->cg_p[0]); cudaFree(ctx->cg_p[1]);
     // cg_zlo / cg_zhi and the level slabs live in the halo pool
     for (int q = 0; q < 2; ++q) { cudaFree(ctx->cg_plo[q]); cudaFree(ctx->cg_phi[q]); }
-    cudaFree(ctx->host_f); cudaFree(ctx->host_u);
+    cudaFree(ctx->host_f); cudaFree(ctx->host_u); cudaFree(ctx->host_u2);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
     if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
     cudaFree(ctx->d_flags);
     if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
@@ -2121,6 +2126,35 @@ tpmg_status tpmg_solve_host(tpmg_ctx* ctx, tpmg_solver solver, const double* f_h
                                                 : tpmg_solve_cg(ctx, ctx->host_f, ctx->host_u, eps, max_iter, res);
     if (st != TPMG_OK) return st;
     CUDA_TRY(ctx, cudaMemcpyAsync(u_host, ctx->host_u, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return TPMG_OK;
+}
+
+tpmg_status tpmg_solve_host_pair(tpmg_ctx* ctx, const double* f_host, double* u_mg_host, double* u_cg_host,
+                                 double eps, int32_t max_iter_mg, int32_t max_iter_cg, tpmg_result* res_mg,
+                                 tpmg_result* res_cg)
+{
+    if (ctx) begin_call(ctx);
+    if (!ctx) return TPMG_E_PARAM;
+    if (!f_host || !u_mg_host || !u_cg_host) return fail(ctx, TPMG_E_PARAM, "tpmg_solve_host_pair: NULL buffer");
+    const size_t n = ctx->lv[ctx->L].n();
+    TRY(dev_alloc(ctx, &ctx->host_f, n));
+    TRY(dev_alloc(ctx, &ctx->host_u, n));
+    TRY(dev_alloc(ctx, &ctx->host_u2, n));
+    if (!ctx->copy_stream) {
+        CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
+    }
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_f, f_host, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    TRY(tpmg_solve_mg(ctx, ctx->host_f, ctx->host_u, eps, max_iter_mg, res_mg));
+    // u_mg leaves on the copy engine while the PCG solve computes (its last writer is ordered by
+    // the event; the PCG solve writes host_u2, not host_u)
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_copy, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_copy, 0));
+    CUDA_TRY(ctx, cudaMemcpyAsync(u_mg_host, ctx->host_u, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->copy_stream));
+    TRY(tpmg_solve_cg(ctx, ctx->host_f, ctx->host_u2, eps, max_iter_cg, res_cg));
+    CUDA_TRY(ctx, cudaMemcpyAsync(u_cg_host, ctx->host_u2, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->copy_stream));
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     return TPMG_OK;
 }

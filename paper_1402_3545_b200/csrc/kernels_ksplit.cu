@@ -174,7 +174,6 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
     // per-level tables, staged in shared memory (warp-uniform broadcast reads)
     for (int q = tid; q < 6 * nz; q += NT) tab[q] = T.t[q / nz][q % nz];   // interior class (0)
     const double c0 = a.L.c, gamma = a.L.gamma, rho = a.rho, scale = a.scale;
-    const bool fld = GEN && a.L.gen >= 2;   // per-column fields (MODE_RESTRICT)
     if (tid == 0) {
         for (int q = 0; q < NS2; ++q) mbar_init(&full_bar[q], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -246,20 +245,6 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
         // halo rows of this warp's row j kept in the slab slots (layout without in-place rows)
         const bool s_slab = G::SROW && a.tma.h[0].has_lo && j0 == 0 && ty == 0;
         const bool n_slab = G::SROW && a.tma.h[0].has_hi && (j0 + ty + 1 == ny);
-        // per-column fields (the residual->restriction only): |T|, alpha_T, face alphas
-        double fT = 1.0, faT = 0.0, fw = 0.0, fe = 0.0, fs = 0.0, fn = 0.0;
-        if constexpr (GEN && MODE == MODE_RESTRICT) {
-            if (fld && valid) {
-                const int64_t ncol = nx * ny;
-                const double* F = a.L.fld + j * nx + i;
-                fT = __ldg(F);
-                faT = __ldg(F + ncol);
-                fw = __ldg(F + 2 * ncol);
-                fe = __ldg(F + 3 * ncol);
-                fs = __ldg(F + 4 * ncol);
-                fn = __ldg(F + 5 * ncol);
-            }
-        }
 
         double yv[THOMAS ? SL : 1];
         double yprev = 0.0;
@@ -307,22 +292,9 @@ __global__ void __launch_bounds__(32 * TY * NSEG, 1) k_linek(const __grid_consta
                     const int dd = kk + 1;                 // box level of k = k0 + kk
                     const int k = s * SL + cc * KB + kk;
                     const double uu = rc[(dd + 1) * HX];
-                    double S = (rc[dd * HX - 1] + rc[dd * HX + 1]) + (rs[dd * HX] + rn[dd * HX]);
-                    double Mu, c = c0;                                          // (M_T u)_k; A u = Mu - c S
-                    if constexpr (GEN && MODE == MODE_RESTRICT) {
-                        if (fld) {   // per-column fields: A_T = |T|(diag(a) + tridiag(-(b+c), b, c)) - alpha_T diag(d),
-                                     // neighbours weighted by the face alpha_{T,T'}
-                            const double* pr = a.L.prof;   // [a-b-c][b][c][d]
-                            const double dk = __ldg(pr + 3 * nz + k);
-                            const double dgk = fma(fT, __ldg(pr + k), -faT * dk);
-                            Mu = fma(fT * __ldg(pr + nz + k), ud, fma(fT * __ldg(pr + 2 * nz + k), uu, dgk * uc));
-                            S = fma(fw, rc[dd * HX - 1], fe * rc[dd * HX + 1]) + fma(fs, rs[dd * HX], fn * rn[dd * HX]);
-                            c = -dk;
-                        } else {
-                            Mu = fma(__ldg(a.L.prof + k), ud, fma(__ldg(a.L.prof + nz + k), uu, diag[k] * uc));
-                            c = __ldg(a.L.prof + 2 * nz + k);
-                        }
-                    } else if constexpr (GEN) {   // general vertical profiles: b_k, c_k, c_l d_k
+                    const double S = (rc[dd * HX - 1] + rc[dd * HX + 1]) + (rs[dd * HX] + rn[dd * HX]);
+                    double Mu, c = c0;                                          // (M_T u)_k
+                    if constexpr (GEN) {   // general vertical profiles: b_k, c_k, c_l d_k
                         Mu = fma(__ldg(a.L.prof + k), ud, fma(__ldg(a.L.prof + nz + k), uu, diag[k] * uc));
                         c = __ldg(a.L.prof + 2 * nz + k);
                     } else {

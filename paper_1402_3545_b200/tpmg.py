@@ -80,6 +80,7 @@ _SIGS = {
     "tpmg_set_profiles": ([_vp, _P(_d), _P(_d), _P(_d), _P(_d)], C.c_int),
     "tpmg_set_fields": ([_vp, _P(_d), _P(_d), _P(_d)], C.c_int),
     "tpmg_profile_read": ([_vp, _i32, _P(_i64), _P(_d), _P(_d)], C.c_int),
+    "tpmg_solve_host_pair": ([_vp, _vp, _vp, _vp, _d, _i32, _i32, _P(tpmg_result), _P(tpmg_result)], C.c_int),
     "tpmg_halo_push": ([_vp, _i32, _vp, _vp, _vp], C.c_int),
     "tpmg_cg_halo": ([_vp, _d, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "tpmg_last_error": ([_vp], C.c_char_p),
@@ -335,6 +336,28 @@ def tpmg_cg_halo(ctx: int, beta: float, out_lo=None, z_lo=None, p_lo=None, out_h
     _check(_lib.tpmg_cg_halo(ctx, float(beta), *args), ctx)
 
 
+def tpmg_solve_host_pair(ctx: int, f_host, u_mg_host, u_cg_host, eps: float = 1e-5, max_iter_mg: int = 50,
+                         max_iter_cg: int = 1000):
+    """MG and PCG solves of one host RHS: f copied in once, u_mg's copy out overlapping the PCG
+    solve.  Host buffers as tpmg_solve_host.  Returns (SolveResult mg, SolveResult cg)."""
+    import torch
+    n = _level_numel(ctx, _fine(ctx))
+
+    def hptr(x):
+        if isinstance(x, int):
+            return x
+        if not isinstance(x, torch.Tensor) or x.device.type != "cpu" or not x.is_contiguous():
+            raise ValueError("host buffers must be contiguous CPU tensors")
+        if x.dtype != torch.float64 or x.numel() != n:
+            raise ValueError(f"host buffers must be float64 with {n} elements (got {x.dtype}, {x.numel()})")
+        return x.data_ptr()
+    rm, hm = _result(max_iter_mg)
+    rc, hc = _result(max_iter_cg)
+    _check(_lib.tpmg_solve_host_pair(ctx, hptr(f_host), hptr(u_mg_host), hptr(u_cg_host), eps, max_iter_mg,
+                                     max_iter_cg, C.byref(rm), C.byref(rc)), ctx)
+    return _to_py(rm, hm), _to_py(rc, hc)
+
+
 def tpmg_get_stats(ctx: int) -> dict:
     s = tpmg_stats()
     _check(_lib.tpmg_get_stats(ctx, C.byref(s)), ctx)
@@ -477,6 +500,9 @@ class Context:
 
     def solve_host(self, solver, f_host, u_host, eps=1e-5, max_iter=1000):
         return tpmg_solve_host(self.handle, solver, f_host, u_host, eps, max_iter)
+
+    def solve_host_pair(self, f_host, u_mg_host, u_cg_host, eps=1e-5, max_iter_mg=50, max_iter_cg=1000):
+        return tpmg_solve_host_pair(self.handle, f_host, u_mg_host, u_cg_host, eps, max_iter_mg, max_iter_cg)
 
     def solve_host_zc(self, solver, f_host, u_host, eps=1e-5, max_iter=1000):
         return tpmg_solve_host_zc(self.handle, solver, f_host, u_host, eps, max_iter)
