@@ -217,6 +217,27 @@ def test_solve_host_matches_device():
     assert torch.equal(uh, u.cpu())
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+def test_solve_host_pair_matches_device(pinned):
+    """tpmg_solve_host_pair (the e2e step: f in once, the MG solution's copy overlapping the
+    PCG solve) returns exactly the device solves' results, with pinned or pageable buffers."""
+    p = O.Params(nx=64, ny=64, nz=32)
+    ctx = ctx_for(p)
+    import torch
+    f = rhs_zc(64, 64, 32, seed=10)
+    fh = torch.from_numpy(O.to_lambda(f))
+    um, uc = torch.full_like(fh, float("nan")), torch.full_like(fh, float("nan"))
+    if pinned:
+        fh, um, uc = fh.pin_memory(), um.pin_memory(), uc.pin_memory()
+    rm, rc = ctx.solve_host_pair(fh, um, uc)
+    dm, dc = ctx.empty(p.L), ctx.empty(p.L)
+    rdm = ctx.solve_mg(fh.cuda(), dm)
+    rdc = ctx.solve_cg(fh.cuda(), dc)
+    assert (rm.iterations, rc.iterations) == (rdm.iterations, rdc.iterations) and rm.converged and rc.converged
+    assert torch.equal(um, dm.cpu()) and torch.equal(uc, dc.cpu())
+    assert close(O.from_lambda(uc.numpy()), O.solve_cg(p, f).u, 1e-9)
+
+
 def test_native_kernels_launched():
     p = O.Params(nx=32, ny=32, nz=16)
     ctx = ctx_for(p)
