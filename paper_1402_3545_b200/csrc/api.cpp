@@ -139,6 +139,7 @@ struct tpmg_ctx {
     struct ProfRec { int cls; double cells; cudaEvent_t a, b; const int* skip; };
     std::vector<ProfRec> prof_pending;
     int dbg = 0;                        // LineArgs::dbg (timing experiments)
+    int band_w = 32;                    // k_line tile bands on wide grids (TPMG_BAND=0: row by row)
     bool prof_detail = false;           // TPMG_PROF_DETAIL=1: per-level breakdown on stderr at tpmg_destroy
     std::map<std::pair<int, double>, std::pair<int64_t, double>> prof_by_size;
     std::vector<cudaEvent_t> prof_pool;
@@ -512,6 +513,7 @@ LineArgs line_args(tpmg_ctx* ctx, int level)
     a.red = ReduceSlot{ctx->d_partials, ctx->d_ticket, nullptr, 0};
     a.skip = ctx->skip;
     a.dbg = ctx->dbg;
+    a.band_w = ctx->band_w;
     a.im = (ctx->lv[level].lc.gen >= 2 && ctx->lv[level].im_ok) ? ctx->lv[level].d_im : nullptr;
     return a;
 }
@@ -1853,6 +1855,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->sync_debug = sd && sd[0] == '1';
         const char* tm = std::getenv("TPMG_TMEM");   // "0": g' of the column kernels in shared memory
         ctx->tmem = !(tm && tm[0] == '0');
+        const char* bnd = std::getenv("TPMG_BAND");
+        if (bnd) ctx->band_w = std::max(0, std::atoi(bnd));
         const char* dpr = std::getenv("TPMG_DBG_PERROW");
         ctx->dbg = (dpr && dpr[0] == '1') ? 1 : 0;
         const char* pdt = std::getenv("TPMG_PROF_DETAIL");

@@ -273,11 +273,25 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     int p_count = 0, p_ch = 0, p_slot = 0, p_tile = blockIdx.x;
     const bool plo = a.push.dst_lo != nullptr, phi = a.push.dst_hi != nullptr;
     const int nrows = part_rows(a.part, nty);
-    auto row_of = [&](int t) {
-        if constexpr (HW) return boundary_deferred_row(t / ntx, nrows, kHaloDefer);   // in-kernel halo wait
-        return part_row(a.part, nty, push_row(t / ntx, nrows, plo, phi));
+    // Wide grids (a.band_w > 0 tile columns per band, ntx > band_w): the tiles are walked band by
+    // band, so the CTAs working at any moment cover a band_w-tile-wide strip several tile rows
+    // deep -- vertically adjacent tiles (which share halo rows) are in flight together and the
+    // halo rows are re-read from L2, as on a 1024-wide grid (round 1: 2.1x the algorithmic
+    // reads at nx = 4096 without it).
+    const int bw = (a.band_w > 0 && ntx > a.band_w) ? a.band_w : ntx;
+    auto col_of = [&](int t) {
+        const int b = t / (bw * nrows), rt = t - b * bw * nrows, w = min(bw, ntx - b * bw);
+        return b * bw + rt % w;
     };
-    int p_i0 = (p_tile % ntx) * TX, p_j0 = row_of(p_tile) * TY;
+    auto raw_row = [&](int t) {
+        const int b = t / (bw * nrows), rt = t - b * bw * nrows, w = min(bw, ntx - b * bw);
+        return rt / w;
+    };
+    auto row_of = [&](int t) {
+        if constexpr (HW) return boundary_deferred_row(raw_row(t), nrows, kHaloDefer);   // in-kernel halo wait
+        return part_row(a.part, nty, push_row(raw_row(t), nrows, plo, phi));
+    };
+    int p_i0 = col_of(p_tile) * TX, p_j0 = row_of(p_tile) * TY;
     auto issue = [&]() {
         if (p_count < total) {
             double* st = stage + p_slot * G::STAGE;
@@ -296,7 +310,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             if (++p_ch == nch) {
                 p_ch = 0;
                 p_tile += gridDim.x;
-                p_i0 = (p_tile % ntx) * TX;
+                p_i0 = col_of(p_tile) * TX;
                 p_j0 = row_of(p_tile) * TY;
             }
         }
@@ -329,7 +343,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     auto tile_body = [&](auto bnd_t, int tl) {
         constexpr bool BND = decltype(bnd_t)::value;
         const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
-        const int64_t i0 = (int64_t)(tile % ntx) * TX, j0 = (int64_t)row_of(tile) * TY;
+        const int64_t i0 = (int64_t)col_of(tile) * TX, j0 = (int64_t)row_of(tile) * TY;
         const int64_t i = i0 + tx, j = j0 + ty;
         const bool valid = (i < nx) && (j < ny);
         const int64_t colbase = j * nx * (int64_t)nz + i;  // + k*nx
@@ -698,7 +712,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     };
     for (int tl = 0; tl < my_tiles; ++tl) {
         const int tile = (int)blockIdx.x + tl * (int)gridDim.x;
-        if (GEN < 2 && tile_on_boundary(a.L, (int64_t)(tile % ntx) * TX, (int64_t)row_of(tile) * TY, TX, TY))
+        if (GEN < 2 && tile_on_boundary(a.L, (int64_t)col_of(tile) * TX, (int64_t)row_of(tile) * TY, TX, TY))
             tile_body(std::true_type{}, tl);
         else
             tile_body(std::false_type{}, tl);
@@ -760,7 +774,7 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
     // rows from HBM (2.1x the algorithmic reads at 4096 x 1024 x 128, ncu); one CTA per SM
     // avoids it.  Measured (TB/s, 2 vs 1 CTA/SM): nx = 1024: 4.8-5.0 vs 4.7-4.8;
     // nx = 2048: 4.0 vs 4.8; nx = 4096: 3.5 vs 4.7.
-    if (MODE == MODE_CGDIR && a.L.nx > 32 * TX) per_sm = 1;
+    if (MODE == MODE_CGDIR && a.L.nx > 32 * TX && a.band_w <= 0) per_sm = 1;
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, ln.num_sms - ln.reserve_sms) * per_sm);
     if (grid <= 0) return cudaSuccess;
     return launch_kernel(ln, kern, dim3((unsigned)grid), dim3(TX * TY), smem, a);

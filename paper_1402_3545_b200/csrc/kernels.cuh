@@ -191,6 +191,7 @@ struct LineArgs {
     int part;          // TilePart: which tile rows this launch covers
     HaloPush push;     // fused halo push of the output (dst == nullptr: none)
     HaloWait hw;       // in-kernel wait for the halo'd input's slabs (P2P overlap)
+    int band_w;        // k_line: tile columns per band on wide grids (0: row by row)
     int dbg;           // debug experiments: bit 0 = k-split in-place boxes row by row (TPMG_DBG_PERROW)
     const double* im;  // per-column fields: 1/m_k of every column's line block (Lambda layout, this
                        // level), precomputed once per operator (launch_pivots); the Thomas modes then
