@@ -139,7 +139,10 @@ struct tpmg_ctx {
     struct ProfRec { int cls; double cells; cudaEvent_t a, b; const int* skip; };
     std::vector<ProfRec> prof_pending;
     int dbg = 0;                        // LineArgs::dbg (timing experiments)
-    int band_w = 32;                    // k_line tile bands on wide grids (TPMG_BAND=0: row by row)
+    int tma_promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;   // TMA L2 promotion (TPMG_TMA_PROMO 0..3: none, 64, 128, 256 B)
+    int l2hint = 3;                     // k_line TMA L2 policies (TPMG_L2HINT bits: 1 halo'd evict_last, 2 plain evict_first; r2aj/r2ak)
+    int cgdir_ctas = 0;                 // k_line<CGDIR> CTAs per SM (TPMG_CGDIR_CTAS; 0 automatic)
+    int band_w = 0;                     // k_line tile bands on wide grids (TPMG_BAND=n; r2ag: slower, off)
     bool prof_detail = false;           // TPMG_PROF_DETAIL=1: per-level breakdown on stderr at tpmg_destroy
     std::map<std::pair<int, double>, std::pair<int64_t, double>> prof_by_size;
     std::vector<cudaEvent_t> prof_pool;
@@ -514,6 +517,8 @@ LineArgs line_args(tpmg_ctx* ctx, int level)
     a.skip = ctx->skip;
     a.dbg = ctx->dbg;
     a.band_w = ctx->band_w;
+    a.l2hint = ctx->l2hint;
+    a.cgdir_ctas = ctx->cgdir_ctas;
     a.im = (ctx->lv[level].lc.gen >= 2 && ctx->lv[level].im_ok) ? ctx->lv[level].d_im : nullptr;
     return a;
 }
@@ -630,7 +635,7 @@ bool tensor_map(tpmg_ctx* ctx, const double* base, int64_t nx, int nz, int64_t n
     cuuint32_t estr[3] = {1, 1, 1};
     CUtensorMap m;
     CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, (CUtensorMapL2promotion)ctx->tma_promo,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return false;
     if (ctx->tmaps.size() > 4096) ctx->tmaps.clear();
@@ -655,7 +660,7 @@ void fill_tma(tpmg_ctx* ctx, int mode, LineArgs& a)
     const int64_t nx = a.L.nx, ny = a.L.ny;
     const int nz = a.L.nz;
     if (nx % 2) return;
-    const int TY = line_tile_rows(mode, nz, a.L.gen, ctx->tmem);
+    const int TY = line_tile_rows(mode, nz, a.L.gen, ctx->tmem, nx);
     int nh, np;
     mode_fields(mode, &nh, &np);
     const HaloField* H[2] = {&a.h0, &a.h1};
@@ -758,7 +763,7 @@ bool ksplit_usable(tpmg_ctx* ctx, int mode, const LevelConst& lc)
 int launch_rows(tpmg_ctx* ctx, int mode, const LevelConst& lc)
 {
     return ksplit_usable(ctx, mode, lc) ? ksplit_boxes(mode, ksplit_cfg_of(ctx, lc)).ty
-                                        : line_tile_rows(mode, lc.nz, lc.gen, ctx->tmem && ctx->use_tma);
+                                        : line_tile_rows(mode, lc.nz, lc.gen, ctx->tmem && ctx->use_tma, lc.nx);
 }
 
 // Fraction of the level's cells a launch covers (interior / boundary tile rows).
@@ -1857,6 +1862,12 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->tmem = !(tm && tm[0] == '0');
         const char* bnd = std::getenv("TPMG_BAND");
         if (bnd) ctx->band_w = std::max(0, std::atoi(bnd));
+        const char* tpr = std::getenv("TPMG_TMA_PROMO");
+        if (tpr) ctx->tma_promo = std::min(3, std::max(0, std::atoi(tpr)));
+        const char* l2h = std::getenv("TPMG_L2HINT");
+        if (l2h) ctx->l2hint = std::atoi(l2h) & 3;
+        const char* cdc = std::getenv("TPMG_CGDIR_CTAS");
+        if (cdc) ctx->cgdir_ctas = std::max(0, std::atoi(cdc));
         const char* dpr = std::getenv("TPMG_DBG_PERROW");
         ctx->dbg = (dpr && dpr[0] == '1') ? 1 : 0;
         const char* pdt = std::getenv("TPMG_PROF_DETAIL");

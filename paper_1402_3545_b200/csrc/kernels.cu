@@ -122,8 +122,13 @@ __device__ __forceinline__ void load_stage(double* st, const LineArgs& a, int64_
 // memory is identical to load_stage's: halo field f, row r, level kk, x.
 template <int NH, int NP, int TY>
 __device__ __forceinline__ void tma_stage(double* st, const LineArgs& a, int64_t i0, int64_t j0, int k0,
-                                          uint64_t* bar)
+                                          uint64_t* bar, uint64_t pol_h = 0, uint64_t pol_q = 0)
 {
+    // a.l2hint: the main boxes carry an L2 policy (pol_h for the halo'd fields, pol_q for the plain ones)
+    auto load_h = [&](double* dst, const CUtensorMap* m, int x, int y, int z) {
+        if (a.l2hint & 1) tma_load_3d_hint(dst, m, x, y, z, bar, pol_h);
+        else tma_load_3d(dst, m, x, y, z, bar);
+    };
     using G = Geom<NH, NP, TY>;
     mbar_expect_tx(bar, (uint32_t)(G::STAGE * sizeof(double)));
     const int64_t ny = a.L.ny;
@@ -134,7 +139,7 @@ __device__ __forceinline__ void tma_stage(double* st, const LineArgs& a, int64_t
         double* dst = st + f * G::HY * G::HALO_ROW;
         const bool lo = M.has_lo && j0 == 0, hi = M.has_hi && j0 + TY >= ny;
         if (!lo && !hi) {
-            tma_load_3d(dst, &M.main, x0, k0, (int)j0 - 1, bar);
+            load_h(dst, &M.main, x0, k0, (int)j0 - 1);
         } else if (M.has_m1 && lo != hi && (lo || j0 + TY == ny)) {   // (a ragged last row: row by row)
             // strip-boundary tile: the in-domain rows as one box, the slab row by itself (a
             // row-by-row tile is several times slower and its CTA sets the kernel time)
@@ -157,8 +162,10 @@ __device__ __forceinline__ void tma_stage(double* st, const LineArgs& a, int64_t
         }
     }
 #pragma unroll
-    for (int f = 0; f < NP; ++f)
-        tma_load_3d(st + G::PLAIN_BASE + f * TY * KB * TX, &a.tma.q[f], (int)i0, k0, (int)j0, bar);
+    for (int f = 0; f < NP; ++f) {
+        if (a.l2hint & 2) tma_load_3d_hint(st + G::PLAIN_BASE + f * TY * KB * TX, &a.tma.q[f], (int)i0, k0, (int)j0, bar, pol_q);
+        else tma_load_3d(st + G::PLAIN_BASE + f * TY * KB * TX, &a.tma.q[f], (int)i0, k0, (int)j0, bar);
+    }
 }
 
 // The line kernel.  LOADER = 0: cp.async (all threads); 1: TMA (thread 0) with an
@@ -292,6 +299,12 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
         return part_row(a.part, nty, push_row(raw_row(t), nrows, plo, phi));
     };
     int p_i0 = col_of(p_tile) * TX, p_j0 = row_of(p_tile) * TY;
+    uint64_t pol_h = 0, pol_q = 0;
+    if constexpr (LOADER == 1)
+        if (tid == 0 && a.l2hint) {
+            pol_h = l2_policy_evict_last();
+            pol_q = l2_policy_evict_first();
+        }
     auto issue = [&]() {
         if (p_count < total) {
             double* st = stage + p_slot * G::STAGE;
@@ -302,7 +315,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             } else {
                 if (tid == 0) {
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                    tma_stage<NH, NP, TY>(st, a, p_i0, p_j0, p_ch * KB, &full_bar[p_slot]);
+                    tma_stage<NH, NP, TY>(st, a, p_i0, p_j0, p_ch * KB, &full_bar[p_slot], pol_h, pol_q);
                 }
             }
             ++p_count;
@@ -770,11 +783,11 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
     if (TM) per_sm = std::min<int>(per_sm, std::min<int>(ln.tm_ctas, 512 / kTmemCols));   // resident CTAs must all get their TMEM
     if (GEN == 3) per_sm = 1;   // 512 TMEM columns per CTA
     const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * part_rows(a.part, (int)((a.L.ny + TY - 1) / TY));
-    // CG direction (two halo'd fields): on wide grids two CTAs per SM re-read the halo
-    // rows from HBM (2.1x the algorithmic reads at 4096 x 1024 x 128, ncu); one CTA per SM
-    // avoids it.  Measured (TB/s, 2 vs 1 CTA/SM): nx = 1024: 4.8-5.0 vs 4.7-4.8;
-    // nx = 2048: 4.0 vs 4.8; nx = 4096: 3.5 vs 4.7.
-    if (MODE == MODE_CGDIR && a.L.nx > 32 * TX && a.band_w <= 0) per_sm = 1;
+    // CG direction (two halo'd fields) with 4-row tiles: on wide grids two CTAs per SM
+    // re-read the halo rows from HBM (2.1x the algorithmic reads at 4096 x 1024 x 128, ncu),
+    // so one CTA per SM there (the 8-row default fits one CTA per SM anyway).
+    if (MODE == MODE_CGDIR && a.L.nx > 32 * TX && a.cgdir_ctas == 0) per_sm = 1;
+    if (MODE == MODE_CGDIR && a.cgdir_ctas > 0) per_sm = std::min(per_sm, a.cgdir_ctas);
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, ln.num_sms - ln.reserve_sms) * per_sm);
     if (grid <= 0) return cudaSuccess;
     return launch_kernel(ln, kern, dim3((unsigned)grid), dim3(TX * TY), smem, a);
@@ -786,6 +799,8 @@ cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
     if (a.hw.flag[0] || a.hw.flag[1]) {   // P2P overlap with the in-kernel halo wait (line_halo_wait())
         if constexpr (TY == 4 && (MODE == MODE_CGDIR || MODE == MODE_RESTRICT))
             if (!a.L.gen && a.use_tma) return launch_line_l<MODE, 4, 1, 0, 0, true>(ln, a);
+        if constexpr (TY == 8 && MODE == MODE_CGDIR)
+            if (!a.L.gen && a.use_tma) return launch_line_l<MODE, 8, 1, 0, 0, true>(ln, a);
         if constexpr (TY == 4 && MODE == MODE_SMOOTH)
             if (!a.L.gen && a.use_tma && ln.tmem && a.L.nz <= (int)(kTmemCols / 2))
                 return launch_line_l<MODE, 4, 1, 0, 3, true>(ln, a);
@@ -1168,13 +1183,24 @@ bool line_halo_wait(int mode, int nz, int gen, bool use_tma, bool tmem)
 int line_launch_rows(int mode, int nz, int nx, int use_tma, int ksplit_cfg)
 {
     if (use_tma && ksplit_cfg >= 0 && ksplit_supported(mode, nz, nx)) return ksplit_boxes(mode, ksplit_cfg).ty;
-    return line_tile_rows(mode, nz, 0);
+    return line_tile_rows(mode, nz, 0, false, nx);
 }
 
 bool line_gen_fits(int nz, int gen) { return line_smem_bytes<MODE_CGPREC, 1>(nz, gen) <= kMaxSmem; }
 
-int line_tile_rows(int mode, int nz, int gen, bool tm)
+// CG direction tile rows: 8 (one 8-warp CTA per SM: the warps of two 4-row CTAs, one halo
+// box for both -- (TY+2)/TY = 1.25 instead of 1.5 halo rows per row, and no second CTA
+// re-reading the halo rows on wide grids).  r2ak, TB/s under the power cap, 8 vs 4 rows:
+// nx = 1024 5.84 vs 5.46; 2048 5.78 vs 4.31; 4096 5.63 vs 4.21.  TPMG_CGDIR_TY=4: 4 rows.
+static int cgdir_rows(int64_t)
 {
+    const char* e = std::getenv("TPMG_CGDIR_TY");   // (read per call: the tests switch it per context)
+    return (e && std::atoi(e) == 4) ? 4 : 8;
+}
+
+int line_tile_rows(int mode, int nz, int gen, bool tm, int64_t nx)
+{
+    if (mode == MODE_CGDIR) return cgdir_rows(nx);
     // the Tensor Memory form of the Thomas modes always runs 4 tile rows (the lane quarters)
     if (tm && nz <= (int)(kTmemCols / 2) && (mode == MODE_PREC || mode == MODE_SMOOTH || is_cgprec(mode))) return 4;
     switch (mode) {
@@ -1202,7 +1228,7 @@ cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a)
     case MODE_RESID: return launch_line_t<MODE_RESID, 4>(ln, a);
     case MODE_PREC: return launch_line_ty<MODE_PREC>(ln, a);
     case MODE_SMOOTH: return launch_line_ty<MODE_SMOOTH>(ln, a);
-    case MODE_CGDIR: return launch_line_t<MODE_CGDIR, 4>(ln, a);
+    case MODE_CGDIR: return cgdir_rows(a.L.nx) == 8 ? launch_line_t<MODE_CGDIR, 8>(ln, a) : launch_line_t<MODE_CGDIR, 4>(ln, a);
     case MODE_CGPREC: return launch_line_ty<MODE_CGPREC>(ln, a);
     case MODE_CGPREC_D: return launch_line_ty<MODE_CGPREC_D>(ln, a);
     case MODE_CGPREC_P: return launch_line_ty<MODE_CGPREC_P>(ln, a);

@@ -192,6 +192,8 @@ struct LineArgs {
     HaloPush push;     // fused halo push of the output (dst == nullptr: none)
     HaloWait hw;       // in-kernel wait for the halo'd input's slabs (P2P overlap)
     int band_w;        // k_line: tile columns per band on wide grids (0: row by row)
+    int cgdir_ctas;    // k_line<CGDIR> CTAs per SM (0: automatic)
+    int l2hint;        // k_line TMA loads: bit 0 = halo'd fields evict_last in L2, bit 1 = plain fields evict_first
     int dbg;           // debug experiments: bit 0 = k-split in-place boxes row by row (TPMG_DBG_PERROW)
     const double* im;  // per-column fields: 1/m_k of every column's line block (Lambda layout, this
                        // level), precomputed once per operator (launch_pivots); the Thomas modes then
@@ -238,7 +240,7 @@ int line_launch_rows(int mode, int nz, int nx, int use_tma, int ksplit_cfg);
 
 cudaError_t launch_line(const Launcher& ln, int mode, const LineArgs& a);
 // Tile rows TY the launcher uses for `mode` at this nz (the TMA boxes depend on it).
-int line_tile_rows(int mode, int nz, int gen = 0, bool tm = false);   // gen: vertical profiles / fields; tm: TMEM form
+int line_tile_rows(int mode, int nz, int gen = 0, bool tm = false, int64_t nx = 0);   // gen: vertical profiles / fields; tm: TMEM form
 bool line_gen_fits(int nz, int gen = 1);   // the line kernels' on-chip buffers fit nz (gen 1: profiles, 2: fields)
 // Largest nz the on-chip Thomas buffer supports.
 int line_max_nz();

@@ -21,6 +21,13 @@ if os.environ.get("PROF_FIELDS"):   # per-column fields (tpmg_set_fields), e.g. 
     from inputs import horizontal_fields
     ctx.set_fields(*horizontal_fields(n, n, 8.4 * 8.4 / 4, 1, os.environ["PROF_FIELDS"]))
 f = ctx.empty(5)
+if os.environ.get("PROF_CG_ONLY"):   # wide grids: the CG kernels only (fewer buffers)
+    G.fill_rhs(f, n, seed=0)
+    z = ctx.empty(5)
+    ctx.solve_cg(f, z, max_iter=1)
+    torch.cuda.synchronize()
+    print("profile_kernels done", ctx.stats())
+    sys.exit(0)
 u = ctx.empty(5)
 G.fill_rhs(f, n, seed=0)
 G.fill_rhs(u, n, seed=1)

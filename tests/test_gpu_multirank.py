@@ -24,6 +24,7 @@ CASES = [  # (world, TPMG_OVERLAP, halo transport, boundary / coefficients)
     (4, "", "p2p", "0"), (2, "", "p2p", "1"),
     (2, "0", "p2p-fused", "0"), (4, "0", "p2p-fused", "1"),
     (2, "", "p2p", "profiles"), (2, "", "p2p", "fields"), (4, "0", "nccl", "fields"),
+    (2, "ty4", "p2p", "0"), (2, "cg4", "p2p", "0"),   # the 4-row CG direction tiles (TPMG_CGDIR_TY=4)
 ]
 
 
@@ -51,9 +52,12 @@ def test_multirank_parity(world, overlap, halo, bc):
                TPMG_FUSED_PUSH="1" if fused else "0")
     env.pop("TPMG_OVERLAP", None)
     env.pop("TPMG_OVERLAP_CG", None)
-    if overlap == "cg":
+    env.pop("TPMG_CGDIR_TY", None)
+    if overlap in ("ty4", "cg4"):
+        env["TPMG_CGDIR_TY"] = "4"
+    if overlap in ("cg", "cg4"):
         env["TPMG_OVERLAP_CG"] = "1"
-    elif overlap:
+    elif overlap and overlap != "ty4":
         env["TPMG_OVERLAP"] = overlap
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 0, (r.stdout[-4000:], r.stderr[-4000:])

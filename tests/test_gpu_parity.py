@@ -279,6 +279,27 @@ def test_profile_mask_times_only_selected_class():
     assert {"cg_precondition", "cg_direction"} <= set(prof)
 
 
+@pytest.mark.parametrize("ty", ["4", ""])
+@pytest.mark.parametrize("p", [SOLVE_SHAPES[1], O.Params(nx=80, ny=44, nz=64, L=1), O.Params(nx=2048, ny=12, nz=16, L=1)],
+                         ids=["128x128x128", "80x44x64", "2048x12x16"])
+def test_cg_direction_row_tiles(p, ty, monkeypatch):
+    """The CG direction kernel with 8-row tiles (one 8-warp CTA per SM, the default) and with
+    4-row tiles (TPMG_CGDIR_TY=4): the oracle's CG solve, ragged y tiles (44 and 12 rows)
+    and a wide grid (2048 columns: one CTA per SM for the 4-row form) included."""
+    if ty:
+        monkeypatch.setenv("TPMG_CGDIR_TY", ty)
+    ctx = ctx_for(p)
+    f = rhs_zc(p.nx, p.ny, p.nz, seed=0)
+    u = ctx.empty(p.L)
+    res, ref = ctx.solve_cg(to_dev(f), u), O.solve_cg(p, f)
+    assert res.converged and abs(res.iterations - ref.iterations) <= 1
+    if res.iterations == ref.iterations:
+        assert close(to_host_zc(u), ref.u, 1e-9)
+        assert np.allclose(res.history, ref.history, rtol=1e-8)
+    rr = np.linalg.norm(O.residual(p, to_host_zc(u), f)) / np.linalg.norm(f)
+    assert rr < 2e-5
+
+
 @pytest.mark.parametrize("p", [SOLVE_SHAPES[0], SOLVE_SHAPES[1], O.Params(nx=80, ny=48, nz=64, L=3)],
                          ids=["32x32x16", "128x128x128", "80x48x64"])
 def test_cg_ksplit_preconditioner_opt_in(p, monkeypatch):
