@@ -50,6 +50,14 @@ __device__ __forceinline__ double rcp_nr(double x)
     return fma(r, e, r);
 }
 
+// CG preconditioner tile rows in the TMEM form: 4 (one 4-warp CTA per SM, default) or 8
+// (TPMG_CGPREC_TY=8: one 8-warp CTA, g' of warps 4..7 in TMEM columns 256..511).
+static int cgprec_rows()
+{
+    const char* e = std::getenv("TPMG_CGPREC_TY");   // (read per call, like TPMG_CGDIR_TY)
+    return (e && std::atoi(e) == 8) ? 8 : 4;
+}
+
 template <int MODE>
 struct Traits;
 template <> struct Traits<MODE_APPLY>  { static constexpr int NH = 1, NP = 0, THOMAS = 0, NR = 0; };
@@ -195,11 +203,12 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 {
     using T = Traits<MODE>;
     constexpr bool TM = TMS > 0;   // TMS: pipeline stages of the TMEM form (the freed shared memory deepens it)
-    static_assert(!TM || (TY == 4 && T::THOMAS), "TMEM g' buffer: 4 warps (the 4 TMEM lane quarters), Thomas modes");
+    static_assert(!TM || ((TY == 4 || (TY == 8 && GEN == 0)) && T::THOMAS),
+                  "TMEM g' buffer: 4 warps (the 4 TMEM lane quarters) or 8 (two column halves), Thomas modes");
     static_assert(GEN != 3 || (TM && T::THOMAS), "precomputed pivots: TMEM form of the Thomas modes");
     constexpr int NH = T::NH, NR = T::NR;
     constexpr int NP = T::NP + (GEN == 3 ? 1 : 0);   // + the pivot field
-    constexpr uint32_t NCOL = (GEN == 3) ? 512u : kTmemCols;
+    constexpr uint32_t NCOL = (GEN == 3 || TY == 8) ? 512u : kTmemCols;
     using G = Geom<NH, NP, TY>;
     constexpr int NT = G::NT;
     constexpr int NS = TM ? TMS : stages<MODE, GEN>();
@@ -273,7 +282,8 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     uint32_t tbase = 0;   // TM: this warp's lane quarter, column 0
     if constexpr (TM) {
         tmem_fence_after();
-        tbase = tmem_slot + ((uint32_t)(ty * 32) << 16);
+        // warp ty: lane quarter ty % 4; with 8 warps the second four use columns 256..511
+        tbase = tmem_slot + ((uint32_t)((ty & 3) * 32) << 16) + (uint32_t)(ty >> 2) * kTmemCols;
     }
 
     // producer cursor: next chunk to load
@@ -781,7 +791,7 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
     if (e != cudaSuccess) return e;
     per_sm = std::max(per_sm, 1);
     if (TM) per_sm = std::min<int>(per_sm, std::min<int>(ln.tm_ctas, 512 / kTmemCols));   // resident CTAs must all get their TMEM
-    if (GEN == 3) per_sm = 1;   // 512 TMEM columns per CTA
+    if (GEN == 3 || (TM && TY == 8)) per_sm = 1;   // 512 TMEM columns per CTA
     const int64_t ntiles = ((a.L.nx + TX - 1) / TX) * part_rows(a.part, (int)((a.L.ny + TY - 1) / TY));
     // CG direction (two halo'd fields) with 4-row tiles: on wide grids two CTAs per SM
     // re-read the halo rows from HBM (2.1x the algorithmic reads at 4096 x 1024 x 128, ncu),
@@ -796,6 +806,11 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
 template <int MODE, int TY>
 cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
 {
+    if constexpr (MODE == MODE_CGPREC && TY == 8) {   // 8 warps, g' in both TMEM column halves
+        if (!a.hw.flag[0] && !a.hw.flag[1] && !a.L.gen && ln.tmem && a.use_tma && a.L.nz <= (int)(kTmemCols / 2))
+            return launch_line_l<MODE, 8, 1, 0, 3>(ln, a);
+        return cudaErrorNotSupported;
+    } else {
     if (a.hw.flag[0] || a.hw.flag[1]) {   // P2P overlap with the in-kernel halo wait (line_halo_wait())
         if constexpr (TY == 4 && (MODE == MODE_CGDIR || MODE == MODE_RESTRICT))
             if (!a.L.gen && a.use_tma) return launch_line_l<MODE, 4, 1, 0, 0, true>(ln, a);
@@ -830,12 +845,17 @@ cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
             return launch_line_l<MODE, 4, 1, 0, 3>(ln, a);
         }
     return a.use_tma ? launch_line_l<MODE, TY, 1, 0>(ln, a) : launch_line_l<MODE, TY, 0, 0>(ln, a);
+    }
 }
 
 template <int MODE>
 cudaError_t launch_line_ty(const Launcher& ln, const LineArgs& a)
 {
-    if (ln.tmem && a.use_tma && a.L.nz <= (int)(kTmemCols / 2)) return launch_line_t<MODE, 4>(ln, a);
+    if (ln.tmem && a.use_tma && a.L.nz <= (int)(kTmemCols / 2)) {
+        if constexpr (MODE == MODE_CGPREC)
+            if (cgprec_rows() == 8 && !a.L.gen) return launch_line_t<MODE, 8>(ln, a);
+        return launch_line_t<MODE, 4>(ln, a);
+    }
     if (line_smem_bytes<MODE, 4>(a.L.nz, a.L.gen) <= kMaxSmem) return launch_line_t<MODE, 4>(ln, a);
     if (line_smem_bytes<MODE, 2>(a.L.nz, a.L.gen) <= kMaxSmem) return launch_line_t<MODE, 2>(ln, a);
     return launch_line_t<MODE, 1>(ln, a);
@@ -1201,6 +1221,7 @@ static int cgdir_rows(int64_t)
 int line_tile_rows(int mode, int nz, int gen, bool tm, int64_t nx)
 {
     if (mode == MODE_CGDIR) return cgdir_rows(nx);
+    if (tm && nz <= (int)(kTmemCols / 2) && mode == MODE_CGPREC && !gen) return cgprec_rows();
     // the Tensor Memory form of the Thomas modes always runs 4 tile rows (the lane quarters)
     if (tm && nz <= (int)(kTmemCols / 2) && (mode == MODE_PREC || mode == MODE_SMOOTH || is_cgprec(mode))) return 4;
     switch (mode) {

@@ -279,14 +279,18 @@ def test_profile_mask_times_only_selected_class():
     assert {"cg_precondition", "cg_direction"} <= set(prof)
 
 
-@pytest.mark.parametrize("ty", ["4", ""])
+@pytest.mark.parametrize("ty", ["4", "", "prec8"])
 @pytest.mark.parametrize("p", [SOLVE_SHAPES[1], O.Params(nx=80, ny=44, nz=64, L=1), O.Params(nx=2048, ny=12, nz=16, L=1)],
                          ids=["128x128x128", "80x44x64", "2048x12x16"])
 def test_cg_direction_row_tiles(p, ty, monkeypatch):
     """The CG direction kernel with 8-row tiles (one 8-warp CTA per SM, the default) and with
     4-row tiles (TPMG_CGDIR_TY=4): the oracle's CG solve, ragged y tiles (44 and 12 rows)
-    and a wide grid (2048 columns: one CTA per SM for the 4-row form) included."""
-    if ty:
+    and a wide grid (2048 columns: one CTA per SM for the 4-row form) included.  prec8: the CG
+    preconditioner kernel with 8-row tiles too (TPMG_CGPREC_TY=8: 8 warps, g' of warps 4..7
+    in TMEM columns 256..511)."""
+    if ty == "prec8":
+        monkeypatch.setenv("TPMG_CGPREC_TY", "8")
+    elif ty:
         monkeypatch.setenv("TPMG_CGDIR_TY", ty)
     ctx = ctx_for(p)
     f = rhs_zc(p.nx, p.ny, p.nz, seed=0)
