@@ -139,6 +139,9 @@ struct tpmg_ctx {
     struct ProfRec { int cls; double cells; cudaEvent_t a, b; const int* skip; };
     std::vector<ProfRec> prof_pending;
     int dbg = 0;                        // LineArgs::dbg (timing experiments)
+    bool dev_publish = false;           // P2P: the push kernel stores the epoch flags (TPMG_DEV_PUBLISH=1)
+    bool skip_finish = false;           // P2P: no stream waits after an in-kernel-waiting consumer (TPMG_SKIP_FINISH=1)
+    unsigned* d_push_done = nullptr;    // k_halo_push ticket counter (device publish)
     int tma_promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;   // TMA L2 promotion (TPMG_TMA_PROMO 0..3: none, 64, 128, 256 B)
     int l2hint = 3;                     // k_line TMA L2 policies (TPMG_L2HINT bits: 1 halo'd evict_last, 2 plain evict_first; r2aj/r2ak)
     int cgdir_ctas = 0;                 // k_line<CGDIR> CTAs per SM (TPMG_CGDIR_CTAS; 0 automatic)
@@ -356,8 +359,15 @@ tpmg_status p2p_begin(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, const double* x, int* E
     HaloPush hp = push_desc(ctx, ch, E);
     hp.src_first = x;
     hp.src_last = x + (size_t)(ch.nyl - 1) * ch.plane;
+    if (ctx->dev_publish) {   // the push kernel's last CTA stores the epoch flags itself
+        hp.flag_lo = ctx->rank > 0 ? reinterpret_cast<unsigned*>(ctx->peer_pool[0] + ch.off_flags + 1 * 4) : nullptr;
+        hp.flag_hi = ctx->rank < ctx->nranks - 1 ? reinterpret_cast<unsigned*>(ctx->peer_pool[1] + ch.off_flags + 0 * 4)
+                                                 : nullptr;
+        hp.done = ctx->d_push_done;
+        hp.epoch = (unsigned)E;
+    }
     CUDA_TRY(ctx, launch_halo_push(launcher(ctx), hp));
-    TRY(publish_epoch(ctx, ch, E));
+    if (!ctx->dev_publish) TRY(publish_epoch(ctx, ch, E));
     *E_out = E;
     return TPMG_OK;
 }
@@ -365,6 +375,18 @@ tpmg_status p2p_begin(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, const double* x, int* E
 tpmg_status p2p_finish(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int E)
 {
     return E ? wait_epoch(ctx, ch, E) : TPMG_OK;
+}
+
+// p2p_finish after a consumer kernel that waited in the kernel for epoch E (HaloWait): its
+// completion implies both flags reached E, so the stream waits are redundant (TPMG_SKIP_FINISH);
+// the slab pointers and the stats advance as in wait_epoch.
+tpmg_status p2p_finish_waited(tpmg_ctx* ctx, tpmg_ctx::Chan& ch, int E)
+{
+    if (!E || !ctx->skip_finish) return p2p_finish(ctx, ch, E);
+    *ch.cur_lo = ch.lo[E & 1];
+    *ch.cur_hi = ch.hi[E & 1];
+    ++ctx->stats.halo_exchanges;
+    return TPMG_OK;
 }
 
 // x with the slabs of epoch E of channel ch (E = 0: the current slabs)
@@ -847,7 +869,7 @@ tpmg_status run_line_halo(tpmg_ctx* ctx, int level, int mode, LineArgs a, const 
         if (a.h0.base == x) a.h0 = halo_epoch_view(ctx, ch, x, E);
         if (E) a.hw = halo_wait_of(ctx, ch, E);
         TRY(run_line(ctx, mode, a));
-        TRY(p2p_finish(ctx, ch, E));   // stream order for the channel's next push (the kernel already waited)
+        TRY(p2p_finish_waited(ctx, ch, E));   // stream order for the channel's next push (the kernel already waited)
         return pre_boundary(a);
     }
     if (!ctx->overlap_nccl || ctx->p2p || nty < 3) {
@@ -959,7 +981,7 @@ tpmg_status prolong_overlapped(tpmg_ctx* ctx, int lc_)
             CUDA_TRY(ctx, launch_prolong_add(launcher(ctx), Cc.lc, F.lc, ucE, F.u[F.cur], ctx->skip, PART_ALL, nullptr,
                                              E ? &hw : nullptr));
         }
-        return p2p_finish(ctx, ch, E);
+        return p2p_finish_waited(ctx, ch, E);
     }
     if (ctx->nranks == 1 || !ctx->overlap_nccl || ctx->p2p || Cc.lc.ny < 3) {
         TRY(exchange(ctx, lc_, Cc.u[Cc.cur]));
@@ -1469,12 +1491,14 @@ tpmg_status halo_setup(tpmg_ctx* ctx)
     }
     ctx->off_red = take(sizeof(double) * 2 * kMaxP2PRanks * 4);
     ctx->off_redflags = take(sizeof(unsigned) * kMaxP2PRanks);
+    const size_t off_pushdone = take(sizeof(unsigned));
     ctx->halo_pool_bytes = off;
     tpmg_status st = TPMG_OK;
     if (cudaMalloc(&ctx->halo_pool, off) != cudaSuccess || cudaMemset(ctx->halo_pool, 0, off) != cudaSuccess)
         st = fail(ctx, TPMG_E_CUDA, "halo pool: cudaMalloc/cudaMemset of %zu bytes", off);
     TRY(agree(ctx, st));
     char* base = static_cast<char*>(ctx->halo_pool);
+    ctx->d_push_done = reinterpret_cast<unsigned*>(base + off_pushdone);
     for (int c = 1; c <= L + 1; ++c) {
         tpmg_ctx::Chan& ch = ctx->chans[c];
         for (int b = 0; b < 2; ++b) {
@@ -1862,6 +1886,10 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->tmem = !(tm && tm[0] == '0');
         const char* bnd = std::getenv("TPMG_BAND");
         if (bnd) ctx->band_w = std::max(0, std::atoi(bnd));
+        const char* dpb = std::getenv("TPMG_DEV_PUBLISH");
+        ctx->dev_publish = dpb && dpb[0] == '1';
+        const char* skf = std::getenv("TPMG_SKIP_FINISH");
+        ctx->skip_finish = skf && skf[0] == '1';
         const char* tpr = std::getenv("TPMG_TMA_PROMO");
         if (tpr) ctx->tma_promo = std::min(3, std::max(0, std::atoi(tpr)));
         const char* l2h = std::getenv("TPMG_L2HINT");

@@ -1061,6 +1061,19 @@ __global__ void __launch_bounds__(256) k_halo_push(const HaloPush hp, int64_t n)
         if (dl) dl[q] = sf[q];
         if (dh) dh[q] = sl[q];
     }
+    if (hp.done) {   // device-side publish: the last CTA releases the epoch to both neighbours
+        __threadfence_system();   // my CTA's remote stores before its ticket
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned t = atomicAdd(hp.done, 1u);
+            if (t == gridDim.x - 1) {
+                *hp.done = 0u;          // every CTA has taken its ticket: reset for the next push
+                __threadfence_system(); // (cumulative) every CTA's stores before the flags
+                if (hp.flag_lo) asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(hp.flag_lo), "r"(hp.epoch) : "memory");
+                if (hp.flag_hi) asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(hp.flag_hi), "r"(hp.epoch) : "memory");
+            }
+        }
+    }
 }
 
 __global__ void __launch_bounds__(32) k_allreduce_p2p(double* d, int n, const P2PReduce P, unsigned E)

@@ -149,6 +149,13 @@ struct HaloPush {
     double* dst_lo;
     double* dst_hi;
     int64_t n;
+    // k_halo_push only (device-side publish, TPMG_DEV_PUBLISH): the last CTA to finish its
+    // remote stores (ticket counter `done`, reset by it) stores `epoch` into the neighbours'
+    // flag words with st.release.sys -- instead of two stream write-values after the kernel
+    unsigned* flag_lo;
+    unsigned* flag_hi;
+    unsigned* done;
+    unsigned epoch;
 };
 // In-kernel halo wait (P2P overlap in ONE launch): flag[0] / flag[1] are my pool's epoch
 // flags "data from the lower / upper neighbour".  When set, the line kernels walk their
