@@ -82,11 +82,13 @@ def dist_env():
 def workload(args, world):
     if args.global_nx:
         g = args.global_nx
-        return g, g, f"C5 strong scaling: {g}x{g}x{args.nz} global, {world} B200 y-strips of {g}x{g // world}"
+        tag = "C5 strong scaling" if g == 4096 else "strong scaling"
+        return g, g, f"{tag}: {g}x{g}x{args.nz} global, {world} B200 y-strips of {g}x{g // world}"
     nx = args.per_gpu_nx
     ny = nx * world
     name = ("C2: MG + PCG on 1024x1024x128 fp64, 1 B200" if world == 1 and nx == 1024 else
-            f"weak scaling: {nx}x{nx}x{args.nz} per GPU, global {nx}x{ny}x{args.nz}, {world} B200 y-strips")
+            f"{'C4 ' if nx == 2048 else ''}weak scaling: {nx}x{nx}x{args.nz} per GPU, global {nx}x{ny}x{args.nz}, "
+            f"{world} B200 y-strips")
     return nx, ny, name
 
 
