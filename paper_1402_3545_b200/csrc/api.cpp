@@ -139,6 +139,7 @@ struct tpmg_ctx {
     struct ProfRec { int cls; double cells; cudaEvent_t a, b; const int* skip; };
     std::vector<ProfRec> prof_pending;
     int dbg = 0;                        // LineArgs::dbg (timing experiments)
+    bool tma_store = false;             // CGPREC outputs by TMA stores (TPMG_TMA_STORE=1)
     bool dev_publish = false;           // P2P: the push kernel stores the epoch flags (TPMG_DEV_PUBLISH=1)
     bool skip_finish = false;           // P2P: no stream waits after an in-kernel-waiting consumer (TPMG_SKIP_FINISH=1)
     unsigned* d_push_done = nullptr;    // k_halo_push ticket counter (device publish)
@@ -709,6 +710,15 @@ void fill_tma(tpmg_ctx* ctx, int mode, LineArgs& a)
     if (thomas && a.im && (!aligned(a.im) || !tensor_map(ctx, a.im, nx, nz, ny, kTileX, TY, &a.tma.q[np]))) a.im = nullptr;
     if (!thomas) a.im = nullptr;
     a.use_tma = 1;
+    // TMA stores of the TMEM CG preconditioner (TPMG_TMA_STORE=1): r, u in 4-row boxes, z in rows
+    a.tst = 0;
+    if (mode == MODE_CGPREC && ctx->tma_store && ctx->tmem && !a.L.gen && TY == 4 && nz % kStageK == 0 &&
+        nz >= 2 * kStageK && nz <= 128 && !a.push.dst_lo && !a.push.dst_hi && a.out0 && a.out1 && a.out2 &&
+        aligned(a.out0) && aligned(a.out1) && aligned(a.out2) &&
+        tensor_map(ctx, a.out0, nx, nz, ny, kTileX, 4, &a.tma.o[0]) &&
+        tensor_map(ctx, a.out1, nx, nz, ny, kTileX, 4, &a.tma.o[1]) &&
+        tensor_map(ctx, a.out2, nx, nz, ny, kTileX, 1, &a.tma.o[2]))
+        a.tst = 1;
 }
 
 // The level whose constants a LineArgs carries (by its table pointer).
@@ -1886,6 +1896,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->tmem = !(tm && tm[0] == '0');
         const char* bnd = std::getenv("TPMG_BAND");
         if (bnd) ctx->band_w = std::max(0, std::atoi(bnd));
+        const char* tst = std::getenv("TPMG_TMA_STORE");
+        ctx->tma_store = tst && tst[0] == '1';
         const char* dpb = std::getenv("TPMG_DEV_PUBLISH");
         ctx->dev_publish = dpb && dpb[0] == '1';
         const char* skf = std::getenv("TPMG_SKIP_FINISH");

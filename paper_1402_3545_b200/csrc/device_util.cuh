@@ -142,6 +142,22 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first()
     return p;
 }
 
+// TMA store of a box from shared memory (bulk async-group of the issuing thread); the writers
+// of the box fence.proxy.async before the barrier that precedes the issue.
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int x, int y, int z, const void* src)
+{
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;\n" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 // ------------------------------------------------------------------ Tensor Memory (TMEM)
 // The line kernels use TMEM (512 columns x 128 lanes x 32 bit per SM) as per-thread scratch
 // for the Thomas intermediates g'_k: thread t of warp w owns lane 32 w + t, level k sits in

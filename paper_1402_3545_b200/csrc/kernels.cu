@@ -198,9 +198,15 @@ constexpr uint32_t kTmemCols = 256;
 // GEN 3: per-column fields with the pivots precomputed (LineArgs::im): like GEN 2, but 1/m_k
 // arrives as one more plain field through the TMA ring and the Thomas sweeps run no pivot
 // recurrence; g'_k and 1/m_k both live in TMEM (4 columns per level, the whole TMEM of the SM).
-template <int MODE, int TY, int LOADER, int GEN, int TMS = 0, bool HW = false>
+// TST: the CG preconditioner's outputs r, u (forward sweep) and z (backward sweep) are staged
+// in shared memory and written by TMA stores (LineArgs::tst, tma.o) instead of one STG per cell
+// and output with its 64-bit address arithmetic: r, u in groups of KB levels (3 buffers: the
+// group being written, the one whose last level is finalised one chunk later, the one in
+// flight), z per warp in KB-level rows (2 buffers).
+template <int MODE, int TY, int LOADER, int GEN, int TMS = 0, bool HW = false, bool TST = false>
 __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArgs a)
 {
+    static_assert(!TST || (MODE == MODE_CGPREC && TMS > 0 && GEN == 0 && LOADER == 1 && !HW), "TMA stores: TMEM CGPREC");
     using T = Traits<MODE>;
     constexpr bool TM = TMS > 0;   // TMS: pipeline stages of the TMEM form (the freed shared memory deepens it)
     static_assert(!TM || ((TY == 4 || (TY == 8 && GEN == 0)) && T::THOMAS),
@@ -232,6 +238,10 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
     constexpr int RS = KB + 1;
     double* rbuf = gbuf + (T::THOMAS ? ((TM ? 0 : nz) + (GEN == 2 ? nck : 0)) * NT : 0);
     double* scratch = rbuf + (MODE == MODE_RESTRICT ? 2 * TY * RS * (TX / 2) : 0);  // reduction scratch
+    // TST staging (128-byte aligned TMA sources): sfw[3][2][KB][TY][TX] (r, u), sbw[2][TY][KB][TX] (z)
+    // (pointer arithmetic only, so that the compiler keeps the shared state space: STS, not ST)
+    double* sfw = scratch + 64 + ((128u - (smem_u32(scratch + 64) & 127u)) & 127u) / 8u;
+    double* sbw = sfw + 3 * 2 * KB * G::NT;
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     for (int q = tid; q < 3 * nz; q += NT) tab[q] = a.L.tab[q];   // interior class (0)
@@ -413,7 +423,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 
         // Complete level km (its upper neighbour up1 has arrived): stencil, the mode's
         // pointwise work and one Thomas forward-elimination step.
-        auto finalize = [&](double up1, double dgk, double imk, double* gslot, int rslot, int km) {
+        auto finalize = [&](double up1, double dgk, double imk, double* gslot, int rslot, int km, double* sbo) {
             // (M_T u)_k and the coefficient of the horizontal neighbour sum: -gamma and c in
             // the flat box; b_k, c_k and c_l d_k with general profiles (GEN, shared memory)
             double Mu, c, sk = -gamma, tk = 0.0;
@@ -458,6 +468,13 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 const double r = fma(c, S0, qa) - Mu;
                 const double rs = r + __shfl_xor_sync(0xffffffffu, r, 1);
                 if ((tx & 1) == 0) rbuf_cur[(ty * RS + rslot) * (TX / 2) + (tx >> 1)] = rs;
+            } else if constexpr (TST) {   // (MODE_CGPREC) r, u staged for the group's TMA stores
+                const double Ap = fma(-c, S0, Mu);
+                const double rn = fma(-ratio, Ap, qa);
+                sbo[0] = rn;
+                sbo[KB * NT] = fma(ratio, u0, qb);
+                if (valid) acc[0] = fma(rn, rn, acc[0]);
+                g = rn;
             } else if constexpr (CGP) {
                 const double Ap = fma(-c, S0, Mu);
                 const double rn = fma(-ratio, Ap, qa);
@@ -469,7 +486,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 }
                 g = rn;
             }
-            if constexpr (MODE == MODE_APPLY || MODE == MODE_RESID || MODE == MODE_CGDIR || CGP) {
+            if constexpr ((MODE == MODE_APPLY || MODE == MODE_RESID || MODE == MODE_CGDIR || CGP) && !TST) {
                 if constexpr (MODE == MODE_RESID) {   // the only mode whose out0 may be absent
                     if (ofw0) ofw0 += nx;
                 } else {
@@ -531,16 +548,31 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                 if constexpr (T::NP >= 3) pdv[kk] = pp[2 * TY * KB * TX + kk * TX];   // MODE_CGPREC_P: p_prev
                 if constexpr (GEN == 3) pcv[kk] = pp[T::NP * TY * KB * TX + kk * TX];   // the pivot field
             }
+            if constexpr (TST) {
+                fence_proxy_async_smem();           // my staged r, u before the barrier
+                if (tid == 0) bulk_wait_read<0>();  // the group stored one chunk ago has left its buffer
+            }
             __syncthreads();   // slot gi % NS is free for chunk gi + NS
+            if constexpr (TST)
+                if (tid == 0 && ch >= 2) {   // group ch-2 is complete (its last level was finalised in chunk ch-1)
+                    const double* src = sfw + ((gi + 1) % 3) * (2 * KB * NT);
+                    tma_store_3d(&a.tma.o[0], (int)i0, (ch - 2) * KB, (int)j0, src);
+                    tma_store_3d(&a.tma.o[1], (int)i0, (ch - 2) * KB, (int)j0, src + KB * NT);
+                    bulk_commit();
+                }
             if constexpr (MODE == MODE_RESTRICT) rbuf_cur = rbuf + (gi & 1) * (TY * RS * (TX / 2));
             const double* dg = diag + (k0 - 1);      // level km = k0 - 1 + kk
             const double* im = invm + (k0 - 1);
             double* gb = gbuf + (k0 - 1) * NT + tid;
+            // TST staging: level k0-1 closes the previous group (buffer (gi+2)%3, slot KB-1), the
+            // chunk's other levels open group gi (buffer gi%3); box layout [row][level][x]
+            double* sbp = sfw + ((gi + 2) % 3) * (2 * KB * NT) + ty * (KB * TX) + tx + (KB - 1) * TX;
+            double* sbc = sfw + (gi % 3) * (2 * KB * NT) + ty * (KB * TX) + tx - TX;
 #pragma unroll
             for (int kk = 0; kk < KB; ++kk) {
                 const int k = k0 + kk;
                 if (FULL || k < nz) {
-                    if (FULL || k > 0) finalize(ecv[kk], dg[kk], im[kk], gb + kk * NT, kk, k - 1);
+                    if (FULL || k > 0) finalize(ecv[kk], dg[kk], im[kk], gb + kk * NT, kk, k - 1, kk == 0 ? sbp : sbc + kk * TX);
                     if constexpr (GEN == 2 && T::THOMAS)
                         if (kk == 0 && ch > 0) {   // renormalise and checkpoint m_{k0-1}
                             const double m = pm1 * rcp_nr(pm2);
@@ -563,7 +595,8 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             else
                 do_chunk(std::false_type{}, ch, st);
             if (ch == nch - 1)
-                finalize(0.0, diag[nz - 1], invm[nz - 1], gbuf + (nz - 1) * NT + tid, nz - ch * KB, nz - 1);
+                finalize(0.0, diag[nz - 1], invm[nz - 1], gbuf + (nz - 1) * NT + tid, nz - ch * KB, nz - 1,
+                         sfw + (gi % 3) * (2 * KB * NT) + ty * (KB * TX) + tx + (KB - 1) * TX);
             if constexpr (MODE == MODE_RESTRICT) {
                 // f_c(I, J, k) = 1/4 (x-pair sum of row 2J + x-pair sum of row 2J+1);
                 // this chunk completed levels ch*KB-1 .. ch*KB+KB-2 (and nz-1 if last), slot
@@ -588,6 +621,20 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                                         rbuf_cur[((2 * jp + 1) * RS + slot) * (TX / 2) + l]);
                     }
                 }
+            }
+        }
+        if constexpr (TST) {   // the tile's last two groups (gi is one past the last chunk)
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (tid == 0) {
+                const double* s1 = sfw + ((gi + 1) % 3) * (2 * KB * NT);   // group nch-2
+                const double* s2 = sfw + ((gi + 2) % 3) * (2 * KB * NT);   // group nch-1
+                tma_store_3d(&a.tma.o[0], (int)i0, (nch - 2) * KB, (int)j0, s1);
+                tma_store_3d(&a.tma.o[1], (int)i0, (nch - 2) * KB, (int)j0, s1 + KB * NT);
+                bulk_commit();
+                tma_store_3d(&a.tma.o[0], (int)i0, (nch - 1) * KB, (int)j0, s2);
+                tma_store_3d(&a.tma.o[1], (int)i0, (nch - 1) * KB, (int)j0, s2 + KB * NT);
+                bulk_commit();
             }
         }
 
@@ -678,6 +725,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             // TM: the chunk's g' comes from Tensor Memory, 8 levels per load (a software-pipelined
             // form with the next chunk's load in flight measured the same, r2k, at 237 registers)
             if constexpr (TM) tmem_wait_st();   // the forward sweep's g' stores have landed
+            int bg = 0;   // TST: this warp's z staging buffer
             for (; k >= KB - 1; k -= KB) {
                 const double* gq = gbuf + (k - (KB - 1)) * NT + tid;   // levels k-KB+1 .. k
                 const double* mq = gim + (k - (KB - 1));
@@ -694,11 +742,29 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
                     if constexpr (!TM) gv[q] = gq[(KB - 1 - q) * NT];
                     gm[q] = mq[KB - 1 - q];
                 }
+                if constexpr (TST) {
+                    double* zb = sbw + (bg * TY + ty) * (KB * TX);
+                    if (tx == 0) bulk_wait_read<1>();   // this buffer's store (two groups ago) has read it
+                    __syncwarp();
 #pragma unroll
-                for (int q = 0; q < KB; ++q) {
-                    x = fma(gm[q], x, gv[q]);
-                    if (valid) put(op, x);
-                    op -= nx;
+                    for (int q = 0; q < KB; ++q) {
+                        x = fma(gm[q], x, gv[q]);
+                        zb[(KB - 1 - q) * TX + tx] = x;   // box [level][x] of row j
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (tx == 0) {
+                        tma_store_3d(&a.tma.o[2], (int)i0, k - (KB - 1), (int)j, zb);
+                        bulk_commit();
+                    }
+                    bg ^= 1;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < KB; ++q) {
+                        x = fma(gm[q], x, gv[q]);
+                        if (valid) put(op, x);
+                        op -= nx;
+                    }
                 }
             }
             for (; k >= 0; --k) {
@@ -741,6 +807,8 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
             tile_body(std::false_type{}, tl);
     }
     if constexpr (LOADER == 0) cp_async_wait<0>();
+    if constexpr (TST)
+        if (tx == 0) bulk_wait<0>();   // my TMA stores are complete before the CTA (and its staging) ends
     if constexpr (TM) {   // every warp is done with its lanes; the allocating warp frees them
         tmem_fence_before();
         __syncthreads();
@@ -753,7 +821,7 @@ __global__ void __launch_bounds__(TX* TY) k_line(const __grid_constant__ LineArg
 }
 
 template <int MODE, int TY>
-size_t line_smem_bytes(int nz, int gen = 0, int tms = 0)
+size_t line_smem_bytes(int nz, int gen = 0, int tms = 0, bool tst = false)
 {
     using T = Traits<MODE>;
     using G = Geom<T::NH, T::NP, TY>;
@@ -763,18 +831,19 @@ size_t line_smem_bytes(int nz, int gen = 0, int tms = 0)
     const bool tm = tms > 0;
     size_t d = ((3 * nz + 15) & ~15) + (gen >= 2 ? ((4 * nz + 15) & ~15) : gen ? ((3 * nz + 15) & ~15) : 0) +
                (size_t)(tm ? tms : gen == 2 ? stages<MODE, 2>() : kNS) * G::STAGE + (T::THOMAS ? (size_t)((tm ? 0 : nz) + (gen == 2 ? (nz + KB - 1) / KB : 0)) * G::NT : 0) + 64 + 16 +
-               (MODE == MODE_RESTRICT ? 2 * TY * (KB + 1) * (TX / 2) : 0);
+               (MODE == MODE_RESTRICT ? 2 * TY * (KB + 1) * (TX / 2) : 0) +
+               (tst ? 16 + (3 * 2 + 2) * KB * TY * TX : 0);   // TST staging + its 128-byte alignment
     return d * sizeof(double);
 }
 
 constexpr size_t kMaxSmem = 227 * 1024 - 1024;  // leave room for static smem (barriers, flags)
 
-template <int MODE, int TY, int LOADER, int GEN, int TMS = 0, bool HW = false>
+template <int MODE, int TY, int LOADER, int GEN, int TMS = 0, bool HW = false, bool TST = false>
 cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
 {
     constexpr bool TM = TMS > 0;
-    const size_t smem = line_smem_bytes<MODE, TY>(a.L.nz, GEN, TMS);
-    auto kern = k_line<MODE, TY, LOADER, GEN, TMS, HW>;
+    const size_t smem = line_smem_bytes<MODE, TY>(a.L.nz, GEN, TMS, TST);
+    auto kern = k_line<MODE, TY, LOADER, GEN, TMS, HW, TST>;
     static size_t limit = 0;   // per instantiation
     if (!limit) {
         limit = dyn_smem_limit(kern);
@@ -839,6 +908,7 @@ cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
             // but 7 measured 16% slower than 3 for CGPREC (r2e: 1.29 vs 1.11 ms); TPMG_TM_STAGES
             // selects 3 (default), 4 or 5 for the CG preconditioner
             if constexpr (MODE == MODE_CGPREC) {
+                if (a.tst) return launch_line_l<MODE, 4, 1, 0, 3, false, true>(ln, a);
                 if (ln.tm_stages == 4) return launch_line_l<MODE, 4, 1, 0, 4>(ln, a);
                 if (ln.tm_stages == 5) return launch_line_l<MODE, 4, 1, 0, 5>(ln, a);
             }

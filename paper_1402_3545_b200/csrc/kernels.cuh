@@ -128,6 +128,7 @@ struct TmaHalo {
 struct TmaMaps {
     TmaHalo h[2];
     CUtensorMap q[4];   // plain inputs; q[NP] = the pivot field of the precomputed-pivot form
+    CUtensorMap o[3];   // TMA stores of the CG preconditioner (LineArgs::tst): r, u (TY-row boxes), z (one row)
 };
 
 // Tile geometry of the line kernels: TX = 32 columns along x per tile row,
@@ -200,6 +201,7 @@ struct LineArgs {
     HaloWait hw;       // in-kernel wait for the halo'd input's slabs (P2P overlap)
     int band_w;        // k_line: tile columns per band on wide grids (0: row by row)
     int cgdir_ctas;    // k_line<CGDIR> CTAs per SM (0: automatic)
+    int tst;           // k_line<CGPREC>: outputs staged in shared memory and written by TMA stores (tma.o)
     int l2hint;        // k_line TMA loads: bit 0 = halo'd fields evict_last in L2, bit 1 = plain fields evict_first
     int dbg;           // debug experiments: bit 0 = k-split in-place boxes row by row (TPMG_DBG_PERROW)
     const double* im;  // per-column fields: 1/m_k of every column's line block (Lambda layout, this

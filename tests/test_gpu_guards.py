@@ -163,6 +163,50 @@ def test_tmem_form_bit_identical_to_shared_memory_form(shape):
     assert h1 == h0
 
 
+@pytest.mark.parametrize("shape", [(64, 64, 128, 3), (80, 44, 64, 1), (96, 36, 16, 2)],
+                         ids=["64x64x128", "80x44x64", "96x36x16"])
+def test_tma_store_form_bit_identical(shape):
+    """The CG preconditioner with its outputs staged in shared memory and written by TMA stores
+    (TPMG_TMA_STORE=1) vs the per-thread stores: the same arithmetic on the same grid, so every
+    CG iterate and the residual history are bit-identical; ragged x and y tiles (the TMA store
+    clips the phantom columns and rows) included."""
+    import torch
+    nx, ny, nz, L = shape
+    outs = []
+    for ts in ("1", "0"):
+        os.environ["TPMG_TMA_STORE"] = ts
+        try:
+            ctx = ctx_for(O.Params(nx=nx, ny=ny, nz=nz, L=L))
+        finally:
+            os.environ.pop("TPMG_TMA_STORE")
+        f = torch.from_numpy(np.random.default_rng(8).standard_normal(ctx.shape(L))).cuda()
+        x = torch.empty_like(f)
+        r = ctx.solve_cg(f, x, eps=1e-10, max_iter=40)
+        torch.cuda.synchronize()
+        outs.append((x.cpu().numpy(), r.history, r.iterations))
+        ctx.close()
+    (x1, h1, i1), (x0, h0, i0) = outs
+    assert i1 == i0 and h1 == h0
+    assert np.array_equal(x1.view(np.int64), x0.view(np.int64))
+
+
+def test_tma_store_guard_bands():
+    """TPMG_TMA_STORE=1: the TMA stores of r, u, z stay inside their vectors (NaN guard bands
+    around every CG vector the caller passes, ragged tiles)."""
+    import torch
+    os.environ["TPMG_TMA_STORE"] = "1"
+    try:
+        ctx = ctx_for(O.Params(nx=80, ny=44, nz=64, L=1))
+    finally:
+        os.environ.pop("TPMG_TMA_STORE")
+    fb, f = guarded(ctx.shape(1), seed=3)
+    xb, x = guarded(ctx.shape(1), seed=4)
+    r = ctx.solve_cg(f, x, max_iter=12)
+    assert r.iterations >= 1 and finite(x)
+    assert guards_intact(fb) and guards_intact(xb)
+    ctx.close()
+
+
 @pytest.mark.parametrize("max_iter", [7, 8, 1000])
 def test_paired_u_update_changes_only_u_rounding(max_iter):
     """PCG with the u update paired over two iterations (TPMG_PAIR_U=1) vs every iteration
