@@ -72,3 +72,19 @@ def test_oracle_counts_and_config_block():
     assert cfg["workload"].startswith("C2") and (cfg["nx"], cfg["ny"], cfg["nz"]) == (1024, 1024, 128)
     src_text = open(os.path.join(ROOT, "bench.py")).read()
     assert "for name, sv, on in" not in src_text
+
+
+def test_workload_names_follow_the_configs():
+    """C4 (2048^2 per GPU, weak) and C5 (4096^2 global, strong) are named only for their sizes;
+    other sizes are plain weak / strong scaling lines (BASELINE.json configs)."""
+    sys.path.insert(0, ROOT)
+    import argparse
+    import bench
+    a = argparse.Namespace(nz=128, per_gpu_nx=2048, global_nx=0)
+    assert bench.workload(a, 4)[2].startswith("C4 weak scaling") and bench.workload(a, 4)[:2] == (2048, 8192)
+    a.per_gpu_nx = 512
+    assert bench.workload(a, 2)[2].startswith("weak scaling")
+    a.global_nx = 4096
+    assert bench.workload(a, 4)[2].startswith("C5 strong scaling") and bench.workload(a, 4)[:2] == (4096, 4096)
+    a.global_nx = 1024
+    assert bench.workload(a, 2)[2].startswith("strong scaling")
