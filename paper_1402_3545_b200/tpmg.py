@@ -16,7 +16,7 @@ import os
 from dataclasses import dataclass, field
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libtpmg.so")
+LIB_PATH = os.environ.get("TPMG_LIB_PATH") or os.path.join(_PKG, "libtpmg.so")   # (override: A/B builds)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
