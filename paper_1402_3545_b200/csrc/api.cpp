@@ -139,6 +139,7 @@ struct tpmg_ctx {
     struct ProfRec { int cls; double cells; cudaEvent_t a, b; const int* skip; };
     std::vector<ProfRec> prof_pending;
     int dbg = 0;                        // LineArgs::dbg (timing experiments)
+    bool carveout_fit = false;          // line kernels' carveout sized to their CTAs (TPMG_CARVEOUT=fit)
     bool tma_store = false;             // CGPREC outputs by TMA stores (TPMG_TMA_STORE=1)
     bool dev_publish = false;           // P2P: the push kernel stores the epoch flags (TPMG_DEV_PUBLISH=1)
     bool skip_finish = false;           // P2P: no stream waits after an in-kernel-waiting consumer (TPMG_SKIP_FINISH=1)
@@ -212,6 +213,7 @@ Launcher launcher(tpmg_ctx* ctx)
     ln.tmem = ctx->tmem;
     ln.tm_ctas = ctx->tm_ctas;
     ln.tm_stages = ctx->tm_stages;
+    ln.carveout_fit = ctx->carveout_fit;
     return ln;
 }
 
@@ -1896,6 +1898,8 @@ tpmg_status tpmg_create(const tpmg_params* params, int32_t rank, int32_t nranks,
         ctx->tmem = !(tm && tm[0] == '0');
         const char* bnd = std::getenv("TPMG_BAND");
         if (bnd) ctx->band_w = std::max(0, std::atoi(bnd));
+        const char* cvo = std::getenv("TPMG_CARVEOUT");
+        ctx->carveout_fit = cvo && std::strcmp(cvo, "fit") == 0;
         const char* tst = std::getenv("TPMG_TMA_STORE");
         ctx->tma_store = tst && tst[0] == '1';
         const char* dpb = std::getenv("TPMG_DEV_PUBLISH");

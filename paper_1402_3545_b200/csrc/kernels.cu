@@ -33,9 +33,10 @@ using namespace dev;
 constexpr int TX = kTileX;  // columns per tile row (one warp, 256 B per row segment)
 constexpr int KB = kStageK; // vertical levels per pipeline stage
 constexpr int kNS = 3;  // pipeline stages
+constexpr int kNsCgdir = 3;   // the CG direction kernel (8-row tiles, one CTA per SM; 4 stages: r2ay, 20% slower)
 // the CG preconditioner with per-column fields keeps 4 tile rows (4 warps per SM) with 2 stages
 template <int MODE, int GEN>
-__host__ __device__ constexpr int stages() { return (GEN == 2 && is_cgprec(MODE)) ? 2 : kNS; }
+__host__ __device__ constexpr int stages() { return (GEN == 2 && is_cgprec(MODE)) ? 2 : (MODE == MODE_CGDIR ? kNsCgdir : kNS); }
 
 // 1/x for the per-column pivots: the approximate reciprocal (MUFU) refined by two Newton
 // steps (error ~2^-92 before rounding, i.e. correctly rounded up to an ulp) -- 5 instructions
@@ -830,7 +831,7 @@ size_t line_smem_bytes(int nz, int gen = 0, int tms = 0, bool tst = false)
         return (size_t)(((3 * nz + 15) & ~15) + ((4 * nz + 15) & ~15) + (size_t)tms * G3::STAGE + 64 + 16) * sizeof(double);
     const bool tm = tms > 0;
     size_t d = ((3 * nz + 15) & ~15) + (gen >= 2 ? ((4 * nz + 15) & ~15) : gen ? ((3 * nz + 15) & ~15) : 0) +
-               (size_t)(tm ? tms : gen == 2 ? stages<MODE, 2>() : kNS) * G::STAGE + (T::THOMAS ? (size_t)((tm ? 0 : nz) + (gen == 2 ? (nz + KB - 1) / KB : 0)) * G::NT : 0) + 64 + 16 +
+               (size_t)(tm ? tms : gen == 2 ? stages<MODE, 2>() : gen ? stages<MODE, 1>() : stages<MODE, 0>()) * G::STAGE + (T::THOMAS ? (size_t)((tm ? 0 : nz) + (gen == 2 ? (nz + KB - 1) / KB : 0)) * G::NT : 0) + 64 + 16 +
                (MODE == MODE_RESTRICT ? 2 * TY * (KB + 1) * (TX / 2) : 0) +
                (tst ? 16 + (3 * 2 + 2) * KB * TY * TX : 0);   // TST staging + its 128-byte alignment
     return d * sizeof(double);
@@ -856,6 +857,12 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
     }
     if (smem > limit) return cudaErrorInvalidConfiguration;
     int per_sm = 0;
+    static int carve = 100;   // per instantiation: the carveout last set
+    if (ln.carveout_fit && carve != 100) {   // query the occupancy at the largest carveout
+        cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e2 != cudaSuccess) return e2;
+        carve = 100;
+    }
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TX * TY, smem);
     if (e != cudaSuccess) return e;
     per_sm = std::max(per_sm, 1);
@@ -869,6 +876,14 @@ cudaError_t launch_line_l(const Launcher& ln, const LineArgs& a)
     if (MODE == MODE_CGDIR && a.cgdir_ctas > 0) per_sm = std::min(per_sm, a.cgdir_ctas);
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, ln.num_sms - ln.reserve_sms) * per_sm);
     if (grid <= 0) return cudaSuccess;
+    if (ln.carveout_fit) {   // the smallest carveout that holds the resident CTAs: the rest stays L1
+        const int pct = carveout_pct(smem, std::min<int64_t>(per_sm, grid));
+        if (pct != carve) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+            if (e != cudaSuccess) return e;
+            carve = pct;
+        }
+    }
     return launch_kernel(ln, kern, dim3((unsigned)grid), dim3(TX * TY), smem, a);
 }
 

@@ -219,8 +219,19 @@ struct Launcher {
                        // prologue with the previous kernel's tail (griddepcontrol)
     bool tmem = true;  // one-thread-per-column Thomas kernels keep g' in Tensor Memory (nz <= 128)
     int tm_stages = 3; // their TMA ring depth (3; 4, 5 for CGPREC A/B)
+    bool carveout_fit = false;   // line kernels: the smallest shared-memory carveout for their resident CTAs (TPMG_CARVEOUT=fit)
     int tm_ctas = 1;   // CTAs per SM of those kernels (TMEM holds 2; 1 and 2 measured equal: r2c, r2f, r2k, r2p; 1 keeps every CG variant on the same grid, so the reductions -- and the iteration -- are identical)
 };
+
+// Shared-memory carveout (percent of the 228 KB maximum) that holds `ctas` CTAs of `smem`
+// dynamic bytes each (+ the 1 KB per-CTA reserve); the rest of the SM's 256 KB is L1.
+inline int carveout_pct(size_t smem, int64_t ctas)
+{
+    const size_t need = (size_t)ctas * (smem + 1024);
+    const size_t maxs = (size_t)228 * 1024;
+    int pct = (int)((need * 100 + maxs - 1) / maxs);
+    return pct < 1 ? 1 : pct > 100 ? 100 : pct;
+}
 
 // Launch with the PDL attribute when ln.pdl.  Every kernel launched this way executes
 // griddepcontrol.wait (dev::pdl_wait) in every CTA before touching global data, so it
