@@ -33,7 +33,7 @@ using namespace dev;
 constexpr int TX = kTileX;  // columns per tile row (one warp, 256 B per row segment)
 constexpr int KB = kStageK; // vertical levels per pipeline stage
 constexpr int kNS = 3;  // pipeline stages
-constexpr int kNsCgdir = 3;   // the CG direction kernel (8-row tiles, one CTA per SM; 4 stages: r2ay, 20% slower)
+constexpr int kNsCgdir = 3;   // the CG direction kernel (8-row tiles, one CTA per SM): 2 stages = 3 (r2ba), 4 stages 20% slower (r2ay)
 // the CG preconditioner with per-column fields keeps 4 tile rows (4 warps per SM) with 2 stages
 template <int MODE, int GEN>
 __host__ __device__ constexpr int stages() { return (GEN == 2 && is_cgprec(MODE)) ? 2 : (MODE == MODE_CGDIR ? kNsCgdir : kNS); }
@@ -924,6 +924,7 @@ cudaError_t launch_line_t(const Launcher& ln, const LineArgs& a)
             // selects 3 (default), 4 or 5 for the CG preconditioner
             if constexpr (MODE == MODE_CGPREC) {
                 if (a.tst) return launch_line_l<MODE, 4, 1, 0, 3, false, true>(ln, a);
+                if (ln.tm_stages == 2) return launch_line_l<MODE, 4, 1, 0, 2>(ln, a);
                 if (ln.tm_stages == 4) return launch_line_l<MODE, 4, 1, 0, 4>(ln, a);
                 if (ln.tm_stages == 5) return launch_line_l<MODE, 4, 1, 0, 5>(ln, a);
             }
