@@ -10,7 +10,7 @@ while read -r line; do
   i=$((i + 1))
   set -- $line
   nx=$1; shift
-  name=$(echo "$nx $*" | sed 's/[ =]//g;s/TPMG_//g')
+  name=$(echo "$nx $*" | sed 's/[ =/.]//g;s/TPMG_//g')
   [ -n "$REPNAMES" ] && name="${name}_$i"
   env "$@" timeout 900 python bench.py --global-nx $nx --solver ${SOLVER:-cg} --steps 2 --warmup 3 --no-cpu-baseline --no-e2e \
     > gpurun_out/wide_${TAG}_${name}.json 2> gpurun_out/wide_${TAG}_${name}.err
